@@ -1,0 +1,90 @@
+"""In-tree build of the native libraries (sm_100a only).
+
+  libstk_b200.so   : CUDA kernels + the C-ABI (include/stk_b200.h) + the C++
+                     stereotk:: drop-in shim (include/stereotk/...).
+  libstk_synth.so  : host-side synthetic scene generators (plain C).
+
+Built with nvcc / gcc directly so the .so files live next to this file and
+travel with the repo snapshot to the GPU box.  Rebuilds only when a source is
+newer than its output.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+INCLUDE = ROOT / "include"
+
+LIB = PKG / "libstk_b200.so"
+SYNTH = PKG / "libstk_synth.so"
+
+CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+CU_SOURCES = [
+    "k_lightness.cu",
+    "k_kmeans.cu",
+    "k_boundary.cu",
+    "k_ccl.cu",
+    "k_sad.cu",
+    "k_reconstruct.cu",
+    "k_blur.cu",
+    "stk_capi.cu",
+]
+CXX_SOURCES: list = []  # stereotk_shim.cpp added with the C++ drop-in
+HEADERS = ["stk_internal.cuh", "stk_device.cuh"]
+
+
+def _newer(srcs, out: Path) -> bool:
+    if not out.exists():
+        return True
+    t = out.stat().st_mtime
+    return any(Path(s).stat().st_mtime > t for s in srcs if Path(s).exists())
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(map(str, cmd)), file=sys.stderr)
+    r = subprocess.run(list(map(str, cmd)), capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"build failed: {' '.join(map(str, cmd))}\n{r.stdout}\n{r.stderr}")
+    return r
+
+
+def build(verbose: bool = False, force: bool = False) -> None:
+    objdir = PKG / "build"
+    objdir.mkdir(exist_ok=True)
+    deps = [CSRC / h for h in HEADERS] + [INCLUDE / "stk_b200.h"]
+    deps += list((INCLUDE / "stereotk").glob("*.hpp"))
+    objs = []
+    for src in CU_SOURCES:
+        s = CSRC / src
+        o = objdir / (src + ".o")
+        objs.append(o)
+        if force or _newer([s] + deps, o):
+            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                  "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr",
+                  "-I", INCLUDE, "-I", CSRC, "-rdc=false", "-c", s, "-o", o], verbose)
+    for src in CXX_SOURCES:
+        s = CSRC / src
+        o = objdir / (src + ".o")
+        objs.append(o)
+        if force or _newer([s] + deps, o):
+            _run(["/usr/bin/g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-I", INCLUDE,
+                  "-c", s, "-o", o], verbose)
+    if force or _newer(objs, LIB):
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt",
+              "-ldl", "-lpthread"], verbose)
+    if force or _newer([CSRC / "synth.c"], SYNTH):
+        _run(["/usr/bin/gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-Wall", "-o", SYNTH,
+              CSRC / "synth.c"], verbose)
+
+
+if __name__ == "__main__":
+    build(verbose=True, force="--force" in sys.argv)

@@ -1,0 +1,216 @@
+// K6 fill_rows + K7 peek_cols -- dense reconstruction from the sparse map
+// (reference: reconstruct.cpp:11-109, the paper's Algorithms 1 and 2).
+//
+// K6: one CTA per row; the row is staged in shared memory, every thread owns a
+//     contiguous chunk, and two block scans give each chunk the nearest known
+//     (x, d) on either side.  A run of unknowns between consecutive knowns of
+//     equal disparity is filled; knowns never change (reconstruct.cpp:11-33).
+// K7: one CTA per 32 columns x 16 row segments.  Phase 1 summarises each
+//     segment (known count, first/last known); phase 2 derives, per segment,
+//     the nearest known above/below and, per column, the first two / last two
+//     knowns; phase 3 walks the segment again and resolves each run of
+//     unknowns with peek_estimate (reconstruct.cpp:40-46) on the snapshot:
+//       0 knowns -> stays unknown, 1 known -> copy,
+//       above & below -> est(above, below),
+//       nothing above -> est(first two), nothing below -> est(last two).
+#include "stk_device.cuh"
+
+namespace stk {
+
+namespace {
+
+constexpr int kFillThreads = 256;
+
+__device__ __forceinline__ int16_t peek_estimate(int a, int b, int thr) {
+    const int r = a >= b ? a - b : b - a;
+    if (r > thr) return (int16_t)(a < b ? a : b);
+    return (int16_t)((a + b) / 2);
+}
+
+// ------------------------------------------------------------------ K6 ----
+__global__ void __launch_bounds__(kFillThreads) k_fill_rows(Frame f, const int16_t* __restrict__ in,
+                                                            int16_t* __restrict__ out) {
+    extern __shared__ int16_t row[];
+    __shared__ uint32_t wl[kFillThreads / 32], wf[kFillThreads / 32];
+    const int W = f.W, y = blockIdx.x, tid = threadIdx.x;
+    const int16_t* src = in + (size_t)y * W;
+    for (int x = tid; x < W; x += kFillThreads) row[x] = src[x];
+    __syncthreads();
+    const int ch = (W + kFillThreads - 1) / kFillThreads;
+    const int a = min(W, tid * ch), b = min(W, a + ch);
+    // last known in my chunk as ((x+1)<<16 | d), first known as (x<<16 | d)
+    uint32_t klast = 0, kfirst = 0xffffffffu;
+    for (int x = a; x < b; ++x) {
+        const int16_t d = row[x];
+        if (d >= 0) {
+            klast = ((uint32_t)(x + 1) << 16) | (uint16_t)d;
+            if (kfirst == 0xffffffffu) kfirst = ((uint32_t)x << 16) | (uint16_t)d;
+        }
+    }
+    // exclusive max-scan (prev) and exclusive reverse min-scan (next)
+    const int lane = tid & 31, wid = tid >> 5;
+    uint32_t incl_l = klast;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl_l, o);
+        if (lane >= o) incl_l = max(incl_l, v);
+    }
+    uint32_t incl_f = kfirst;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_down_sync(0xffffffffu, incl_f, o);
+        if (lane + o < 32) incl_f = min(incl_f, v);
+    }
+    if (lane == 31) wl[wid] = incl_l;
+    if (lane == 0) wf[wid] = incl_f;
+    __syncthreads();
+    uint32_t prev = __shfl_up_sync(0xffffffffu, incl_l, 1);
+    if (lane == 0) prev = 0;
+    for (int i = 0; i < wid; ++i) prev = max(prev, wl[i]);
+    uint32_t next = __shfl_down_sync(0xffffffffu, incl_f, 1);
+    if (lane == 31) next = 0xffffffffu;
+    for (int i = wid + 1; i < kFillThreads / 32; ++i) next = min(next, wf[i]);
+    // walk my chunk
+    bool have_prev = prev != 0;
+    int pd = have_prev ? (int)(prev & 0xffffu) : -1;
+    int rs = -1;
+    for (int x = a; x < b; ++x) {
+        const int16_t d = row[x];
+        if (d >= 0) {
+            if (rs >= 0 && have_prev && pd == d)
+                for (int q = rs; q < x; ++q) row[q] = d;
+            rs = -1;
+            have_prev = true;
+            pd = d;
+        } else if (rs < 0) {
+            rs = x;
+        }
+    }
+    if (rs >= 0 && have_prev && next != 0xffffffffu && (int)(next & 0xffffu) == pd)
+        for (int q = rs; q < b; ++q) row[q] = (int16_t)pd;
+    __syncthreads();
+    int16_t* dst = out + (size_t)y * W;
+    for (int x = tid; x < W; x += kFillThreads) dst[x] = row[x];
+}
+
+// ------------------------------------------------------------------ K7 ----
+constexpr int PC = 32;  // columns per CTA
+constexpr int PS = 16;  // row segments per column
+
+struct SegSum {
+    int count;     // knowns in the segment
+    int16_t f1, f2;  // first two knowns (top-down), -1 if absent
+    int16_t l1, l2;  // last known, second last, -1 if absent
+};
+
+__global__ void __launch_bounds__(PC * PS) k_peek_cols(Frame f, const int16_t* __restrict__ in,
+                                                       int16_t* __restrict__ out) {
+    __shared__ SegSum seg[PS][PC];
+    __shared__ unsigned long long red[PS];
+    const int W = f.W, H = f.H, thr = f.thr;
+    const int cx = threadIdx.x, s = threadIdx.y;
+    const int x = blockIdx.x * PC + cx;
+    const int sr = (H + PS - 1) / PS;
+    const int ya = min(H, s * sr), yb = min(H, ya + sr);
+    const bool col = x < W;
+    // phase 1
+    SegSum m{0, -1, -1, -1, -1};
+    if (col)
+        for (int y = ya; y < yb; ++y) {
+            const int16_t d = in[(size_t)y * W + x];
+            if (d >= 0) {
+                if (m.count == 0) m.f1 = d;
+                else if (m.count == 1) m.f2 = d;
+                m.l2 = m.l1;
+                m.l1 = d;
+                ++m.count;
+            }
+        }
+    seg[s][cx] = m;
+    __syncthreads();
+    // phase 2
+    int total = 0;
+    for (int i = 0; i < PS; ++i) total += seg[i][cx].count;
+    int above = -1, below = -1;
+    for (int i = s - 1; i >= 0 && above < 0; --i)
+        if (seg[i][cx].count) above = seg[i][cx].l1;
+    for (int i = s + 1; i < PS && below < 0; ++i)
+        if (seg[i][cx].count) below = seg[i][cx].f1;
+    int cf1 = -1, cf2 = -1, cl1 = -1, cl2 = -1;  // column first two / last two
+    for (int i = 0; i < PS && cf2 < 0; ++i) {
+        const SegSum& g = seg[i][cx];
+        if (!g.count) continue;
+        if (cf1 < 0) {
+            cf1 = g.f1;
+            if (g.count > 1) cf2 = g.f2;
+        } else {
+            cf2 = g.f1;
+        }
+    }
+    for (int i = PS - 1; i >= 0 && cl2 < 0; --i) {
+        const SegSum& g = seg[i][cx];
+        if (!g.count) continue;
+        if (cl1 < 0) {
+            cl1 = g.l1;
+            if (g.count > 1) cl2 = g.l2;
+        } else {
+            cl2 = g.l1;
+        }
+    }
+    // phase 3
+    unsigned long long known = 0;
+    if (col) {
+        int cur = above;  // nearest known above the current run
+        int rs = -1;
+        for (int y = ya; y <= yb; ++y) {
+            const int16_t d = y < yb ? in[(size_t)y * W + x] : (int16_t)-2;
+            if (y < yb && d < 0) {
+                if (rs < 0) rs = y;
+                continue;
+            }
+            const int nb = y < yb ? d : below;  // nearest known below the run
+            if (rs >= 0) {
+                int16_t v;
+                if (total == 0) v = -1;
+                else if (total == 1) v = (int16_t)(cur >= 0 ? cur : nb);
+                else if (cur >= 0 && nb >= 0) v = peek_estimate(cur, nb, thr);
+                else if (cur < 0) v = peek_estimate(cf1, cf2, thr);
+                else v = peek_estimate(cl2, cl1, thr);
+                for (int q = rs; q < y; ++q) out[(size_t)q * W + x] = v;
+                if (v >= 0) known += (unsigned long long)(y - rs);
+                rs = -1;
+            }
+            if (y < yb) {
+                out[(size_t)y * W + x] = d;
+                ++known;
+                cur = d;
+            }
+        }
+    }
+    // known count for DepthStats::known_fraction
+    for (int o = 16; o > 0; o >>= 1) known += __shfl_xor_sync(0xffffffffu, known, o);
+    if (cx == 0) red[s] = known;
+    __syncthreads();
+    if (s == 0 && cx == 0) {
+        unsigned long long t = 0;
+        for (int i = 0; i < PS; ++i) t += red[i];
+        if (t) atomicAdd(&f.sc->known, t);
+    }
+}
+
+}  // namespace
+
+void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStream_t st) {
+    if (f.N == 0) return;
+    const size_t sm = (size_t)f.W * sizeof(int16_t);
+    if (sm > 48 * 1024)
+        cudaFuncSetAttribute(k_fill_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_fill_rows<<<f.H, kFillThreads, sm, st>>>(f, in, out);
+}
+
+void launch_peek_cols(const Frame& f, const int16_t* in, int16_t* out, int16_t*, cudaStream_t st) {
+    if (f.N == 0) return;
+    k_peek_cols<<<(f.W + PC - 1) / PC, dim3(PC, PS), 0, st>>>(f, in, out);
+}
+
+size_t peek_scratch_bytes(int, int) { return 0; }
+
+}  // namespace stk

@@ -1,0 +1,1127 @@
+// stk_capi.cu -- the C-ABI (include/stk_b200.h): context, per-slot HBM
+// planes, TMA descriptors, frame enqueue (optionally as a CUDA graph), and the
+// synchronous per-stage entries used as the parity surface.
+//
+// Validation mirrors the reference's checks and message text so the C++ shim
+// can rethrow stereotk::ParamError verbatim (pipeline.cpp:23-60,
+// segmentation.cpp:64-93, boundary.cpp:150-185, stereo.cpp:32-58,
+// reconstruct.cpp:50-55, refocus.cpp:16-57).
+#include <cub/device/device_radix_sort.cuh>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "stk_b200.h"
+#include "stk_internal.cuh"
+
+using namespace stk;
+
+struct stk_ctx;
+
+namespace {
+
+thread_local std::string t_err;
+
+constexpr int kMaxWindow = 63;     // nw <= 16 words per window row (k_sad_list)
+constexpr int kMaxDisparity = 1023;  // argmin key packs d in 10 bits
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+struct TMap {
+    CUtensorMap map;
+    const void* ptr = nullptr;
+    int W = -1, H = -1, pitch = -1, bw = -1, bh = -1, esz = -1;
+};
+
+struct GraphKey {
+    int W = -1, H = -1, kcfg, window, D, thr, full, focus, hw, exact, lut_len, sad, want_raw;
+    double frac;
+    const void *rgbL, *rgbR, *out_rgb, *dense;
+    bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
+};
+
+struct Slot {
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev[8] = {};
+    cudaEvent_t done = nullptr;
+    char* base = nullptr;
+    size_t bytes = 0;
+    // layout for the current frame geometry
+    int W = 0, H = 0, P = 0;
+    uint8_t *rgbL, *rgbR, *grayL, *grayR, *mraw, *mref, *mprn, *manc, *out_rgb;
+    uint16_t *labels16, *scratch16;
+    uint32_t* mbits;
+    int32_t *par, *rank, *roots;
+    uint32_t *cnt, *szhist, *list, *tile_off;
+    unsigned long long* lb;
+    int lb_stride = 0;
+    int16_t *sparse, *rowf, *dense;
+    DevScalars* sc = nullptr;
+    DevScalars* h_sc = nullptr;  // pinned mirror
+    // focus tables
+    uint8_t* d_lut = nullptr;
+    int lut_cap = 0;
+    float* d_g1 = nullptr;
+    double* d_g2 = nullptr;
+    int g_cap = 0;
+    std::vector<uint8_t> h_lut;
+    std::vector<float> h_g1;
+    std::vector<double> h_g2;
+    // label_components scratch
+    void* cub_tmp = nullptr;
+    size_t cub_bytes = 0;
+    // tensor maps
+    TMap tm_morph, tm_sadL, tm_sadR, tm_stage;
+    // graph
+    cudaGraphExec_t gexec = nullptr;
+    GraphKey gkey;
+    // pending frame
+    bool pending = false;
+    bool timed = false;
+    bool graph = false;
+    int kernels = 0;
+    int k_for_out = 0;
+    Frame f{};
+    stk_frame_out out{};
+};
+
+}  // namespace
+
+struct stk_ctx {
+    int device = 0;
+    std::string err;
+    LstarTables* d_tab = nullptr;
+    std::vector<Slot> slots;
+    int sad_kernel = SAD_AUTO;
+    int use_graphs = 1;
+    EncodeTiledFn encode = nullptr;
+};
+
+namespace {
+
+stk_status fail(stk_ctx* ctx, stk_status s, const std::string& msg) {
+    t_err = msg;
+    if (ctx) ctx->err = msg;
+    return s;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(ctx, STK_ECUDA, std::string("cuda: ") + #call + ": " +            \
+                                            cudaGetErrorString(e_));                      \
+    } while (0)
+
+std::string dims(int w, int h) { return std::to_string(w) + "x" + std::to_string(h); }
+
+// ------------------------------------------------ L* tables (host libm) ---
+// lightness.cpp:14-21, 44-49 evaluated with the same libm as the reference.
+double srgb_to_linear(int v) {
+    const double c = v / 255.0;
+    return c <= 0.04045 ? c / 12.92 : std::pow((c + 0.055) / 1.055, 2.4);
+}
+
+int lstar_byte(double y) {
+    const double eps = 216.0 / 24389.0, kappa = 24389.0 / 27.0;
+    const double f = y > eps ? std::cbrt(y) : (kappa * y + 16.0) / 116.0;
+    const double lstar = 116.0 * f - 16.0;
+    long s = std::lround(lstar * 255.0 / 100.0);
+    return (int)(s < 0 ? 0 : (s > 255 ? 255 : s));
+}
+
+void make_lstar_tables(LstarTables* t) {
+    for (int v = 0; v < 256; ++v) t->linear[v] = srgb_to_linear(v);
+    t->thr[0] = -1.0;
+    uint64_t hi_bits;
+    const double two = 2.0;
+    std::memcpy(&hi_bits, &two, 8);
+    for (int v = 1; v < 256; ++v) {
+        // smallest non-negative double y with L*(y) >= v, by bisection over the
+        // IEEE-754 bit patterns (monotone for y >= 0)
+        uint64_t lo = 0, hi = hi_bits;
+        while (hi - lo > 1) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            double y;
+            std::memcpy(&y, &mid, 8);
+            if (lstar_byte(y) >= v) hi = mid;
+            else lo = mid;
+        }
+        std::memcpy(&t->thr[v], &hi, 8);
+    }
+}
+
+// --------------------------------------------------------------- layout ---
+struct Layout {
+    size_t off[32];
+    size_t total;
+};
+
+enum {
+    L_RGBL, L_RGBR, L_OUT, L_GRAYL, L_GRAYR, L_MRAW, L_MREF, L_MPRN, L_MANC, L_LAB16, L_SCR16,
+    L_MBITS, L_PAR, L_CNT, L_RANK, L_SZH, L_ROOTS, L_LIST, L_TOFF, L_LB, L_SPARSE, L_ROWF,
+    L_DENSE, L_SC, L_COUNT
+};
+
+Layout layout_for(int W, int H, int* P_out, int* lb_stride_out) {
+    const size_t N = (size_t)W * H;
+    const int P = (int)align_up((size_t)std::max(W, 1), 64);
+    const size_t PH = (size_t)P * H;
+    const int TX = (W + kRowTile - 1) / kRowTile;
+    const size_t n_tiles = (size_t)H * TX;
+    const size_t n_chunks = (n_tiles + kTilesPerChunk - 1) / kTilesPerChunk;
+    const int lb_stride = (int)n_chunks + 1;
+    size_t sz[L_COUNT];
+    sz[L_RGBL] = sz[L_RGBR] = sz[L_OUT] = 3 * N + 64;
+    sz[L_GRAYL] = sz[L_GRAYR] = sz[L_MRAW] = sz[L_MREF] = sz[L_MPRN] = sz[L_MANC] = PH + 64;
+    sz[L_LAB16] = 2 * N + 64;
+    sz[L_SCR16] = 2 * PH + 64;
+    sz[L_MBITS] = (size_t)H * TX * 4 * 4 + 64;
+    sz[L_PAR] = sz[L_CNT] = sz[L_RANK] = sz[L_ROOTS] = sz[L_LIST] = 4 * N + 64;
+    sz[L_SZH] = 4 * (N + 2) + 64;
+    sz[L_TOFF] = 4 * (n_tiles + 1) + 64;
+    sz[L_LB] = 8 * (size_t)LB_COUNT * lb_stride + 64;
+    sz[L_SPARSE] = sz[L_ROWF] = sz[L_DENSE] = 2 * N + 64;
+    sz[L_SC] = sizeof(DevScalars);
+    Layout L;
+    size_t o = 0;
+    for (int i = 0; i < L_COUNT; ++i) {
+        L.off[i] = o;
+        o = align_up(o + sz[i], 256);
+    }
+    L.total = o;
+    *P_out = P;
+    *lb_stride_out = lb_stride;
+    return L;
+}
+
+stk_status ensure_slot(stk_ctx* ctx, Slot& s, int W, int H) {
+    if (s.W == W && s.H == H && s.base) return STK_OK;
+    int P, lbs;
+    const Layout L = layout_for(W, H, &P, &lbs);
+    if (L.total > s.bytes) {
+        if (s.base) {
+            CK(cudaStreamSynchronize(s.st));
+            CK(cudaFree(s.base));
+            s.base = nullptr;
+        }
+        CK(cudaMalloc(&s.base, L.total));
+        s.bytes = L.total;
+    }
+    char* b = s.base;
+    s.W = W;
+    s.H = H;
+    s.P = P;
+    s.lb_stride = lbs;
+    s.rgbL = (uint8_t*)(b + L.off[L_RGBL]);
+    s.rgbR = (uint8_t*)(b + L.off[L_RGBR]);
+    s.out_rgb = (uint8_t*)(b + L.off[L_OUT]);
+    s.grayL = (uint8_t*)(b + L.off[L_GRAYL]);
+    s.grayR = (uint8_t*)(b + L.off[L_GRAYR]);
+    s.mraw = (uint8_t*)(b + L.off[L_MRAW]);
+    s.mref = (uint8_t*)(b + L.off[L_MREF]);
+    s.mprn = (uint8_t*)(b + L.off[L_MPRN]);
+    s.manc = (uint8_t*)(b + L.off[L_MANC]);
+    s.labels16 = (uint16_t*)(b + L.off[L_LAB16]);
+    s.scratch16 = (uint16_t*)(b + L.off[L_SCR16]);
+    s.mbits = (uint32_t*)(b + L.off[L_MBITS]);
+    s.par = (int32_t*)(b + L.off[L_PAR]);
+    s.cnt = (uint32_t*)(b + L.off[L_CNT]);
+    s.rank = (int32_t*)(b + L.off[L_RANK]);
+    s.szhist = (uint32_t*)(b + L.off[L_SZH]);
+    s.roots = (int32_t*)(b + L.off[L_ROOTS]);
+    s.list = (uint32_t*)(b + L.off[L_LIST]);
+    s.tile_off = (uint32_t*)(b + L.off[L_TOFF]);
+    s.lb = (unsigned long long*)(b + L.off[L_LB]);
+    s.sparse = (int16_t*)(b + L.off[L_SPARSE]);
+    s.rowf = (int16_t*)(b + L.off[L_ROWF]);
+    s.dense = (int16_t*)(b + L.off[L_DENSE]);
+    s.sc = (DevScalars*)(b + L.off[L_SC]);
+    if (s.gexec) {
+        cudaGraphExecDestroy(s.gexec);
+        s.gexec = nullptr;
+        s.gkey = GraphKey{};
+    }
+    return STK_OK;
+}
+
+Frame make_frame(const Slot& s, int W, int H, const stk_config* cfg) {
+    Frame f{};
+    f.W = W;
+    f.H = H;
+    f.P = s.P;
+    f.N = (long long)W * H;
+    f.TX = (W + kRowTile - 1) / kRowTile;
+    f.n_tiles = H * f.TX;
+    f.n_chunks = (f.n_tiles + kTilesPerChunk - 1) / kTilesPerChunk;
+    f.bits_words = f.TX * 4;
+    if (cfg) {
+        f.kcfg = cfg->k;
+        f.window = cfg->window;
+        f.hw = cfg->window / 2;
+        f.D = cfg->max_disparity;
+        f.thr = cfg->threshold;
+        f.frac = cfg->prune_fraction;
+    }
+    f.rgbL = s.rgbL;
+    f.rgbR = s.rgbR;
+    f.grayL = s.grayL;
+    f.grayR = s.grayR;
+    f.labels16 = s.labels16;
+    f.mraw = s.mraw;
+    f.mref = s.mref;
+    f.mprn = nullptr;
+    f.manc = nullptr;
+    f.mbits = s.mbits;
+    f.par = s.par;
+    f.cnt = s.cnt;
+    f.rank = s.rank;
+    f.szhist = s.szhist;
+    f.roots = s.roots;
+    f.list = s.list;
+    f.tile_off = s.tile_off;
+    f.lb = s.lb;
+    f.lb_stride = s.lb_stride;
+    f.sparse = s.sparse;
+    f.rowf = s.rowf;
+    f.dense = s.dense;
+    f.out_rgb = s.out_rgb;
+    f.sc = s.sc;
+    return f;
+}
+
+stk_status encode(stk_ctx* ctx, TMap& t, const void* ptr, int esz, int W, int H, int pitch_bytes,
+                  int bw, int bh) {
+    if (t.ptr == ptr && t.W == W && t.H == H && t.pitch == pitch_bytes && t.bw == bw &&
+        t.bh == bh && t.esz == esz)
+        return STK_OK;
+    const cuuint64_t gdim[2] = {(cuuint64_t)W, (cuuint64_t)H};
+    const cuuint64_t gstride[1] = {(cuuint64_t)pitch_bytes};
+    const cuuint32_t box[2] = {(cuuint32_t)bw, (cuuint32_t)bh};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = ctx->encode(&t.map, esz == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                                    : CU_TENSOR_MAP_DATA_TYPE_UINT16,
+                                   2, const_cast<void*>(ptr), gdim, gstride, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(ctx, STK_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    t.ptr = ptr;
+    t.W = W;
+    t.H = H;
+    t.pitch = pitch_bytes;
+    t.bw = bw;
+    t.bh = bh;
+    t.esz = esz;
+    return STK_OK;
+}
+
+#define TRY(x)                          \
+    do {                                \
+        stk_status s_ = (x);            \
+        if (s_ != STK_OK) return s_;    \
+    } while (0)
+
+// ----------------------------------------------------------- validation ---
+stk_status check_config(stk_ctx* ctx, const stk_config* c) {
+    if (!c) return fail(ctx, STK_EPARAM, "pipeline: null config");
+    if (c->k < 1) return fail(ctx, STK_EPARAM, "pipeline: k must be at least 1, got " + std::to_string(c->k));
+    if (c->window < 1 || c->window % 2 == 0)
+        return fail(ctx, STK_EPARAM, "pipeline: window must be odd and positive, got " + std::to_string(c->window));
+    if (c->max_disparity < 0)
+        return fail(ctx, STK_EPARAM, "pipeline: max_disparity must be >= 0, got " + std::to_string(c->max_disparity));
+    if (c->threshold < 0)
+        return fail(ctx, STK_EPARAM, "pipeline: threshold must be >= 0, got " + std::to_string(c->threshold));
+    if (!(c->prune_fraction >= 0.0 && c->prune_fraction < 1.0))
+        return fail(ctx, STK_EPARAM, "pipeline: prune_fraction must be in [0, 1), got " + std::to_string(c->prune_fraction));
+    if (c->workers < 1)
+        return fail(ctx, STK_EPARAM, "pipeline: workers must be at least 1, got " + std::to_string(c->workers));
+    return STK_OK;
+}
+
+stk_status check_gpu_limits(stk_ctx* ctx, int window, int D) {
+    if (window > kMaxWindow)
+        return fail(ctx, STK_EPARAM, "stk_b200: window " + std::to_string(window) +
+                                         " exceeds the GPU kernel limit " + std::to_string(kMaxWindow));
+    if (D > kMaxDisparity)
+        return fail(ctx, STK_EPARAM, "stk_b200: max_disparity " + std::to_string(D) +
+                                         " exceeds the GPU kernel limit " + std::to_string(kMaxDisparity));
+    return STK_OK;
+}
+
+stk_status check_focus(stk_ctx* ctx, const stk_focus* fo, int D, int* size_out) {
+    if (fo->n_ranges <= 0 || !fo->lo || !fo->hi)
+        return fail(ctx, STK_EPARAM, "build_blur_map: no focus ranges given");
+    for (int i = 0; i < fo->n_ranges; ++i)
+        if (fo->lo[i] < 0 || fo->lo[i] > fo->hi[i] || fo->hi[i] > D)
+            return fail(ctx, STK_EPARAM, "build_blur_map: bad focus range [" + std::to_string(fo->lo[i]) +
+                                             ", " + std::to_string(fo->hi[i]) + "] for max disparity " +
+                                             std::to_string(D));
+    const int size = fo->kernel_size > 0 ? fo->kernel_size : stk_default_kernel_size(fo->sigma);
+    if (!(fo->sigma > 0.0))
+        return fail(ctx, STK_EPARAM, "gaussian_kernel: sigma must be positive, got " + std::to_string(fo->sigma));
+    if (size < 1 || size % 2 == 0)
+        return fail(ctx, STK_EPARAM, "gaussian_kernel: size must be odd and positive, got " + std::to_string(size));
+    if (blur_smem_bytes(size / 2, fo->exact_blur != 0) > 220 * 1024)
+        return fail(ctx, STK_EPARAM, "stk_b200: blur kernel size " + std::to_string(size) +
+                                         " exceeds the GPU tile limit");
+    *size_out = size;
+    return STK_OK;
+}
+
+// Upload the focus LUT and blur weights for slot s (host-cached).
+stk_status upload_focus(stk_ctx* ctx, Slot& s, const int* lo, const int* hi, int n, int D,
+                        double sigma, int size, bool exact, BlurParams* bp) {
+    const int lut_len = D + 1;
+    std::vector<uint8_t> lut(lut_len, 0);
+    for (int d = 0; d < lut_len; ++d)
+        for (int r = 0; r < n; ++r)
+            if (d >= lo[r] && d <= hi[r]) lut[d] = 1;
+    const int hw = size / 2;
+    std::vector<float> g1(size);
+    std::vector<double> g2((size_t)size * size);
+    {
+        double sum = 0.0;
+        std::vector<double> t(size);
+        for (int i = -hw; i <= hw; ++i) {
+            t[i + hw] = std::exp(-(double)(i * i) / (2.0 * sigma * sigma));
+            sum += t[i + hw];
+        }
+        for (int i = 0; i < size; ++i) g1[i] = (float)(t[i] / sum);
+        stk_gaussian_kernel(sigma, size, g2.data());
+    }
+    if (lut_len > s.lut_cap) {
+        if (s.d_lut) CK(cudaFree(s.d_lut));
+        s.lut_cap = std::max(lut_len, 1024);
+        CK(cudaMalloc(&s.d_lut, s.lut_cap));
+        s.h_lut.clear();
+    }
+    if ((int)g2.size() > s.g_cap) {
+        if (s.d_g1) CK(cudaFree(s.d_g1));
+        if (s.d_g2) CK(cudaFree(s.d_g2));
+        s.g_cap = std::max((int)g2.size(), 4096);
+        CK(cudaMalloc(&s.d_g1, s.g_cap * sizeof(float)));
+        CK(cudaMalloc(&s.d_g2, s.g_cap * sizeof(double)));
+        s.h_g1.clear();
+        s.h_g2.clear();
+    }
+    if (s.h_lut != lut) {
+        CK(cudaStreamSynchronize(s.st));  // a previous frame may still read it
+        CK(cudaMemcpy(s.d_lut, lut.data(), lut_len, cudaMemcpyHostToDevice));
+        s.h_lut = lut;
+    }
+    if (s.h_g1 != g1 || s.h_g2 != g2) {
+        CK(cudaStreamSynchronize(s.st));
+        CK(cudaMemcpy(s.d_g1, g1.data(), g1.size() * sizeof(float), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(s.d_g2, g2.data(), g2.size() * sizeof(double), cudaMemcpyHostToDevice));
+        s.h_g1 = g1;
+        s.h_g2 = g2;
+    }
+    bp->hw = hw;
+    bp->exact = exact ? 1 : 0;
+    bp->g1 = s.d_g1;
+    bp->g2 = s.d_g2;
+    bp->sharp_lut = s.d_lut;
+    bp->lut_len = lut_len;
+    bp->blur_map = nullptr;
+    return STK_OK;
+}
+
+// --------------------------------------------------------- frame enqueue ---
+int enqueue_kernels(stk_ctx* ctx, Slot& s, const Frame& f, const BlurParams* bp, bool timed,
+                    bool want_labels) {
+    cudaStream_t st = s.st;
+    int n = 0;
+    auto rec = [&](int i) {
+        if (timed) cudaEventRecord(s.ev[i], st);
+    };
+    cudaMemsetAsync(f.sc, 0, sizeof(DevScalars), st);
+    cudaMemsetAsync(f.lb, 0, sizeof(unsigned long long) * LB_COUNT * f.lb_stride, st);
+    rec(0);
+    launch_lightness(f, ctx->d_tab, true, true, true, st);
+    ++n;
+    rec(1);
+    launch_kmeans(f, 0, 100, 0.5, st);
+    ++n;
+    if (want_labels) {
+        launch_assign(f, f.grayL, f.labels16, st);
+        ++n;
+    }
+    rec(2);
+    launch_morph(f, MORPH_FUSED, &s.tm_morph.map, f.full ? f.mraw : nullptr, f.mref, st);
+    launch_ccl(f, st);
+    launch_prune(f, true, st);
+    n += 8;
+    rec(3);
+    if (f.W >= f.window && f.H >= f.window) {
+        launch_sad(f, ctx->sad_kernel, &s.tm_sadL.map, &s.tm_sadR.map, st);
+        ++n;
+    }
+    rec(4);
+    launch_fill_rows(f, f.sparse, f.rowf, st);
+    ++n;
+    rec(5);
+    launch_peek_cols(f, f.rowf, f.dense, nullptr, st);
+    ++n;
+    rec(6);
+    if (bp) {
+        launch_blur(f, *bp, f.rgbL, f.out_rgb, f.dense, st);
+        ++n;
+    }
+    rec(7);
+    cudaMemcpyAsync(s.h_sc, f.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
+    return n;
+}
+
+bool want_full(const stk_frame_out* o) {
+    return o && (o->left_lightness || o->right_lightness || o->labels || o->boundary_raw ||
+                 o->boundary_refined || o->boundary_anchored || o->sparse || o->row_filled);
+}
+
+stk_status check_frame_args(stk_ctx* ctx, int slot, int w, int h, const stk_config* cfg,
+                            const stk_focus* focus, int* ksize) {
+    if (!ctx) return fail(ctx, STK_EPARAM, "stk: null context");
+    if (slot < 0 || slot >= (int)ctx->slots.size())
+        return fail(ctx, STK_EPARAM, "stk: slot " + std::to_string(slot) + " out of range");
+    TRY(check_config(ctx, cfg));
+    if (w < 0 || h < 0) return fail(ctx, STK_EPARAM, "pipeline: bad frame size " + dims(w, h));
+    if ((long long)w * h == 0)  // k = min(cfg.k, 0 occupied bins) -> kmeans throws
+        return fail(ctx, STK_EPARAM, "kmeans: k must be at least 1, got 0");
+    const int margin = cfg->window / 2;
+    if (2 * margin >= w)
+        return fail(ctx, STK_EPARAM, "add_border_anchors: margin " + std::to_string(margin) +
+                                         " does not fit in width " + std::to_string(w));
+    TRY(check_gpu_limits(ctx, cfg->window, cfg->max_disparity));
+    if (w > 65535 || h > 65535)
+        return fail(ctx, STK_EPARAM, "stk_b200: frame " + dims(w, h) + " exceeds 65535 per side");
+    if (focus) TRY(check_focus(ctx, focus, cfg->max_disparity, ksize));
+    if (ctx->slots[slot].pending)
+        return fail(ctx, STK_EPARAM, "stk: slot " + std::to_string(slot) + " still has a frame in flight");
+    return STK_OK;
+}
+
+// Common body of stk_frame_submit / stk_frame_submit_device.
+stk_status submit(stk_ctx* ctx, int slot, const uint8_t* rgbL, const uint8_t* rgbR, bool host_in,
+                  int w, int h, const stk_config* cfg, const stk_focus* focus,
+                  const stk_frame_out* out, bool host_out, uint8_t* d_refocused, int16_t* d_dense,
+                  bool timed) {
+    int ksize = 0;
+    TRY(check_frame_args(ctx, slot, w, h, cfg, focus, &ksize));
+    CK(cudaSetDevice(ctx->device));
+    Slot& s = ctx->slots[slot];
+    TRY(ensure_slot(ctx, s, w, h));
+    Frame f = make_frame(s, w, h, cfg);
+    const size_t N = (size_t)w * h;
+    const bool full = host_out && want_full(out);
+    f.full = full ? 1 : 0;
+    if (full) {
+        f.mprn = s.mprn;
+        f.manc = s.manc;
+    }
+    if (!host_in) {
+        f.rgbL = rgbL;
+        f.rgbR = rgbR;
+    }
+    if (!host_out) {
+        if (d_refocused) f.out_rgb = d_refocused;
+        if (d_dense) f.dense = d_dense;
+    }
+    BlurParams bp{};
+    if (focus)
+        TRY(upload_focus(ctx, s, focus->lo, focus->hi, focus->n_ranges, cfg->max_disparity,
+                         focus->sigma, ksize, focus->exact_blur != 0, &bp));
+    TRY(encode(ctx, s.tm_morph, s.grayL, 1, w, h, s.P, 160, 38));
+    TRY(encode(ctx, s.tm_sadL, s.grayL, 1, w, h, s.P, 128, cfg->window));
+    TRY(encode(ctx, s.tm_sadR, s.grayR, 1, w, h, s.P, 128, cfg->window));
+    cudaStream_t st = s.st;
+    if (host_in) {
+        CK(cudaMemcpyAsync(s.rgbL, rgbL, 3 * N, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(s.rgbR, rgbR, 3 * N, cudaMemcpyHostToDevice, st));
+    }
+    const bool want_labels = full && out->labels;
+    int nk = 0;
+    bool graphed = false;
+    if (!timed && ctx->use_graphs) {
+        GraphKey key{};
+        key.W = w;
+        key.H = h;
+        key.kcfg = cfg->k;
+        key.window = cfg->window;
+        key.D = cfg->max_disparity;
+        key.thr = cfg->threshold;
+        key.frac = cfg->prune_fraction;
+        key.full = f.full;
+        key.focus = focus ? 1 : 0;
+        key.hw = bp.hw;
+        key.exact = bp.exact;
+        key.lut_len = bp.lut_len;
+        key.sad = ctx->sad_kernel;
+        key.want_raw = want_labels;
+        key.rgbL = f.rgbL;
+        key.rgbR = f.rgbR;
+        key.out_rgb = f.out_rgb;
+        key.dense = f.dense;
+        if (!(s.gexec && s.gkey == key)) {
+            if (s.gexec) {
+                cudaGraphExecDestroy(s.gexec);
+                s.gexec = nullptr;
+            }
+            cudaGraph_t g;
+            CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            s.kernels = enqueue_kernels(ctx, s, f, focus ? &bp : nullptr, false, want_labels);
+            CK(cudaStreamEndCapture(st, &g));
+            const cudaError_t ie = cudaGraphInstantiate(&s.gexec, g, 0);
+            cudaGraphDestroy(g);
+            CK(ie);
+            s.gkey = key;
+        }
+        CK(cudaGraphLaunch(s.gexec, st));
+        nk = s.kernels;
+        graphed = true;
+    } else {
+        nk = enqueue_kernels(ctx, s, f, focus ? &bp : nullptr, timed, want_labels);
+        CK(cudaGetLastError());
+    }
+    if (host_out && out) {
+        if (out->dense) CK(cudaMemcpyAsync(out->dense, f.dense, 2 * N, cudaMemcpyDeviceToHost, st));
+        if (out->refocused && focus)
+            CK(cudaMemcpyAsync(out->refocused, f.out_rgb, 3 * N, cudaMemcpyDeviceToHost, st));
+        auto plane = [&](void* dst, const void* src) -> cudaError_t {
+            return cudaMemcpy2DAsync(dst, w, src, s.P, w, h, cudaMemcpyDeviceToHost, st);
+        };
+        if (out->left_lightness) CK(plane(out->left_lightness, f.grayL));
+        if (out->right_lightness) CK(plane(out->right_lightness, f.grayR));
+        if (out->boundary_raw) CK(plane(out->boundary_raw, f.mraw));
+        if (out->boundary_refined) CK(plane(out->boundary_refined, f.mprn));
+        if (out->boundary_anchored) CK(plane(out->boundary_anchored, f.manc));
+        if (out->labels) CK(cudaMemcpyAsync(out->labels, f.labels16, 2 * N, cudaMemcpyDeviceToHost, st));
+        if (out->sparse) CK(cudaMemcpyAsync(out->sparse, f.sparse, 2 * N, cudaMemcpyDeviceToHost, st));
+        if (out->row_filled) CK(cudaMemcpyAsync(out->row_filled, f.rowf, 2 * N, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaEventRecord(s.done, st));
+    s.pending = true;
+    s.timed = timed;
+    s.graph = graphed;
+    s.kernels = nk;
+    s.f = f;
+    s.out = (host_out && out) ? *out : stk_frame_out{};
+    return STK_OK;
+}
+
+}  // namespace
+
+// =================================================================== ABI ===
+extern "C" {
+
+int stk_abi_version(void) { return STK_ABI_VERSION; }
+
+const char* stk_status_string(stk_status s) {
+    switch (s) {
+        case STK_OK: return "ok";
+        case STK_EPARAM: return "parameter error";
+        case STK_EIO: return "io error";
+        case STK_EFORMAT: return "format error";
+        case STK_ECUDA: return "cuda error";
+        default: return "internal error";
+    }
+}
+
+const char* stk_last_error(const stk_ctx* ctx) { return ctx ? ctx->err.c_str() : t_err.c_str(); }
+
+stk_status stk_create(int device, int max_width, int max_height, int slots, stk_ctx** out) {
+    stk_ctx* ctx = nullptr;
+    if (!out) return fail(nullptr, STK_EPARAM, "stk_create: null out");
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(nullptr, STK_ECUDA, "stk_create: no CUDA device (this library has no CPU path)");
+    if (device < 0 || device >= ndev)
+        return fail(nullptr, STK_EPARAM, "stk_create: device " + std::to_string(device) + " out of range");
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10)
+        return fail(nullptr, STK_ECUDA, "stk_create: device is not sm_100 (Blackwell B200)");
+    ctx = new stk_ctx();
+    ctx->device = device;
+    stk_status rc = STK_OK;
+    do {
+        if (cudaSetDevice(device) != cudaSuccess) {
+            rc = fail(ctx, STK_ECUDA, "cudaSetDevice failed");
+            break;
+        }
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess || !fn) {
+            rc = fail(ctx, STK_ECUDA, "cuTensorMapEncodeTiled unavailable");
+            break;
+        }
+        ctx->encode = (EncodeTiledFn)fn;
+        LstarTables tab;
+        make_lstar_tables(&tab);
+        if (cudaMalloc(&ctx->d_tab, sizeof(LstarTables)) != cudaSuccess ||
+            cudaMemcpy(ctx->d_tab, &tab, sizeof(tab), cudaMemcpyHostToDevice) != cudaSuccess) {
+            rc = fail(ctx, STK_ECUDA, "stk_create: table upload failed");
+            break;
+        }
+        ctx->slots.resize(std::max(slots, 1));
+        for (Slot& s : ctx->slots) {
+            if (cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaEventCreate(&s.done) != cudaSuccess ||
+                cudaMallocHost(&s.h_sc, sizeof(DevScalars)) != cudaSuccess) {
+                rc = fail(ctx, STK_ECUDA, "stk_create: stream/event setup failed");
+                break;
+            }
+            for (auto& e : s.ev) cudaEventCreate(&e);
+        }
+        if (rc != STK_OK) break;
+        if (max_width > 0 && max_height > 0) rc = ensure_slot(ctx, ctx->slots[0], max_width, max_height);
+    } while (0);
+    if (rc != STK_OK) {
+        stk_destroy(ctx);
+        return rc;
+    }
+    *out = ctx;
+    return STK_OK;
+}
+
+void stk_destroy(stk_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    for (Slot& s : ctx->slots) {
+        if (s.st) cudaStreamSynchronize(s.st);
+        if (s.gexec) cudaGraphExecDestroy(s.gexec);
+        if (s.base) cudaFree(s.base);
+        if (s.d_lut) cudaFree(s.d_lut);
+        if (s.d_g1) cudaFree(s.d_g1);
+        if (s.d_g2) cudaFree(s.d_g2);
+        if (s.cub_tmp) cudaFree(s.cub_tmp);
+        if (s.h_sc) cudaFreeHost(s.h_sc);
+        for (auto& e : s.ev)
+            if (e) cudaEventDestroy(e);
+        if (s.done) cudaEventDestroy(s.done);
+        if (s.st) cudaStreamDestroy(s.st);
+    }
+    if (ctx->d_tab) cudaFree(ctx->d_tab);
+    delete ctx;
+}
+
+stk_status stk_set_sad_kernel(stk_ctx* ctx, int kernel) {
+    if (!ctx || kernel < 0 || kernel > 2) return fail(ctx, STK_EPARAM, "stk_set_sad_kernel: bad kernel");
+    ctx->sad_kernel = kernel;
+    for (Slot& s : ctx->slots) s.gkey = GraphKey{};
+    return STK_OK;
+}
+
+stk_status stk_set_use_graphs(stk_ctx* ctx, int on) {
+    if (!ctx) return fail(ctx, STK_EPARAM, "stk_set_use_graphs: null ctx");
+    ctx->use_graphs = on ? 1 : 0;
+    return STK_OK;
+}
+
+stk_status stk_host_alloc(size_t bytes, void** out) {
+    stk_ctx* ctx = nullptr;
+    CK(cudaMallocHost(out, bytes));
+    return STK_OK;
+}
+
+void stk_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+stk_status stk_validate_config(const stk_config* cfg) { return check_config(nullptr, cfg); }
+
+int stk_default_kernel_size(double sigma) { return 2 * (int)std::ceil(3.0 * sigma) + 1; }
+
+stk_status stk_gaussian_kernel(double sigma, int size, double* weights) {
+    if (!(sigma > 0.0))
+        return fail(nullptr, STK_EPARAM, "gaussian_kernel: sigma must be positive, got " + std::to_string(sigma));
+    if (size < 1 || size % 2 == 0)
+        return fail(nullptr, STK_EPARAM, "gaussian_kernel: size must be odd and positive, got " + std::to_string(size));
+    const int h = size / 2;
+    double sum = 0.0;
+    for (int i = -h; i <= h; ++i)
+        for (int j = -h; j <= h; ++j) {
+            const double w = std::exp(-(i * i + j * j) / (2.0 * sigma * sigma));
+            weights[(size_t)(i + h) * size + (j + h)] = w;
+            sum += w;
+        }
+    for (size_t t = 0; t < (size_t)size * size; ++t) weights[t] /= sum;
+    return STK_OK;
+}
+
+// ------------------------------------------------------------- frames -----
+stk_status stk_frame_submit(stk_ctx* ctx, int slot, const uint8_t* rgb_left,
+                            const uint8_t* rgb_right, int w, int h, const stk_config* cfg,
+                            const stk_focus* focus, const stk_frame_out* out, int want_times) {
+    return submit(ctx, slot, rgb_left, rgb_right, true, w, h, cfg, focus, out, true, nullptr,
+                  nullptr, want_times != 0);
+}
+
+stk_status stk_frame_submit_device(stk_ctx* ctx, int slot, const uint8_t* d_rgb_left,
+                                   const uint8_t* d_rgb_right, int w, int h,
+                                   const stk_config* cfg, const stk_focus* focus,
+                                   uint8_t* d_refocused, int16_t* d_dense, int want_times) {
+    return submit(ctx, slot, d_rgb_left, d_rgb_right, false, w, h, cfg, focus, nullptr, false,
+                  d_refocused, d_dense, want_times != 0);
+}
+
+stk_status stk_frame_wait(stk_ctx* ctx, int slot, stk_stats* stats, stk_times* times,
+                          stk_frame_info* info) {
+    if (!ctx || slot < 0 || slot >= (int)ctx->slots.size())
+        return fail(ctx, STK_EPARAM, "stk_frame_wait: bad slot");
+    Slot& s = ctx->slots[slot];
+    if (!s.pending) return fail(ctx, STK_EPARAM, "stk_frame_wait: no frame in flight on slot");
+    CK(cudaSetDevice(ctx->device));
+    s.pending = false;
+    CK(cudaEventSynchronize(s.done));
+    CK(cudaGetLastError());
+    const DevScalars& h = *s.h_sc;
+    if (h.kerr) return fail(ctx, STK_EINTERNAL, "kmeans failed on device (code " + std::to_string(h.kerr) + ")");
+    const double n = (double)s.f.N;
+    if (stats) {
+        stats->pixels = (uint64_t)s.f.N;
+        stats->boundary_raw = h.raw_count;
+        stats->boundary_refined = h.pruned_count;
+        stats->matched = h.matched;
+        stats->matched_fraction = n > 0 ? (double)h.matched / n : 0.0;
+        stats->known_fraction = n > 0 ? (double)h.known / n : 0.0;
+    }
+    if (times) {
+        std::memset(times, 0, sizeof(*times));
+        if (s.timed) {
+            float ms[7];
+            for (int i = 0; i < 7; ++i) cudaEventElapsedTime(&ms[i], s.ev[i], s.ev[i + 1]);
+            times->convert = ms[0];
+            times->segment = ms[1];
+            times->boundary = ms[2];
+            times->match = ms[3];
+            times->fill = ms[4];
+            times->peek = ms[5];
+            times->blur = ms[6];
+        }
+    }
+    if (s.out.centers)
+        for (int j = 0; j < 256; ++j) s.out.centers[j] = j < h.k ? h.centers[j] : 0.0;
+    if (s.out.bin_assignment) std::memcpy(s.out.bin_assignment, h.assign16, 512);
+    if (info) {
+        info->sad_ops = h.sad_ops;
+        info->components = h.n_roots;
+        info->k = h.k;
+        info->iterations_run = h.iters;
+        info->kernels = s.kernels;
+        info->graph = s.graph ? 1 : 0;
+    }
+    return STK_OK;
+}
+
+void* stk_slot_stream(stk_ctx* ctx, int slot) {
+    if (!ctx || slot < 0 || slot >= (int)ctx->slots.size()) return nullptr;
+    return (void*)ctx->slots[slot].st;
+}
+
+stk_status stk_run_frame(stk_ctx* ctx, const uint8_t* rgb_left, const uint8_t* rgb_right, int w,
+                         int h, const stk_config* cfg, const stk_focus* focus,
+                         const stk_frame_out* out, stk_stats* stats, stk_times* times) {
+    TRY(stk_frame_submit(ctx, 0, rgb_left, rgb_right, w, h, cfg, focus, out, times != nullptr));
+    return stk_frame_wait(ctx, 0, stats, times, nullptr);
+}
+
+// ---------------------------------------------------- per-stage entries ---
+#define STAGE_BEGIN(w, h)                                                     \
+    if (!ctx) return fail(ctx, STK_EPARAM, "stk: null context");              \
+    if ((w) < 0 || (h) < 0) return fail(ctx, STK_EPARAM, "stk: bad size");    \
+    CK(cudaSetDevice(ctx->device));                                           \
+    Slot& s = ctx->slots[0];                                                  \
+    if (s.pending) return fail(ctx, STK_EPARAM, "stk: slot 0 busy");          \
+    TRY(ensure_slot(ctx, s, std::max((w), 1), std::max((h), 1)));             \
+    Frame f = make_frame(s, (w), (h), nullptr);                               \
+    const size_t N = (size_t)(w) * (h);                                       \
+    cudaStream_t st = s.st;                                                   \
+    (void)N;
+
+#define H2D_PLANE(dst, src, esz)                                                              \
+    if (N) CK(cudaMemcpy2DAsync((dst), (size_t)s.P * (esz), (src), (size_t)f.W * (esz),      \
+                                (size_t)f.W * (esz), f.H, cudaMemcpyHostToDevice, st))
+#define D2H_PLANE(dst, src, esz)                                                              \
+    if (N) CK(cudaMemcpy2DAsync((dst), (size_t)f.W * (esz), (src), (size_t)s.P * (esz),      \
+                                (size_t)f.W * (esz), f.H, cudaMemcpyDeviceToHost, st))
+#define FINISH()                              \
+    CK(cudaGetLastError());                   \
+    CK(cudaStreamSynchronize(st));            \
+    return STK_OK
+
+stk_status stk_rgb_to_lightness(stk_ctx* ctx, const uint8_t* rgb, int w, int h, uint8_t* gray) {
+    STAGE_BEGIN(w, h);
+    if (N) CK(cudaMemcpyAsync(s.rgbL, rgb, 3 * N, cudaMemcpyHostToDevice, st));
+    launch_lightness(f, ctx->d_tab, true, false, false, st);
+    D2H_PLANE(gray, s.grayL, 1);
+    FINISH();
+}
+
+stk_status stk_build_histogram(stk_ctx* ctx, const uint8_t* gray, int w, int h,
+                               uint64_t counts[256]) {
+    STAGE_BEGIN(w, h);
+    H2D_PLANE(s.grayL, gray, 1);
+    CK(cudaMemsetAsync(s.sc, 0, sizeof(DevScalars), st));
+    launch_histogram(f, s.grayL, st);
+    CK(cudaMemcpyAsync(s.h_sc, s.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    for (int v = 0; v < 256; ++v) counts[v] = s.h_sc->hist[v];
+    return STK_OK;
+}
+
+stk_status stk_kmeans_histogram(stk_ctx* ctx, const uint64_t counts[256], int k, int max_iter,
+                                double tol, double* centers, uint16_t bin_assignment[256],
+                                int* iterations_run) {
+    if (k < 1) return fail(ctx, STK_EPARAM, "kmeans: k must be at least 1, got " + std::to_string(k));
+    if (max_iter < 1)
+        return fail(ctx, STK_EPARAM, "kmeans: max_iter must be at least 1, got " + std::to_string(max_iter));
+    int occ = 0;
+    for (int v = 0; v < 256; ++v) occ += counts[v] > 0;
+    if (occ == 0) return fail(ctx, STK_EPARAM, "kmeans: empty histogram");
+    if (k > occ)
+        return fail(ctx, STK_EPARAM, "kmeans: k=" + std::to_string(k) + " exceeds the " +
+                                         std::to_string(occ) + " occupied bins");
+    STAGE_BEGIN(1, 1);
+    CK(cudaMemsetAsync(s.sc, 0, sizeof(DevScalars), st));
+    CK(cudaMemcpyAsync(s.sc->hist, counts, 256 * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    launch_kmeans(f, k, max_iter, tol, st);
+    CK(cudaMemcpyAsync(s.h_sc, s.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    if (s.h_sc->kerr) return fail(ctx, STK_EINTERNAL, "kmeans: device error");
+    for (int j = 0; j < k; ++j) centers[j] = s.h_sc->centers[j];
+    std::memcpy(bin_assignment, s.h_sc->assign16, 512);
+    *iterations_run = s.h_sc->iters;
+    return STK_OK;
+}
+
+stk_status stk_assign_pixels(stk_ctx* ctx, const uint8_t* gray, int w, int h,
+                             const uint16_t bin_assignment[256], int k, uint16_t* labels) {
+    if (k < 1) return fail(ctx, STK_EPARAM, "assign_pixels: clustering has no centers");
+    STAGE_BEGIN(w, h);
+    H2D_PLANE(s.grayL, gray, 1);
+    CK(cudaMemcpyAsync(s.sc->assign16, bin_assignment, 512, cudaMemcpyHostToDevice, st));
+    launch_assign(f, s.grayL, s.labels16, st);
+    if (N) CK(cudaMemcpyAsync(labels, s.labels16, 2 * N, cudaMemcpyDeviceToHost, st));
+    FINISH();
+}
+
+static stk_status morph_stage(stk_ctx* ctx, int mode, const void* in, int w, int h, uint8_t* out) {
+    STAGE_BEGIN(w, h);
+    if (N == 0) return STK_OK;
+    if (mode == MORPH_DETECT16) {
+        H2D_PLANE(s.scratch16, in, 2);
+        TRY(encode(ctx, s.tm_stage, s.scratch16, 2, w, h, s.P * 2, 160, 38));
+    } else {
+        H2D_PLANE(s.mref, in, 1);
+        TRY(encode(ctx, s.tm_stage, s.mref, 1, w, h, s.P, 160, 38));
+    }
+    launch_morph(f, mode, &s.tm_stage.map, s.mraw, nullptr, st);
+    D2H_PLANE(out, s.mraw, 1);
+    FINISH();
+}
+
+stk_status stk_detect_boundaries(stk_ctx* ctx, const uint16_t* labels, int w, int h,
+                                 uint8_t* mask) {
+    return morph_stage(ctx, MORPH_DETECT16, labels, w, h, mask);
+}
+
+stk_status stk_morph_fill(stk_ctx* ctx, const uint8_t* mask, int w, int h, uint8_t* out) {
+    return morph_stage(ctx, MORPH_FILL, mask, w, h, out);
+}
+
+stk_status stk_morph_remove(stk_ctx* ctx, const uint8_t* mask, int w, int h, uint8_t* out) {
+    return morph_stage(ctx, MORPH_REMOVE, mask, w, h, out);
+}
+
+stk_status stk_label_components(stk_ctx* ctx, const uint8_t* mask, int w, int h, int32_t* labels,
+                                uint32_t* sizes, int32_t* by_size, size_t cap,
+                                int* n_components) {
+    STAGE_BEGIN(w, h);
+    *n_components = 0;
+    if (N == 0) return STK_OK;
+    H2D_PLANE(s.mref, mask, 1);
+    CK(cudaMemsetAsync(s.sc, 0, sizeof(DevScalars), st));
+    CK(cudaMemsetAsync(s.lb, 0, sizeof(unsigned long long) * LB_COUNT * s.lb_stride, st));
+    f.full = 1;
+    f.frac = 0.0;
+    launch_ccl(f, st);
+    CK(cudaMemcpyAsync(s.h_sc, s.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    const int C = (int)s.h_sc->n_roots;
+    if ((size_t)C > cap) return fail(ctx, STK_EPARAM, "label_components: capacity too small");
+    // ComponentTable (boundary.hpp:39-45): canonical labels = rank of the root
+    // in raster order; sizes by label; by_size = STABLE radix sort of the
+    // label ids by size, i.e. (size asc, label asc) as boundary.cpp:136-146.
+    // 8-connected components are >= 2 px apart, so C <= N/4 + W + H fits the
+    // 2*P*H-byte scratch plane used for the ids.
+    uint32_t* d_sizes = s.szhist;                       // C
+    int32_t* d_ids = reinterpret_cast<int32_t*>(s.scratch16);  // C
+    int32_t* d_labels = reinterpret_cast<int32_t*>(s.list);    // N
+    launch_component_table(f, d_labels, d_sizes, d_ids, st);   // reads mref, par, rank, cnt, roots
+    CK(cudaMemcpyAsync(labels, d_labels, 4 * N, cudaMemcpyDeviceToHost, st));
+    if (C > 0) CK(cudaMemcpyAsync(sizes, d_sizes, 4 * (size_t)C, cudaMemcpyDeviceToHost, st));
+    if (C > 0) {
+        size_t need = 0;
+        uint32_t* k_out = reinterpret_cast<uint32_t*>(s.roots);  // read above, free now
+        int32_t* v_out = reinterpret_cast<int32_t*>(s.cnt);      // read above, free now
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, need, d_sizes, k_out, d_ids, v_out, C, 0, 32, st));
+        if (need > s.cub_bytes) {
+            if (s.cub_tmp) CK(cudaFree(s.cub_tmp));
+            CK(cudaMalloc(&s.cub_tmp, need));
+            s.cub_bytes = need;
+        }
+        CK(cub::DeviceRadixSort::SortPairs(s.cub_tmp, need, d_sizes, k_out, d_ids, v_out, C, 0, 32, st));
+        CK(cudaMemcpyAsync(by_size, v_out, 4 * (size_t)C, cudaMemcpyDeviceToHost, st));
+    }
+    *n_components = C;
+    FINISH();
+}
+
+stk_status stk_prune_components(stk_ctx* ctx, const uint8_t* mask, int w, int h, double fraction,
+                                uint8_t* out) {
+    if (!(fraction >= 0.0 && fraction < 1.0))
+        return fail(ctx, STK_EPARAM, "prune_components: fraction must be in [0, 1), got " + std::to_string(fraction));
+    STAGE_BEGIN(w, h);
+    if (N == 0) return STK_OK;
+    H2D_PLANE(s.mref, mask, 1);
+    CK(cudaMemsetAsync(s.sc, 0, sizeof(DevScalars), st));
+    CK(cudaMemsetAsync(s.lb, 0, sizeof(unsigned long long) * LB_COUNT * s.lb_stride, st));
+    f.frac = fraction;
+    f.window = 1;
+    f.hw = 0;
+    f.mprn = s.mprn;
+    launch_count_mask(f, s.mref, st);
+    launch_ccl(f, st);
+    launch_prune(f, false, st);
+    D2H_PLANE(out, s.mprn, 1);
+    FINISH();
+}
+
+stk_status stk_add_border_anchors(stk_ctx* ctx, const uint8_t* mask, int w, int h, int margin,
+                                  uint8_t* out) {
+    if (margin < 0 || 2 * margin >= w)
+        return fail(ctx, STK_EPARAM, "add_border_anchors: margin " + std::to_string(margin) +
+                                         " does not fit in width " + std::to_string(w));
+    STAGE_BEGIN(w, h);
+    H2D_PLANE(s.mref, mask, 1);
+    launch_anchor_only(f, s.mref, s.manc, margin, st);
+    D2H_PLANE(out, s.manc, 1);
+    FINISH();
+}
+
+stk_status stk_sad_cost(stk_ctx* ctx, const uint8_t* left, const uint8_t* right, int w, int h,
+                        int x, int y, int d, int window, uint32_t* cost) {
+    const int hw = window / 2;
+    if (window < 1 || window % 2 == 0)
+        return fail(ctx, STK_EPARAM, "stereo: window must be odd and positive, got " + std::to_string(window));
+    if (x - hw < 0 || x + hw >= w || y - hw < 0 || y + hw >= h || x - d - hw < 0 || x - d + hw >= w)
+        return fail(ctx, STK_EPARAM, "sad_cost: window outside the images");
+    STAGE_BEGIN(w, h);
+    H2D_PLANE(s.grayL, left, 1);
+    H2D_PLANE(s.grayR, right, 1);
+    f.window = window;
+    f.hw = hw;
+    launch_sad_cost(f, x, y, d, s.tile_off, st);
+    CK(cudaMemcpyAsync(cost, s.tile_off, 4, cudaMemcpyDeviceToHost, st));
+    FINISH();
+}
+
+stk_status stk_match_boundary_pixels(stk_ctx* ctx, const uint8_t* left, const uint8_t* right,
+                                     const uint8_t* mask, int w, int h, int window,
+                                     int max_disparity, int16_t* out) {
+    if (window < 1 || window % 2 == 0)
+        return fail(ctx, STK_EPARAM, "stereo: window must be odd and positive, got " + std::to_string(window));
+    if (max_disparity < 0)
+        return fail(ctx, STK_EPARAM, "stereo: max_disparity must be >= 0, got " + std::to_string(max_disparity));
+    TRY(check_gpu_limits(ctx, window, max_disparity));
+    STAGE_BEGIN(w, h);
+    if (N == 0) return STK_OK;
+    H2D_PLANE(s.grayL, left, 1);
+    H2D_PLANE(s.grayR, right, 1);
+    H2D_PLANE(s.mref, mask, 1);
+    CK(cudaMemsetAsync(s.sc, 0, sizeof(DevScalars), st));
+    CK(cudaMemsetAsync(s.lb, 0, sizeof(unsigned long long) * LB_COUNT * s.lb_stride, st));
+    f.window = window;
+    f.hw = window / 2;
+    f.D = max_disparity;
+    TRY(encode(ctx, s.tm_sadL, s.grayL, 1, w, h, s.P, 128, window));
+    TRY(encode(ctx, s.tm_sadR, s.grayR, 1, w, h, s.P, 128, window));
+    launch_apply(f, false, false, st);
+    if (w >= window && h >= window) launch_sad(f, ctx->sad_kernel, &s.tm_sadL.map, &s.tm_sadR.map, st);
+    CK(cudaMemcpyAsync(out, s.sparse, 2 * N, cudaMemcpyDeviceToHost, st));
+    FINISH();
+}
+
+stk_status stk_fill_scanlines(stk_ctx* ctx, const int16_t* sparse, int w, int h, int16_t* out) {
+    STAGE_BEGIN(w, h);
+    if (N == 0) return STK_OK;
+    CK(cudaMemcpyAsync(s.sparse, sparse, 2 * N, cudaMemcpyHostToDevice, st));
+    launch_fill_rows(f, s.sparse, s.rowf, st);
+    CK(cudaMemcpyAsync(out, s.rowf, 2 * N, cudaMemcpyDeviceToHost, st));
+    FINISH();
+}
+
+stk_status stk_peek_columns(stk_ctx* ctx, const int16_t* map, int w, int h, int threshold,
+                            int16_t* out) {
+    if (threshold < 0)
+        return fail(ctx, STK_EPARAM, "peek_columns: threshold must be >= 0, got " + std::to_string(threshold));
+    STAGE_BEGIN(w, h);
+    if (N == 0) return STK_OK;
+    CK(cudaMemcpyAsync(s.rowf, map, 2 * N, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(s.sc, 0, sizeof(DevScalars), st));
+    f.thr = threshold;
+    launch_peek_cols(f, s.rowf, s.dense, nullptr, st);
+    CK(cudaMemcpyAsync(out, s.dense, 2 * N, cudaMemcpyDeviceToHost, st));
+    FINISH();
+}
+
+stk_status stk_build_blur_map(stk_ctx* ctx, const int16_t* depth, int w, int h, const int* lo,
+                              const int* hi, int n_ranges, int max_disparity, uint8_t* map) {
+    stk_focus fo{lo, hi, n_ranges, 1.0, 1, 0};
+    int ks;
+    TRY(check_focus(ctx, &fo, max_disparity, &ks));
+    STAGE_BEGIN(w, h);
+    if (N == 0) return STK_OK;
+    BlurParams bp{};
+    TRY(upload_focus(ctx, s, lo, hi, n_ranges, max_disparity, 1.0, 1, false, &bp));
+    CK(cudaMemcpyAsync(s.dense, depth, 2 * N, cudaMemcpyHostToDevice, st));
+    launch_blur_map(f, s.dense, bp.sharp_lut, bp.lut_len, s.mraw, st);
+    D2H_PLANE(map, s.mraw, 1);
+    FINISH();
+}
+
+stk_status stk_selective_blur(stk_ctx* ctx, const uint8_t* rgb, const uint8_t* map, int w, int h,
+                              double sigma, int size, int exact, uint8_t* out) {
+    if (!(sigma > 0.0))
+        return fail(ctx, STK_EPARAM, "gaussian_kernel: sigma must be positive, got " + std::to_string(sigma));
+    if (size < 1 || size % 2 == 0)
+        return fail(ctx, STK_EPARAM, "gaussian_kernel: size must be odd and positive, got " + std::to_string(size));
+    if (blur_smem_bytes(size / 2, exact != 0) > 220 * 1024)
+        return fail(ctx, STK_EPARAM, "stk_b200: blur kernel size exceeds the GPU tile limit");
+    STAGE_BEGIN(w, h);
+    if (N == 0) return STK_OK;
+    const int lo0 = 0, hi0 = 0;
+    BlurParams bp{};
+    TRY(upload_focus(ctx, s, &lo0, &hi0, 1, 0, sigma, size, exact != 0, &bp));
+    bp.blur_map = s.mraw;
+    CK(cudaMemcpyAsync(s.rgbL, rgb, 3 * N, cudaMemcpyHostToDevice, st));
+    H2D_PLANE(s.mraw, map, 1);
+    launch_blur(f, bp, s.rgbL, s.out_rgb, nullptr, st);
+    CK(cudaMemcpyAsync(out, s.out_rgb, 3 * N, cudaMemcpyDeviceToHost, st));
+    FINISH();
+}
+
+}  // extern "C"

@@ -1,0 +1,141 @@
+// stk_internal.cuh -- types shared by the sm_100a kernels and the C-ABI host
+// code.  One stereo frame lives in HBM as the planes below (see DESIGN.md
+// "Data layout in HBM").  8-bit planes are row-pitched (pitch P, a multiple of
+// 64 bytes, as TMA needs 16-byte strides); 16/32-bit planes are dense with
+// index y*W+x, so a union-find root index IS the raster index the reference's
+// discovery order is defined on (boundary.cpp:96-107).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <type_traits>
+
+namespace stk {
+
+constexpr int kRowTile = 128;         // columns per row-tile (compaction + SAD list tiles)
+constexpr int kTilesPerChunk = 8;     // row-tiles per look-back chunk (one warp each)
+constexpr uint32_t kRemoved = 0x80000000u;  // prune flag OR-ed into cnt[root]
+
+// Counters for the single-pass decoupled look-back scans.
+enum LookbackUse { LB_ROOTS = 0, LB_RANK = 1, LB_LIST = 2, LB_SAD = 3, LB_COUNT = 4 };
+
+// Frame-wide scalars, device resident; zeroed (cudaMemsetAsync) at frame start.
+struct DevScalars {
+    unsigned long long hist[256];      // left-lightness histogram (K1)
+    double centers[256];               // K-Means centers (K2)
+    unsigned short assign16[256];      // bin_assignment (K2)
+    unsigned char lut[256];            // gray -> cluster index (K2, k <= 256)
+    int k;                             // min(cfg.k, occupied)   (pipeline.cpp:76-80)
+    int iters;                         // iterations_run
+    int kerr;                          // 1: empty histogram, 2: k > occupied, 3: k < 1
+    int pad0;
+    unsigned long long raw_count;      // boundary_raw.count()
+    unsigned long long refined_count;  // after fill + remove (prune input)
+    unsigned long long pruned_count;   // boundary_refined.count() (after prune)
+    unsigned long long matched;        // M = list length (sparse.known_count())
+    unsigned long long known;          // dense.known_count()
+    unsigned long long sad_ops;        // sum over list of (d_lim+1)*w*w (roofline)
+    unsigned long long budget;         // floor(fraction * refined_count)
+    unsigned long long s_star;         // prune: sizes < s_star go ...
+    unsigned long long q;              // ... and the first q of size s_star
+    unsigned int n_roots;              // component count C
+    unsigned int n_list;               // == matched
+    unsigned int ctr[LB_COUNT];        // dynamic chunk counters
+};
+
+// Everything a kernel needs to know about one frame, passed by value.
+struct Frame {
+    int W, H, P;        // width, height, pitch of u8 planes (bytes)
+    long long N;        // W*H
+    int TX;             // row-tiles per row = ceil(W / kRowTile)
+    int n_tiles;        // H * TX
+    int n_chunks;       // ceil(n_tiles / kTilesPerChunk)
+    int bits_words;     // u32 words per row of the matchable bit-mask
+    // configuration (PipelineConfig, pipeline.hpp:18-25)
+    int kcfg, window, hw, D, thr;
+    double frac;
+    int full;           // write every DepthResult intermediate
+    // planes
+    const uint8_t* rgbL;
+    const uint8_t* rgbR;
+    uint8_t* grayL;
+    uint8_t* grayR;
+    uint16_t* labels16;   // full mode only (dense)
+    uint8_t* mraw;        // raw boundary (pitched)
+    uint8_t* mref;        // after fill+remove (pitched)
+    uint8_t* mprn;        // after prune (pitched, full mode only)
+    uint8_t* manc;        // anchored (pitched, full mode only)
+    uint32_t* mbits;      // matchable bits (anchored & window fits), bits_words per row
+    int32_t* par;         // union-find parent / root index (dense)
+    uint32_t* cnt;        // component size at root index (dense)
+    int32_t* rank;        // canonical component label at root index (dense)
+    uint32_t* szhist;     // component-size histogram (N + 2)
+    int32_t* roots;       // root raster indices in raster order (C)
+    uint32_t* list;       // matchable pixels (y << 16 | x) in raster order (M)
+    uint32_t* tile_off;   // list offset of each row-tile (n_tiles + 1)
+    unsigned long long* lb;  // look-back status words, LB_COUNT * lb_stride
+    int lb_stride;
+    int16_t* sparse;
+    int16_t* rowf;
+    int16_t* dense;
+    uint8_t* out_rgb;
+    DevScalars* sc;
+};
+
+// Host-side constant tables for K1 (computed with the host libm, see
+// stk_capi.cu: linear[] = srgb_to_linear, thr[v] = smallest Y with L*(Y) >= v).
+struct LstarTables {
+    double linear[256];
+    double thr[256];   // thr[0] = -1 (always passes), thr[1..255] ascending
+};
+
+// ---------------------------------------------------------------- launchers --
+// Every launcher enqueues on `st` and never synchronises.  Implementations in
+// k_*.cu.
+void launch_lightness(const Frame& f, const LstarTables* dtab, bool left, bool right,
+                      bool hist, cudaStream_t st);
+void launch_histogram(const Frame& f, const uint8_t* gray, cudaStream_t st);
+void launch_kmeans(const Frame& f, int k_fixed, int max_iter, double tol, cudaStream_t st);
+void launch_assign(const Frame& f, const uint8_t* gray, uint16_t* out, cudaStream_t st);
+
+enum MorphMode { MORPH_FUSED = 0, MORPH_DETECT16 = 1, MORPH_FILL = 2, MORPH_REMOVE = 3 };
+void launch_morph(const Frame& f, int mode, const CUtensorMap* tmap, uint8_t* out_a,
+                  uint8_t* out_b, cudaStream_t st);
+
+void launch_ccl(const Frame& f, cudaStream_t st);                 // K4a-c (+ roots, hist)
+void launch_prune(const Frame& f, bool anchors, cudaStream_t st); // K4e-g
+void launch_apply(const Frame& f, bool use_prune, bool anchors, cudaStream_t st);
+void launch_count_mask(const Frame& f, const uint8_t* mask, cudaStream_t st);
+void launch_anchor_only(const Frame& f, const uint8_t* in, uint8_t* out, int margin, cudaStream_t st);
+void launch_component_table(const Frame& f, int32_t* d_labels, uint32_t* d_sizes, int32_t* d_ids,
+                            cudaStream_t st);
+size_t sad_list_smem_bytes(int window, int D);
+size_t blur_smem_bytes(int hw, bool exact);
+void launch_sad_cost(const Frame& f, int x, int y, int d, uint32_t* out, cudaStream_t st);
+
+enum SadKernel { SAD_AUTO = 0, SAD_LIST = 1, SAD_STRIP = 2 };
+void launch_sad(const Frame& f, int kernel, const CUtensorMap* tmL, const CUtensorMap* tmR,
+                cudaStream_t st);
+void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStream_t st);
+void launch_peek_cols(const Frame& f, const int16_t* in, int16_t* out, int16_t* seg_scratch,
+                      cudaStream_t st);
+size_t peek_scratch_bytes(int W, int H);
+
+struct BlurParams {
+    int hw;              // kernel half width (size / 2)
+    int exact;           // 1: FP64 2-D in the reference's summation order
+    const float* g1;     // separable 1-D weights (size), device
+    const double* g2;    // 2-D weights (size*size), device (exact mode)
+    const uint8_t* sharp_lut;  // sharp_lut[d] for d in [0, lut_len)
+    int lut_len;
+    const uint8_t* blur_map;   // if non-null: explicit map (stage entry), pitched P
+};
+void launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, uint8_t* out_rgb,
+                 const int16_t* depth, cudaStream_t st);
+void launch_blur_map(const Frame& f, const int16_t* depth, const uint8_t* sharp_lut,
+                     int lut_len, uint8_t* out, cudaStream_t st);
+
+}  // namespace stk
