@@ -33,6 +33,7 @@ CU_SOURCES = [
     "k_boundary.cu",
     "k_ccl.cu",
     "k_sad.cu",
+    "k_sad_strip.cu",
     "k_reconstruct.cu",
     "k_blur.cu",
     "stk_capi.cu",

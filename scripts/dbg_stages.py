@@ -55,3 +55,24 @@ if __name__ == "__main__":
         p = subprocess.run([sys.executable, __file__, st], capture_output=True, text=True, timeout=120)
         tail = (p.stdout + p.stderr).strip().splitlines()[-8:]
         print(f"== {st} rc={p.returncode}\n   " + "\n   ".join(tail), flush=True)
+
+def sad_cross(cfgname, n=3000, seed=0):
+    """strip vs list kernels on a full frame + oracle spot checks (scratch)."""
+    import numpy as np, oracle, bench
+    from paper_2001_07809_b200 import stereotk as s, synth
+    W, H, D, win, K, focus, sigma = bench.CONFIGS[cfgname]
+    l, r = synth.dead_leaves(W, H, D, 0)
+    dev = s.Device(0)
+    cfg = s.PipelineConfig(k=K, window=win, max_disparity=D)
+    dev.set_sad_kernel("strip"); a = s.run_depth_pipeline(l, r, cfg, device=dev)
+    dev.set_sad_kernel("list"); b = s.run_depth_pipeline(l, r, cfg, device=dev)
+    print(cfgname, "strip==list sparse", (a.sparse == b.sparse).all(), "dense", (a.dense == b.dense).all(), "matched", a.stats.matched)
+    o = oracle.port()
+    ys, xs = np.nonzero(a.sparse >= 0)
+    rng = np.random.default_rng(seed); idx = rng.choice(len(ys), size=min(n, len(ys)), replace=False)
+    bad = 0
+    for i in idx:
+        y, x = int(ys[i]), int(xs[i]); dl = min(D, x - win // 2)
+        costs = [o.sad_cost(a.left_lightness, a.right_lightness, x, y, d, win) for d in range(dl + 1)]
+        bad += int(np.argmin(costs)) != int(a.sparse[y, x])
+    print(cfgname, "spot-check mismatches", bad, "of", len(idx))
