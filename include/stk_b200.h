@@ -134,6 +134,10 @@ stk_status stk_validate_config(const stk_config* cfg);
  * in the reference (size^2 FP64 weights are a tiny host table). */
 int stk_default_kernel_size(double sigma);
 stk_status stk_gaussian_kernel(double sigma, int size, double* weights);
+/* The host tables K1 uses (no GPU needed): linear[v] = srgb_to_linear(v)
+ * (lightness.cpp:14-17) and thr[v] = smallest Y >= 0 whose 8-bit L* is >= v
+ * (thr[0] = -1); gray(Y) = #{v >= 1 : thr[v] <= Y}. */
+void stk_lstar_tables(double linear[256], double thr[256]);
 
 /* ------------------------------------------ per-stage entries (parity) -- */
 /* rgb_to_lightness (image.hpp:82) */

@@ -67,6 +67,7 @@ SIGNATURES = {
     "stk_validate_config": (I, [C.POINTER(StkConfig)]),
     "stk_default_kernel_size": (I, [D]),
     "stk_gaussian_kernel": (I, [D, I, VP]),
+    "stk_lstar_tables": (None, [VP, VP]),
     "stk_rgb_to_lightness": (I, [VP, VP, I, I, VP]),
     "stk_build_histogram": (I, [VP, VP, I, I, VP]),
     "stk_kmeans_histogram": (I, [VP, VP, I, I, D, VP, VP, C.POINTER(C.c_int)]),

@@ -739,6 +739,13 @@ void stk_host_free(void* p) {
 
 stk_status stk_validate_config(const stk_config* cfg) { return check_config(nullptr, cfg); }
 
+void stk_lstar_tables(double linear[256], double thr[256]) {
+    LstarTables t;
+    make_lstar_tables(&t);
+    std::memcpy(linear, t.linear, sizeof(t.linear));
+    std::memcpy(thr, t.thr, sizeof(t.thr));
+}
+
 int stk_default_kernel_size(double sigma) { return 2 * (int)std::ceil(3.0 * sigma) + 1; }
 
 stk_status stk_gaussian_kernel(double sigma, int size, double* weights) {

@@ -1,0 +1,225 @@
+"""GPU parity of the whole frame (run_depth_pipeline / run_refocus_pipeline
+through the C-ABI): every DepthResult intermediate bit-exact against the
+compiled reference's golden frames and the oracle, the refocused image within
+1 LSB (bit-exact in exact-blur mode), plus size-independent properties at the
+benchmark's full 4096x2304 size, determinism and the async frame slots."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+BLUR_TOL_LSB = 1
+INTERMEDIATES = ("left_lightness", "right_lightness", "labels", "boundary_raw", "boundary_refined",
+                 "boundary_anchored", "sparse", "row_filled", "dense")
+
+
+def eq(a, b, what=""):
+    a, b = np.asarray(a), np.asarray(b)
+    assert a.shape == b.shape, (what, a.shape, b.shape)
+    bad = int((a != b).sum())
+    assert bad == 0, f"{what}: {bad} mismatching elements"
+
+
+def run(stk, dev, l, r, k=10, window=9, D=16, thr=1, prune=0.04, focus=None, sigma=2.0,
+        exact=False):
+    cfg = stk.PipelineConfig(k=k, window=window, max_disparity=D, threshold=thr,
+                             prune_fraction=prune)
+    if focus is None:
+        return stk.run_depth_pipeline(l, r, cfg, device=dev), None
+    out = []
+    img = stk.run_refocus_pipeline(l, r, cfg, stk.FocusSpec(focus, sigma, exact), depth_out=out,
+                                   device=dev)
+    return out[0], img
+
+
+def check_golden(golden, tag, res, img, exact=False):
+    for k in INTERMEDIATES:
+        key = f"{tag}_{k}"
+        if key in golden.files:
+            eq(getattr(res, k), golden[key], key)
+    st = golden[f"{tag}_stats"]
+    assert [res.stats.pixels, res.stats.boundary_raw, res.stats.boundary_refined,
+            res.stats.matched] == st.tolist()
+    kit = golden[f"{tag}_kit"]
+    assert res.clustering.k() == kit[0] and res.clustering.iterations_run == kit[1]
+    assert (res.clustering.centers == golden[f"{tag}_centers"][: kit[0]]).all()
+    key = f"{tag}_refocused"
+    if img is not None and key in golden.files:
+        d = np.abs(img.astype(int) - golden[key].astype(int)).max()
+        assert d <= (0 if exact else BLUR_TOL_LSB), d
+
+
+def test_pipeline_rectangle_scene_golden(dev, stk, golden, synth):
+    l, r = synth.rectangle_scene_pair(96, 72, 4, 63)
+    res, img = run(stk, dev, l, r, k=2, D=8, focus=[(3, 8)])
+    check_golden(golden, "pipe_rect", res, img)
+    res, img = run(stk, dev, l, r, k=2, D=8, focus=[(3, 8)], exact=True)
+    check_golden(golden, "pipe_rect", res, img, exact=True)
+
+
+def test_pipeline_self_match_golden(dev, stk, golden, synth):
+    l, _ = synth.rectangle_scene_pair(96, 72, 0, 60)
+    res, _ = run(stk, dev, l, l, k=2, D=8)
+    check_golden(golden, "pipe_self", res, None)
+    assert set(np.unique(res.sparse)) <= {-1, 0} and set(np.unique(res.dense)) <= {-1, 0}
+    assert res.stats.matched > 0
+
+
+@pytest.mark.parametrize("i", range(20))
+def test_pipeline_criterion5_golden(dev, stk, golden, synth, i):
+    """acceptance_main.cpp:262-272: 20 translated-noise scenes, D=12, focus {2,6}."""
+    l, r = synth.translated_noise_pair(128, 96, i % 9, 500 + i)
+    res, img = run(stk, dev, l, r, k=10, D=12, focus=[(2, 6)], sigma=1.5)
+    check_golden(golden, f"crit5_{i}", res, img)
+
+
+@pytest.mark.parametrize("s", range(1, 9))
+def test_pipeline_criterion8_translation_recovery(dev, stk, golden, synth, s):
+    """acceptance_main.cpp:443-489: shifts 1..8 recovered exactly."""
+    l, r = synth.rectangle_scene_pair(160, 120, s, 700 + s)
+    res, _ = run(stk, dev, l, r, k=2, window=9, D=16)
+    check_golden(golden, f"crit8_{s}", res, None)
+
+
+@pytest.mark.parametrize("tag", ["g2A", "g1"])
+def test_pipeline_bench_scenes_golden(dev, stk, golden, synth, tag):
+    if tag == "g2A":
+        l, r = synth.dead_leaves(450, 375, 16, frame=0)
+        kw = dict(k=4, window=9, D=16, focus=[(8, 16)])
+    else:
+        l, r = synth.bench_frame(200, 150, 7)
+        kw = dict(k=10, window=9, D=16, focus=[(8, 16)])
+    res, img = run(stk, dev, l, r, **kw)
+    check_golden(golden, tag, res, img)
+    res, img = run(stk, dev, l, r, exact=True, **kw)
+    check_golden(golden, tag, res, img, exact=True)
+
+
+@pytest.mark.parametrize("W,H,D,win,K,frame", [(1920, 1080, 64, 15, 6, 0), (640, 360, 40, 11, 5, 3),
+                                               (301, 203, 20, 7, 3, 1), (128, 64, 31, 31, 8, 2)])
+def test_pipeline_vs_oracle(dev, stk, port, synth, W, H, D, win, K, frame):
+    l, r = synth.dead_leaves(W, H, D, frame=frame)
+    focus = [(D // 2, D)]
+    res, img = run(stk, dev, l, r, k=K, window=win, D=D, focus=focus)
+    want = port.run_frame(l, r, k=K, window=win, max_disparity=D, focus=focus, sigma=2.0)
+    for k in INTERMEDIATES:
+        eq(getattr(res, k), want[k], k)
+    assert np.abs(img.astype(int) - want["refocused"].astype(int)).max() <= BLUR_TOL_LSB
+    assert res.stats.matched == want["stats"]["matched"]
+
+
+def test_pipeline_4k_properties(dev, stk, port, synth):
+    """Full benchmark size (4096x2304, D=128, w=21, K=8): the cheap stages are
+    checked exactly against the oracle; SAD through list == strip kernels and
+    an oracle spot check; structural invariants of the reconstruction."""
+    W, H, D, win, K = 4096, 2304, 128, 21, 8
+    l, r = synth.dead_leaves(W, H, D, frame=0)
+    dev.set_sad_kernel("strip")
+    a, img = run(stk, dev, l, r, k=K, window=win, D=D, focus=[(64, 128)])
+    dev.set_sad_kernel("list")
+    b, _ = run(stk, dev, l, r, k=K, window=win, D=D)
+    dev.set_sad_kernel("auto")
+    eq(a.sparse, b.sparse, "strip vs list")
+    eq(a.left_lightness, port.lightness(l), "L*")
+    eq(a.labels, a.clustering.bin_assignment[a.left_lightness], "labels")
+    c, asg, it = port.kmeans(port.histogram(a.left_lightness), K)
+    assert (a.clustering.centers == c).all() and a.clustering.iterations_run == it
+    eq(a.boundary_raw, port.detect(a.labels), "detect")
+    refined = port.prune(port.remove(port.fill(a.boundary_raw)), 0.04)
+    eq(a.boundary_refined, refined, "refine")
+    eq(a.boundary_anchored, port.anchors(refined, win // 2), "anchors")
+    eq(a.row_filled, port.fill_scanlines(a.sparse), "fill")
+    eq(a.dense, port.peek_columns(a.row_filled, 1), "peek")
+    # SAD spot check against the per-pixel oracle cost
+    ys, xs = np.nonzero(a.sparse >= 0)
+    assert len(ys) == a.stats.matched and 0.17 < a.stats.matched_fraction < 0.21
+    pick = np.random.default_rng(0).choice(len(ys), 300, replace=False)
+    for i in pick:
+        y, x = int(ys[i]), int(xs[i])
+        dl = min(D, x - win // 2)
+        costs = [port.sad_cost(a.left_lightness, a.right_lightness, x, y, d, win)
+                 for d in range(dl + 1)]
+        assert int(np.argmin(costs)) == a.sparse[y, x]
+    # known pixels are never modified; sharp pixels keep their bytes
+    k = a.sparse >= 0
+    assert (a.row_filled[k] == a.sparse[k]).all()
+    k = a.row_filled >= 0
+    assert (a.dense[k] == a.row_filled[k]).all()
+    sharp = (a.dense >= 64) & (a.dense <= 128)
+    assert (img[sharp] == l[sharp]).all()
+
+
+def test_pipeline_determinism_and_modes(dev, stk, synth):
+    l, r = synth.dead_leaves(640, 480, 32, frame=5)
+    outs = []
+    for graphs in (True, False, True):
+        dev.set_use_graphs(graphs)
+        res, img = run(stk, dev, l, r, k=6, window=11, D=32, focus=[(10, 20)])
+        outs.append((res.dense.copy(), img.copy()))
+    dev.set_use_graphs(True)
+    for d, i in outs[1:]:
+        eq(d, outs[0][0], "dense")
+        eq(i, outs[0][1], "refocused")
+    lean = stk.run_depth_pipeline(l, r, stk.PipelineConfig(k=6, window=11, max_disparity=32),
+                                  full=False, device=dev)
+    eq(lean.dense, outs[0][0], "lean mode")
+
+
+def test_pipeline_stage_times(dev, stk, synth):
+    l, r = synth.dead_leaves(450, 375, 16, frame=1)
+    t = stk.StageTimes()
+    res = stk.run_depth_pipeline(l, r, stk.PipelineConfig(k=4), times=t, device=dev)
+    assert t.total() > 0.0
+    assert t.total() == pytest.approx(t.convert + t.segment + t.boundary + t.match + t.fill + t.peek)
+    assert res.stats.pixels == 450 * 375
+
+
+def test_pipeline_errors(dev, stk):
+    with pytest.raises(stk.ParamError) as e:
+        stk.run_depth_pipeline(np.zeros((48, 64, 3), np.uint8), np.zeros((48, 32, 3), np.uint8),
+                               device=dev)
+    assert "64x48" in str(e.value) and "32x48" in str(e.value)
+    z = np.zeros((10, 10, 3), np.uint8)
+    with pytest.raises(stk.ParamError, match="window"):
+        stk.run_depth_pipeline(z, z, stk.PipelineConfig(window=4), device=dev)
+    with pytest.raises(stk.ParamError, match="add_border_anchors"):
+        stk.run_depth_pipeline(z, z, stk.PipelineConfig(window=11), device=dev)
+    with pytest.raises(stk.ParamError, match="k must be at least 1, got 0"):
+        e0 = np.zeros((0, 0, 3), np.uint8)
+        stk.run_depth_pipeline(e0, e0, device=dev)
+    with pytest.raises(stk.ParamError, match="bad focus range"):
+        stk.run_refocus_pipeline(z, z, stk.PipelineConfig(window=3), stk.FocusSpec([(3, 17)]),
+                                 device=dev)
+
+
+def test_async_slots_match_sync(dev, stk, synth):
+    """Three frames in flight on three slots (pinned host buffers) give the same
+    bytes as synchronous frames."""
+    from paper_2001_07809_b200 import _lib
+
+    L = _lib.lib()
+    W, H = 512, 256
+    cfg = stk.PipelineConfig(k=5, window=9, max_disparity=24)
+    focus = stk.FocusSpec([(8, 24)], 2.0)
+    frames = [synth.dead_leaves(W, H, 24, frame=i) for i in range(6)]
+    want = [stk.run_refocus_pipeline(l, r, cfg, focus, device=dev) for l, r in frames]
+    c_cfg = cfg.c()
+    c_focus, _keep = stk._focus_c(focus, 0)
+    outs = [np.empty((H, W, 3), np.uint8) for _ in frames]
+    fo = [_lib.StkFrameOut() for _ in frames]
+    for i in range(len(frames)):
+        fo[i].refocused = outs[i].ctypes.data
+    pending = [None] * 3
+    for i, (l, r) in enumerate(frames):
+        s = i % 3
+        if pending[s] is not None:
+            stk._raise(L.stk_frame_wait(dev.h, s, None, None, None), dev.h)
+        stk._raise(L.stk_frame_submit(dev.h, s, l.ctypes.data, r.ctypes.data, W, H, C.byref(c_cfg),
+                                      C.byref(c_focus), C.byref(fo[i]), 0), dev.h)
+        pending[s] = i
+    for s in range(3):
+        stk._raise(L.stk_frame_wait(dev.h, s, None, None, None), dev.h)
+    for a, b in zip(outs, want):
+        eq(a, b, "async")
