@@ -2,15 +2,23 @@
 // all on the device with no host round trip (reference: boundary.cpp:87-195,
 // pipeline.cpp:92-94).
 //
-//   K4a ccl_local    32x32 tile union-find in shared memory (atomicMin union,
-//                    path compression), min-index roots.
+//   K4a ccl_local    one warp per 32x32 tile: lane = row, the row is a 32-bit
+//                    mask, runs (maximal horizontal segments) are the
+//                    union-find nodes; runs of adjacent rows that touch
+//                    (8-connectivity) are united with atomicMin in shared
+//                    memory, paths compressed, and run lengths summed into
+//                    local component sizes.  Every pixel's parent becomes its
+//                    local root (min raster index of the local component); the
+//                    local roots go to a list with their sizes.
 //   K4b ccl_merge    tile-border pixels unite across tiles in global memory
 //                    (lock-free atomicMin union on raster indices).
-//   K4c ccl_flatten  every pixel -> its root (= min raster index of its
-//                    component); component sizes by warp-aggregated atomics.
-//   K4d ccl_roots    ordered compaction of roots (decoupled look-back):
-//                    canonical label = rank of the root in raster order, which
-//                    is exactly the reference's discovery order; size
+//   K4c ccl_compress one thread per local root: find + path compression to the
+//                    global root (= min raster index of the component), local
+//                    size added to the global size.  A pixel's root is then
+//                    par[par[i]].
+//   K4d ccl_roots    ordered compaction of global roots (single-pass decoupled
+//                    look-back): canonical label = rank of the root in raster
+//                    order, exactly the reference's discovery order; size
 //                    histogram for the prune.
 //   K4e prune_select counting-sort form of the reference's by_size walk.
 //   K4f prune_mark   marks removed components (rank among size-s* roots).
@@ -31,7 +39,8 @@ namespace stk {
 
 namespace {
 
-constexpr int CT = 32;  // CCL tile side
+constexpr int CT = 32;          // CCL tile side
+constexpr int kLocalWarps = 4;  // tiles per K4a CTA
 
 // ------------------------------------------------------------ union-find --
 __device__ __forceinline__ int sfind(volatile int* p, int x) {
@@ -90,53 +99,114 @@ __device__ __forceinline__ unsigned long long budget_of(const Frame& f) {
     return (unsigned long long)floor(__dmul_rn(f.frac, (double)f.sc->refined_count));
 }
 
+__device__ __forceinline__ uint32_t upto_mask(int j) {  // bits 0..j
+    return j >= 31 ? 0xffffffffu : ((2u << j) - 1u);
+}
+
+__device__ __forceinline__ int run_len(uint32_t m, int a) {  // set bits from a upward
+    const uint32_t inv = ~(m >> a);
+    return inv ? __ffs(inv) - 1 : 32 - a;
+}
+
+// 32 mask bytes (0 / nonzero) -> 32-bit row mask
+__device__ __forceinline__ uint32_t bytes_to_bits(uint4 a, uint4 b) {
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t m = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t v = __vcmpne4(w[i], 0u) & 0x01010101u;
+        m |= ((v * 0x01020408u) >> 24) << (4 * i);
+    }
+    return m;
+}
+
 // ----------------------------------------------------------------- K4a ----
-__global__ void __launch_bounds__(256) k_ccl_local(Frame f) {
-    __shared__ int lp[CT * CT];
-    const int x0 = blockIdx.x * CT, y0 = blockIdx.y * CT;
-    const int tid = threadIdx.x;
-    for (int i = tid; i < CT * CT; i += 256) {
-        const int x = x0 + (i & (CT - 1)), y = y0 + i / CT;
-        const bool set = x < f.W && y < f.H && f.mref[(size_t)y * f.P + x];
-        lp[i] = set ? i : -1;
-    }
-    // zero the size histogram bins the prune will use (0..B+1)
-    {
+__global__ void __launch_bounds__(32 * kLocalWarps) k_ccl_local(Frame f) {
+    __shared__ int sp[kLocalWarps][CT * CT];
+    __shared__ int ssz[kLocalWarps][CT * CT];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    {   // zero the size-histogram bins the prune will use (0..B+1)
         const unsigned long long B = budget_of(f);
-        const long long nb = (long long)gridDim.x * gridDim.y;
-        const long long bid = blockIdx.y * (long long)gridDim.x + blockIdx.x;
-        for (long long s = bid * 256 + tid; s <= (long long)B + 1; s += nb * 256) f.szhist[s] = 0;
-        if (bid == 0 && tid == 0) f.sc->budget = B;
+        const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+        const long long stride = (long long)gridDim.x * blockDim.x;
+        for (long long s = gt; s <= (long long)B + 1; s += stride) f.szhist[s] = 0;
+        if (gt == 0) f.sc->budget = B;
     }
-    __syncthreads();
-    for (int i = tid; i < CT * CT; i += 256) {
-        if (lp[i] < 0) continue;
-        const int c = i & (CT - 1), r = i / CT;
-        // backward Moore neighbours W, NW, N, NE
-        if (c > 0 && lp[i - 1] >= 0) sunite(lp, i, i - 1);
-        if (r > 0) {
-            if (c > 0 && lp[i - CT - 1] >= 0) sunite(lp, i, i - CT - 1);
-            if (lp[i - CT] >= 0) sunite(lp, i, i - CT);
-            if (c < CT - 1 && lp[i - CT + 1] >= 0) sunite(lp, i, i - CT + 1);
+    const int TXc = (f.W + CT - 1) / CT, TYc = (f.H + CT - 1) / CT;
+    const int tile = blockIdx.x * kLocalWarps + wid;
+    if (tile >= TXc * TYc) return;
+    const int x0 = (tile % TXc) * CT, y0 = (tile / TXc) * CT;
+    int* p = sp[wid];
+    int* sz = ssz[wid];
+    uint32_t m = 0;
+    if (y0 + lane < f.H) {
+        const uint4* row = reinterpret_cast<const uint4*>(f.mref + (size_t)(y0 + lane) * f.P + x0);
+        m = bytes_to_bits(row[0], row[1]);
+        if (f.W - x0 < 32) m &= (1u << (f.W - x0)) - 1u;
+    }
+    const uint32_t s = m & ~(m << 1);  // run starts
+    for (uint32_t t = s; t; t &= t - 1) {
+        const int node = lane * 32 + __ffs(t) - 1;
+        p[node] = node;
+        sz[node] = 0;
+    }
+    __syncwarp();
+    uint32_t mu = __shfl_up_sync(0xffffffffu, m, 1), su = __shfl_up_sync(0xffffffffu, s, 1);
+    if (lane == 0) mu = su = 0;
+    for (uint32_t t = s; t; t &= t - 1) {
+        const int a = __ffs(t) - 1;
+        const int b = a + run_len(m, a) - 1;
+        const int lo = a > 0 ? a - 1 : 0, hi = b < 31 ? b + 1 : 31;
+        uint32_t T = mu & upto_mask(hi) & ~((1u << lo) - 1u);
+        while (T) {
+            const int j = __ffs(T) - 1;
+            const int sa = 31 - __clz(su & upto_mask(j));
+            sunite(p, lane * 32 + a, (lane - 1) * 32 + sa);
+            const int e = sa + run_len(mu, sa) - 1;
+            T &= e >= 31 ? 0u : ~upto_mask(e);
         }
     }
-    __syncthreads();
-    int roots[CT * CT / 256];
-#pragma unroll
-    for (int k = 0; k < CT * CT / 256; ++k) {
-        const int i = tid + k * 256;
-        roots[k] = lp[i] >= 0 ? sfind(lp, i) : -1;
+    __syncwarp();
+    int nroots = 0;
+    for (uint32_t t = s; t; t &= t - 1) {
+        const int a = __ffs(t) - 1, node = lane * 32 + a;
+        const int r = sfind(p, node);
+        p[node] = r;
+        atomicAdd(&sz[r], run_len(m, a));
+        nroots += r == node;
     }
-    __syncthreads();
+    __syncwarp();
+    // local roots -> list (unordered), zero their global size
+    int incl = nroots;
 #pragma unroll
-    for (int k = 0; k < CT * CT / 256; ++k) {
-        const int i = tid + k * 256;
-        if (roots[k] < 0) continue;
-        const int x = x0 + (i & (CT - 1)), y = y0 + i / CT;
-        const int rx = x0 + (roots[k] & (CT - 1)), ry = y0 + roots[k] / CT;
-        const int g = y * f.W + x, gr = ry * f.W + rx;
-        f.par[g] = gr;
-        if (gr == g) f.cnt[g] = 0;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    unsigned base = 0;
+    if (lane == 31 && incl) base = atomicAdd(&f.sc->n_lroots, (unsigned)incl);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    unsigned pos = base + incl - nroots;
+    uint32_t* lr_idx = f.list;
+    uint32_t* lr_size = reinterpret_cast<uint32_t*>(f.rank);
+    for (uint32_t t = s; t; t &= t - 1) {
+        const int node = lane * 32 + __ffs(t) - 1;
+        if (p[node] == node) {
+            const int g = (y0 + lane) * f.W + x0 + (node & 31);
+            lr_idx[pos] = (uint32_t)g;
+            lr_size[pos] = (uint32_t)sz[node];
+            f.cnt[g] = 0;
+            ++pos;
+        }
+    }
+    // every pixel -> its local root (coalesced: the warp walks the rows)
+    for (int rr = 0; rr < CT; ++rr) {
+        const uint32_t mr = __shfl_sync(0xffffffffu, m, rr), sr = __shfl_sync(0xffffffffu, s, rr);
+        if ((mr >> lane) & 1u) {
+            const int st = 31 - __clz(sr & upto_mask(lane));
+            const int root = p[rr * 32 + st];
+            f.par[(y0 + rr) * f.W + x0 + lane] = (y0 + (root >> 5)) * f.W + x0 + (root & 31);
+        }
     }
 }
 
@@ -171,23 +241,29 @@ __global__ void __launch_bounds__(128) k_ccl_merge(Frame f) {
 }
 
 // ----------------------------------------------------------------- K4c ----
-__global__ void __launch_bounds__(256) k_ccl_flatten(Frame f) {
-    const int y = blockIdx.y;
-    const int x = blockIdx.x * 256 + threadIdx.x;
-    int r = -1;
-    if (x < f.W && f.mref[(size_t)y * f.P + x]) {
-        const int g = y * f.W + x;
-        r = gfind(f.par, g);
-        f.par[g] = r;
+__global__ void __launch_bounds__(256) k_ccl_compress(Frame f) {
+    const unsigned n = f.sc->n_lroots;
+    const uint32_t* lr_idx = f.list;
+    const uint32_t* lr_size = reinterpret_cast<const uint32_t*>(f.rank);
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int lr = (int)lr_idx[i];
+        const int r = gfind(f.par, lr);
+        int x = lr;
+        while (true) {  // path compression (all writers store the same root)
+            const int nx = __ldcg(f.par + x);
+            if (nx == x || nx == r) break;
+            f.par[x] = r;
+            x = nx;
+        }
+        if (x != r) f.par[x] = r;
+        atomicAdd(f.cnt + r, lr_size[i]);
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, r);
-    if (r >= 0 && (__ffs(peers) - 1) == (int)(threadIdx.x & 31))
-        atomicAdd(f.cnt + r, (unsigned)__popc(peers));
 }
 
 // ----------------------------------------------------------------- K4d ----
-// Chunk = 8 row-tiles (one warp each, 128 pixels of one row, 4 per lane at
-// x = seg*128 + j*32 + lane so ballots come out in raster order).
+// Chunk = 32 row-tiles; warp w owns tiles 4w..4w+3 of the chunk (128 pixels
+// of one row each, 4 per lane at x = seg*128 + j*32 + lane) so ballots come
+// out in raster order.
 __global__ void __launch_bounds__(256) k_ccl_roots(Frame f, int write_rank) {
     __shared__ uint32_t s_chunk, s_excl;
     __shared__ uint32_t wcount[8];
@@ -196,46 +272,57 @@ __global__ void __launch_bounds__(256) k_ccl_roots(Frame f, int write_rank) {
     if (threadIdx.x == 0) s_chunk = atomicAdd(&f.sc->ctr[LB_ROOTS], 1u);
     __syncthreads();
     const int c = s_chunk;
-    const int t = c * kTilesPerChunk + wid;
-    uint32_t balls[4] = {0, 0, 0, 0};
-    int gidx[4];
-    if (t < f.n_tiles) {
+    const int t0 = c * kTilesPerChunk + wid * kTilesPerWarp;
+    uint32_t balls[kTilesPerWarp][4];
+    uint32_t wc = 0;
+#pragma unroll
+    for (int k = 0; k < kTilesPerWarp; ++k) {
+        const int t = t0 + k;
         const int y = t / f.TX, seg = t % f.TX;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int x = seg * kRowTile + j * 32 + lane;
-            gidx[j] = y * f.W + x;
             bool isroot = false;
-            if (x < f.W && f.mref[(size_t)y * f.P + x]) isroot = f.par[gidx[j]] == gidx[j];
-            balls[j] = __ballot_sync(0xffffffffu, isroot);
+            if (t < f.n_tiles && x < f.W && f.mref[(size_t)y * f.P + x]) {
+                const int g = y * f.W + x;
+                isroot = __ldg(f.par + g) == g;
+            }
+            balls[k][j] = __ballot_sync(0xffffffffu, isroot);
+            wc += __popc(balls[k][j]);
         }
     }
-    const uint32_t wc = __popc(balls[0]) + __popc(balls[1]) + __popc(balls[2]) + __popc(balls[3]);
     if (lane == 0) wcount[wid] = wc;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t agg = 0;
-        for (int i = 0; i < 8; ++i) agg += wcount[i];
-        const uint32_t excl = lb_exclusive(status, c, agg);
-        s_excl = excl;
-        if (c == f.n_chunks - 1) f.sc->n_roots = excl + agg;
+    if (wid == 0) {
+        uint32_t v = lane < 8 ? wcount[lane] : 0u;
+        const uint32_t agg = __reduce_add_sync(0xffffffffu, v);
+        const uint32_t excl = lb_exclusive_warp(status, c, agg);
+        if (lane == 0) {
+            s_excl = excl;
+            if (c == f.n_chunks - 1) f.sc->n_roots = excl + agg;
+        }
     }
     __syncthreads();
-    if (t >= f.n_tiles) return;
     uint32_t pos = s_excl;
     for (int i = 0; i < wid; ++i) pos += wcount[i];
     const unsigned long long B = f.sc->budget;
     const uint32_t lanemask = (1u << lane) - 1u;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        if (balls[j] >> lane & 1u) {
-            const uint32_t p = pos + __popc(balls[j] & lanemask);
-            f.roots[p] = gidx[j];
-            if (write_rank) f.rank[gidx[j]] = (int)p;
-            const uint32_t sz = f.cnt[gidx[j]];
-            if (sz <= B + 1) atomicAdd(f.szhist + sz, 1u);
+    for (int k = 0; k < kTilesPerWarp; ++k) {
+        const int t = t0 + k;
+        const int y = t / f.TX, seg = t % f.TX;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (balls[k][j] >> lane & 1u) {
+                const int g = y * f.W + seg * kRowTile + j * 32 + lane;
+                const uint32_t p = pos + __popc(balls[k][j] & lanemask);
+                f.roots[p] = g;
+                if (write_rank) f.rank[g] = (int)p;
+                const uint32_t sz = f.cnt[g];
+                if (sz <= B + 1) atomicAdd(f.szhist + sz, 1u);
+            }
+            pos += __popc(balls[k][j]);
         }
-        pos += __popc(balls[j]);
     }
 }
 
@@ -310,10 +397,10 @@ __global__ void __launch_bounds__(256) k_prune_mark(Frame f) {
                 __popc(balls[0]) + __popc(balls[1]) + __popc(balls[2]) + __popc(balls[3]);
             if (lane == 0) wcount[wid] = wc;
             __syncthreads();
-            if (threadIdx.x == 0) {
-                uint32_t agg = 0;
-                for (int i = 0; i < 8; ++i) agg += wcount[i];
-                s_excl = lb_exclusive(status, (int)c, agg);
+            if (wid == 0) {
+                const uint32_t agg = __reduce_add_sync(0xffffffffu, lane < 8 ? wcount[lane] : 0u);
+                const uint32_t excl = lb_exclusive_warp(status, (int)c, agg);
+                if (lane == 0) s_excl = excl;
             }
             __syncthreads();
             pos = s_excl;
@@ -342,23 +429,31 @@ __global__ void __launch_bounds__(256) k_apply(Frame f, int use_prune, int ancho
     if (threadIdx.x == 0) s_chunk = atomicAdd(&f.sc->ctr[LB_LIST], 1u);
     __syncthreads();
     const int c = s_chunk;
-    const int t = c * kTilesPerChunk + wid;
+    const int t0 = c * kTilesPerChunk + wid * kTilesPerWarp;
     const int m = f.hw, W = f.W, H = f.H;
-    uint32_t balls[4] = {0, 0, 0, 0};
-    uint32_t kept = 0;
+    uint32_t balls[kTilesPerWarp][4];
+    uint32_t wc = 0, kept = 0;
     unsigned long long ops = 0;
-    int y = 0, seg = 0;
-    if (t < f.n_tiles) {
-        y = t / f.TX;
-        seg = t % f.TX;
+#pragma unroll
+    for (int k = 0; k < kTilesPerWarp; ++k) {
+        const int t = t0 + k;
+        const bool tv = t < f.n_tiles;
+        const int y = t / f.TX, seg = t % f.TX;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int x = seg * kRowTile + j * 32 + lane;
             bool keep = false, anc = false;
-            if (x < W) {
+            if (tv && x < W) {
                 const size_t po = (size_t)y * f.P + x;
                 const int g = y * W + x;
-                if (f.mref[po]) keep = use_prune ? !(f.cnt[f.par[g]] & kRemoved) : true;
+                if (f.mref[po]) {
+                    if (use_prune) {
+                        const int r = __ldg(f.par + __ldg(f.par + g));
+                        keep = !(__ldg(f.cnt + r) & kRemoved);
+                    } else {
+                        keep = true;
+                    }
+                }
                 anc = keep;
                 if (anchors && (x == m || x == W - 1 - m) && y >= m && y <= H - 1 - m) anc = true;
                 if (f.mprn) f.mprn[po] = keep;
@@ -367,12 +462,12 @@ __global__ void __launch_bounds__(256) k_apply(Frame f, int use_prune, int ancho
             }
             kept += keep;
             const bool matchable = anc && y >= m && y < H - m && x >= m && x < W - m;
-            balls[j] = __ballot_sync(0xffffffffu, matchable);
+            balls[k][j] = __ballot_sync(0xffffffffu, matchable);
+            wc += __popc(balls[k][j]);
             if (matchable) ops += (unsigned long long)(min(f.D, x - m) + 1);
-            if (lane == 0) f.mbits[(size_t)y * f.bits_words + seg * 4 + j] = balls[j];
+            if (tv && lane == 0) f.mbits[(size_t)y * f.bits_words + seg * 4 + j] = balls[k][j];
         }
     }
-    const uint32_t wc = __popc(balls[0]) + __popc(balls[1]) + __popc(balls[2]) + __popc(balls[3]);
     if (lane == 0) wcount[wid] = wc;
     unsigned long long kk = kept, oo = ops;
     for (int o = 16; o > 0; o >>= 1) {
@@ -384,37 +479,43 @@ __global__ void __launch_bounds__(256) k_apply(Frame f, int use_prune, int ancho
         red2[wid] = oo;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t agg = 0;
-        unsigned long long ka = 0, oa = 0;
-        for (int i = 0; i < 8; ++i) {
-            agg += wcount[i];
-            ka += red[i];
-            oa += red2[i];
-        }
-        const uint32_t excl = lb_exclusive(status, c, agg);
-        s_excl = excl;
-        if (ka) atomicAdd(&f.sc->pruned_count, ka);
-        if (oa) atomicAdd(&f.sc->sad_ops, oa * (unsigned long long)(f.window * f.window));
-        if (c == f.n_chunks - 1) {
-            f.sc->n_list = excl + agg;
-            f.sc->matched = excl + agg;
-            f.tile_off[f.n_tiles] = excl + agg;
+    if (wid == 0) {
+        const uint32_t agg = __reduce_add_sync(0xffffffffu, lane < 8 ? wcount[lane] : 0u);
+        const uint32_t excl = lb_exclusive_warp(status, c, agg);
+        if (lane == 0) {
+            s_excl = excl;
+            unsigned long long ka = 0, oa = 0;
+            for (int i = 0; i < 8; ++i) {
+                ka += red[i];
+                oa += red2[i];
+            }
+            if (ka) atomicAdd(&f.sc->pruned_count, ka);
+            if (oa) atomicAdd(&f.sc->sad_ops, oa * (unsigned long long)(f.window * f.window));
+            if (c == f.n_chunks - 1) {
+                f.sc->n_list = excl + agg;
+                f.sc->matched = excl + agg;
+                f.tile_off[f.n_tiles] = excl + agg;
+            }
         }
     }
     __syncthreads();
-    if (t >= f.n_tiles) return;
     uint32_t pos = s_excl;
     for (int i = 0; i < wid; ++i) pos += wcount[i];
-    if (lane == 0) f.tile_off[t] = pos;
     const uint32_t lanemask = (1u << lane) - 1u;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        if (balls[j] >> lane & 1u) {
-            const int x = seg * kRowTile + j * 32 + lane;
-            f.list[pos + __popc(balls[j] & lanemask)] = ((uint32_t)y << 16) | (uint32_t)x;
+    for (int k = 0; k < kTilesPerWarp; ++k) {
+        const int t = t0 + k;
+        if (t >= f.n_tiles) break;
+        const int y = t / f.TX, seg = t % f.TX;
+        if (lane == 0) f.tile_off[t] = pos;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (balls[k][j] >> lane & 1u) {
+                const int x = seg * kRowTile + j * 32 + lane;
+                f.list[pos + __popc(balls[k][j] & lanemask)] = ((uint32_t)y << 16) | (uint32_t)x;
+            }
+            pos += __popc(balls[k][j]);
         }
-        pos += __popc(balls[j]);
     }
 }
 
@@ -433,7 +534,7 @@ __global__ void k_labels_out(Frame f, int32_t* out) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const int y = (int)(i / f.W), x = (int)(i - (long long)y * f.W);
-        out[i] = f.mref[(size_t)y * f.P + x] ? f.rank[f.par[i]] : -1;
+        out[i] = f.mref[(size_t)y * f.P + x] ? f.rank[f.par[f.par[i]]] : -1;
     }
 }
 
@@ -486,9 +587,10 @@ void launch_anchor_only(const Frame& f, const uint8_t* in, uint8_t* out, int mar
 void launch_ccl(const Frame& f, cudaStream_t st) {
     if (f.N == 0) return;
     const dim3 tiles((f.W + CT - 1) / CT, (f.H + CT - 1) / CT);
-    k_ccl_local<<<tiles, 256, 0, st>>>(f);
+    const int ntiles = tiles.x * tiles.y;
+    k_ccl_local<<<(ntiles + kLocalWarps - 1) / kLocalWarps, 32 * kLocalWarps, 0, st>>>(f);
     k_ccl_merge<<<tiles, 128, 0, st>>>(f);
-    k_ccl_flatten<<<dim3((f.W + 255) / 256, f.H), 256, 0, st>>>(f);
+    k_ccl_compress<<<148 * 8, 256, 0, st>>>(f);
     k_ccl_roots<<<f.n_chunks, 256, 0, st>>>(f, f.full);
 }
 

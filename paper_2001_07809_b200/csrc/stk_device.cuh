@@ -97,6 +97,38 @@ __device__ __forceinline__ unsigned long long lb_load(const unsigned long long* 
     return v;
 }
 
+// Called by ALL 32 lanes of one warp: returns (on every lane) the exclusive
+// prefix of chunk `c` whose own total is `agg`, and publishes the inclusive
+// prefix.  The warp polls 32 predecessors per round, so an aggregate-only
+// run of predecessors costs one round trip per 32 chunks.
+__device__ __forceinline__ uint32_t lb_exclusive_warp(unsigned long long* status, int c,
+                                                      uint32_t agg) {
+    const int lane = threadIdx.x & 31;
+    if (c == 0) {
+        if (lane == 0) lb_publish(status, 2ull, agg);
+        return 0;
+    }
+    if (lane == 0) lb_publish(status + c, 1ull, agg);
+    uint32_t excl = 0;
+    int j = c - 1;
+    while (true) {
+        const int idx = j - lane;
+        const unsigned long long v = idx >= 0 ? lb_load(status + idx) : (2ull << 62);
+        const unsigned flag = (unsigned)(v >> 62);
+        const unsigned incl = __ballot_sync(0xffffffffu, flag == 2u);
+        const unsigned zero = __ballot_sync(0xffffffffu, flag == 0u);
+        const int first = incl ? __ffs(incl) - 1 : 32;
+        const unsigned upto = first >= 31 ? 0xffffffffu : ((2u << first) - 1u);
+        if (zero & upto) continue;  // a predecessor we need has not published yet
+        const uint32_t val = lane <= first ? (uint32_t)(v & 0xffffffffu) : 0u;
+        excl += __reduce_add_sync(0xffffffffu, val);
+        if (first < 32) break;
+        j -= 32;
+    }
+    if (lane == 0) lb_publish(status + c, 2ull, excl + agg);
+    return excl;
+}
+
 // Called by ONE thread: returns the exclusive prefix of chunk `c` whose own
 // total is `agg`, and publishes the inclusive prefix.
 __device__ __forceinline__ uint32_t lb_exclusive(unsigned long long* status, int c, uint32_t agg) {

@@ -16,7 +16,8 @@
 namespace stk {
 
 constexpr int kRowTile = 128;         // columns per row-tile (compaction + SAD list tiles)
-constexpr int kTilesPerChunk = 8;     // row-tiles per look-back chunk (one warp each)
+constexpr int kTilesPerWarp = 4;      // consecutive row-tiles one warp compacts
+constexpr int kTilesPerChunk = 32;    // row-tiles per look-back chunk (8 warps x 4)
 constexpr uint32_t kRemoved = 0x80000000u;  // prune flag OR-ed into cnt[root]
 
 // Counters for the single-pass decoupled look-back scans.
@@ -43,6 +44,8 @@ struct DevScalars {
     unsigned long long q;              // ... and the first q of size s_star
     unsigned int n_roots;              // component count C
     unsigned int n_list;               // == matched
+    unsigned int n_lroots;             // tile-local roots (K4a -> K4c)
+    unsigned int pad1;
     unsigned int ctr[LB_COUNT];        // dynamic chunk counters
 };
 
