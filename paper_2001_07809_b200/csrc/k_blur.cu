@@ -1,16 +1,19 @@
 // K8 blur_sep -- depth-range-masked Gaussian blur of the left view
 // (reference: refocus.cpp:45-113, pipeline.cpp:141-146).
 //
-// A CTA owns a 64x16 output tile.  The RGB tile plus a kernel-half-width halo
+// A CTA owns a 64x32 output tile.  The RGB tile plus a kernel-half-width halo
 // is staged in shared memory with the reference's replicate-border rule coded
 // explicitly (clamped source coordinates, refocus.cpp:97-99).  The blur
 // decision is fused: a pixel stays sharp iff its dense disparity is known and
 // inside a focus range (refocus.cpp:45-73, as a per-disparity LUT), so the
 // blur map never exists in HBM.  Tiles with no blurred pixel just copy.
 //
-//   default : separable FP32 (horizontal pass into shared memory, vertical
-//             pass in registers) -- within 1 LSB of the reference's 2-D FP64
-//             sum (tests bound it);
+//   default : separable FP32, register-blocked: a thread computes 4
+//             horizontally adjacent outputs of one staged row (16+2h bytes
+//             per channel converted once with the 2^23 magic-number trick),
+//             then 4 vertically adjacent outputs of one column from float4
+//             shared rows -- within 1 LSB of the reference's 2-D FP64 sum
+//             (tests bound it);
 //   exact   : 2-D FP64 in the reference's i-outer / j-inner order with
 //             __dmul_rn/__dadd_rn and lround -- bit-identical.
 #include "stk_device.cuh"
@@ -19,7 +22,7 @@ namespace stk {
 
 namespace {
 
-constexpr int BX = 64, BY = 16, kThreads = 256;
+constexpr int BX = 64, BY = 32, kThreads = 256;
 
 __device__ __forceinline__ bool sharp_px(const BlurParams& bp, const Frame& f, const int16_t* depth,
                                          int x, int y) {
@@ -28,17 +31,29 @@ __device__ __forceinline__ bool sharp_px(const BlurParams& bp, const Frame& f, c
     return d >= 0 && d < bp.lut_len && bp.sharp_lut[d];
 }
 
-template <bool EXACT>
-__global__ void __launch_bounds__(kThreads) k_blur(Frame f, BlurParams bp,
-                                                   const uint8_t* __restrict__ in,
-                                                   uint8_t* __restrict__ out,
-                                                   const int16_t* __restrict__ depth) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int h = bp.hw, W = f.W, H = f.H;
-    const int x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
-    const int IW = BX + 2 * h, IH = BY + 2 * h;
-    const int tid = threadIdx.x;
-    // any pixel of this tile blurred?
+__device__ __forceinline__ float byte_f(uint32_t w, int k) {  // byte k of w as float, exact
+    return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540 | k)) - 8388608.0f;
+}
+
+struct TileGeom {
+    int h, IW, IH, rowb;  // staged tile: IH rows of IW pixels, rowb bytes per row (16-aligned)
+};
+
+__device__ __forceinline__ TileGeom tile_geom(int h) {
+    TileGeom g;
+    g.h = h;
+    g.IW = BX + 2 * h;
+    g.IH = BY + 2 * h;
+    g.rowb = ((g.IW * 3 + 15) & ~15) + 16;
+    return g;
+}
+
+// returns false when every pixel of the tile is sharp (and copies it)
+__device__ __forceinline__ bool stage_tile(const Frame& f, const BlurParams& bp,
+                                           const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                           const int16_t* __restrict__ depth, uint8_t* tile,
+                                           const TileGeom& g, int x0, int y0) {
+    const int W = f.W, H = f.H, tid = threadIdx.x;
     bool any = false;
     for (int i = tid; i < BX * BY; i += kThreads) {
         const int x = x0 + (i % BX), y = y0 + i / BX;
@@ -51,95 +66,148 @@ __global__ void __launch_bounds__(kThreads) k_blur(Frame f, BlurParams bp,
             const int x = x0 + (p % BX), y = y0 + p / BX;
             if (x < W && y < H) out[((size_t)y * W + x) * 3 + c] = in[((size_t)y * W + x) * 3 + c];
         }
-        return;
+        return false;
     }
-    uint8_t* tile = smem;  // IH x IW x 3
-    for (int i = tid; i < IW * IH; i += kThreads) {
-        const int r = i / IW, c = i % IW;
-        const int sy = min(max(y0 - h + r, 0), H - 1), sx = min(max(x0 - h + c, 0), W - 1);
+    for (int i = tid; i < g.IW * g.IH; i += kThreads) {
+        const int r = i / g.IW, c = i % g.IW;
+        const int sy = min(max(y0 - g.h + r, 0), H - 1), sx = min(max(x0 - g.h + c, 0), W - 1);
         const uint8_t* p = in + ((size_t)sy * W + sx) * 3;
-        uint8_t* q = tile + (size_t)i * 3;
+        uint8_t* q = tile + (size_t)r * g.rowb + c * 3;
         q[0] = p[0];
         q[1] = p[1];
         q[2] = p[2];
     }
-    const int K = 2 * h + 1;
-    if (EXACT) {
-        double* w2 = reinterpret_cast<double*>(smem + (((size_t)IW * IH * 3 + 15) & ~(size_t)15));
-        for (int i = tid; i < K * K; i += kThreads) w2[i] = bp.g2[i];
-        __syncthreads();
-        for (int i = tid; i < BX * BY; i += kThreads) {
-            const int ox = i % BX, oy = i / BX;
-            const int x = x0 + ox, y = y0 + oy;
-            if (x >= W || y >= H) continue;
-            const size_t o = ((size_t)y * W + x) * 3;
-            if (sharp_px(bp, f, depth, x, y)) {
-                out[o] = in[o];
-                out[o + 1] = in[o + 1];
-                out[o + 2] = in[o + 2];
-                continue;
+    __syncthreads();
+    return true;
+}
+
+__global__ void __launch_bounds__(kThreads) k_blur_sep(Frame f, BlurParams bp,
+                                                       const uint8_t* __restrict__ in,
+                                                       uint8_t* __restrict__ out,
+                                                       const int16_t* __restrict__ depth) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const TileGeom g = tile_geom(bp.hw);
+    const int h = g.h, K = 2 * h + 1, W = f.W, H = f.H, tid = threadIdx.x;
+    const int x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
+    float* gw = reinterpret_cast<float*>(smem);                        // K weights
+    float4* hs = reinterpret_cast<float4*>(smem + (((size_t)K * 4 + 15) & ~(size_t)15));  // IH x BX
+    uint8_t* tile = reinterpret_cast<uint8_t*>(hs + (size_t)g.IH * BX);
+    for (int i = tid; i < K; i += kThreads) gw[i] = bp.g1[i];
+    if (!stage_tile(f, bp, in, out, depth, tile, g, x0, y0)) return;
+    // horizontal: item = (staged row r, 4 consecutive outputs 4q..4q+3)
+    for (int it = tid; it < g.IH * (BX / 4); it += kThreads) {
+        const int r = it / (BX / 4), q4 = (it % (BX / 4)) * 4;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(tile + (size_t)r * g.rowb + q4 * 3);
+        float a[4][3];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) a[o][0] = a[o][1] = a[o][2] = 0.f;
+        // pixels q4 .. q4+3+2h; pixel p channel c = byte 3p+c of the run
+        const int np = 4 + 2 * h;
+        uint32_t wcur = src[0];
+        int wi = 0;
+        for (int p = 0; p < np; ++p) {
+            float v[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int b = 3 * p + c;
+                if ((b >> 2) != wi) {
+                    wi = b >> 2;
+                    wcur = src[wi];
+                }
+                v[c] = byte_f(wcur, b & 3);
             }
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-            for (int r = 0; r < K; ++r) {
-                const uint8_t* row = tile + ((size_t)(oy + r) * IW + ox) * 3;
-                const double* wr = w2 + r * K;
-                for (int c = 0; c < K; ++c) {
-                    const double wt = wr[c];
-                    a0 = __dadd_rn(a0, __dmul_rn(wt, (double)row[c * 3]));
-                    a1 = __dadd_rn(a1, __dmul_rn(wt, (double)row[c * 3 + 1]));
-                    a2 = __dadd_rn(a2, __dmul_rn(wt, (double)row[c * 3 + 2]));
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                const int k = p - o;
+                if (k >= 0 && k < K) {
+                    const float wt = gw[k];
+                    a[o][0] = fmaf(wt, v[0], a[o][0]);
+                    a[o][1] = fmaf(wt, v[1], a[o][1]);
+                    a[o][2] = fmaf(wt, v[2], a[o][2]);
                 }
             }
-            out[o] = (uint8_t)min(max(lround(a0), 0L), 255L);
-            out[o + 1] = (uint8_t)min(max(lround(a1), 0L), 255L);
-            out[o + 2] = (uint8_t)min(max(lround(a2), 0L), 255L);
         }
-        return;
-    }
-    // separable FP32: horizontal pass for all IH rows into hs[IH][BX][3]
-    float* g = reinterpret_cast<float*>(smem + (((size_t)IW * IH * 3 + 15) & ~(size_t)15));
-    float* hs = g + ((K + 3) & ~3);
-    for (int i = tid; i < K; i += kThreads) g[i] = bp.g1[i];
-    __syncthreads();
-    for (int i = tid; i < IH * BX; i += kThreads) {
-        const int r = i / BX, ox = i % BX;
-        const uint8_t* row = tile + ((size_t)r * IW + ox) * 3;
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-        for (int c = 0; c < K; ++c) {
-            const float wt = g[c];
-            a0 = fmaf(wt, (float)row[c * 3], a0);
-            a1 = fmaf(wt, (float)row[c * 3 + 1], a1);
-            a2 = fmaf(wt, (float)row[c * 3 + 2], a2);
-        }
-        float* o = hs + ((size_t)r * BX + ox) * 3;
-        o[0] = a0;
-        o[1] = a1;
-        o[2] = a2;
+#pragma unroll
+        for (int o = 0; o < 4; ++o) hs[(size_t)r * BX + q4 + o] = make_float4(a[o][0], a[o][1], a[o][2], 0.f);
     }
     __syncthreads();
+    // vertical: item = (column x, 4 consecutive output rows)
+    for (int it = tid; it < BX * (BY / 4); it += kThreads) {
+        const int ox = it % BX, oy4 = (it / BX) * 4;
+        const int x = x0 + ox;
+        if (x >= W) continue;
+        float a[4][3];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) a[o][0] = a[o][1] = a[o][2] = 0.f;
+        for (int r = 0; r < 4 + 2 * h; ++r) {
+            const float4 v = hs[(size_t)(oy4 + r) * BX + ox];
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                const int k = r - o;
+                if (k >= 0 && k < K) {
+                    const float wt = gw[k];
+                    a[o][0] = fmaf(wt, v.x, a[o][0]);
+                    a[o][1] = fmaf(wt, v.y, a[o][1]);
+                    a[o][2] = fmaf(wt, v.z, a[o][2]);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            const int y = y0 + oy4 + o;
+            if (y >= H) break;
+            uint8_t* dst = out + ((size_t)y * W + x) * 3;
+            if (sharp_px(bp, f, depth, x, y)) {
+                const uint8_t* t = tile + (size_t)(oy4 + o + h) * g.rowb + (ox + h) * 3;
+                dst[0] = t[0];
+                dst[1] = t[1];
+                dst[2] = t[2];
+            } else {
+                dst[0] = (uint8_t)min(max((int)floorf(a[o][0] + 0.5f), 0), 255);
+                dst[1] = (uint8_t)min(max((int)floorf(a[o][1] + 0.5f), 0), 255);
+                dst[2] = (uint8_t)min(max((int)floorf(a[o][2] + 0.5f), 0), 255);
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_blur_exact(Frame f, BlurParams bp,
+                                                         const uint8_t* __restrict__ in,
+                                                         uint8_t* __restrict__ out,
+                                                         const int16_t* __restrict__ depth) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const TileGeom g = tile_geom(bp.hw);
+    const int K = 2 * g.h + 1, W = f.W, H = f.H, tid = threadIdx.x;
+    const int x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
+    double* w2 = reinterpret_cast<double*>(smem);
+    uint8_t* tile = smem + (size_t)K * K * sizeof(double);
+    for (int i = tid; i < K * K; i += kThreads) w2[i] = bp.g2[i];
+    if (!stage_tile(f, bp, in, out, depth, tile, g, x0, y0)) return;
     for (int i = tid; i < BX * BY; i += kThreads) {
         const int ox = i % BX, oy = i / BX;
         const int x = x0 + ox, y = y0 + oy;
         if (x >= W || y >= H) continue;
         const size_t o = ((size_t)y * W + x) * 3;
         if (sharp_px(bp, f, depth, x, y)) {
-            const uint8_t* t = tile + ((size_t)(oy + h) * IW + ox + h) * 3;
-            out[o] = t[0];
-            out[o + 1] = t[1];
-            out[o + 2] = t[2];
+            out[o] = in[o];
+            out[o + 1] = in[o + 1];
+            out[o + 2] = in[o + 2];
             continue;
         }
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-        for (int r = 0; r < K; ++r) {
-            const float wt = g[r];
-            const float* s = hs + ((size_t)(oy + r) * BX + ox) * 3;
-            a0 = fmaf(wt, s[0], a0);
-            a1 = fmaf(wt, s[1], a1);
-            a2 = fmaf(wt, s[2], a2);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        for (int r = 0; r < K; ++r) {  // i outer, j inner (refocus.cpp:95-105)
+            const uint8_t* row = tile + (size_t)(oy + r) * g.rowb + ox * 3;
+            const double* wr = w2 + r * K;
+            for (int c = 0; c < K; ++c) {
+                const double wt = wr[c];
+                a0 = __dadd_rn(a0, __dmul_rn(wt, (double)row[c * 3]));
+                a1 = __dadd_rn(a1, __dmul_rn(wt, (double)row[c * 3 + 1]));
+                a2 = __dadd_rn(a2, __dmul_rn(wt, (double)row[c * 3 + 2]));
+            }
         }
-        out[o] = (uint8_t)min(max((int)floorf(a0 + 0.5f), 0), 255);
-        out[o + 1] = (uint8_t)min(max((int)floorf(a1 + 0.5f), 0), 255);
-        out[o + 2] = (uint8_t)min(max((int)floorf(a2 + 0.5f), 0), 255);
+        out[o] = (uint8_t)min(max(lround(a0), 0L), 255L);
+        out[o + 1] = (uint8_t)min(max(lround(a1), 0L), 255L);
+        out[o + 2] = (uint8_t)min(max(lround(a2), 0L), 255L);
     }
 }
 
@@ -156,13 +224,17 @@ __global__ void k_blur_map(Frame f, const int16_t* __restrict__ depth, const uin
     }
 }
 
+size_t tile_bytes(int hw) {
+    const int IW = BX + 2 * hw, IH = BY + 2 * hw;
+    return (size_t)IH * ((((size_t)IW * 3 + 15) & ~(size_t)15) + 16);
+}
+
 }  // namespace
 
 size_t blur_smem_bytes(int hw, bool exact) {
-    const int IW = BX + 2 * hw, IH = BY + 2 * hw, K = 2 * hw + 1;
-    size_t b = (((size_t)IW * IH * 3) + 15) & ~(size_t)15;
-    if (exact) return b + (size_t)K * K * sizeof(double);
-    return b + (((size_t)K + 3) & ~(size_t)3) * sizeof(float) + (size_t)IH * BX * 3 * sizeof(float);
+    const int K = 2 * hw + 1, IH = BY + 2 * hw;
+    if (exact) return (size_t)K * K * sizeof(double) + tile_bytes(hw);
+    return (((size_t)K * 4 + 15) & ~(size_t)15) + (size_t)IH * BX * sizeof(float4) + tile_bytes(hw);
 }
 
 void launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, uint8_t* out_rgb,
@@ -171,11 +243,11 @@ void launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, ui
     const dim3 grid((f.W + BX - 1) / BX, (f.H + BY - 1) / BY);
     const size_t sm = blur_smem_bytes(bp.hw, bp.exact != 0);
     if (bp.exact) {
-        cudaFuncSetAttribute(k_blur<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_blur<true><<<grid, kThreads, sm, st>>>(f, bp, in_rgb, out_rgb, depth);
+        cudaFuncSetAttribute(k_blur_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_blur_exact<<<grid, kThreads, sm, st>>>(f, bp, in_rgb, out_rgb, depth);
     } else {
-        cudaFuncSetAttribute(k_blur<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_blur<false><<<grid, kThreads, sm, st>>>(f, bp, in_rgb, out_rgb, depth);
+        cudaFuncSetAttribute(k_blur_sep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_blur_sep<<<grid, kThreads, sm, st>>>(f, bp, in_rgb, out_rgb, depth);
     }
 }
 

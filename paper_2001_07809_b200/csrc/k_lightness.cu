@@ -1,5 +1,5 @@
-// K1 lstar_hist -- RGB -> CIE L* (8-bit) for both views in one launch, with the
-// left view's 256-bin histogram fused in (shared-memory privatised atomics).
+// K1 lstar_hist -- RGB -> CIE L* (8-bit) for both views, with the left view's
+// 256-bin histogram fused in.
 //
 // Reference: lightness.cpp:25-53 (per pixel, FP64), segmentation.cpp:11-44
 // (histogram).  Bit-exactness without device transcendentals:
@@ -8,8 +8,14 @@
 //     contraction), lin[] computed by the host libm (lightness.cpp:29-32).
 //   * The reference's 8-bit L* is non-decreasing in Y, so gray(Y) is the
 //     number of host thresholds thr[v] (v = 1..255, smallest Y with L* >= v)
-//     that are <= Y: an 8-step binary search in shared memory replaces
-//     cbrt/lround.  Verified over all 2^24 RGB triples (tests).
+//     that are <= Y.  The thresholds are bucketed (4096 buckets of Y, at most
+//     one threshold per bucket), so gray = base[b] + (Y >= tb[b]) with
+//     b = floor(4096 Y): two cached loads and one compare instead of cbrt and
+//     lround.  Verified over all 2^24 RGB triples (tests).
+//   * Histogram without atomics: every thread owns one byte counter per bin
+//     in shared memory (bin-major, 64 KB), bumps it with a plain
+//     load/add/store, and a rotated (bank-conflict-free) pass sums the 256
+//     counters of each bin with byte-SAD and adds them to the global counts.
 #include "stk_device.cuh"
 
 namespace stk {
@@ -17,49 +23,40 @@ namespace stk {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kRowsPerBlock = 4;
 
-__device__ __forceinline__ uint32_t lstar_of(const double* lin, const double* thr, uint32_t r,
-                                             uint32_t g, uint32_t b) {
+__device__ __forceinline__ uint32_t lstar_of(const double* lin, const LstarTables* __restrict__ t,
+                                             uint32_t r, uint32_t g, uint32_t b) {
     const double y =
         __dadd_rn(__dadd_rn(__dmul_rn(0.2126, lin[r]), __dmul_rn(0.7152, lin[g])),
                   __dmul_rn(0.0722, lin[b]));
-    uint32_t v = 0;
-#pragma unroll
-    for (uint32_t step = 128; step > 0; step >>= 1)
-        if (thr[v + step] <= y) v += step;
-    return v;
+    const int bk = min((int)__dmul_rz(y, (double)kLstarBuckets), kLstarBuckets);
+    return (uint32_t)__ldg(&t->base[bk]) + (y >= __ldg(&t->tb[bk]) ? 1u : 0u);
 }
 
-// grid.x: row groups, grid.y: view (0 = left, 1 = right); `views` selects
-// which views exist in this launch (bit 0 left, bit 1 right).
+// HIST: left view with the histogram (64 KB dynamic shared counters)
+template <bool HIST>
 __global__ void __launch_bounds__(kThreads) k_lstar(Frame f, const LstarTables* __restrict__ tab,
-                                                    int views, int do_hist, int vec) {
+                                                    int left, int rows_per_block, int vec) {
+    extern __shared__ __align__(16) unsigned char hc[];  // [256 bins][256 threads]
     __shared__ double lin[256];
-    __shared__ double thr[256];
-    __shared__ uint32_t hist[kThreads / 32][256];
-    const int view = (views == 2) ? 1 : (int)blockIdx.y;
-    const bool left = view == 0;
-    const bool hist_on = do_hist && left;
-    for (int i = threadIdx.x; i < 256; i += kThreads) {
-        lin[i] = tab->linear[i];
-        thr[i] = tab->thr[i];
+    const int tid = threadIdx.x;
+    for (int i = tid; i < 256; i += kThreads) lin[i] = tab->linear[i];
+    if (HIST) {
+        uint4* z = reinterpret_cast<uint4*>(hc);
+        for (int i = tid; i < 256 * kThreads / 16; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
     }
-    if (hist_on)
-        for (int i = threadIdx.x; i < (kThreads / 32) * 256; i += kThreads) (&hist[0][0])[i] = 0;
     __syncthreads();
     const uint8_t* __restrict__ rgb = left ? f.rgbL : f.rgbR;
     uint8_t* __restrict__ gray = left ? f.grayL : f.grayR;
-    uint32_t* myh = hist[threadIdx.x >> 5];
-    const int y0 = blockIdx.x * kRowsPerBlock;
-    for (int y = y0; y < min(y0 + kRowsPerBlock, f.H); ++y) {
+    const int y0 = blockIdx.x * rows_per_block;
+    for (int y = y0; y < min(y0 + rows_per_block, f.H); ++y) {
         const uint8_t* src = rgb + (size_t)y * f.W * 3;
         uint8_t* dst = gray + (size_t)y * f.P;
         if (vec) {
             // 16 pixels = 48 bytes = 3 x uint4 per thread
-            for (int x = threadIdx.x * 16; x < f.W; x += kThreads * 16) {
+            for (int x = tid * 16; x < f.W; x += kThreads * 16) {
                 const uint4* s4 = reinterpret_cast<const uint4*>(src + (size_t)x * 3);
-                uint4 a = __ldcs(s4), b = __ldcs(s4 + 1), c = __ldcs(s4 + 2);
+                const uint4 a = __ldcs(s4), b = __ldcs(s4 + 1), c = __ldcs(s4 + 2);
                 const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w,
                                         c.x, c.y, c.z, c.w};
                 uint32_t out[4] = {0, 0, 0, 0};
@@ -69,29 +66,33 @@ __global__ void __launch_bounds__(kThreads) k_lstar(Frame f, const LstarTables* 
                     const uint32_t r = (w[o >> 2] >> ((o & 3) * 8)) & 0xffu;
                     const uint32_t g = (w[(o + 1) >> 2] >> (((o + 1) & 3) * 8)) & 0xffu;
                     const uint32_t bb = (w[(o + 2) >> 2] >> (((o + 2) & 3) * 8)) & 0xffu;
-                    const uint32_t v = lstar_of(lin, thr, r, g, bb);
+                    const uint32_t v = lstar_of(lin, tab, r, g, bb);
                     out[p >> 2] |= v << ((p & 3) * 8);
-                    if (hist_on) atomicAdd(&myh[v], 1u);
                 }
                 *reinterpret_cast<uint4*>(dst + x) = make_uint4(out[0], out[1], out[2], out[3]);
+                if (HIST) {
+#pragma unroll
+                    for (int p = 0; p < 16; ++p)
+                        ++hc[((out[p >> 2] >> ((p & 3) * 8)) & 0xffu) * kThreads + tid];
+                }
             }
         } else {
-            for (int x = threadIdx.x; x < f.W; x += kThreads) {
+            for (int x = tid; x < f.W; x += kThreads) {
                 const uint8_t* p = src + (size_t)x * 3;
-                const uint32_t v = lstar_of(lin, thr, p[0], p[1], p[2]);
+                const uint32_t v = lstar_of(lin, tab, p[0], p[1], p[2]);
                 dst[x] = (uint8_t)v;
-                if (hist_on) atomicAdd(&myh[v], 1u);
+                if (HIST) ++hc[v * kThreads + tid];
             }
         }
     }
-    if (hist_on) {
+    if (HIST) {
         __syncthreads();
-        for (int v = threadIdx.x; v < 256; v += kThreads) {
-            uint32_t s = 0;
-#pragma unroll
-            for (int wi = 0; wi < kThreads / 32; ++wi) s += hist[wi][v];
-            if (s) atomicAdd(&f.sc->hist[v], (unsigned long long)s);
-        }
+        // thread t sums bin t over the 256 byte counters (rotated: conflict-free)
+        const uint32_t* row = reinterpret_cast<const uint32_t*>(hc + tid * kThreads);
+        uint32_t s = 0;
+#pragma unroll 8
+        for (int i = 0; i < kThreads / 4; ++i) s += __vsadu4(row[(i + tid) & (kThreads / 4 - 1)], 0u);
+        if (s) atomicAdd(&f.sc->hist[tid], (unsigned long long)s);
     }
 }
 
@@ -131,13 +132,25 @@ __global__ void k_assign(Frame f, const uint8_t* __restrict__ gray, uint16_t* __
 void launch_lightness(const Frame& f, const LstarTables* dtab, bool left, bool right, bool hist,
                       cudaStream_t st) {
     if (f.N == 0) return;
-    const int views = (left && right) ? 3 : (left ? 1 : 2);
-    const dim3 grid((f.H + kRowsPerBlock - 1) / kRowsPerBlock, views == 3 ? 2 : 1);
-    const bool aligned =
-        ((reinterpret_cast<uintptr_t>(left ? f.rgbL : f.rgbR) |
-          reinterpret_cast<uintptr_t>(right ? f.rgbR : f.rgbL)) & 15) == 0;
-    const int vec = (f.W % 16 == 0) && aligned;
-    k_lstar<<<grid, kThreads, 0, st>>>(f, dtab, views, hist ? 1 : 0, vec);
+    // byte counters: at most 240 pixels per thread per block
+    const int per_row = f.W % 16 == 0 ? 16 * ((f.W + kThreads * 16 - 1) / (kThreads * 16))
+                                      : (f.W + kThreads - 1) / kThreads;
+    const int rpb = std::max(1, std::min(8, 240 / std::max(per_row, 1)));
+    const bool byte_hist_ok = per_row * rpb <= 240;
+    const int blocks = (f.H + rpb - 1) / rpb;
+    for (int view = 0; view < 2; ++view) {
+        if ((view == 0 && !left) || (view == 1 && !right)) continue;
+        const uint8_t* src = view == 0 ? f.rgbL : f.rgbR;
+        const int vec = (f.W % 16 == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+        if (view == 0 && hist && byte_hist_ok) {
+            const int sm = 256 * kThreads;
+            cudaFuncSetAttribute(k_lstar<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+            k_lstar<true><<<blocks, kThreads, sm, st>>>(f, dtab, 1, rpb, vec);
+        } else {
+            k_lstar<false><<<blocks, kThreads, 0, st>>>(f, dtab, view == 0, rpb, vec);
+            if (view == 0 && hist) launch_histogram(f, f.grayL, st);
+        }
+    }
 }
 
 void launch_histogram(const Frame& f, const uint8_t* gray, cudaStream_t st) {

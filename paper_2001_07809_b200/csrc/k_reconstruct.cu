@@ -93,7 +93,8 @@ __global__ void __launch_bounds__(kFillThreads) k_fill_rows(Frame f, const int16
 
 // ------------------------------------------------------------------ K7 ----
 constexpr int PC = 32;  // columns per CTA
-constexpr int PS = 16;  // row segments per column
+constexpr int PS = 32;  // row segments per column
+constexpr int PB = 8;   // rows loaded per batch (independent loads in flight)
 
 struct SegSum {
     int count;     // knowns in the segment
@@ -114,14 +115,20 @@ __global__ void __launch_bounds__(PC * PS) k_peek_cols(Frame f, const int16_t* _
     // phase 1
     SegSum m{0, -1, -1, -1, -1};
     if (col)
-        for (int y = ya; y < yb; ++y) {
-            const int16_t d = in[(size_t)y * W + x];
-            if (d >= 0) {
-                if (m.count == 0) m.f1 = d;
-                else if (m.count == 1) m.f2 = d;
-                m.l2 = m.l1;
-                m.l1 = d;
-                ++m.count;
+        for (int yy = ya; yy < yb; yy += PB) {
+            int16_t v[PB];
+#pragma unroll
+            for (int k = 0; k < PB; ++k) v[k] = yy + k < yb ? __ldg(in + (size_t)(yy + k) * W + x) : -1;
+#pragma unroll
+            for (int k = 0; k < PB; ++k) {
+                const int16_t d = v[k];
+                if (d >= 0) {
+                    if (m.count == 0) m.f1 = d;
+                    else if (m.count == 1) m.f2 = d;
+                    m.l2 = m.l1;
+                    m.l1 = d;
+                    ++m.count;
+                }
             }
         }
     seg[s][cx] = m;
@@ -159,31 +166,38 @@ __global__ void __launch_bounds__(PC * PS) k_peek_cols(Frame f, const int16_t* _
     unsigned long long known = 0;
     if (col) {
         int cur = above;  // nearest known above the current run
-        int rs = -1;
-        for (int y = ya; y <= yb; ++y) {
-            const int16_t d = y < yb ? in[(size_t)y * W + x] : (int16_t)-2;
-            if (y < yb && d < 0) {
-                if (rs < 0) rs = y;
-                continue;
-            }
-            const int nb = y < yb ? d : below;  // nearest known below the run
-            if (rs >= 0) {
-                int16_t v;
-                if (total == 0) v = -1;
-                else if (total == 1) v = (int16_t)(cur >= 0 ? cur : nb);
-                else if (cur >= 0 && nb >= 0) v = peek_estimate(cur, nb, thr);
-                else if (cur < 0) v = peek_estimate(cf1, cf2, thr);
-                else v = peek_estimate(cl2, cl1, thr);
-                for (int q = rs; q < y; ++q) out[(size_t)q * W + x] = v;
-                if (v >= 0) known += (unsigned long long)(y - rs);
-                rs = -1;
-            }
-            if (y < yb) {
+        int rs = -1;      // first row of the pending run of unknowns
+        auto resolve = [&](int nb, int y_end) {  // nb: nearest known below the run
+            int16_t v;
+            if (total == 0) v = -1;
+            else if (total == 1) v = (int16_t)(cur >= 0 ? cur : nb);
+            else if (cur >= 0 && nb >= 0) v = peek_estimate(cur, nb, thr);
+            else if (cur < 0) v = peek_estimate(cf1, cf2, thr);
+            else v = peek_estimate(cl2, cl1, thr);
+            for (int q = rs; q < y_end; ++q) out[(size_t)q * W + x] = v;
+            if (v >= 0) known += (unsigned long long)(y_end - rs);
+            rs = -1;
+        };
+        for (int yy = ya; yy < yb; yy += PB) {
+            int16_t v[PB];
+#pragma unroll
+            for (int k = 0; k < PB; ++k) v[k] = yy + k < yb ? __ldg(in + (size_t)(yy + k) * W + x) : -1;
+#pragma unroll
+            for (int k = 0; k < PB; ++k) {
+                const int y = yy + k;
+                if (y >= yb) break;
+                const int16_t d = v[k];
+                if (d < 0) {
+                    if (rs < 0) rs = y;
+                    continue;
+                }
+                if (rs >= 0) resolve(d, y);
                 out[(size_t)y * W + x] = d;
                 ++known;
                 cur = d;
             }
         }
+        if (rs >= 0) resolve(below, yb);
     }
     // known count for DepthStats::known_fraction
     for (int o = 16; o > 0; o >>= 1) known += __shfl_xor_sync(0xffffffffu, known, o);

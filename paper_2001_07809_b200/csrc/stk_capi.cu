@@ -157,6 +157,23 @@ void make_lstar_tables(LstarTables* t) {
         }
         std::memcpy(&t->thr[v], &hi, 8);
     }
+    // bucketed lookup: base[b] = #{v >= 1 : thr[v] <= b/NB}, tb[b] = the one
+    // threshold strictly inside (b/NB, (b+1)/NB), or +inf
+    const double NB = kLstarBuckets;
+    int v = 1;
+    for (int b = 0; b <= kLstarBuckets; ++b) {
+        const double lo = b / NB, hi = (b + 1) / NB;
+        while (v < 256 && t->thr[v] <= lo) ++v;
+        t->base[b] = (unsigned char)(v - 1);
+        t->tb[b] = (v < 256 && t->thr[v] < hi) ? t->thr[v] : INFINITY;
+        if (v + 1 < 256 && t->thr[v + 1] < hi && t->thr[v] < hi) t->tb[b] = -INFINITY;  // flagged
+    }
+}
+
+bool lstar_buckets_ok(const LstarTables* t) {
+    for (int b = 0; b <= kLstarBuckets; ++b)
+        if (t->tb[b] == -INFINITY) return false;
+    return true;
 }
 
 // --------------------------------------------------------------- layout ---
@@ -447,8 +464,8 @@ int enqueue_kernels(stk_ctx* ctx, Slot& s, const Frame& f, const BlurParams* bp,
     cudaMemsetAsync(f.sc, 0, sizeof(DevScalars), st);
     cudaMemsetAsync(f.lb, 0, sizeof(unsigned long long) * LB_COUNT * f.lb_stride, st);
     rec(0);
-    launch_lightness(f, ctx->d_tab, true, true, true, st);
-    ++n;
+    launch_lightness(f, ctx->d_tab, true, true, true, st);  // left (+histogram), right
+    n += 2;
     rec(1);
     launch_kmeans(f, 0, 100, 0.5, st);
     ++n;
@@ -667,6 +684,10 @@ stk_status stk_create(int device, int max_width, int max_height, int slots, stk_
         ctx->encode = (EncodeTiledFn)fn;
         LstarTables tab;
         make_lstar_tables(&tab);
+        if (!lstar_buckets_ok(&tab)) {
+            rc = fail(ctx, STK_EINTERNAL, "stk_create: L* bucket table has a bucket with 2 thresholds");
+            break;
+        }
         if (cudaMalloc(&ctx->d_tab, sizeof(LstarTables)) != cudaSuccess ||
             cudaMemcpy(ctx->d_tab, &tab, sizeof(tab), cudaMemcpyHostToDevice) != cudaSuccess) {
             rc = fail(ctx, STK_ECUDA, "stk_create: table upload failed");

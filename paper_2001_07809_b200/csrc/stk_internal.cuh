@@ -93,7 +93,13 @@ struct Frame {
 struct LstarTables {
     double linear[256];
     double thr[256];   // thr[0] = -1 (always passes), thr[1..255] ascending
+    // Bucketed form used by K1: for Y in [b/4096, (b+1)/4096),
+    // gray = base[b] + (Y >= tb[b]); every bucket holds at most one threshold
+    // (checked on the host; the minimum threshold spacing is 4.3e-4 > 1/4096).
+    double tb[4097];
+    unsigned char base[4097];
 };
+constexpr int kLstarBuckets = 4096;
 
 // ---------------------------------------------------------------- launchers --
 // Every launcher enqueues on `st` and never synchronises.  Implementations in
