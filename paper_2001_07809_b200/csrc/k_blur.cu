@@ -171,6 +171,89 @@ __global__ void __launch_bounds__(kThreads) k_blur_sep(Frame f, BlurParams bp,
     }
 }
 
+// Same algorithm with the kernel size known at compile time: the 4-output
+// horizontal / vertical loops unroll completely, weights live in registers and
+// byte positions are constants (the common sizes of default_kernel_size).
+template <int K>
+__global__ void __launch_bounds__(kThreads) k_blur_sep_k(Frame f, BlurParams bp,
+                                                         const uint8_t* __restrict__ in,
+                                                         uint8_t* __restrict__ out,
+                                                         const int16_t* __restrict__ depth) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int h = K / 2, NP = 4 + 2 * h, NWB = (3 * NP + 3) / 4;
+    const TileGeom g = tile_geom(h);
+    const int W = f.W, H = f.H, tid = threadIdx.x;
+    const int x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
+    float4* hs = reinterpret_cast<float4*>(smem);  // IH x BX
+    uint8_t* tile = reinterpret_cast<uint8_t*>(hs + (size_t)g.IH * BX);
+    float wk[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) wk[i] = __ldg(bp.g1 + i);
+    if (!stage_tile(f, bp, in, out, depth, tile, g, x0, y0)) return;
+    for (int it = tid; it < g.IH * (BX / 4); it += kThreads) {
+        const int r = it / (BX / 4), q4 = (it % (BX / 4)) * 4;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(tile + (size_t)r * g.rowb + q4 * 3);
+        uint32_t wv[NWB];
+#pragma unroll
+        for (int i = 0; i < NWB; ++i) wv[i] = src[i];
+        float a[4][3];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) a[o][0] = a[o][1] = a[o][2] = 0.f;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            float v[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) v[c] = byte_f(wv[(3 * p + c) >> 2], (3 * p + c) & 3);
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                if (p - o >= 0 && p - o < K) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) a[o][c] = fmaf(wk[p - o], v[c], a[o][c]);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < 4; ++o) hs[(size_t)r * BX + q4 + o] = make_float4(a[o][0], a[o][1], a[o][2], 0.f);
+    }
+    __syncthreads();
+    for (int it = tid; it < BX * (BY / 4); it += kThreads) {
+        const int ox = it % BX, oy4 = (it / BX) * 4;
+        const int x = x0 + ox;
+        if (x >= W) continue;
+        float a[4][3];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) a[o][0] = a[o][1] = a[o][2] = 0.f;
+#pragma unroll
+        for (int r = 0; r < NP; ++r) {
+            const float4 v = hs[(size_t)(oy4 + r) * BX + ox];
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                if (r - o >= 0 && r - o < K) {
+                    a[o][0] = fmaf(wk[r - o], v.x, a[o][0]);
+                    a[o][1] = fmaf(wk[r - o], v.y, a[o][1]);
+                    a[o][2] = fmaf(wk[r - o], v.z, a[o][2]);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            const int y = y0 + oy4 + o;
+            if (y >= H) break;
+            uint8_t* dst = out + ((size_t)y * W + x) * 3;
+            if (sharp_px(bp, f, depth, x, y)) {
+                const uint8_t* t = tile + (size_t)(oy4 + o + h) * g.rowb + (ox + h) * 3;
+                dst[0] = t[0];
+                dst[1] = t[1];
+                dst[2] = t[2];
+            } else {
+                dst[0] = (uint8_t)min(max((int)floorf(a[o][0] + 0.5f), 0), 255);
+                dst[1] = (uint8_t)min(max((int)floorf(a[o][1] + 0.5f), 0), 255);
+                dst[2] = (uint8_t)min(max((int)floorf(a[o][2] + 0.5f), 0), 255);
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) k_blur_exact(Frame f, BlurParams bp,
                                                          const uint8_t* __restrict__ in,
                                                          uint8_t* __restrict__ out,
@@ -246,6 +329,28 @@ void launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, ui
         cudaFuncSetAttribute(k_blur_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         k_blur_exact<<<grid, kThreads, sm, st>>>(f, bp, in_rgb, out_rgb, depth);
     } else {
+        const int K = 2 * bp.hw + 1;
+        // templated sizes: no weight array in shared memory
+        const size_t smk = (size_t)(BY + 2 * bp.hw) * BX * sizeof(float4) + tile_bytes(bp.hw);
+#define STK_BLUR_K(KK)                                                                          \
+    case KK:                                                                                    \
+        cudaFuncSetAttribute(k_blur_sep_k<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                             (int)smk);                                                         \
+        k_blur_sep_k<KK><<<grid, kThreads, smk, st>>>(f, bp, in_rgb, out_rgb, depth);           \
+        return;
+        switch (K) {
+            STK_BLUR_K(3)
+            STK_BLUR_K(5)
+            STK_BLUR_K(7)
+            STK_BLUR_K(9)
+            STK_BLUR_K(11)
+            STK_BLUR_K(13)
+            STK_BLUR_K(17)
+            STK_BLUR_K(25)
+            STK_BLUR_K(49)
+            default: break;
+        }
+#undef STK_BLUR_K
         cudaFuncSetAttribute(k_blur_sep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         k_blur_sep<<<grid, kThreads, sm, st>>>(f, bp, in_rgb, out_rgb, depth);
     }

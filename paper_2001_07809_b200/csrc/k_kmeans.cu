@@ -1,11 +1,14 @@
-// K2 kmeans_warp -- Lloyd K-Means over the 256 histogram bins, one warp,
-// exact FP64 (reference: segmentation.cpp:49-144, caller pipeline.cpp:72-85).
+// K2 kmeans_hist -- Lloyd K-Means over the 256 histogram bins, one CTA of 256
+// threads (one bin each), exact FP64 (reference: segmentation.cpp:49-144,
+// caller pipeline.cpp:72-85).
 //
-// Lane l owns bins 8l..8l+7.  Every floating-point step uses the _rn
-// intrinsics in the reference's operation order so no DFMA contraction can
-// change a center: init lo + (hi-lo)*(j/(k-1.0)); |v - c| distances with
-// strict '<' (ties to the lowest index); center = double(sum)/double(weight)
-// from exact u64 sums; stop when max movement < tol or after max_iter.  The
+// Every floating-point step uses the _rn intrinsics in the reference's
+// operation order so no DFMA contraction can change a center: init
+// lo + (hi-lo)*(j/(k-1.0)); |v - c| distances with strict '<' (ties to the
+// lowest index); center = double(sum)/double(weight) from exact u64 sums;
+// stop when max movement < tol or after max_iter.  Per-cluster sums: lanes of
+// a warp holding the same cluster are grouped with __match_any_sync and the
+// group leader adds the group's sums (one shared u64 atomic per group).  The
 // effective k = min(cfg.k, occupied bins) is decided on the device, so the
 // frame never syncs with the host.
 #include "stk_device.cuh"
@@ -29,87 +32,90 @@ __device__ __forceinline__ int nearest(const double* c, int k, double v) {
 
 // k_fixed > 0: use exactly that k (stage entry kmeans_histogram, which must
 // reject k > occupied); k_fixed <= 0: k = min(f.kcfg, occupied) (pipeline).
-__global__ void __launch_bounds__(32) k_kmeans(Frame f, int k_fixed, int max_iter, double tol) {
+__global__ void __launch_bounds__(256) k_kmeans(Frame f, int k_fixed, int max_iter, double tol) {
     __shared__ double c[256];
     __shared__ unsigned long long wsum[256], vsum[256];
+    __shared__ unsigned long long gw[256], gv[256];  // per-lane staging for group sums
+    __shared__ double wmove[8];
+    __shared__ int s_lo[8], s_hi[8];
     DevScalars* sc = f.sc;
-    const int lane = threadIdx.x;
-    unsigned long long cnt[8];
-    int occ = 0, lo = 256, hi = -1;
-#pragma unroll
+    const int v = threadIdx.x, lane = v & 31, wid = v >> 5;
+    const unsigned long long cnt = sc->hist[v];
+    const int occ = __syncthreads_count(cnt != 0);
+    int lo = __reduce_min_sync(0xffffffffu, cnt ? v : 256);
+    int hi = __reduce_max_sync(0xffffffffu, cnt ? v : -1);
+    if (lane == 0) {
+        s_lo[wid] = lo;
+        s_hi[wid] = hi;
+    }
+    __syncthreads();
+    lo = 256;
+    hi = -1;
     for (int i = 0; i < 8; ++i) {
-        const int v = lane * 8 + i;
-        cnt[i] = sc->hist[v];
-        if (cnt[i]) {
-            ++occ;
-            lo = min(lo, v);
-            hi = max(hi, v);
-        }
+        lo = min(lo, s_lo[i]);
+        hi = max(hi, s_hi[i]);
     }
-    occ = __reduce_add_sync(0xffffffffu, occ);
-    lo = __reduce_min_sync(0xffffffffu, lo);
-    hi = __reduce_max_sync(0xffffffffu, hi);
-    int k;
-    if (k_fixed > 0) {
-        k = k_fixed;
-    } else {
-        k = min(f.kcfg, occ);
-    }
+    const int k = k_fixed > 0 ? k_fixed : min(f.kcfg, occ);
     if (occ == 0 || k < 1 || k > occ) {
-        if (lane == 0) {
+        if (v == 0) {
             sc->kerr = occ == 0 ? 1 : (k < 1 ? 3 : 2);
             sc->k = 0;
         }
         return;
     }
     // init (segmentation.cpp:96-102)
-    for (int j = lane; j < k; j += 32) {
+    if (v < k) {
         if (k == 1)
-            c[j] = __ddiv_rn((double)(lo + hi), 2.0);
+            c[v] = __ddiv_rn((double)(lo + hi), 2.0);
         else
-            c[j] = __dadd_rn((double)lo, __dmul_rn((double)(hi - lo),
-                                                   __ddiv_rn((double)j, __dsub_rn((double)k, 1.0))));
+            c[v] = __dadd_rn((double)lo, __dmul_rn((double)(hi - lo),
+                                                   __ddiv_rn((double)v, __dsub_rn((double)k, 1.0))));
     }
-    __syncwarp();
+    __syncthreads();
     int iters = 0;
     for (int it = 1; it <= max_iter; ++it) {
-        for (int j = lane; j < k; j += 32) wsum[j] = vsum[j] = 0ull;
-        __syncwarp();
-        // assignment of all 256 bins; sums over occupied bins (:104-120)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            if (!cnt[i]) continue;
-            const int v = lane * 8 + i;
-            const int a = nearest(c, k, (double)v);
-            atomicAdd(&wsum[a], cnt[i]);
-            atomicAdd(&vsum[a], cnt[i] * (unsigned long long)v);
+        wsum[v] = vsum[v] = 0ull;
+        // assignment of all bins; sums over occupied bins (:104-120)
+        const int a = nearest(c, k, (double)v);
+        gw[v] = cnt;
+        gv[v] = cnt * (unsigned long long)v;
+        __syncthreads();
+        const unsigned peers = __match_any_sync(0xffffffffu, a);
+        if ((__ffs(peers) - 1) == lane) {
+            unsigned long long sw = 0, sv = 0;
+            for (unsigned m = peers; m; m &= m - 1) {
+                const int l = (wid << 5) + __ffs(m) - 1;
+                sw += gw[l];
+                sv += gv[l];
+            }
+            if (sw) {
+                atomicAdd(&wsum[a], sw);
+                atomicAdd(&vsum[a], sv);
+            }
         }
-        __syncwarp();
+        __syncthreads();
         // update (:122-135); movement = max |updated - old| over non-empty clusters
         double move = 0.0;
-        for (int j = lane; j < k; j += 32) {
-            if (wsum[j] == 0ull) continue;
-            const double upd = __ddiv_rn(__ull2double_rn(vsum[j]), __ull2double_rn(wsum[j]));
-            const double m = fabs(__dsub_rn(upd, c[j]));
-            if (move < m) move = m;
-            c[j] = upd;
+        if (v < k && wsum[v] != 0ull) {
+            const double upd = __ddiv_rn(__ull2double_rn(vsum[v]), __ull2double_rn(wsum[v]));
+            move = fabs(__dsub_rn(upd, c[v]));
+            c[v] = upd;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) move = fmax(move, __shfl_xor_sync(0xffffffffu, move, o));
-        __syncwarp();
+        if (lane == 0) wmove[wid] = move;
+        __syncthreads();
+        move = wmove[0];
+        for (int i = 1; i < 8; ++i) move = fmax(move, wmove[i]);
         iters = it;
         if (move < tol) break;
     }
     // final table against final centers (:139-142)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int v = lane * 8 + i;
-        const int a = nearest(c, k, (double)v);
-        sc->assign16[v] = (unsigned short)a;
-        sc->lut[v] = (unsigned char)a;
-    }
-    for (int j = lane; j < 256; j += 32) sc->centers[j] = j < k ? c[j] : 0.0;
-    if (lane == 0) {
+    const int a = nearest(c, k, (double)v);
+    sc->assign16[v] = (unsigned short)a;
+    sc->lut[v] = (unsigned char)a;
+    sc->centers[v] = v < k ? c[v] : 0.0;
+    if (v == 0) {
         sc->k = k;
         sc->iters = iters;
         sc->kerr = 0;
@@ -119,7 +125,7 @@ __global__ void __launch_bounds__(32) k_kmeans(Frame f, int k_fixed, int max_ite
 }  // namespace
 
 void launch_kmeans(const Frame& f, int k_fixed, int max_iter, double tol, cudaStream_t st) {
-    k_kmeans<<<1, 32, 0, st>>>(f, k_fixed, max_iter, tol);
+    k_kmeans<<<1, 256, 0, st>>>(f, k_fixed, max_iter, tol);
 }
 
 }  // namespace stk
