@@ -79,7 +79,11 @@ __device__ __forceinline__ void row_absdiff(const uint32_t* lw, const uint32_t* 
     }
 }
 
-template <int MAXC, int NPART>
+// WIN > 0: the window size is a compile-time constant (the configured sizes
+// 9/15/21/31): the horizontal pass then keeps the 32+WIN-1 column sums of a
+// chunk in registers and slides with compile-time indices (one IADD3 per part
+// per step, no shared loads inside the slide).  WIN == 0: runtime window.
+template <int MAXC, int NPART, int WIN>
 __global__ void __launch_bounds__(SNT, (MAXC <= 12) ? 2 : 1) k_sad_strip(Frame f, SG g) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bar;
@@ -155,20 +159,19 @@ __global__ void __launch_bounds__(SNT, (MAXC <= 12) ? 2 : 1) k_sad_strip(Frame f
                     }
                 }
             } else {
+                // colsum + new - old in one IADD3 per packed word: every u16
+                // lane's result lies in [0, w*255], so the exact 32-bit
+                // arithmetic never carries or borrows across lanes.
                 const int ro = y - yb0 - 1, rn = y - yb0 + 2 * g.h;
+                uint32_t vn[MAXC];
                 row_absdiff<MAXC>(reinterpret_cast<const uint32_t*>(Lp + (size_t)ro * g.LP),
                                   reinterpret_cast<const uint32_t*>(Rp + (size_t)ro * g.RP), sL, sR, v);
-#pragma unroll
-                for (int k = 0; k < MAXC; ++k) {
-                    A[k] -= __byte_perm(v[k], 0u, 0x4243);
-                    B[k] -= __byte_perm(v[k], 0u, 0x4041);
-                }
                 row_absdiff<MAXC>(reinterpret_cast<const uint32_t*>(Lp + (size_t)rn * g.LP),
-                                  reinterpret_cast<const uint32_t*>(Rp + (size_t)rn * g.RP), sL, sR, v);
+                                  reinterpret_cast<const uint32_t*>(Rp + (size_t)rn * g.RP), sL, sR, vn);
 #pragma unroll
                 for (int k = 0; k < MAXC; ++k) {
-                    A[k] += __byte_perm(v[k], 0u, 0x4243);
-                    B[k] += __byte_perm(v[k], 0u, 0x4041);
+                    A[k] = A[k] + __byte_perm(vn[k], 0u, 0x4243) - __byte_perm(v[k], 0u, 0x4243);
+                    B[k] = B[k] + __byte_perm(vn[k], 0u, 0x4041) - __byte_perm(v[k], 0u, 0x4041);
                 }
             }
 #pragma unroll
@@ -186,6 +189,51 @@ __global__ void __launch_bounds__(SNT, (MAXC <= 12) ? 2 : 1) k_sad_strip(Frame f
             for (int cb = 0; cb < g.SEGW; cb += 32) {
                 const int xi0 = seg * g.SEGW + cb;
                 const uint32_t m = __ldg(mrow + (xi0 >> 5));
+                if constexpr (WIN > 0) {
+                    // ring of the WIN+1 most recent column sums, indexed with
+                    // compile-time positions (the 32 steps are unrolled)
+                    constexpr int PW = (WIN + NPART - 1) / NPART;  // columns per part
+                    constexpr int RW = WIN + 1;
+                    uint32_t ring[RW];
+                    const uint32_t* cp = colp + xi0;
+#pragma unroll
+                    for (int k = 0; k < WIN; ++k) ring[k] = cp[k];
+                    uint32_t S[NPART];
+#pragma unroll
+                    for (int j = 0; j < NPART; ++j) {
+                        S[j] = 0;
+#pragma unroll
+                        for (int k = j * PW; k < (j + 1) * PW && k < WIN; ++k) S[j] += ring[k];
+                    }
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        if (i > 0) {
+                            ring[(i + WIN - 1) % RW] = cp[i + WIN - 1];
+#pragma unroll
+                            for (int j = 0; j < NPART; ++j) {
+                                const int ks = j * PW;
+                                const int ke = ((j + 1) * PW < WIN ? (j + 1) * PW : WIN) - 1;
+                                S[j] = S[j] + ring[(i + ke) % RW] - ring[(i - 1 + ks) % RW];
+                            }
+                        }
+                        if ((m >> i) & 1u) {
+                            const int x = x0 + xi0 + i;
+                            const int dl = min(g.D, x + dl_base);
+                            uint32_t c0v = 0, c1v = 0;
+#pragma unroll
+                            for (int j = 0; j < NPART; ++j) {
+                                c0v += S[j] & 0xffffu;
+                                c1v += S[j] >> 16;
+                            }
+                            uint32_t key = 0xffffffffu;
+                            if (qvalid && dlo <= dl) key = (c0v << 10) | (uint32_t)dlo;
+                            if (qvalid && dlo + 1 <= dl) key = min(key, (c1v << 10) | (uint32_t)(dlo + 1));
+                            key = __reduce_min_sync(0xffffffffu, key);
+                            if (lane == 0) atomicMin(&best[xi0 + i], key);
+                        }
+                    }
+                    continue;
+                }
                 // part j covers window offsets [j*PART, min((j+1)*PART, w))
                 uint32_t S[NPART];
                 const uint32_t* po[NPART];
@@ -234,19 +282,26 @@ __global__ void __launch_bounds__(SNT, (MAXC <= 12) ? 2 : 1) k_sad_strip(Frame f
     }
 }
 
-template <int MAXC, int NPART>
+template <int MAXC, int NPART, int WIN>
 void run(const Frame& f, const SG& g, size_t sm, cudaStream_t st) {
-    cudaFuncSetAttribute(k_sad_strip<MAXC, NPART>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_sad_strip<MAXC, NPART, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
     const dim3 grid((f.W + SW - 1) / SW, (f.H - 2 * g.h + g.TH - 1) / g.TH);
-    k_sad_strip<MAXC, NPART><<<grid, SNT, sm, st>>>(f, g);
+    k_sad_strip<MAXC, NPART, WIN><<<grid, SNT, sm, st>>>(f, g);
 }
 
 template <int MAXC>
 void run_np(const Frame& f, const SG& g, int npart, size_t sm, cudaStream_t st) {
-    if (npart == 1) run<MAXC, 1>(f, g, sm, st);
-    else if (npart == 2) run<MAXC, 2>(f, g, sm, st);
-    else run<MAXC, 4>(f, g, sm, st);
+    switch (g.w) {  // compile-time windows (npart follows from w, see launch_sad_strip)
+        case 9: run<MAXC, 1, 9>(f, g, sm, st); return;
+        case 15: run<MAXC, 1, 15>(f, g, sm, st); return;
+        case 21: run<MAXC, 2, 21>(f, g, sm, st); return;
+        case 31: run<MAXC, 4, 31>(f, g, sm, st); return;
+        default: break;
+    }
+    if (npart == 1) run<MAXC, 1, 0>(f, g, sm, st);
+    else if (npart == 2) run<MAXC, 2, 0>(f, g, sm, st);
+    else run<MAXC, 4, 0>(f, g, sm, st);
 }
 
 }  // namespace
