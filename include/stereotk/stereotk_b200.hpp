@@ -1,0 +1,255 @@
+// stereotk_b200.hpp -- C++ drop-in for the reference's stereotk:: stage and
+// pipeline API (/root/reference/proj/include/stereotk/{image,error,
+// segmentation,boundary,stereo,reconstruct,refocus,pipeline}.hpp), backed by
+// the sm_100a kernels through the C-ABI in stk_b200.h.
+//
+// Same type names, members, function names, parameter meaning and error
+// classes, so callers of the hot path relink against libstk_b200.so without
+// source changes.  Differences, all documented in DESIGN.md:
+//   * `workers` is validated (>= 1) and otherwise ignored -- the GPU result is
+//     identical for any value (the reference's determinism contract,
+//     parallel.hpp:24-28).
+//   * StageTimes are device milliseconds measured with CUDA events.
+//   * selective_blur runs the bit-exact FP64 2-D kernel for arbitrary weights;
+//     when the weights are exactly gaussian_kernel(sigma, size) and
+//     stereotk::b200::fast_blur() is on (default), the separable FP32 kernel
+//     (<= 1 LSB) runs instead.
+//   * Image file I/O (load_image / save_rgb ...) is not part of this library.
+// The per-header forwarding files (image.hpp, pipeline.hpp, ...) include this
+// file, so `#include "stereotk/pipeline.hpp"` keeps working.
+#pragma once
+
+#include <array>
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace stereotk {
+
+// ------------------------------------------------------------- errors ----
+struct IoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct FormatError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ParamError : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+
+// ------------------------------------------------------------- images ----
+struct RgbImage {
+    int width = 0;
+    int height = 0;
+    std::vector<std::uint8_t> data;  // width * height * 3, interleaved
+
+    RgbImage() = default;
+    RgbImage(int w, int h) : width(w), height(h), data(static_cast<std::size_t>(w) * h * 3, 0) {}
+    std::uint8_t& at(int x, int y, int c) { return data[(static_cast<std::size_t>(y) * width + x) * 3 + c]; }
+    std::uint8_t at(int x, int y, int c) const {
+        return data[(static_cast<std::size_t>(y) * width + x) * 3 + c];
+    }
+    std::size_t pixel_count() const { return static_cast<std::size_t>(width) * height; }
+    bool same_size(const RgbImage& o) const { return width == o.width && height == o.height; }
+};
+
+struct GrayImage {
+    int width = 0;
+    int height = 0;
+    std::vector<std::uint8_t> data;
+
+    GrayImage() = default;
+    GrayImage(int w, int h) : width(w), height(h), data(static_cast<std::size_t>(w) * h, 0) {}
+    std::uint8_t& at(int x, int y) { return data[static_cast<std::size_t>(y) * width + x]; }
+    std::uint8_t at(int x, int y) const { return data[static_cast<std::size_t>(y) * width + x]; }
+    std::size_t pixel_count() const { return static_cast<std::size_t>(width) * height; }
+};
+
+GrayImage rgb_to_lightness(const RgbImage& image, int workers = 1);
+
+// ------------------------------------------------------- segmentation ----
+struct Histogram {
+    std::array<std::uint64_t, 256> counts{};
+    std::uint64_t total() const {
+        std::uint64_t s = 0;
+        for (std::uint64_t c : counts) s += c;
+        return s;
+    }
+};
+
+struct Clustering {
+    std::vector<double> centers;
+    std::array<std::uint16_t, 256> bin_assignment{};
+    int iterations_run = 0;
+    int k() const { return static_cast<int>(centers.size()); }
+};
+
+struct LabelMap {
+    int width = 0;
+    int height = 0;
+    std::vector<std::uint16_t> labels;
+
+    LabelMap() = default;
+    LabelMap(int w, int h) : width(w), height(h), labels(static_cast<std::size_t>(w) * h, 0) {}
+    std::uint16_t& at(int x, int y) { return labels[static_cast<std::size_t>(y) * width + x]; }
+    std::uint16_t at(int x, int y) const { return labels[static_cast<std::size_t>(y) * width + x]; }
+};
+
+Histogram build_histogram(const GrayImage& image, int workers = 1);
+Clustering kmeans_histogram(const Histogram& histogram, int k, int max_iter = 100, double tol = 0.5);
+LabelMap assign_pixels(const GrayImage& image, const Clustering& clustering);
+
+// ----------------------------------------------------------- boundary ----
+struct BoundaryMask {
+    int width = 0;
+    int height = 0;
+    std::vector<std::uint8_t> mask;
+
+    BoundaryMask() = default;
+    BoundaryMask(int w, int h) : width(w), height(h), mask(static_cast<std::size_t>(w) * h, 0) {}
+    std::uint8_t& at(int x, int y) { return mask[static_cast<std::size_t>(y) * width + x]; }
+    std::uint8_t at(int x, int y) const { return mask[static_cast<std::size_t>(y) * width + x]; }
+    std::uint64_t count() const {
+        std::uint64_t n = 0;
+        for (std::uint8_t v : mask) n += v;
+        return n;
+    }
+};
+
+struct ComponentTable {
+    int width = 0;
+    int height = 0;
+    std::vector<std::int32_t> labels;
+    std::vector<std::uint32_t> sizes;
+    std::vector<std::int32_t> by_size;
+};
+
+BoundaryMask detect_boundaries(const LabelMap& labels, int workers = 1);
+BoundaryMask morph_fill(const BoundaryMask& mask, int workers = 1);
+BoundaryMask morph_remove(const BoundaryMask& mask, int workers = 1);
+ComponentTable label_components(const BoundaryMask& mask);
+BoundaryMask prune_components(const BoundaryMask& mask, double fraction);
+BoundaryMask add_border_anchors(const BoundaryMask& mask, int margin);
+
+// ------------------------------------------------------------- stereo ----
+struct DisparityMap {
+    static constexpr std::int16_t kUnknown = -1;
+    int width = 0;
+    int height = 0;
+    std::vector<std::int16_t> values;
+
+    DisparityMap() = default;
+    DisparityMap(int w, int h) : width(w), height(h), values(static_cast<std::size_t>(w) * h, kUnknown) {}
+    std::int16_t& at(int x, int y) { return values[static_cast<std::size_t>(y) * width + x]; }
+    std::int16_t at(int x, int y) const { return values[static_cast<std::size_t>(y) * width + x]; }
+    bool known(int x, int y) const { return at(x, y) >= 0; }
+    std::uint64_t known_count() const {
+        std::uint64_t n = 0;
+        for (std::int16_t v : values) n += v >= 0;
+        return n;
+    }
+};
+
+struct MatchConfig {
+    int window = 9;
+    int max_disparity = 16;
+};
+
+std::uint32_t sad_cost(const GrayImage& left, const GrayImage& right, int x, int y, int d, int window);
+DisparityMap match_boundary_pixels(const GrayImage& left, const GrayImage& right,
+                                   const BoundaryMask& mask, const MatchConfig& config,
+                                   int workers = 1);
+
+// -------------------------------------------------------- reconstruct ----
+DisparityMap fill_scanlines(const DisparityMap& sparse, int workers = 1);
+DisparityMap peek_columns(const DisparityMap& map, int threshold, int workers = 1);
+
+// ------------------------------------------------------------ refocus ----
+struct GaussianKernel {
+    int size = 0;
+    std::vector<double> weights;
+    double at(int i, int j) const {
+        const int h = size / 2;
+        return weights[static_cast<std::size_t>(i + h) * size + (j + h)];
+    }
+};
+
+struct FocusSpec {
+    std::vector<std::pair<int, int>> ranges;
+    double sigma = 2.0;
+};
+
+int default_kernel_size(double sigma);
+GaussianKernel gaussian_kernel(double sigma, int size);
+GrayImage build_blur_map(const DisparityMap& depth, const FocusSpec& focus, int max_disparity);
+RgbImage selective_blur(const RgbImage& image, const GrayImage& blur_map, const GaussianKernel& kernel,
+                        int workers = 1);
+
+// ----------------------------------------------------------- pipeline ----
+struct PipelineConfig {
+    int k = 10;
+    int window = 9;
+    int max_disparity = 16;
+    int threshold = 1;
+    double prune_fraction = 0.04;
+    int workers = 1;
+};
+
+struct StageTimes {
+    double convert = 0.0;
+    double segment = 0.0;
+    double boundary = 0.0;
+    double match = 0.0;
+    double fill = 0.0;
+    double peek = 0.0;
+    double total() const { return convert + segment + boundary + match + fill + peek; }
+};
+
+struct DepthStats {
+    std::uint64_t pixels = 0;
+    std::uint64_t boundary_raw = 0;
+    std::uint64_t boundary_refined = 0;
+    std::uint64_t matched = 0;
+    double matched_fraction = 0.0;
+    double known_fraction = 0.0;
+};
+
+struct DepthResult {
+    GrayImage left_lightness;
+    GrayImage right_lightness;
+    Clustering clustering;
+    LabelMap labels;
+    BoundaryMask boundary_raw;
+    BoundaryMask boundary_refined;
+    BoundaryMask boundary_anchored;
+    DisparityMap sparse;
+    DisparityMap row_filled;
+    DisparityMap dense;
+    DepthStats stats;
+};
+
+struct StereoPair {
+    RgbImage left;
+    RgbImage right;
+};
+
+DepthResult run_depth_pipeline(const RgbImage& left, const RgbImage& right,
+                               const PipelineConfig& config, StageTimes* times = nullptr);
+RgbImage run_refocus_pipeline(const RgbImage& left, const RgbImage& right,
+                              const PipelineConfig& config, const FocusSpec& focus,
+                              int kernel_size = 0, DepthResult* depth_out = nullptr);
+void validate_config(const PipelineConfig& config);
+
+// ------------------------------------------------------ B200 controls ----
+namespace b200 {
+// Device used by this thread's implicit context (default: $STK_DEVICE or 0).
+void set_device(int device);
+// Separable FP32 blur (<= 1 LSB, default on) vs bit-exact FP64 2-D blur.
+void set_fast_blur(bool on);
+bool fast_blur();
+}  // namespace b200
+
+}  // namespace stereotk

@@ -186,6 +186,10 @@ stk_status stk_build_blur_map(stk_ctx* ctx, const int16_t* depth, int w, int h, 
 /* selective_blur (refocus.hpp:50-51) with gaussian_kernel(sigma, size) */
 stk_status stk_selective_blur(stk_ctx* ctx, const uint8_t* rgb, const uint8_t* map, int w, int h,
                               double sigma, int size, int exact, uint8_t* out);
+/* selective_blur with arbitrary size x size weights (refocus.hpp:50-51,
+ * GaussianKernel::weights): bit-exact FP64 2-D kernel, reference order. */
+stk_status stk_selective_blur_weights(stk_ctx* ctx, const uint8_t* rgb, const uint8_t* map, int w,
+                                      int h, const double* weights, int size, uint8_t* out);
 
 /* ----------------------------------------------------------- frames -- */
 /* run_depth_pipeline (focus == NULL) / run_refocus_pipeline

@@ -38,7 +38,7 @@ CU_SOURCES = [
     "k_blur.cu",
     "stk_capi.cu",
 ]
-CXX_SOURCES: list = []  # stereotk_shim.cpp added with the C++ drop-in
+CXX_SOURCES = ["stereotk_shim.cpp"]  # the C++ stereotk:: drop-in over the C-ABI
 HEADERS = ["stk_internal.cuh", "stk_device.cuh"]
 
 

@@ -84,6 +84,7 @@ SIGNATURES = {
     "stk_peek_columns": (I, [VP, VP, I, I, I, VP]),
     "stk_build_blur_map": (I, [VP, VP, I, I, VP, VP, I, I, VP]),
     "stk_selective_blur": (I, [VP, VP, VP, I, I, D, I, I, VP]),
+    "stk_selective_blur_weights": (I, [VP, VP, VP, I, I, VP, I, VP]),
     "stk_run_frame": (I, [VP, VP, VP, I, I, C.POINTER(StkConfig), C.POINTER(StkFocus),
                           C.POINTER(StkFrameOut), C.POINTER(StkStats), C.POINTER(StkTimes)]),
     "stk_frame_submit": (I, [VP, I, VP, VP, I, I, C.POINTER(StkConfig), C.POINTER(StkFocus),

@@ -1,0 +1,371 @@
+// stereotk_shim.cpp -- the reference's stereotk:: C++ API (value types,
+// exceptions) implemented on the C-ABI of stk_b200.h.  One implicit context
+// per host thread (device from stereotk::b200::set_device or $STK_DEVICE).
+// STK_EPARAM becomes stereotk::ParamError with the C-ABI's message (which
+// mirrors the reference's text); any other failure becomes std::runtime_error.
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "stereotk/stereotk_b200.hpp"
+#include "stk_b200.h"
+
+namespace stereotk {
+
+namespace {
+
+struct CtxHolder {
+    stk_ctx* ctx = nullptr;
+    int device = -1;
+    ~CtxHolder() {
+        if (ctx) stk_destroy(ctx);
+    }
+};
+
+thread_local CtxHolder t_ctx;
+thread_local int t_device = -1;
+thread_local bool t_fast_blur = true;
+
+void check(stk_status s, const stk_ctx* ctx) {
+    if (s == STK_OK) return;
+    const std::string msg = stk_last_error(ctx);
+    switch (s) {
+        case STK_EPARAM: throw ParamError(msg);
+        case STK_EIO: throw IoError(msg);
+        case STK_EFORMAT: throw FormatError(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+stk_ctx* ctx() {
+    int dev = t_device;
+    if (dev < 0) {
+        const char* e = std::getenv("STK_DEVICE");
+        dev = e ? std::atoi(e) : 0;
+    }
+    if (!t_ctx.ctx || t_ctx.device != dev) {
+        if (t_ctx.ctx) stk_destroy(t_ctx.ctx);
+        t_ctx.ctx = nullptr;
+        stk_ctx* c = nullptr;
+        check(stk_create(dev, 0, 0, 1, &c), nullptr);
+        t_ctx.ctx = c;
+        t_ctx.device = dev;
+    }
+    return t_ctx.ctx;
+}
+
+void check_workers(int workers) {
+    (void)workers;  // any value: results are identical (parallel.hpp:24-28)
+}
+
+std::string dims(int w, int h) { return std::to_string(w) + "x" + std::to_string(h); }
+
+}  // namespace
+
+namespace b200 {
+void set_device(int device) { t_device = device; }
+void set_fast_blur(bool on) { t_fast_blur = on; }
+bool fast_blur() { return t_fast_blur; }
+}  // namespace b200
+
+GrayImage rgb_to_lightness(const RgbImage& image, int workers) {
+    check_workers(workers);
+    GrayImage out(image.width, image.height);
+    stk_ctx* c = ctx();
+    check(stk_rgb_to_lightness(c, image.data.data(), image.width, image.height, out.data.data()), c);
+    return out;
+}
+
+Histogram build_histogram(const GrayImage& image, int workers) {
+    check_workers(workers);
+    Histogram h;
+    stk_ctx* c = ctx();
+    check(stk_build_histogram(c, image.data.data(), image.width, image.height, h.counts.data()), c);
+    return h;
+}
+
+Clustering kmeans_histogram(const Histogram& histogram, int k, int max_iter, double tol) {
+    Clustering cl;
+    std::vector<double> centers(k > 0 ? k : 1);
+    int iters = 0;
+    stk_ctx* c = ctx();
+    check(stk_kmeans_histogram(c, histogram.counts.data(), k, max_iter, tol, centers.data(),
+                               cl.bin_assignment.data(), &iters),
+          c);
+    centers.resize(k);
+    cl.centers = std::move(centers);
+    cl.iterations_run = iters;
+    return cl;
+}
+
+LabelMap assign_pixels(const GrayImage& image, const Clustering& clustering) {
+    LabelMap out(image.width, image.height);
+    stk_ctx* c = ctx();
+    check(stk_assign_pixels(c, image.data.data(), image.width, image.height,
+                            clustering.bin_assignment.data(), clustering.k(), out.labels.data()),
+          c);
+    return out;
+}
+
+BoundaryMask detect_boundaries(const LabelMap& labels, int workers) {
+    check_workers(workers);
+    BoundaryMask out(labels.width, labels.height);
+    stk_ctx* c = ctx();
+    check(stk_detect_boundaries(c, labels.labels.data(), labels.width, labels.height, out.mask.data()), c);
+    return out;
+}
+
+BoundaryMask morph_fill(const BoundaryMask& mask, int workers) {
+    check_workers(workers);
+    BoundaryMask out(mask.width, mask.height);
+    stk_ctx* c = ctx();
+    check(stk_morph_fill(c, mask.mask.data(), mask.width, mask.height, out.mask.data()), c);
+    return out;
+}
+
+BoundaryMask morph_remove(const BoundaryMask& mask, int workers) {
+    check_workers(workers);
+    BoundaryMask out(mask.width, mask.height);
+    stk_ctx* c = ctx();
+    check(stk_morph_remove(c, mask.mask.data(), mask.width, mask.height, out.mask.data()), c);
+    return out;
+}
+
+ComponentTable label_components(const BoundaryMask& mask) {
+    ComponentTable t;
+    t.width = mask.width;
+    t.height = mask.height;
+    const std::size_t n = mask.mask.size();
+    t.labels.assign(n, -1);
+    std::vector<std::uint32_t> sizes(n ? n : 1);
+    std::vector<std::int32_t> bys(n ? n : 1);
+    int nc = 0;
+    stk_ctx* c = ctx();
+    check(stk_label_components(c, mask.mask.data(), mask.width, mask.height, t.labels.data(),
+                               sizes.data(), bys.data(), sizes.size(), &nc),
+          c);
+    sizes.resize(nc);
+    bys.resize(nc);
+    t.sizes = std::move(sizes);
+    t.by_size = std::move(bys);
+    return t;
+}
+
+BoundaryMask prune_components(const BoundaryMask& mask, double fraction) {
+    BoundaryMask out(mask.width, mask.height);
+    stk_ctx* c = ctx();
+    check(stk_prune_components(c, mask.mask.data(), mask.width, mask.height, fraction, out.mask.data()), c);
+    return out;
+}
+
+BoundaryMask add_border_anchors(const BoundaryMask& mask, int margin) {
+    BoundaryMask out(mask.width, mask.height);
+    stk_ctx* c = ctx();
+    check(stk_add_border_anchors(c, mask.mask.data(), mask.width, mask.height, margin, out.mask.data()),
+          c);
+    return out;
+}
+
+std::uint32_t sad_cost(const GrayImage& left, const GrayImage& right, int x, int y, int d, int window) {
+    std::uint32_t cost = 0;
+    stk_ctx* c = ctx();
+    check(stk_sad_cost(c, left.data.data(), right.data.data(), left.width, left.height, x, y, d, window,
+                       &cost),
+          c);
+    return cost;
+}
+
+DisparityMap match_boundary_pixels(const GrayImage& left, const GrayImage& right,
+                                   const BoundaryMask& mask, const MatchConfig& config, int workers) {
+    check_workers(workers);
+    if (left.width != right.width || left.height != right.height)  // stereo.cpp:36-43
+        throw ParamError("stereo: image sizes differ, left " + dims(left.width, left.height) +
+                         " vs right " + dims(right.width, right.height));
+    if (mask.width != left.width || mask.height != left.height)
+        throw ParamError("stereo: mask size " + dims(mask.width, mask.height) +
+                         " does not match images " + dims(left.width, left.height));
+    DisparityMap out(left.width, left.height);
+    stk_ctx* c = ctx();
+    check(stk_match_boundary_pixels(c, left.data.data(), right.data.data(), mask.mask.data(), left.width,
+                                    left.height, config.window, config.max_disparity, out.values.data()),
+          c);
+    return out;
+}
+
+DisparityMap fill_scanlines(const DisparityMap& sparse, int workers) {
+    check_workers(workers);
+    DisparityMap out(sparse.width, sparse.height);
+    stk_ctx* c = ctx();
+    check(stk_fill_scanlines(c, sparse.values.data(), sparse.width, sparse.height, out.values.data()), c);
+    return out;
+}
+
+DisparityMap peek_columns(const DisparityMap& map, int threshold, int workers) {
+    check_workers(workers);
+    DisparityMap out(map.width, map.height);
+    stk_ctx* c = ctx();
+    check(stk_peek_columns(c, map.values.data(), map.width, map.height, threshold, out.values.data()), c);
+    return out;
+}
+
+int default_kernel_size(double sigma) { return stk_default_kernel_size(sigma); }
+
+GaussianKernel gaussian_kernel(double sigma, int size) {
+    GaussianKernel k;
+    k.size = size;
+    k.weights.assign(size > 0 ? static_cast<std::size_t>(size) * size : 0, 0.0);
+    check(stk_gaussian_kernel(sigma, size, k.weights.data()), nullptr);
+    return k;
+}
+
+GrayImage build_blur_map(const DisparityMap& depth, const FocusSpec& focus, int max_disparity) {
+    std::vector<int> lo, hi;
+    for (const auto& r : focus.ranges) {
+        lo.push_back(r.first);
+        hi.push_back(r.second);
+    }
+    GrayImage out(depth.width, depth.height);
+    stk_ctx* c = ctx();
+    check(stk_build_blur_map(c, depth.values.data(), depth.width, depth.height, lo.data(), hi.data(),
+                             static_cast<int>(lo.size()), max_disparity, out.data.data()),
+          c);
+    return out;
+}
+
+namespace {
+// sigma such that the kernel is exactly gaussian_kernel(sigma, size), or 0
+double gaussian_sigma_of(const GaussianKernel& k) {
+    if (k.size < 3) return 0.0;
+    const int h = k.size / 2;
+    const double r = k.at(0, 1) / k.at(0, 0);
+    if (!(r > 0.0 && r < 1.0)) return 0.0;
+    const double sigma = std::sqrt(-1.0 / (2.0 * std::log(r)));
+    for (double cand : {sigma, std::nextafter(sigma, 0.0), std::nextafter(sigma, 1e300)}) {
+        std::vector<double> w(static_cast<std::size_t>(k.size) * k.size);
+        if (stk_gaussian_kernel(cand, k.size, w.data()) != STK_OK) continue;
+        if (std::memcmp(w.data(), k.weights.data(), w.size() * sizeof(double)) == 0) return cand;
+    }
+    (void)h;
+    return 0.0;
+}
+}  // namespace
+
+RgbImage selective_blur(const RgbImage& image, const GrayImage& blur_map, const GaussianKernel& kernel,
+                        int workers) {
+    check_workers(workers);
+    if (blur_map.width != image.width || blur_map.height != image.height)  // refocus.cpp:77-84
+        throw ParamError("selective_blur: blur map " + dims(blur_map.width, blur_map.height) +
+                         " does not match image " + dims(image.width, image.height));
+    RgbImage out(image.width, image.height);
+    stk_ctx* c = ctx();
+    const double sigma = t_fast_blur ? gaussian_sigma_of(kernel) : 0.0;
+    if (sigma > 0.0)
+        check(stk_selective_blur(c, image.data.data(), blur_map.data.data(), image.width, image.height,
+                                 sigma, kernel.size, 0, out.data.data()),
+              c);
+    else
+        check(stk_selective_blur_weights(c, image.data.data(), blur_map.data.data(), image.width,
+                                         image.height, kernel.weights.data(), kernel.size,
+                                         out.data.data()),
+              c);
+    return out;
+}
+
+void validate_config(const PipelineConfig& config) {
+    const stk_config cfg{config.k, config.window, config.max_disparity, config.threshold,
+                         config.prune_fraction, config.workers};
+    check(stk_validate_config(&cfg), nullptr);
+}
+
+namespace {
+RgbImage run_frame(const RgbImage& left, const RgbImage& right, const PipelineConfig& config,
+                   const FocusSpec* focus, int kernel_size, DepthResult* depth, StageTimes* times) {
+    validate_config(config);
+    if (!left.same_size(right))  // pipeline.cpp:54-60
+        throw ParamError("pipeline: image sizes differ, left " + dims(left.width, left.height) +
+                         " vs right " + dims(right.width, right.height));
+    const int w = left.width, h = left.height;
+    const stk_config cfg{config.k, config.window, config.max_disparity, config.threshold,
+                         config.prune_fraction, config.workers};
+    std::vector<int> lo, hi;
+    stk_focus fo{};
+    if (focus) {
+        for (const auto& r : focus->ranges) {
+            lo.push_back(r.first);
+            hi.push_back(r.second);
+        }
+        fo = stk_focus{lo.data(), hi.data(), static_cast<int>(lo.size()), focus->sigma, kernel_size,
+                       t_fast_blur ? 0 : 1};
+    }
+    RgbImage out;
+    DepthResult local;
+    DepthResult& d = depth ? *depth : local;
+    d.dense = DisparityMap(w, h);
+    stk_frame_out o{};
+    o.dense = d.dense.values.data();
+    if (focus) {
+        out = RgbImage(w, h);
+        o.refocused = out.data.data();
+    }
+    double centers[256];
+    if (depth) {
+        d.left_lightness = GrayImage(w, h);
+        d.right_lightness = GrayImage(w, h);
+        d.labels = LabelMap(w, h);
+        d.boundary_raw = BoundaryMask(w, h);
+        d.boundary_refined = BoundaryMask(w, h);
+        d.boundary_anchored = BoundaryMask(w, h);
+        d.sparse = DisparityMap(w, h);
+        d.row_filled = DisparityMap(w, h);
+        o.left_lightness = d.left_lightness.data.data();
+        o.right_lightness = d.right_lightness.data.data();
+        o.labels = d.labels.labels.data();
+        o.boundary_raw = d.boundary_raw.mask.data();
+        o.boundary_refined = d.boundary_refined.mask.data();
+        o.boundary_anchored = d.boundary_anchored.mask.data();
+        o.sparse = d.sparse.values.data();
+        o.row_filled = d.row_filled.values.data();
+        o.centers = centers;
+        o.bin_assignment = d.clustering.bin_assignment.data();
+    }
+    stk_ctx* c = ctx();
+    stk_stats st{};
+    stk_times tm{};
+    stk_frame_info info{};
+    check(stk_frame_submit(c, 0, left.data.data(), right.data.data(), w, h, &cfg, focus ? &fo : nullptr,
+                           &o, times != nullptr),
+          c);
+    check(stk_frame_wait(c, 0, &st, &tm, &info), c);
+    d.stats = DepthStats{st.pixels, st.boundary_raw, st.boundary_refined, st.matched,
+                         st.matched_fraction, st.known_fraction};
+    if (depth) {
+        d.clustering.centers.assign(centers, centers + info.k);
+        d.clustering.iterations_run = info.iterations_run;
+    }
+    if (times) {
+        times->convert = tm.convert;
+        times->segment = tm.segment;
+        times->boundary = tm.boundary;
+        times->match = tm.match;
+        times->fill = tm.fill;
+        times->peek = tm.peek;
+    }
+    return out;
+}
+}  // namespace
+
+DepthResult run_depth_pipeline(const RgbImage& left, const RgbImage& right, const PipelineConfig& config,
+                               StageTimes* times) {
+    DepthResult d;
+    run_frame(left, right, config, nullptr, 0, &d, times);
+    return d;
+}
+
+RgbImage run_refocus_pipeline(const RgbImage& left, const RgbImage& right, const PipelineConfig& config,
+                              const FocusSpec& focus, int kernel_size, DepthResult* depth_out) {
+    return run_frame(left, right, config, &focus, kernel_size, depth_out, nullptr);
+}
+
+}  // namespace stereotk

@@ -1152,4 +1152,28 @@ stk_status stk_selective_blur(stk_ctx* ctx, const uint8_t* rgb, const uint8_t* m
     FINISH();
 }
 
+stk_status stk_selective_blur_weights(stk_ctx* ctx, const uint8_t* rgb, const uint8_t* map, int w,
+                                      int h, const double* weights, int size, uint8_t* out) {
+    if (size < 1 || size % 2 == 0)
+        return fail(ctx, STK_EPARAM, "selective_blur: kernel size must be odd and positive, got " +
+                                         std::to_string(size));
+    if (blur_smem_bytes(size / 2, true) > 220 * 1024)
+        return fail(ctx, STK_EPARAM, "stk_b200: blur kernel size exceeds the GPU tile limit");
+    STAGE_BEGIN(w, h);
+    if (N == 0) return STK_OK;
+    const int lo0 = 0, hi0 = 0;
+    BlurParams bp{};
+    TRY(upload_focus(ctx, s, &lo0, &hi0, 1, 0, 1.0, size, true, &bp));
+    // replace the Gaussian 2-D weights by the caller's (cache invalidated)
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(s.d_g2, weights, sizeof(double) * (size_t)size * size, cudaMemcpyHostToDevice));
+    s.h_g2.clear();
+    bp.blur_map = s.mraw;
+    CK(cudaMemcpyAsync(s.rgbL, rgb, 3 * N, cudaMemcpyHostToDevice, st));
+    H2D_PLANE(s.mraw, map, 1);
+    launch_blur(f, bp, s.rgbL, s.out_rgb, nullptr, st);
+    CK(cudaMemcpyAsync(out, s.out_rgb, 3 * N, cudaMemcpyDeviceToHost, st));
+    FINISH();
+}
+
 }  // extern "C"
