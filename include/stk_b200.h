@@ -120,7 +120,8 @@ void stk_destroy(stk_ctx* ctx);
 const char* stk_last_error(const stk_ctx* ctx); /* ctx may be NULL (thread-local) */
 const char* stk_status_string(stk_status s);
 int stk_abi_version(void);
-/* 0 = auto, 1 = per-pixel list kernel, 2 = column-sum strip kernel */
+/* 0 = auto (3, else 2, else 1), 1 = per-pixel list kernel, 2 = column-sum strip
+ * kernel, 3 = warp-specialised column-sum kernel (windows 9/15/21/31) */
 stk_status stk_set_sad_kernel(stk_ctx* ctx, int kernel);
 /* 1 = capture each frame's kernels in a CUDA graph and replay (default 1) */
 stk_status stk_set_use_graphs(stk_ctx* ctx, int on);

@@ -34,6 +34,7 @@ CU_SOURCES = [
     "k_ccl.cu",
     "k_sad.cu",
     "k_sad_strip.cu",
+    "k_sad_ws.cu",
     "k_reconstruct.cu",
     "k_blur.cu",
     "stk_capi.cu",

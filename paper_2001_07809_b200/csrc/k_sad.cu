@@ -174,6 +174,7 @@ size_t sad_list_smem_bytes(int window, int D) {
 void launch_sad(const Frame& f, int kernel, const CUtensorMap* tmL, const CUtensorMap* tmR,
                 cudaStream_t st) {
     if (f.N == 0 || f.W < f.window || f.H < f.window) return;
+    if ((kernel == SAD_AUTO || kernel == SAD_WS) && launch_sad_ws(f, st)) return;
     if (kernel != SAD_LIST && launch_sad_strip(f, st)) return;
     const int J = (f.D + 1 + 31) / 32;
     if (J <= 1) run_list<1>(f, tmL, tmR, st);

@@ -37,13 +37,6 @@ struct SG {
     int h, w, D, Q, NCH, NWP, NSEG, SEGW, CW, PART, TH, offL, offR2, LP, RP, NR, CS, R1;
 };
 
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
 
 // |L(c) - R(c-d)| for the 4 disparities of quad q at the MAXC columns of this
 // thread's chunk, for one staged row.  lw / rw point at the 4-byte aligned

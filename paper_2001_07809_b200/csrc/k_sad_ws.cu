@@ -1,0 +1,494 @@
+// K5c sad_ws -- warp-specialised column-sum SAD matching (default SAD kernel).
+//
+// Same arithmetic as K5b (integer sums are associative, so sliding column and
+// window sums give exactly the cost of the reference's per-pixel loop,
+// stereo.cpp:12-28, and therefore the same winner, stereo.cpp:90-97), with
+// the work split into two warp roles that run concurrently inside one CTA
+// instead of alternating behind __syncthreads():
+//
+//   staging   the band's rows of both gray views stream through a ring of RS
+//             row slots with 1-D bulk TMA (cp.async.bulk, UBLKCP) and a full
+//             mbarrier per slot; vertical thread 0 refills a slot as soon as
+//             the EMPTY hand-off below proves every vertical thread is past it.
+//   vertical  (NVW warps) thread = (G disparity quads, K consecutive colsum
+//             columns).  colsum(c, d) = sum over the w window rows of
+//             |L(c) - R(c-d)|, kept in registers as u16x2 words
+//             A = (4q, 4q+1), B = (4q+2, 4q+3).  One VABSDIFF4 of the
+//             replicated L byte against R(c-4q-3 .. c-4q) gives 4 disparities;
+//             each row step adds the entering row and subtracts the leaving
+//             one in a single IADD3 per word.  All byte alignments are
+//             compile-time (K % 4 == 0, strip origin % 16 == 0, WIN fixed), so
+//             every shift/permute has an immediate selector.  The row's
+//             colsums go to shared memory buffer (row & 1).
+//   horizontal (NHW warps) warp = one 32-column segment x 32 quads (HQ = 2,
+//             lane = quad) or x 16 quads x {A, B} (HQ = 1, lane = word).  The
+//             window sum over w colsums slides along x in NPART u16x2 partial
+//             sums that never overflow; at matchable pixels the 2*HQ costs
+//             become keys cost << 10 | d, min'ed in-lane, __reduce_min_sync
+//             across the warp, and one shared atomicMin per warp: strict '<',
+//             ties to the smallest d.  Disparity quads beyond the last full
+//             warp (one quad at D = 16k) are summed directly per matchable
+//             pixel by the lanes of the segment's first warp.
+//
+// Hand-off: named barriers FULL[b] (vertical arrive, horizontal sync) and
+// EMPTY[b] (horizontal arrive, vertical sync) on the double-buffered colsum
+// rows, so row t's horizontal pass overlaps row t+1's vertical pass.  Only
+// pixels whose matchable bit is set (K4g) are evaluated and written.
+#include <type_traits>
+
+#include "stk_device.cuh"
+
+namespace stk {
+
+namespace {
+
+constexpr int kMaxThreads = 512;  // 4 warps per SMSP: 128 registers
+constexpr int kSegW = 32;  // output columns per horizontal segment
+enum { BAR_FULL0 = 1, BAR_FULL1 = 2, BAR_EMPTY0 = 3, BAR_EMPTY1 = 4, BAR_H = 5 };
+
+struct WP {
+    int h, D, Q, QP, NG, NCH, CW, SW, CSW, TH;
+    int NVW, NHW, QMAIN, NSEG;
+    int RS, LP, RP, oL, oRw;  // ring slots, slot bytes, L offset, R word base offset
+    int nthreads;             // 32 * (1 + NVW + NHW)
+};
+
+__device__ __forceinline__ uint32_t lo16(uint32_t v) { return v & 0xffffu; }
+__device__ __forceinline__ uint32_t hi16(uint32_t v) { return v >> 16; }
+
+// Vertical update of the G x K colsum units of one thread for one row pair.
+// INIT: add the new row only.  Rw/Lw: R and L words of the row(s).
+template <int WIN, int G, int K, bool INIT>
+__device__ __forceinline__ void v_rows(const uint32_t* __restrict__ Ln, const uint32_t* __restrict__ Rn,
+                                       const uint32_t* __restrict__ Lo, const uint32_t* __restrict__ Ro,
+                                       uint32_t (&A)[G][K], uint32_t (&B)[G][K]) {
+    constexpr int h = WIN / 2;
+    constexpr int rL = ((-h) % 4 + 4) % 4;        // byte residue of the L column base
+    constexpr int rR = ((1 - h) % 4 + 4) % 4;     // byte residue of the R window base
+    constexpr int NWL = (rL + K - 1) / 4 + 1;
+    constexpr int NWR = (G - 1) + (rR + K - 1) / 4 + 2;
+    uint32_t ln[NWL], rn[NWR], lo[NWL], ro[NWR];
+#pragma unroll
+    for (int i = 0; i < NWL; ++i) ln[i] = Ln[i];
+#pragma unroll
+    for (int i = 0; i < NWR; ++i) rn[i] = Rn[i];
+    if (!INIT) {
+#pragma unroll
+        for (int i = 0; i < NWL; ++i) lo[i] = Lo[i];
+#pragma unroll
+        for (int i = 0; i < NWR; ++i) ro[i] = Ro[i];
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int lb = rL + k;
+        const uint32_t repn = __byte_perm(ln[lb >> 2], 0u, (lb & 3) * 0x1111);
+        uint32_t repo = 0;
+        if (!INIT) repo = __byte_perm(lo[lb >> 2], 0u, (lb & 3) * 0x1111);
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            // R window bytes for (k, quad j): offset o = rR + k - 4j relative to
+            // word index (G-1) of the loaded run
+            const int o = rR + k - 4 * j + 4 * (G - 1);
+            const int wi = o >> 2, sh = o & 3;
+            const uint32_t wn = sh ? __funnelshift_r(rn[wi], rn[wi + 1], sh * 8) : rn[wi];
+            const uint32_t vn = __vabsdiffu4(repn, wn);
+            if (INIT) {
+                A[j][k] += __byte_perm(vn, 0u, 0x4243);
+                B[j][k] += __byte_perm(vn, 0u, 0x4041);
+            } else {
+                const uint32_t wo = sh ? __funnelshift_r(ro[wi], ro[wi + 1], sh * 8) : ro[wi];
+                const uint32_t vo = __vabsdiffu4(repo, wo);
+                A[j][k] = A[j][k] + __byte_perm(vn, 0u, 0x4243) - __byte_perm(vo, 0u, 0x4243);
+                B[j][k] = B[j][k] + __byte_perm(vn, 0u, 0x4041) - __byte_perm(vo, 0u, 0x4041);
+            }
+        }
+    }
+}
+
+// Window sum over colsum columns [a, a+WIN) from the chunk-local prefixes:
+//   P[a+WIN-1] + sum_{c = a/K}^{(a+WIN-1)/K - 1} P[cK+K-1] - (a % K ? P[a-1] : 0).
+// The 2 + NT column offsets of each segment position are precomputed (table
+// `ent`, byte offsets within a quad row); absent terms point at the zeroed
+// column ZC, so the sum is branch-free.  NW u16x2 words (NW == 1: word y if
+// sel_y, else x); lo/hi are the two lanes' exact 32-bit sums.
+template <int WIN, int K>
+struct WinTab {
+    static constexpr int NT = (WIN - 1 + K - 1) / K;  // most chunk totals a window spans
+    static constexpr int NE = (2 + NT + 3) / 4 * 4;   // entry words (uint4 multiple)
+};
+
+template <int WIN, int K, int NW>
+__device__ __forceinline__ void window_sum(const char* __restrict__ cq, const uint32_t* __restrict__ ent,
+                                           bool sel_y, uint32_t (&lo)[NW], uint32_t (&hi)[NW]) {
+    constexpr int NT = WinTab<WIN, K>::NT, NE = WinTab<WIN, K>::NE;
+    uint32_t o[NE];
+#pragma unroll
+    for (int i = 0; i < NE; i += 4) {
+        const uint4 v = *reinterpret_cast<const uint4*>(ent + i);
+        o[i] = v.x, o[i + 1] = v.y, o[i + 2] = v.z, o[i + 3] = v.w;
+    }
+    uint2 t[2 + NT];
+#pragma unroll
+    for (int i = 0; i < 2 + NT; ++i) t[i] = *reinterpret_cast<const uint2*>(cq + o[i]);
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        const bool y = NW == 2 ? w == 1 : sel_y;
+        uint32_t l = 0, hh = 0;
+#pragma unroll
+        for (int i = 0; i < 2 + NT; ++i) {
+            if (i == 1) continue;  // the subtracted term
+            const uint32_t x = y ? t[i].y : t[i].x;
+            l += lo16(x);
+            hh += hi16(x);
+        }
+        const uint32_t xs = y ? t[1].y : t[1].x;
+        lo[w] = l - lo16(xs);
+        hi[w] = hh - hi16(xs);
+    }
+}
+
+template <int WIN, int G, int K, int HQ, int NQB>
+__global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
+    constexpr int h = WIN / 2;
+    static_assert(K * WIN * 255 <= 65535, "chunk prefix must fit a u16 lane");
+    extern __shared__ __align__(128) uint8_t smem[];
+    // layout: cs[2][QP][CSW] uint2 | ring RS x (LP + RP) | full[RS] | best[2][SW] | tab
+    uint2* cs = reinterpret_cast<uint2*>(smem);
+    uint8_t* ring = smem + (size_t)2 * p.QP * p.CSW * sizeof(uint2);
+    uint64_t* fullb = reinterpret_cast<uint64_t*>(ring + (size_t)p.RS * (p.LP + p.RP));
+    uint32_t* best = reinterpret_cast<uint32_t*>(fullb + p.RS);
+    constexpr int NE = WinTab<WIN, K>::NE;
+    uint32_t* tab = best + 2 * p.SW;  // [NSEG][32][NE] byte offsets (16-byte aligned)
+
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+    const int x0 = blockIdx.x * p.SW;
+    const int yb0 = h + blockIdx.y * p.TH;
+    const int yb1 = min(yb0 + p.TH, f.H - h);
+    if (yb0 >= yb1) return;
+    const int T = yb1 - yb0;           // output rows of this band
+    const int NRR = T + WIN - 1;       // raw rows
+    const int ry0 = yb0 - h;
+    const int NVH = 32 * (p.NVW + p.NHW);
+
+    for (int i = tid; i < 2 * p.SW; i += blockDim.x) best[i] = 0xffffffffu;
+    const int ZC = p.NCH * K;  // never written by the vertical warps: the zero term
+    for (int i = tid; i < 2 * p.QP; i += blockDim.x) cs[(size_t)i * p.CSW + ZC] = make_uint2(0u, 0u);
+    if (tid == 0) {
+        for (int s = 0; s < p.RS; ++s) {
+            mbar_init(&fullb[s], 1);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    // ---- row staging (issued by vertical thread 0): image columns
+    // [xsL, xsL + LP) of L and [xsRa, xsRa + RP) of R, clamped to the plane.
+    const int xsL = x0 - h - p.oL;
+    const int xsR = x0 - h - 4 * p.QP + 1;
+    const int xsRa = xsR - (((xsR % 16) + 16) % 16);  // 16-aligned start
+    const int l0 = max(xsL, 0), l1 = min(xsL + p.LP, f.P);
+    const int r0 = max(xsRa, 0), r1 = min(xsRa + p.RP, f.P);
+    const uint32_t bl = l1 > l0 ? (uint32_t)(l1 - l0) : 0u;
+    const uint32_t br = r1 > r0 ? (uint32_t)(r1 - r0) : 0u;
+    auto issue_row = [&](int i) {
+        const int s = i % p.RS;
+        uint8_t* slot = ring + (size_t)s * (p.LP + p.RP);
+        const size_t row = (size_t)(ry0 + i) * f.P;
+        mbar_expect_tx(&fullb[s], bl + br);
+        if (bl) bulk_g2s(slot + (l0 - xsL), f.grayL + row + l0, bl, &fullb[s]);
+        if (br) bulk_g2s(slot + p.LP + (r0 - xsRa), f.grayR + row + r0, br, &fullb[s]);
+    };
+
+    if (wp < p.NVW) {
+        // ------------------------------------------------------- vertical --
+        const int tv = tid;
+        if (tv == 0)
+            for (int i = 0; i < min(p.RS, NRR); ++i) issue_row(i);
+        int issued = min(p.RS, NRR);
+        const int g = tv % p.NG, ch = tv / p.NG;
+        const bool act = ch < p.NCH;
+        constexpr int rL = ((-h) % 4 + 4) % 4;
+        // L: column cc = ch*K + k sits at slot byte cc + oL; word base (ch*K + oL - rL)/4
+        const int lw0 = act ? (ch * K + p.oL - rL) >> 2 : 0;
+        // R: window (cc, q) starts at slot byte cc - 4q + oRw*4 + rR
+        const int rw0 = act ? (ch * K) / 4 - g * G - (G - 1) + p.oRw : 0;
+        uint32_t A[G][K], B[G][K];
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+#pragma unroll
+            for (int k = 0; k < K; ++k) A[j][k] = B[j][k] = 0u;
+        uint2* csq = cs + (size_t)(g * G) * p.CSW + ch * K;
+        const size_t bufstride = (size_t)p.QP * p.CSW;
+        for (int t = 0; t < T; ++t) {
+            if (t == 0) {
+                for (int i = 0; i < WIN; ++i) {
+                    const int s = i % p.RS;
+                    mbar_wait(&fullb[s], (uint32_t)((i / p.RS) & 1));
+                    const uint32_t* Ls = reinterpret_cast<const uint32_t*>(ring + (size_t)s * (p.LP + p.RP));
+                    const uint32_t* Rs = reinterpret_cast<const uint32_t*>(ring + (size_t)s * (p.LP + p.RP) + p.LP);
+                    if (act) v_rows<WIN, G, K, true>(Ls + lw0, Rs + rw0, nullptr, nullptr, A, B);
+                }
+            } else {
+                const int in = t + WIN - 1, io = t - 1;
+                const int sn = in % p.RS, so = io % p.RS;
+                mbar_wait(&fullb[sn], (uint32_t)((in / p.RS) & 1));
+                const uint8_t* bn = ring + (size_t)sn * (p.LP + p.RP);
+                const uint8_t* bo = ring + (size_t)so * (p.LP + p.RP);
+                if (act)
+                    v_rows<WIN, G, K, false>(reinterpret_cast<const uint32_t*>(bn) + lw0,
+                                             reinterpret_cast<const uint32_t*>(bn + p.LP) + rw0,
+                                             reinterpret_cast<const uint32_t*>(bo) + lw0,
+                                             reinterpret_cast<const uint32_t*>(bo + p.LP) + rw0, A, B);
+            }
+            const int b = t & 1;
+            if (t >= 2) {
+                named_sync(BAR_EMPTY0 + b, NVH);
+                // every vertical thread has finished reading rows <= t-1: their
+                // slots take rows up to t-1+RS (async-proxy write after generic reads)
+                if (tv == 0) {
+                    fence_proxy_async();
+                    for (; issued < min(t - 1 + p.RS + 1, NRR); ++issued) issue_row(issued);
+                }
+            }
+            if (act) {
+                uint2* dst = csq + b * bufstride;
+#pragma unroll
+                for (int j = 0; j < G; ++j) {
+                    // chunk-local inclusive prefix of the colsums (K * w * 255 < 2^16)
+                    uint32_t pa = 0, pb = 0;
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        pa += A[j][k];
+                        pb += B[j][k];
+                        dst[(size_t)j * p.CSW + k] = make_uint2(pa, pb);
+                    }
+                }
+            }
+            named_arrive(BAR_FULL0 + b, NVH);
+        }
+        return;
+    }
+
+    // ------------------------------------------------------------ horizontal --
+    // cs holds, per quad and colsum column cc, the inclusive prefix of the
+    // colsums over cc's K-column chunk.  The window [a, a+w) of the pixel at
+    // segment offset i (a = xs0 + i) is
+    //   P[a+w-1] + sum_{c = a/K}^{(a+w-1)/K - 1} P[cK+K-1] - (a % K ? P[a-1] : 0),
+    // every term a u16x2 word below 2^16 per lane; the sum is formed per lane
+    // in 32 bits.  Only matchable pixels are visited.
+    const int seg = wp - p.NVW;
+    const int xs0 = seg * kSegW;       // segment start, relative to x0
+    const bool seg_live = x0 + xs0 < f.W;
+    // lane -> quad of block qb: qb*32 + lane (HQ = 2) or qb*16 + lane%16, word lane/16 (HQ = 1)
+    constexpr int QPB = HQ == 2 ? 32 : 16;  // quads per block
+    const int region = HQ == 2 ? 0 : (lane >> 4);
+    const int qlane = HQ == 2 ? lane : (lane & 15);
+    // fast path: every main disparity <= D and every pixel of the segment has
+    // x - h >= D (no left-edge truncation)
+    const bool fast = (4 * p.QMAIN - 1 <= p.D) && (x0 + xs0 - h >= p.D);
+    const size_t bufstride = (size_t)p.QP * p.CSW;
+    uint32_t* stab = tab + (size_t)seg * 32 * NE;
+    {
+        constexpr int NT = WinTab<WIN, K>::NT;
+        const int a = xs0 + lane, e = a + WIN - 1, ca = a / K, ce = e / K;
+        uint32_t* en = stab + lane * NE;
+        en[0] = (uint32_t)e * 8u;
+        en[1] = (uint32_t)(a % K ? a - 1 : ZC) * 8u;
+#pragma unroll
+        for (int t2 = 0; t2 < NT; ++t2) en[2 + t2] = (uint32_t)(ca + t2 < ce ? (ca + t2) * K + K - 1 : ZC) * 8u;
+#pragma unroll
+        for (int t2 = 2 + NT; t2 < NE; ++t2) en[t2] = 0u;
+        __syncwarp();
+    }
+    const uint32_t* mrow0 = f.mbits + ((x0 + xs0) >> 5);
+    uint32_t m = seg_live ? __ldg(mrow0 + (size_t)yb0 * f.bits_words) : 0u;
+    uint32_t mprev = 0;
+    for (int t = 0; t < T; ++t) {
+        const int b = t & 1, y = yb0 + t;
+        const uint32_t mnext = (seg_live && t + 1 < T) ? __ldg(mrow0 + (size_t)(y + 1) * f.bits_words) : 0u;
+        named_sync(BAR_FULL0 + b, NVH);
+        // results of row t-1 are complete: write and reset them
+        if ((mprev >> lane) & 1u) {
+            uint32_t* bp = best + (b ^ 1) * p.SW + xs0;
+            f.sparse[(size_t)(y - 1) * f.W + x0 + xs0 + lane] = (int16_t)(bp[lane] & 1023u);
+            bp[lane] = 0xffffffffu;
+        }
+        if (m) {
+            const uint2* cb = cs + b * bufstride;
+            uint32_t* bp = best + b * p.SW + xs0;
+            auto pixels = [&](auto fast_tag) {
+                constexpr bool FAST = decltype(fast_tag)::value;
+                // in-lane min key of the main quads at segment position i
+                auto keyof = [&](int i) {
+                    const int lim = min(p.D, x0 + xs0 + i - h);
+                    uint32_t key = 0xffffffffu;
+#pragma unroll
+                    for (int qb = 0; qb < NQB; ++qb) {
+                        const int q = qb * QPB + qlane;
+                        const bool qok = q < p.QMAIN;
+                        const char* cq = reinterpret_cast<const char*>(cb + (size_t)(qok ? q : 0) * p.CSW);
+                        const uint32_t dbase = 4 * q + 2 * region;
+                        uint32_t lo[HQ], hi[HQ];
+                        window_sum<WIN, K, HQ>(cq, stab + i * NE, region != 0, lo, hi);
+#pragma unroll
+                        for (int w = 0; w < HQ; ++w) {
+                            // word w: d = dbase + 2w (lo lane), dbase + 2w + 1 (hi lane)
+                            const uint32_t d0 = dbase + 2 * w;
+                            uint32_t k0 = lo[w] * 1024u + d0, k1 = hi[w] * 1024u + d0 + 1;
+                            if (!FAST) {
+                                if ((int)d0 > lim) k0 = 0xffffffffu;
+                                if ((int)d0 + 1 > lim) k1 = 0xffffffffu;
+                            }
+                            const uint32_t kk = min(k0, k1);
+                            key = qok ? min(key, kk) : key;
+                        }
+                    }
+                    return key;
+                };
+                // two matchable pixels per iteration (independent chains)
+                for (uint32_t mm = m; mm;) {
+                    const int i1 = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    const bool two = mm != 0;
+                    const int i2 = two ? __ffs(mm) - 1 : i1;
+                    mm &= mm - 1;
+                    uint32_t k1 = keyof(i1), k2 = keyof(i2);
+                    k1 = __reduce_min_sync(0xffffffffu, k1);
+                    k2 = __reduce_min_sync(0xffffffffu, k2);
+                    if (lane == 0) {
+                        atomicMin(&bp[i1], k1);
+                        atomicMin(&bp[i2], k2);
+                    }
+                }
+            };
+            if (fast) pixels(std::true_type{});
+            else pixels(std::false_type{});
+            // quads beyond the main warps: lanes = matchable pixels
+            if (p.QMAIN < p.Q) {
+                const int nm = __popc(m);
+                if (lane < nm) {
+                    const int i = __fns(m, 0, lane + 1);
+                    const int a = xs0 + i;
+                    const int lim = min(p.D, x0 + a - h);
+                    uint32_t key = 0xffffffffu;
+                    for (int qx = p.QMAIN; qx < p.Q; ++qx) {
+                        uint32_t lo[2], hi[2];
+                        window_sum<WIN, K, 2>(reinterpret_cast<const char*>(cs + b * bufstride + (size_t)qx * p.CSW),
+                                              stab + i * NE, false, lo, hi);
+                        const uint32_t c[4] = {lo[0], hi[0], lo[1], hi[1]};
+#pragma unroll
+                        for (int jj = 0; jj < 4; ++jj) {
+                            const int d = 4 * qx + jj;
+                            if (d <= lim) key = min(key, c[jj] * 1024u + (uint32_t)d);
+                        }
+                    }
+                    atomicMin(&bp[i], key);
+                }
+            }
+        }
+        if (t + 2 < T) named_arrive(BAR_EMPTY0 + b, NVH);
+        mprev = m;
+        m = mnext;
+    }
+    // last row
+    named_sync(BAR_H, 32 * p.NHW);
+    if ((mprev >> lane) & 1u) {
+        const int y = yb1 - 1, b = (T - 1) & 1;
+        f.sparse[(size_t)y * f.W + x0 + xs0 + lane] = (int16_t)(best[b * p.SW + xs0 + lane] & 1023u);
+    }
+}
+
+template <int WIN, int G, int K, int HQ, int NQB>
+void run_ws(const Frame& f, const WP& p, size_t sm, int bands, cudaStream_t st) {
+    auto kern = k_sad_ws<WIN, G, K, HQ, NQB>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const dim3 grid((f.W + p.SW - 1) / p.SW, bands);
+    kern<<<grid, p.nthreads, sm, st>>>(f, p);
+}
+
+// per-window thread shape: K colsum columns (K * w * 255 < 2^16 for the chunk
+// prefix) x G disparity quads per vertical thread
+template <int WIN>
+struct Shape {
+    static constexpr int K = WIN <= 21 ? 12 : 8;
+    static constexpr int G = WIN <= 21 ? 3 : 4;
+};
+
+template <int WIN>
+void run_win(const Frame& f, const WP& p, int HQ, int NQB, size_t sm, int bands, cudaStream_t st) {
+    constexpr int G = Shape<WIN>::G, K = Shape<WIN>::K;
+    if (HQ == 2) {
+        if (NQB == 1) run_ws<WIN, G, K, 2, 1>(f, p, sm, bands, st);
+        else run_ws<WIN, G, K, 2, 2>(f, p, sm, bands, st);
+    } else {
+        if (NQB == 1) run_ws<WIN, G, K, 1, 1>(f, p, sm, bands, st);
+        else run_ws<WIN, G, K, 1, 2>(f, p, sm, bands, st);
+    }
+}
+
+}  // namespace
+
+bool launch_sad_ws(const Frame& f, cudaStream_t st) {
+    const int w = f.window, h = f.hw, D = f.D;
+    if (!(w == 9 || w == 15 || w == 21 || w == 31)) return false;
+    if (f.W > 65535 || D > 1023 || f.H - 2 * h <= 0) return false;
+    const int G = w <= 21 ? Shape<21>::G : Shape<31>::G;
+    const int K = w <= 21 ? Shape<21>::K : Shape<31>::K;
+    WP p{};
+    p.h = h;
+    p.D = D;
+    p.Q = (D + 1 + 3) / 4;
+    p.QP = (p.Q + G - 1) / G * G;
+    p.NG = p.QP / G;
+    // horizontal lanes: quads (HQ = 2) when there are >= 32 of them, else words
+    const int HQ = p.Q >= 32 ? 2 : 1;
+    const int per_block = HQ == 2 ? 32 : 16;
+    p.QMAIN = std::max(1, p.Q / per_block) * per_block;
+    if (p.QMAIN > p.Q || p.Q - p.QMAIN > 2) p.QMAIN = p.Q;  // partial block, no direct quads
+    const int NQB = (p.QMAIN + per_block - 1) / per_block;
+    if (NQB > 2) return false;
+    // strip width: as wide as shared memory allows (fewer halo columns)
+    const int sms = 148;
+    size_t sm = 0;
+    for (int SW : {256, 128, 64}) {
+        p.SW = SW;
+        p.CW = SW + w - 1;
+        p.NCH = (p.CW + K - 1) / K;
+        p.CSW = ((p.NCH * K + 15) & ~15) + 1;
+        p.NSEG = SW / kSegW;
+        p.NHW = p.NSEG;
+        p.NVW = (p.NG * p.NCH + 31) / 32;
+        p.nthreads = 32 * (p.NVW + p.NHW);
+        p.RS = w + 1 + 4;
+        p.oL = ((-h) % 16 + 16) % 16;
+        p.LP = (p.NCH * K + p.oL + 8 + 15) & ~15;
+        // R slot: image column X sits at X - xsRa; window (cc, q) byte
+        // cc - 4q - 3 + (x0 - h - xsRa) = cc - 4q + 4*QP - 4 + oR, oR = (xsR mod 16)
+        const int oR = ((1 - h - 4 * p.QP) % 16 + 16) % 16;
+        const int rR = ((1 - h) % 4 + 4) % 4;
+        p.oRw = (4 * p.QP - 4 + oR - rR) / 4;
+        p.RP = (p.NCH * K + 4 * p.QP + oR + 16 + 15) & ~15;
+        const int NE = w <= 21 ? (w == 21 ? WinTab<21, 12>::NE : WinTab<15, 12>::NE) : WinTab<31, 8>::NE;
+        sm = (size_t)2 * p.QP * p.CSW * 8 + (size_t)p.RS * (p.LP + p.RP) + p.RS * 8 +
+             2 * SW * 4 + (size_t)p.NSEG * 32 * NE * 4;
+        if (sm <= 220 * 1024 && p.nthreads <= kMaxThreads) break;
+        sm = 0;
+    }
+    if (!sm) return false;
+    const int strips = (f.W + p.SW - 1) / p.SW;
+    const int rows = f.H - 2 * h;
+    // one wave of one CTA per SM when possible; bands of >= 32 rows
+    int bands = std::max(1, sms / strips);
+    bands = std::min(bands, std::max(1, rows / 32));
+    p.TH = (rows + bands - 1) / bands;
+    bands = (rows + p.TH - 1) / p.TH;
+    switch (w) {
+        case 9: run_win<9>(f, p, HQ, NQB, sm, bands, st); break;
+        case 15: run_win<15>(f, p, HQ, NQB, sm, bands, st); break;
+        case 21: run_win<21>(f, p, HQ, NQB, sm, bands, st); break;
+        default: run_win<31>(f, p, HQ, NQB, sm, bands, st); break;
+    }
+    return true;
+}
+
+}  // namespace stk

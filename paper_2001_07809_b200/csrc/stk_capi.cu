@@ -736,7 +736,7 @@ void stk_destroy(stk_ctx* ctx) {
 }
 
 stk_status stk_set_sad_kernel(stk_ctx* ctx, int kernel) {
-    if (!ctx || kernel < 0 || kernel > 2) return fail(ctx, STK_EPARAM, "stk_set_sad_kernel: bad kernel");
+    if (!ctx || kernel < 0 || kernel > 3) return fail(ctx, STK_EPARAM, "stk_set_sad_kernel: bad kernel");
     ctx->sad_kernel = kernel;
     for (Slot& s : ctx->slots) s.gkey = GraphKey{};
     return STK_OK;

@@ -125,10 +125,13 @@ size_t sad_list_smem_bytes(int window, int D);
 size_t blur_smem_bytes(int hw, bool exact);
 void launch_sad_cost(const Frame& f, int x, int y, int d, uint32_t* out, cudaStream_t st);
 
-enum SadKernel { SAD_AUTO = 0, SAD_LIST = 1, SAD_STRIP = 2 };
+enum SadKernel { SAD_AUTO = 0, SAD_LIST = 1, SAD_STRIP = 2, SAD_WS = 3 };
 // K5b column-sum strip kernel; returns false (nothing launched) when the
 // configuration is outside its register/shared-memory envelope.
 bool launch_sad_strip(const Frame& f, cudaStream_t st);
+// K5c warp-specialised column-sum kernel (windows 9/15/21/31); false when
+// outside its envelope.
+bool launch_sad_ws(const Frame& f, cudaStream_t st);
 void launch_sad(const Frame& f, int kernel, const CUtensorMap* tmL, const CUtensorMap* tmR,
                 cudaStream_t st);
 void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStream_t st);

@@ -188,7 +188,7 @@ class Device:
             pass
 
     def set_sad_kernel(self, kernel: str) -> None:
-        _raise(_lib.lib().stk_set_sad_kernel(self.h, {"auto": 0, "list": 1, "strip": 2}[kernel]),
+        _raise(_lib.lib().stk_set_sad_kernel(self.h, {"auto": 0, "list": 1, "strip": 2, "ws": 3}[kernel]),
                self.h)
 
     def set_use_graphs(self, on: bool) -> None:

@@ -120,8 +120,11 @@ def test_pipeline_4k_properties(dev, stk, port, synth):
     a, img = run(stk, dev, l, r, k=K, window=win, D=D, focus=[(64, 128)])
     dev.set_sad_kernel("list")
     b, _ = run(stk, dev, l, r, k=K, window=win, D=D)
+    dev.set_sad_kernel("ws")
+    c_, _ = run(stk, dev, l, r, k=K, window=win, D=D)
     dev.set_sad_kernel("auto")
     eq(a.sparse, b.sparse, "strip vs list")
+    eq(c_.sparse, b.sparse, "ws vs list")
     eq(a.left_lightness, port.lightness(l), "L*")
     eq(a.labels, a.clustering.bin_assignment[a.left_lightness], "labels")
     c, asg, it = port.kmeans(port.histogram(a.left_lightness), K)

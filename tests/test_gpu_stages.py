@@ -176,7 +176,7 @@ def test_anchors(dev, stk, golden, synth):
 
 
 # ----------------------------------------------------------------- K5 -------
-@pytest.fixture(params=["strip", "list"])
+@pytest.fixture(params=["ws", "strip", "list"])
 def sad_dev(request, dev):
     dev.set_sad_kernel(request.param)
     yield dev
@@ -218,6 +218,33 @@ def test_match_random_vs_oracle(sad_dev, stk, port, synth, w, h, win, D, pct):
     m = synth.random_mask(w, h, 7 * w + h, pct)
     eq(stk.match_boundary_pixels(l, r, m, stk.MatchConfig(win, D), device=sad_dev),
        port.match(l, r, m, win, D))
+
+
+@pytest.mark.parametrize("win,D", [(9, 16), (15, 64), (21, 128), (31, 256)])
+def test_match_ws_extremes(dev, stk, port, synth, win, D):
+    """K5c at its four compiled windows on multi-strip, multi-band frames with
+    0/255 pixels (largest possible window sums: the u16x2 partial sums must not
+    overflow) and a dense mask, against the per-pixel list kernel and the oracle."""
+    w, h = 700, 160
+    rng = np.random.default_rng(win * 1000 + D)
+    l = (rng.integers(0, 2, (h, w), dtype=np.uint8) * 255).astype(np.uint8)
+    r = np.roll(l, -3, axis=1)
+    r[rng.random((h, w)) < 0.3] ^= 255
+    m = synth.random_mask(w, h, win + D, 60)
+    dev.set_sad_kernel("ws")
+    a = stk.match_boundary_pixels(l, r, m, stk.MatchConfig(win, D), device=dev)
+    dev.set_sad_kernel("list")
+    b = stk.match_boundary_pixels(l, r, m, stk.MatchConfig(win, D), device=dev)
+    dev.set_sad_kernel("auto")
+    eq(a, b)
+    eq(a, port.match(l, r, m, win, D))
+    full = np.full((60, 400), 255, np.uint8)
+    zero = np.zeros((60, 400), np.uint8)
+    dev.set_sad_kernel("ws")
+    out = stk.match_boundary_pixels(full, zero, np.ones((60, 400), np.uint8), stk.MatchConfig(win, D),
+                                    device=dev)
+    dev.set_sad_kernel("auto")
+    eq(out, port.match(full, zero, np.ones((60, 400), np.uint8), win, D))
 
 
 def test_match_ties_pick_smallest_d(sad_dev, stk, port):
