@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
     uint64_t* fullb = reinterpret_cast<uint64_t*>(ring + (size_t)p.RS * (p.LP + p.RP));
     uint32_t* best = reinterpret_cast<uint32_t*>(fullb + p.RS);
     constexpr int NE = WinTab<WIN, K>::NE;
-    uint32_t* tab = best + 2 * p.SW;  // [NSEG][32][NE] byte offsets (16-byte aligned)
+    uint32_t* tab = best + 2 * p.SW;  // [SW][NE] byte offsets (16-byte aligned)
 
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
     const int x0 = blockIdx.x * p.SW;
@@ -171,7 +171,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
     const int NVH = 32 * (p.NVW + p.NHW);
 
     for (int i = tid; i < 2 * p.SW; i += blockDim.x) best[i] = 0xffffffffu;
-    const int ZC = p.NCH * K;  // never written by the vertical warps: the zero term
+    // colsum column cc lives at slot cc + cc / K (one skew slot per chunk: the
+    // vertical warps' 8-byte stores are bank-conflict free); slot ZC is never
+    // written by them and holds the zero term
+    const int ZC = p.NCH * (K + 1);
     for (int i = tid; i < 2 * p.QP; i += blockDim.x) cs[(size_t)i * p.CSW + ZC] = make_uint2(0u, 0u);
     if (tid == 0) {
         for (int s = 0; s < p.RS; ++s) {
@@ -205,8 +208,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
         if (tv == 0)
             for (int i = 0; i < min(p.RS, NRR); ++i) issue_row(i);
         int issued = min(p.RS, NRR);
-        const int g = tv % p.NG, ch = tv / p.NG;
-        const bool act = ch < p.NCH;
+        const int ch = tv % p.NCH, g = tv / p.NCH;
+        const bool gok = g < p.NG;
+        const bool act = gok;
         constexpr int rL = ((-h) % 4 + 4) % 4;
         // L: column cc = ch*K + k sits at slot byte cc + oL; word base (ch*K + oL - rL)/4
         const int lw0 = act ? (ch * K + p.oL - rL) >> 2 : 0;
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
         for (int j = 0; j < G; ++j)
 #pragma unroll
             for (int k = 0; k < K; ++k) A[j][k] = B[j][k] = 0u;
-        uint2* csq = cs + (size_t)(g * G) * p.CSW + ch * K;
+        uint2* csq = cs + (size_t)(g * G) * p.CSW + ch * (K + 1);
         const size_t bufstride = (size_t)p.QP * p.CSW;
         for (int t = 0; t < T; ++t) {
             if (t == 0) {
@@ -272,55 +276,77 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
     // ------------------------------------------------------------ horizontal --
     // cs holds, per quad and colsum column cc, the inclusive prefix of the
     // colsums over cc's K-column chunk.  The window [a, a+w) of the pixel at
-    // segment offset i (a = xs0 + i) is
+    // strip position x (a = x) is
     //   P[a+w-1] + sum_{c = a/K}^{(a+w-1)/K - 1} P[cK+K-1] - (a % K ? P[a-1] : 0),
     // every term a u16x2 word below 2^16 per lane; the sum is formed per lane
-    // in 32 bits.  Only matchable pixels are visited.
-    const int seg = wp - p.NVW;
-    const int xs0 = seg * kSegW;       // segment start, relative to x0
-    const bool seg_live = x0 + xs0 < f.W;
+    // in 32 bits.  Only matchable pixels are visited.  Work split: horizontal
+    // warp hw owns the 4-column groups g of the strip with g % NHW == hw (row
+    // clusters of boundary pixels spread over all warps); its 32 positions
+    // form one 32-bit mask per row.
+    const int hw = wp - p.NVW;
+    const int htid = tid - 32 * p.NVW;
+    const int NW32 = p.SW / 32;                 // mask words per strip row
+    const int NPW = 8 / p.NHW;                  // nibbles per word per warp (1, 2, 4)
+    const int lnpw = NPW == 1 ? 0 : (NPW == 2 ? 1 : 2);
+    // position (strip column) of bit r of this warp's mask
+    auto pos_of = [&](int r) {
+        const int j = r >> (2 + lnpw), k = (r >> 2) & (NPW - 1);
+        return 32 * j + 4 * (hw + p.NHW * k) + (r & 3);
+    };
+    // warp mask of row y: lane gi < 8 fetches nibble group gi (word gi >> lnpw,
+    // nibble hw + NHW * (gi & (NPW-1))) and the warp OR-reduces the groups
+    const uint32_t* mcol = f.mbits + (x0 >> 5);
+    const int mj = (lane & 7) >> lnpw;
+    const int mshift = 4 * (hw + p.NHW * ((lane & 7) & (NPW - 1)));
+    const bool mload = lane < 8 && x0 + 32 * mj < f.W;
+    auto load_mask = [&](int y) {
+        const uint32_t wd = mload ? __ldg(mcol + (size_t)y * f.bits_words + mj) : 0u;
+        return __reduce_or_sync(0xffffffffu, ((wd >> mshift) & 0xfu) << (4 * (lane & 7)));
+    };
     // lane -> quad of block qb: qb*32 + lane (HQ = 2) or qb*16 + lane%16, word lane/16 (HQ = 1)
     constexpr int QPB = HQ == 2 ? 32 : 16;  // quads per block
     const int region = HQ == 2 ? 0 : (lane >> 4);
     const int qlane = HQ == 2 ? lane : (lane & 15);
-    // fast path: every main disparity <= D and every pixel of the segment has
+    // fast path: every main disparity <= D and every pixel of the strip has
     // x - h >= D (no left-edge truncation)
-    const bool fast = (4 * p.QMAIN - 1 <= p.D) && (x0 + xs0 - h >= p.D);
+    const bool fast = (4 * p.QMAIN - 1 <= p.D) && (x0 - h >= p.D);
     const size_t bufstride = (size_t)p.QP * p.CSW;
-    uint32_t* stab = tab + (size_t)seg * 32 * NE;
     {
         constexpr int NT = WinTab<WIN, K>::NT;
-        const int a = xs0 + lane, e = a + WIN - 1, ca = a / K, ce = e / K;
-        uint32_t* en = stab + lane * NE;
-        en[0] = (uint32_t)e * 8u;
-        en[1] = (uint32_t)(a % K ? a - 1 : ZC) * 8u;
+        for (int a = htid; a < p.SW; a += 32 * p.NHW) {
+            const int e = a + WIN - 1, ca = a / K, ce = e / K;
+            uint32_t* en = tab + a * NE;
+            auto slot = [&](int cc) { return (uint32_t)(cc + cc / K) * 8u; };
+            en[0] = slot(e);
+            en[1] = a % K ? slot(a - 1) : (uint32_t)ZC * 8u;
 #pragma unroll
-        for (int t2 = 0; t2 < NT; ++t2) en[2 + t2] = (uint32_t)(ca + t2 < ce ? (ca + t2) * K + K - 1 : ZC) * 8u;
+            for (int t2 = 0; t2 < NT; ++t2) en[2 + t2] = ca + t2 < ce ? slot((ca + t2) * K + K - 1) : (uint32_t)ZC * 8u;
 #pragma unroll
-        for (int t2 = 2 + NT; t2 < NE; ++t2) en[t2] = 0u;
-        __syncwarp();
+            for (int t2 = 2 + NT; t2 < NE; ++t2) en[t2] = 0u;
+        }
+        named_sync(BAR_H, 32 * p.NHW);
     }
-    const uint32_t* mrow0 = f.mbits + ((x0 + xs0) >> 5);
-    uint32_t m = seg_live ? __ldg(mrow0 + (size_t)yb0 * f.bits_words) : 0u;
+    uint32_t m = load_mask(yb0);
     uint32_t mprev = 0;
     for (int t = 0; t < T; ++t) {
         const int b = t & 1, y = yb0 + t;
-        const uint32_t mnext = (seg_live && t + 1 < T) ? __ldg(mrow0 + (size_t)(y + 1) * f.bits_words) : 0u;
+        const uint32_t mnext = t + 1 < T ? load_mask(y + 1) : 0u;
         named_sync(BAR_FULL0 + b, NVH);
         // results of row t-1 are complete: write and reset them
         if ((mprev >> lane) & 1u) {
-            uint32_t* bp = best + (b ^ 1) * p.SW + xs0;
-            f.sparse[(size_t)(y - 1) * f.W + x0 + xs0 + lane] = (int16_t)(bp[lane] & 1023u);
-            bp[lane] = 0xffffffffu;
+            const int x = pos_of(lane);
+            uint32_t* bp = best + (b ^ 1) * p.SW;
+            f.sparse[(size_t)(y - 1) * f.W + x0 + x] = (int16_t)(bp[x] & 1023u);
+            bp[x] = 0xffffffffu;
         }
         if (m) {
             const uint2* cb = cs + b * bufstride;
-            uint32_t* bp = best + b * p.SW + xs0;
+            uint32_t* bp = best + b * p.SW;
             auto pixels = [&](auto fast_tag) {
                 constexpr bool FAST = decltype(fast_tag)::value;
-                // in-lane min key of the main quads at segment position i
-                auto keyof = [&](int i) {
-                    const int lim = min(p.D, x0 + xs0 + i - h);
+                // in-lane min key of the main quads at strip position x
+                auto keyof = [&](int x) {
+                    const int lim = min(p.D, x0 + x - h);
                     uint32_t key = 0xffffffffu;
 #pragma unroll
                     for (int qb = 0; qb < NQB; ++qb) {
@@ -329,7 +355,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                         const char* cq = reinterpret_cast<const char*>(cb + (size_t)(qok ? q : 0) * p.CSW);
                         const uint32_t dbase = 4 * q + 2 * region;
                         uint32_t lo[HQ], hi[HQ];
-                        window_sum<WIN, K, HQ>(cq, stab + i * NE, region != 0, lo, hi);
+                        window_sum<WIN, K, HQ>(cq, tab + x * NE, region != 0, lo, hi);
 #pragma unroll
                         for (int w = 0; w < HQ; ++w) {
                             // word w: d = dbase + 2w (lo lane), dbase + 2w + 1 (hi lane)
@@ -347,43 +373,38 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                 };
                 // two matchable pixels per iteration (independent chains)
                 for (uint32_t mm = m; mm;) {
-                    const int i1 = __ffs(mm) - 1;
+                    const int x1 = pos_of(__ffs(mm) - 1);
                     mm &= mm - 1;
-                    const bool two = mm != 0;
-                    const int i2 = two ? __ffs(mm) - 1 : i1;
+                    const int x2 = mm ? pos_of(__ffs(mm) - 1) : x1;
                     mm &= mm - 1;
-                    uint32_t k1 = keyof(i1), k2 = keyof(i2);
+                    uint32_t k1 = keyof(x1), k2 = keyof(x2);
                     k1 = __reduce_min_sync(0xffffffffu, k1);
                     k2 = __reduce_min_sync(0xffffffffu, k2);
                     if (lane == 0) {
-                        atomicMin(&bp[i1], k1);
-                        atomicMin(&bp[i2], k2);
+                        atomicMin(&bp[x1], k1);
+                        atomicMin(&bp[x2], k2);
                     }
                 }
             };
             if (fast) pixels(std::true_type{});
             else pixels(std::false_type{});
-            // quads beyond the main warps: lanes = matchable pixels
-            if (p.QMAIN < p.Q) {
-                const int nm = __popc(m);
-                if (lane < nm) {
-                    const int i = __fns(m, 0, lane + 1);
-                    const int a = xs0 + i;
-                    const int lim = min(p.D, x0 + a - h);
-                    uint32_t key = 0xffffffffu;
-                    for (int qx = p.QMAIN; qx < p.Q; ++qx) {
-                        uint32_t lo[2], hi[2];
-                        window_sum<WIN, K, 2>(reinterpret_cast<const char*>(cs + b * bufstride + (size_t)qx * p.CSW),
-                                              stab + i * NE, false, lo, hi);
-                        const uint32_t c[4] = {lo[0], hi[0], lo[1], hi[1]};
+            // quads beyond the main blocks: lane r takes the pixel of mask bit r
+            if (p.QMAIN < p.Q && ((m >> lane) & 1u)) {
+                const int x = pos_of(lane);
+                const int lim = min(p.D, x0 + x - h);
+                uint32_t key = 0xffffffffu;
+                for (int qx = p.QMAIN; qx < p.Q; ++qx) {
+                    uint32_t lo[2], hi[2];
+                    window_sum<WIN, K, 2>(reinterpret_cast<const char*>(cb + (size_t)qx * p.CSW),
+                                          tab + x * NE, false, lo, hi);
+                    const uint32_t c[4] = {lo[0], hi[0], lo[1], hi[1]};
 #pragma unroll
-                        for (int jj = 0; jj < 4; ++jj) {
-                            const int d = 4 * qx + jj;
-                            if (d <= lim) key = min(key, c[jj] * 1024u + (uint32_t)d);
-                        }
+                    for (int jj = 0; jj < 4; ++jj) {
+                        const int d = 4 * qx + jj;
+                        if (d <= lim) key = min(key, c[jj] * 1024u + (uint32_t)d);
                     }
-                    atomicMin(&bp[i], key);
                 }
+                atomicMin(&bp[x], key);
             }
         }
         if (t + 2 < T) named_arrive(BAR_EMPTY0 + b, NVH);
@@ -393,8 +414,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
     // last row
     named_sync(BAR_H, 32 * p.NHW);
     if ((mprev >> lane) & 1u) {
-        const int y = yb1 - 1, b = (T - 1) & 1;
-        f.sparse[(size_t)y * f.W + x0 + xs0 + lane] = (int16_t)(best[b * p.SW + xs0 + lane] & 1023u);
+        const int x = pos_of(lane), y = yb1 - 1, b = (T - 1) & 1;
+        f.sparse[(size_t)y * f.W + x0 + x] = (int16_t)(best[b * p.SW + x] & 1023u);
     }
 }
 
@@ -454,7 +475,28 @@ bool launch_sad_ws(const Frame& f, cudaStream_t st) {
         p.SW = SW;
         p.CW = SW + w - 1;
         p.NCH = (p.CW + K - 1) / K;
-        p.CSW = ((p.NCH * K + 15) & ~15) + 1;
+        // quad row stride: odd (the horizontal lanes = quads hit distinct 8-byte
+        // bank pairs), residue chosen to minimise the vertical warps' 8-byte
+        // store conflicts (a half-warp = 16 lanes per shared-memory wavefront)
+        {
+            const int base = (p.NCH * (K + 1) + 1 + 15) & ~15;
+            int bestc = 1, bestcost = 1 << 30;
+            for (int c = 1; c < 16; c += 2) {
+                int cost = 0;
+                for (int t0 = 0; t0 < p.NG * p.NCH; t0 += 16) {
+                    int cnt[16] = {0};
+                    int mx = 0;
+                    for (int l = t0; l < std::min(t0 + 16, p.NG * p.NCH); ++l) {
+                        const int ch = l % p.NCH, g = l / p.NCH;
+                        const int sl = ((g * G) * (base + c) + ch * (K + 1)) & 15;
+                        mx = std::max(mx, ++cnt[sl]);
+                    }
+                    cost += mx;
+                }
+                if (cost < bestcost) bestcost = cost, bestc = c;
+            }
+            p.CSW = base + bestc;
+        }
         p.NSEG = SW / kSegW;
         p.NHW = p.NSEG;
         p.NVW = (p.NG * p.NCH + 31) / 32;
@@ -470,7 +512,7 @@ bool launch_sad_ws(const Frame& f, cudaStream_t st) {
         p.RP = (p.NCH * K + 4 * p.QP + oR + 16 + 15) & ~15;
         const int NE = w <= 21 ? (w == 21 ? WinTab<21, 12>::NE : WinTab<15, 12>::NE) : WinTab<31, 8>::NE;
         sm = (size_t)2 * p.QP * p.CSW * 8 + (size_t)p.RS * (p.LP + p.RP) + p.RS * 8 +
-             2 * SW * 4 + (size_t)p.NSEG * 32 * NE * 4;
+             2 * SW * 4 + (size_t)SW * NE * 4;
         if (sm <= 220 * 1024 && p.nthreads <= kMaxThreads) break;
         sm = 0;
     }
