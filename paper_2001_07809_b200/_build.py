@@ -32,6 +32,7 @@ CU_SOURCES = [
     "k_kmeans.cu",
     "k_boundary.cu",
     "k_ccl.cu",
+    "k_bnd.cu",
     "k_sad.cu",
     "k_sad_strip.cu",
     "k_sad_ws.cu",

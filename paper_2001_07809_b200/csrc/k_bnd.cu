@@ -1,0 +1,689 @@
+// K3b/K4b -- bit-packed boundary stage of the frame path (reference:
+// boundary.cpp:11-195, pipeline.cpp:87-94).  Every mask is a 32-bit word per
+// 32 pixels of a row (bit x & 31 of word x >> 5), so the morphology is a few
+// word-wide logic ops per 32 pixels and the connected components work on runs
+// instead of pixels: no per-pixel label / parent array is ever written.
+//
+//   B1 morph_bits   gray -> K-Means label bit-planes (on chip, via the LUT) ->
+//                   detect (any Moore neighbour label differs) -> fill ->
+//                   remove, one warp per 30 word-columns x 32 rows, rows
+//                   streamed with a 3-row halo; refined bits + raw/refined
+//                   counts (raw bytes too in full mode).
+//   B2 ccl_runs     warp per 32x32 tile, lane = row: runs are union-find nodes
+//                   (atomicMin unions in shared memory, 8-connectivity); every
+//                   local component goes to the root list with its size and
+//                   its minimum raster index g (par[g] = g, the global
+//                   union-find node); each run records its component's g, and
+//                   the tile's four borders record the g of their pixels.
+//   B3 ccl_borders  warp per tile: top-row pixels unite with the three
+//                   neighbours in the row above (tiles above-left / above /
+//                   above-right), left-column pixels with the left tile
+//                   (lock-free atomicMin union on raster indices).
+//   (K4c compress, shared with the per-stage path: global root = minimum
+//                   raster index of the component = the reference's discovery
+//                   order, sizes summed at the root.)
+//   B5 root_stats   global roots (par[g] == g): size histogram for the prune.
+//   (K4e prune_select: s*, q.)
+//   B7 prune_roots  size < s* -> removed; size == s* -> bit g of a raster
+//                   bitmap; B7b then removes the first q of them in raster
+//                   (= label) order with one ordered scan of the bitmap.
+//   B8 apply_runs   warp per tile: runs -> their root -> removed?  -> pruned
+//                   bits, border anchors, window filter -> matchable bits and
+//                   the frame counts (bytes in full mode).
+//   B9 list_bits    (only for the per-pixel SAD list kernel) ordered
+//                   compaction of the matchable bits.
+#include "stk_device.cuh"
+
+namespace stk {
+
+namespace {
+
+constexpr int CT = 32;         // CCL tile side
+constexpr int kRunCap = 512;   // max runs in a 32x32 tile (16 per row)
+constexpr int MB_ROWS = 32;    // B1 output rows per warp
+constexpr int MB_WPW = 30;     // B1 output words per warp (+1 halo word each side)
+
+__device__ __forceinline__ uint32_t upto_mask(int j) {  // bits 0..j
+    return j >= 31 ? 0xffffffffu : ((2u << j) - 1u);
+}
+
+__device__ __forceinline__ int run_len(uint32_t m, int a) {  // set bits from a upward
+    const uint32_t inv = ~(m >> a);
+    return inv ? __ffs(inv) - 1 : 32 - a;
+}
+
+__device__ __forceinline__ uint32_t bits_to_bytes4(uint32_t nib) {  // 4 bits -> 4 bytes 0/1
+    return (nib * 0x00204081u) & 0x01010101u;
+}
+
+__device__ __forceinline__ void store_bits_as_bytes(uint8_t* dst, uint32_t v) {  // 32 bytes
+    uint4 a, b;
+    a.x = bits_to_bytes4(v & 15u), a.y = bits_to_bytes4((v >> 4) & 15u);
+    a.z = bits_to_bytes4((v >> 8) & 15u), a.w = bits_to_bytes4((v >> 12) & 15u);
+    b.x = bits_to_bytes4((v >> 16) & 15u), b.y = bits_to_bytes4((v >> 20) & 15u);
+    b.z = bits_to_bytes4((v >> 24) & 15u), b.w = bits_to_bytes4(v >> 28);
+    reinterpret_cast<uint4*>(dst)[0] = a;
+    reinterpret_cast<uint4*>(dst)[1] = b;
+}
+
+__device__ __forceinline__ int sfind(volatile int* p, int x) {
+    int q = p[x];
+    while (q != x) {
+        x = q;
+        q = p[x];
+    }
+    return x;
+}
+
+__device__ __forceinline__ void sunite(int* p, int a, int b) {
+    while (true) {
+        a = sfind(p, a);
+        b = sfind(p, b);
+        if (a == b) return;
+        if (a > b) {
+            const int t = a;
+            a = b;
+            b = t;
+        }
+        const int old = atomicMin(&p[b], a);
+        if (old == b) return;
+        b = old;
+    }
+}
+
+__device__ __forceinline__ int gfind(const int* p, int x) {
+    int q = __ldcg(p + x);
+    while (q != x) {
+        x = q;
+        q = __ldcg(p + x);
+    }
+    return x;
+}
+
+__device__ __forceinline__ void gunite(int* p, int a, int b) {
+    while (true) {
+        a = gfind(p, a);
+        b = gfind(p, b);
+        if (a == b) return;
+        if (a > b) {
+            const int t = a;
+            a = b;
+            b = t;
+        }
+        const int old = atomicMin(p + b, a);
+        if (old == b) return;
+        b = old;
+    }
+}
+
+// ------------------------------------------------------------------ B1 ----
+// NPL label bit-planes.  lutp[v] holds bit p of lut[v] at bit 8p (p < 4), so
+// 8 pixels combine with shift-adds into one word whose byte p is plane p's
+// 8 bits; planes 4..7 use lutq the same way.
+template <int NPL>
+__global__ void __launch_bounds__(128) k_morph_bits(Frame f, uint32_t* __restrict__ rbits) {
+    __shared__ uint32_t lutp[256], lutq[256];
+    __shared__ unsigned long long red[2][4];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int v = tid; v < 256; v += blockDim.x) {
+        const uint32_t l = f.sc->lut[v];
+        uint32_t a = 0, b = 0;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            a |= ((l >> p) & 1u) << (8 * p);
+            b |= ((l >> (p + 4)) & 1u) << (8 * p);
+        }
+        lutp[v] = a;
+        lutq[v] = b;
+    }
+    __syncthreads();
+    const int W = f.W, H = f.H, BW = (W + 31) >> 5;
+    const int strips = (BW + MB_WPW - 1) / MB_WPW;
+    const int gw = blockIdx.x * 4 + wid;
+    const int strip = gw % strips, band = gw / strips;
+    const int yb = band * MB_ROWS;
+    unsigned long long n_raw = 0, n_ref = 0;
+    if (yb < H) {
+        const int wc = strip * MB_WPW - 1 + lane;                // this lane's word column
+        const bool out_lane = lane >= 1 && lane <= MB_WPW && wc < BW;
+        const int wcl = min(max(wc, 0), BW - 1);                 // clamped for loads
+        const bool first = wc == 0, last = wc == BW - 1;
+        // bits of this word inside the image
+        const int nvalid = W - 32 * wc;
+        const uint32_t valid = nvalid >= 32 ? 0xffffffffu : (nvalid > 0 ? (1u << nvalid) - 1u : 0u);
+        // interior columns 1..W-2
+        uint32_t icol = valid;
+        if (first) icol &= ~1u;
+        if (nvalid >= 1 && nvalid <= 32) icol &= ~(1u << (nvalid - 1));
+        const int replb = (W - 1) & 31;  // bit of pixel W-1 in the last word
+
+        auto shl = [&](uint32_t v) {  // bit x <- pixel x-1 (replicate at x = 0)
+            const uint32_t l = __shfl_up_sync(0xffffffffu, v, 1);
+            return (v << 1) | (first ? (v & 1u) : (l >> 31));
+        };
+        auto shr = [&](uint32_t v) {  // bit x <- pixel x+1 (replicate at the right edge)
+            const uint32_t r = __shfl_down_sync(0xffffffffu, v, 1);
+            return (v >> 1) | ((last ? (v >> 31) : (r & 1u)) << 31);
+        };
+        auto planes_of = [&](int ri, uint32_t (&pl)[NPL]) {
+            ri = min(max(ri, 0), H - 1);
+            const uint4* src = reinterpret_cast<const uint4*>(f.grayL + (size_t)ri * f.P + 32 * wcl);
+            const uint4 g0 = __ldg(src), g1 = __ldg(src + 1);
+            const uint32_t gw8[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+            for (int p = 0; p < NPL; ++p) pl[p] = 0;
+#pragma unroll
+            for (int oct = 0; oct < 4; ++oct) {
+                uint32_t a = 0, b = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const uint32_t v = (gw8[2 * oct + (i >> 2)] >> (8 * (i & 3))) & 0xffu;
+                    a += lutp[v] << i;
+                    if (NPL > 4) b += lutq[v] << i;
+                }
+#pragma unroll
+                for (int p = 0; p < NPL; ++p) {
+                    const uint32_t byte = p < 4 ? (a >> (8 * p)) & 0xffu : (b >> (8 * (p - 4))) & 0xffu;
+                    pl[p] |= byte << (8 * oct);
+                }
+            }
+            if (last && nvalid < 32) {  // pixels beyond W replicate pixel W-1
+#pragma unroll
+                for (int p = 0; p < NPL; ++p) pl[p] = (pl[p] & valid) | (((pl[p] >> replb) & 1u) ? ~valid : 0u);
+            }
+        };
+        // sliding windows: label planes (3 rows + shifted), raw (3 rows), fill (3 rows)
+        uint32_t P0[NPL], P1[NPL], P2[NPL], L1[NPL], R1[NPL], L0[NPL], R0[NPL], L2[NPL], R2[NPL];
+        uint32_t raw0 = 0, raw1 = 0, raw2 = 0, fil0 = 0, fil1 = 0, fil2 = 0;
+        for (int i = 0; i < MB_ROWS + 6; ++i) {
+            const int ri = yb - 3 + i;
+            // shift the plane window: (P0, P1, P2) = rows ri-2, ri-1, ri
+#pragma unroll
+            for (int p = 0; p < NPL; ++p) {
+                P0[p] = P1[p], L0[p] = L1[p], R0[p] = R1[p];
+                P1[p] = P2[p], L1[p] = L2[p], R1[p] = R2[p];
+            }
+            planes_of(ri, P2);
+#pragma unroll
+            for (int p = 0; p < NPL; ++p) {
+                L2[p] = shl(P2[p]);
+                R2[p] = shr(P2[p]);
+            }
+            if (i < 2) continue;
+            // detect row rd = ri - 1 (planes rows ri-2, ri-1, ri)
+            const int rd = ri - 1;
+            uint32_t diff = 0;
+#pragma unroll
+            for (int p = 0; p < NPL; ++p) {
+                const uint32_t c = P1[p];
+                diff |= (c ^ P0[p]) | (c ^ L0[p]) | (c ^ R0[p]) | (c ^ L1[p]) | (c ^ R1[p]) |
+                        (c ^ P2[p]) | (c ^ L2[p]) | (c ^ R2[p]);
+            }
+            const uint32_t rawn = rd >= 0 && rd < H ? diff & valid : 0u;
+            if (out_lane && rd >= yb && rd < yb + MB_ROWS && rd < H) {
+                n_raw += __popc(rawn);
+                if (f.full) store_bits_as_bytes(f.mraw + (size_t)rd * f.P + 32 * wc, rawn);
+            }
+            raw0 = raw1, raw1 = raw2, raw2 = rawn;  // rows rd-2, rd-1, rd
+            if (i < 4) continue;
+            // fill row rf = rd - 1 (raw rows rd-2, rd-1, rd)
+            const int rf = rd - 1;
+            uint32_t filn = raw1;
+            if (rf >= 1 && rf <= H - 2) {
+                const uint32_t all8 = raw0 & shl(raw0) & shr(raw0) & shl(raw1) & shr(raw1) & raw2 &
+                                      shl(raw2) & shr(raw2);
+                filn |= all8 & icol;
+            }
+            fil0 = fil1, fil1 = fil2, fil2 = filn;  // rows rf-2, rf-1, rf
+            if (i < 6) continue;
+            // remove row rr = rf - 1 (fill rows rf-2, rf-1, rf)
+            const int rr = rf - 1;
+            uint32_t refn = fil1;
+            const uint32_t l4 = shl(fil1), r4 = shr(fil1);
+            if (rr >= 1 && rr <= H - 2) refn &= ~(fil0 & fil2 & l4 & r4 & icol);
+            if (out_lane && rr >= yb && rr < H) {
+                rbits[(size_t)rr * f.bits_words + wc] = refn;
+                n_ref += __popc(refn);
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        n_raw += __shfl_xor_sync(0xffffffffu, n_raw, o);
+        n_ref += __shfl_xor_sync(0xffffffffu, n_ref, o);
+    }
+    if (lane == 0) {
+        red[0][wid] = n_raw;
+        red[1][wid] = n_ref;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const unsigned long long a = red[0][0] + red[0][1] + red[0][2] + red[0][3];
+        const unsigned long long b = red[1][0] + red[1][1] + red[1][2] + red[1][3];
+        if (a) atomicAdd(&f.sc->raw_count, a);
+        if (b) atomicAdd(&f.sc->refined_count, b);
+    }
+}
+
+__device__ __forceinline__ unsigned long long budget_of(const Frame& f) {
+    // boundary.cpp:156: fraction * double(mask.count()); integer sizes compare
+    // <= budget  <=>  <= floor(budget)
+    return (unsigned long long)floor(__dmul_rn(f.frac, (double)f.sc->refined_count));
+}
+
+// ------------------------------------------------------------------ B2 ----
+// bord layout per tile: [top 32][bottom 32][left 32][right 32] root g or -1.
+__global__ void __launch_bounds__(128) k_ccl_runs(Frame f, const uint32_t* __restrict__ rbits,
+                                                  int32_t* __restrict__ runroot,
+                                                  int32_t* __restrict__ bord) {
+    __shared__ int sp[4][CT * CT];
+    __shared__ int ssz[4][CT * CT];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    {   // zero the size-histogram bins the prune will use (0..B+1)
+        const unsigned long long B = budget_of(f);
+        const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+        const long long stride = (long long)gridDim.x * blockDim.x;
+        for (long long s = gt; s <= (long long)B + 1; s += stride) f.szhist[s] = 0;
+        if (gt == 0) f.sc->budget = B;
+    }
+    const int TXc = (f.W + CT - 1) / CT, TYc = (f.H + CT - 1) / CT;
+    const int tile = blockIdx.x * 4 + wid;
+    if (tile >= TXc * TYc) return;
+    const int tx = tile % TXc, x0 = tx * CT, y0 = (tile / TXc) * CT;
+    int* p = sp[wid];
+    int* sz = ssz[wid];
+    const uint32_t m = y0 + lane < f.H ? __ldg(rbits + (size_t)(y0 + lane) * f.bits_words + tx) : 0u;
+    const uint32_t s = m & ~(m << 1);  // run starts
+    for (uint32_t t = s; t; t &= t - 1) {
+        const int node = lane * 32 + __ffs(t) - 1;
+        p[node] = node;
+        sz[node] = 0;
+    }
+    __syncwarp();
+    uint32_t mu = __shfl_up_sync(0xffffffffu, m, 1), su = __shfl_up_sync(0xffffffffu, s, 1);
+    if (lane == 0) mu = su = 0;
+    for (uint32_t t = s; t; t &= t - 1) {
+        const int a = __ffs(t) - 1;
+        const int b = a + run_len(m, a) - 1;
+        const int lo = a > 0 ? a - 1 : 0, hi = b < 31 ? b + 1 : 31;
+        uint32_t T = mu & upto_mask(hi) & ~((1u << lo) - 1u);
+        while (T) {
+            const int j = __ffs(T) - 1;
+            const int sa = 31 - __clz(su & upto_mask(j));
+            sunite(p, lane * 32 + a, (lane - 1) * 32 + sa);
+            const int e = sa + run_len(mu, sa) - 1;
+            T &= e >= 31 ? 0u : ~upto_mask(e);
+        }
+    }
+    __syncwarp();
+    int nroots = 0;
+    for (uint32_t t = s; t; t &= t - 1) {
+        const int a = __ffs(t) - 1, node = lane * 32 + a;
+        const int r = sfind(p, node);
+        p[node] = r;
+        atomicAdd(&sz[r], run_len(m, a));
+        nroots += r == node;
+    }
+    __syncwarp();
+    // local roots -> list (unordered) with their sizes; par[g] = g, cnt[g] = 0
+    int incl = nroots;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    unsigned base = 0;
+    if (lane == 31 && incl) base = atomicAdd(&f.sc->n_lroots, (unsigned)incl);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    unsigned pos = base + incl - nroots;
+    uint32_t* lr_idx = f.list;
+    uint32_t* lr_size = reinterpret_cast<uint32_t*>(f.rank);
+    auto gof = [&](int node) { return (y0 + (node >> 5)) * f.W + x0 + (node & 31); };
+    for (uint32_t t = s; t; t &= t - 1) {
+        const int node = lane * 32 + __ffs(t) - 1;
+        if (p[node] == node) {
+            const int g = gof(node);
+            lr_idx[pos] = (uint32_t)g;
+            lr_size[pos] = (uint32_t)sz[node];
+            f.par[g] = g;
+            f.cnt[g] = 0;
+            ++pos;
+        }
+    }
+    // runs -> root g, in (row, start) order
+    const int nr = __popc(s);
+    int rinc = nr;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, rinc, o);
+        if (lane >= o) rinc += v;
+    }
+    int ridx = rinc - nr;
+    int32_t* rr = runroot + (size_t)tile * kRunCap;
+    for (uint32_t t = s; t; t &= t - 1) rr[ridx++] = gof(p[lane * 32 + __ffs(t) - 1]);
+    // borders: root g of every set pixel (-1 when unset)
+    int32_t* bd = bord + (size_t)tile * 128;
+    auto root_at = [&](int row, int col) {  // pixel (row, col) of the tile, set
+        const uint32_t mr = __shfl_sync(0xffffffffu, m, row), sr = __shfl_sync(0xffffffffu, s, row);
+        const bool on = (mr >> col) & 1u;
+        const int st = on ? 31 - __clz(sr & upto_mask(col)) : 0;
+        return on ? gof(p[row * 32 + st]) : -1;
+    };
+    bd[lane] = root_at(0, lane);
+    bd[32 + lane] = root_at(31, lane);
+    const bool lon = m & 1u, ron = (m >> 31) & 1u;
+    bd[64 + lane] = lon ? gof(p[lane * 32]) : -1;  // column 0: run starting at 0
+    bd[96 + lane] = ron ? gof(p[lane * 32 + (31 - __clz(s))]) : -1;  // column 31: last run
+}
+
+// ------------------------------------------------------------------ B3 ----
+__global__ void __launch_bounds__(128) k_ccl_borders(Frame f, const int32_t* __restrict__ bord) {
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int TXc = (f.W + CT - 1) / CT, TYc = (f.H + CT - 1) / CT;
+    const int tile = blockIdx.x * 4 + wid;
+    if (tile >= TXc * TYc) return;
+    const int tx = tile % TXc, ty = tile / TXc;
+    const int32_t* bd = bord + (size_t)tile * 128;
+    if (ty > 0) {
+        const int a = bd[lane];  // top row pixel x0 + lane
+        if (a >= 0) {
+            const int32_t* up = bord + (size_t)(tile - TXc) * 128 + 32;  // bottom row above
+            const int u0 = lane > 0 ? up[lane - 1]
+                                    : (tx > 0 ? bord[(size_t)(tile - TXc - 1) * 128 + 32 + 31] : -1);
+            const int u1 = up[lane];
+            const int u2 = lane < 31 ? up[lane + 1]
+                                     : (tx + 1 < TXc ? bord[(size_t)(tile - TXc + 1) * 128 + 32] : -1);
+            if (u0 >= 0) gunite(f.par, a, u0);
+            if (u1 >= 0) gunite(f.par, a, u1);
+            if (u2 >= 0) gunite(f.par, a, u2);
+        }
+    }
+    if (tx > 0) {
+        const int a = bd[64 + lane];  // left column pixel y0 + lane
+        if (a >= 0) {
+            const int32_t* lf = bord + (size_t)(tile - 1) * 128 + 96;  // right column, left tile
+            const int l0 = lane > 0 ? lf[lane - 1] : -1;  // y-1 across the tile top: done above
+            const int l1 = lf[lane];
+            const int l2 = lane < 31 ? lf[lane + 1] : -1;  // y+1 below: done by the tile below-left
+            if (l0 >= 0) gunite(f.par, a, l0);
+            if (l1 >= 0) gunite(f.par, a, l1);
+            if (l2 >= 0) gunite(f.par, a, l2);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ B5 ----
+__global__ void __launch_bounds__(256) k_root_stats(Frame f) {
+    const unsigned n = f.sc->n_lroots;
+    const unsigned long long B = f.sc->budget;
+    const uint32_t* lr_idx = f.list;
+    unsigned nr = 0;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int g = (int)lr_idx[i];
+        if (__ldcg(f.par + g) == g) {
+            ++nr;
+            const uint32_t sz = __ldcg(f.cnt + g);
+            if (sz <= B + 1) atomicAdd(f.szhist + sz, 1u);
+        }
+    }
+    nr = __reduce_add_sync(0xffffffffu, nr);
+    if ((threadIdx.x & 31) == 0 && nr) atomicAdd(&f.sc->n_roots, nr);
+}
+
+// ------------------------------------------------------------------ B7 ----
+__global__ void __launch_bounds__(256) k_prune_roots(Frame f, uint32_t* __restrict__ sbits) {
+    const unsigned n = f.sc->n_lroots;
+    const unsigned long long sst = f.sc->s_star, q = f.sc->q;
+    const uint32_t* lr_idx = f.list;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int g = (int)lr_idx[i];
+        if (__ldcg(f.par + g) != g) continue;
+        const uint32_t sz = __ldcg(f.cnt + g);
+        if (sz < sst) f.cnt[g] = sz | kRemoved;
+        else if (sz == sst && q > 0) atomicOr(sbits + (g >> 5), 1u << (g & 31));
+    }
+}
+
+// first q set bits of sbits in raster order -> removed.  Chunks of 1024 words
+// claimed in order; decoupled look-back on the per-chunk popcounts.
+__global__ void __launch_bounds__(256) k_prune_first_q(Frame f, const uint32_t* __restrict__ sbits,
+                                                       int nwords) {
+    __shared__ uint32_t s_chunk, s_excl;
+    __shared__ uint32_t wcount[8];
+    const unsigned long long q = f.sc->q;
+    if (q == 0) return;
+    unsigned long long* status = f.lb + LB_RANK * f.lb_stride;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    while (true) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_chunk = atomicAdd(&f.sc->ctr[LB_RANK], 1u);
+        __syncthreads();
+        const int c = (int)s_chunk;
+        if (c * 1024 >= nwords) return;
+        uint32_t w[4], cnt = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int idx = c * 1024 + wid * 128 + j * 32 + lane;
+            w[j] = idx < nwords ? __ldcg(sbits + idx) : 0u;
+            cnt += __popc(w[j]);
+        }
+        // per-lane exclusive prefix within the warp, warp totals across the block
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) wcount[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            const uint32_t agg = __reduce_add_sync(0xffffffffu, lane < 8 ? wcount[lane] : 0u);
+            const uint32_t excl = lb_exclusive_warp(status, c, agg);
+            if (lane == 0) s_excl = excl;
+        }
+        __syncthreads();
+        // words are j-major (index c*1024 + wid*128 + j*32 + lane): rank the
+        // bits in raster order with one lane scan per j
+        uint32_t run = s_excl;
+        for (int i = 0; i < wid; ++i) run += wcount[i];
+        if (run >= q) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t cj = __popc(w[j]);
+            uint32_t inc2 = cj;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, inc2, o);
+                if (lane >= o) inc2 += v;
+            }
+            uint32_t rk = run + inc2 - cj;
+            const int base = (c * 1024 + wid * 128 + j * 32 + lane) * 32;
+            for (uint32_t t = w[j]; t && rk < q; t &= t - 1, ++rk) {
+                const int g = base + __ffs(t) - 1;
+                f.cnt[g] |= kRemoved;
+            }
+            run += __shfl_sync(0xffffffffu, inc2, 31);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ B8 ----
+__global__ void __launch_bounds__(128) k_apply_runs(Frame f, const uint32_t* __restrict__ rbits,
+                                                    const int32_t* __restrict__ runroot, int anchors) {
+    __shared__ unsigned long long red[3][4];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int TXc = (f.W + CT - 1) / CT, TYc = (f.H + CT - 1) / CT;
+    const int tile = blockIdx.x * 4 + wid;
+    unsigned long long kept = 0, matched = 0, ops = 0;
+    if (tile < TXc * TYc) {
+        const int tx = tile % TXc, x0 = tx * CT, y0 = (tile / TXc) * CT;
+        const int y = y0 + lane;
+        const bool rowok = y < f.H;
+        const uint32_t m = rowok ? __ldg(rbits + (size_t)y * f.bits_words + tx) : 0u;
+        const uint32_t s = m & ~(m << 1);
+        const int nr = __popc(s);
+        int rinc = nr;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, rinc, o);
+            if (lane >= o) rinc += v;
+        }
+        const int32_t* rr = runroot + (size_t)tile * kRunCap + (rinc - nr);
+        uint32_t pruned = 0;
+        int k = 0;
+        for (uint32_t t = s; t; t &= t - 1, ++k) {
+            const int a = __ffs(t) - 1, len = run_len(m, a);
+            const int g = __ldg(rr + k);
+            const int r = __ldcg(f.par + g);
+            if (!(__ldcg(f.cnt + r) & kRemoved))
+                pruned |= (len >= 32 ? 0xffffffffu : ((1u << len) - 1u)) << a;
+        }
+        const int mg = f.hw, W = f.W, H = f.H;
+        uint32_t anc = pruned;
+        if (anchors && rowok && y >= mg && y <= H - 1 - mg) {
+            if (mg >= x0 && mg < x0 + 32) anc |= 1u << (mg - x0);
+            const int xr = W - 1 - mg;
+            if (xr >= x0 && xr < x0 + 32) anc |= 1u << (xr - x0);
+        }
+        // matchable: anchored and the window fits (h <= x < W-h, h <= y < H-h)
+        uint32_t mat = 0;
+        if (rowok && y >= mg && y < H - mg) {
+            const int lo = max(mg - x0, 0), hi = min(W - mg - x0, 32);  // [lo, hi)
+            if (hi > lo) {
+                const uint32_t win = (hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
+                mat = anc & win;
+            }
+        }
+        if (rowok) {
+            f.mbits[(size_t)y * f.bits_words + tx] = mat;
+            if (tx == TXc - 1)  // row-tile padding words read by the strip SAD kernel
+                for (int wd = tx + 1; wd < f.bits_words; ++wd) f.mbits[(size_t)y * f.bits_words + wd] = 0u;
+            if (f.mprn) {
+                store_bits_as_bytes(f.mprn + (size_t)y * f.P + x0, pruned);
+                store_bits_as_bytes(f.manc + (size_t)y * f.P + x0, anc);
+            }
+        }
+        kept = __popc(pruned);
+        matched = __popc(mat);
+        if (mat) {
+            // sum over matchable pixels of min(D, x - h) + 1
+            if (x0 - mg >= f.D) {
+                ops = (unsigned long long)matched * (f.D + 1);
+            } else {
+                for (uint32_t t = mat; t; t &= t - 1) ops += min(f.D, x0 + __ffs(t) - 1 - mg) + 1;
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        kept += __shfl_xor_sync(0xffffffffu, kept, o);
+        matched += __shfl_xor_sync(0xffffffffu, matched, o);
+        ops += __shfl_xor_sync(0xffffffffu, ops, o);
+    }
+    if (lane == 0) {
+        red[0][wid] = kept;
+        red[1][wid] = matched;
+        red[2][wid] = ops;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long a = red[0][0] + red[0][1] + red[0][2] + red[0][3];
+        const unsigned long long b = red[1][0] + red[1][1] + red[1][2] + red[1][3];
+        const unsigned long long c = red[2][0] + red[2][1] + red[2][2] + red[2][3];
+        if (a) atomicAdd(&f.sc->pruned_count, a);
+        if (b) {
+            atomicAdd(&f.sc->matched, b);
+            atomicAdd(&f.sc->n_list, (unsigned)b);
+        }
+        if (c) atomicAdd(&f.sc->sad_ops, c * (unsigned long long)(f.window * f.window));
+    }
+}
+
+// ------------------------------------------------------------------ B9 ----
+// Raster-ordered list of matchable pixels + per-row-tile offsets from the
+// matchable bits (the per-pixel list SAD kernel's input).  Chunk = 32 row-tiles
+// of 128 pixels = 128 words; single-pass decoupled look-back.
+__global__ void __launch_bounds__(128) k_list_bits(Frame f) {
+    __shared__ uint32_t s_chunk, s_excl;
+    __shared__ uint32_t wcount[4];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long* status = f.lb + LB_LIST * f.lb_stride;
+    if (threadIdx.x == 0) s_chunk = atomicAdd(&f.sc->ctr[LB_LIST], 1u);
+    __syncthreads();
+    const int c = (int)s_chunk;
+    // thread -> one row-tile (4 words) of the chunk
+    const int t = c * kTilesPerChunk + threadIdx.x;
+    const bool tv = threadIdx.x < kTilesPerChunk && t < f.n_tiles;
+    uint32_t w[4] = {0, 0, 0, 0}, cnt = 0;
+    int y = 0, seg = 0;
+    if (tv) {
+        y = t / f.TX, seg = t % f.TX;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            w[j] = f.mbits[(size_t)y * f.bits_words + seg * 4 + j];
+            cnt += __popc(w[j]);
+        }
+    }
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) wcount[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t agg = __reduce_add_sync(0xffffffffu, lane < 4 ? wcount[lane] : 0u);
+        const uint32_t excl = lb_exclusive_warp(status, c, agg);
+        if (lane == 0) {
+            s_excl = excl;
+            if (c == f.n_chunks - 1) f.tile_off[f.n_tiles] = excl + agg;
+        }
+    }
+    __syncthreads();
+    if (!tv) return;
+    uint32_t pos = s_excl + incl - cnt;
+    for (int i = 0; i < wid; ++i) pos += wcount[i];
+    f.tile_off[t] = pos;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        for (uint32_t b = w[j]; b; b &= b - 1) {
+            const int x = seg * kRowTile + j * 32 + __ffs(b) - 1;
+            f.list[pos++] = ((uint32_t)y << 16) | (uint32_t)x;
+        }
+}
+
+}  // namespace
+
+void launch_boundary_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
+                          uint32_t* sbits, int sbits_words, bool anchors, bool want_list,
+                          cudaStream_t st) {
+    if (f.N == 0) return;
+    // B1
+    const int BW = (f.W + 31) / 32;
+    const int strips = (BW + MB_WPW - 1) / MB_WPW, bands = (f.H + MB_ROWS - 1) / MB_ROWS;
+    const int warps = strips * bands;
+    int npl = 1;
+    while ((1 << npl) < f.kcfg && npl < 8) ++npl;
+    const int gb = (warps + 3) / 4;
+    switch (npl) {
+        case 1: k_morph_bits<1><<<gb, 128, 0, st>>>(f, rbits); break;
+        case 2: k_morph_bits<2><<<gb, 128, 0, st>>>(f, rbits); break;
+        case 3: k_morph_bits<3><<<gb, 128, 0, st>>>(f, rbits); break;
+        case 4: k_morph_bits<4><<<gb, 128, 0, st>>>(f, rbits); break;
+        default: k_morph_bits<8><<<gb, 128, 0, st>>>(f, rbits); break;
+    }
+    // B2, B3
+    const int ntiles = ((f.W + CT - 1) / CT) * ((f.H + CT - 1) / CT);
+    const int tb = (ntiles + 3) / 4;
+    k_ccl_runs<<<tb, 128, 0, st>>>(f, rbits, runroot, bord);
+    k_ccl_borders<<<tb, 128, 0, st>>>(f, bord);
+    launch_ccl_compress(f, st);
+    k_root_stats<<<148 * 4, 256, 0, st>>>(f);
+    launch_prune_select(f, st);
+    cudaMemsetAsync(sbits, 0, (size_t)sbits_words * 4, st);
+    k_prune_roots<<<148 * 4, 256, 0, st>>>(f, sbits);
+    k_prune_first_q<<<148 * 2, 256, 0, st>>>(f, sbits, sbits_words);
+    k_apply_runs<<<tb, 128, 0, st>>>(f, rbits, runroot, anchors ? 1 : 0);
+    if (want_list) k_list_bits<<<f.n_chunks, 128, 0, st>>>(f);
+}
+
+}  // namespace stk

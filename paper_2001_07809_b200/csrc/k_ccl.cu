@@ -594,6 +594,16 @@ void launch_ccl(const Frame& f, cudaStream_t st) {
     k_ccl_roots<<<f.n_chunks, 256, 0, st>>>(f, f.full);
 }
 
+void launch_ccl_compress(const Frame& f, cudaStream_t st) {
+    if (f.N == 0) return;
+    k_ccl_compress<<<148 * 8, 256, 0, st>>>(f);
+}
+
+void launch_prune_select(const Frame& f, cudaStream_t st) {
+    if (f.N == 0) return;
+    k_prune_select<<<1, 1024, 0, st>>>(f);
+}
+
 void launch_prune(const Frame& f, bool anchors, cudaStream_t st) {
     if (f.N == 0) return;
     k_prune_select<<<1, 1024, 0, st>>>(f);

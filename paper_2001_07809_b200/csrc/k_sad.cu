@@ -171,6 +171,13 @@ size_t sad_list_smem_bytes(int window, int D) {
            (size_t)window * (nbR * kBox + 16);
 }
 
+bool sad_uses_list(const Frame& f, int kernel) {
+    if (f.N == 0 || f.W < f.window || f.H < f.window) return false;
+    if ((kernel == SAD_AUTO || kernel == SAD_WS) && launch_sad_ws(f, nullptr, true)) return false;
+    if (kernel != SAD_LIST && launch_sad_strip(f, nullptr, true)) return false;
+    return true;
+}
+
 void launch_sad(const Frame& f, int kernel, const CUtensorMap* tmL, const CUtensorMap* tmR,
                 cudaStream_t st) {
     if (f.N == 0 || f.W < f.window || f.H < f.window) return;

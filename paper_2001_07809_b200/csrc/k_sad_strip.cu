@@ -299,7 +299,7 @@ void run_np(const Frame& f, const SG& g, int npart, size_t sm, cudaStream_t st) 
 
 }  // namespace
 
-bool launch_sad_strip(const Frame& f, cudaStream_t st) {
+bool launch_sad_strip(const Frame& f, cudaStream_t st, bool dry) {
     SG g{};
     g.h = f.hw;
     g.w = f.window;
@@ -345,6 +345,7 @@ bool launch_sad_strip(const Frame& f, cudaStream_t st) {
     g.NR = g.TH + 2 * g.h;
     const size_t sm = (size_t)g.NR * (g.LP + g.RP) + (size_t)(g.R1 + g.Q * g.CS) * 4;
     if (sm > 220 * 1024) return false;
+    if (dry) return true;
     switch (maxc) {
         case 4: run_np<4>(f, g, npart, sm, st); break;
         case 8: run_np<8>(f, g, npart, sm, st); break;

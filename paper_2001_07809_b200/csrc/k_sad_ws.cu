@@ -449,7 +449,7 @@ void run_win(const Frame& f, const WP& p, int HQ, int NQB, size_t sm, int bands,
 
 }  // namespace
 
-bool launch_sad_ws(const Frame& f, cudaStream_t st) {
+bool launch_sad_ws(const Frame& f, cudaStream_t st, bool dry) {
     const int w = f.window, h = f.hw, D = f.D;
     if (!(w == 9 || w == 15 || w == 21 || w == 31)) return false;
     if (f.W > 65535 || D > 1023 || f.H - 2 * h <= 0) return false;
@@ -524,6 +524,7 @@ bool launch_sad_ws(const Frame& f, cudaStream_t st) {
     bands = std::min(bands, std::max(1, rows / 32));
     p.TH = (rows + bands - 1) / bands;
     bands = (rows + p.TH - 1) / p.TH;
+    if (dry) return true;
     switch (w) {
         case 9: run_win<9>(f, p, HQ, NQB, sm, bands, st); break;
         case 15: run_win<15>(f, p, HQ, NQB, sm, bands, st); break;

@@ -64,6 +64,9 @@ struct Slot {
     unsigned long long* lb;
     int lb_stride = 0;
     int16_t *sparse, *rowf, *dense;
+    uint32_t *rbits, *sbits;  // refined bits, size-s* root bitmap (k_bnd.cu)
+    int32_t *runroot, *bord;  // per-run component root, tile border roots
+    int sbits_words = 0;
     DevScalars* sc = nullptr;
     DevScalars* h_sc = nullptr;  // pinned mirror
     // focus tables
@@ -185,7 +188,7 @@ struct Layout {
 enum {
     L_RGBL, L_RGBR, L_OUT, L_GRAYL, L_GRAYR, L_MRAW, L_MREF, L_MPRN, L_MANC, L_LAB16, L_SCR16,
     L_MBITS, L_PAR, L_CNT, L_RANK, L_SZH, L_ROOTS, L_LIST, L_TOFF, L_LB, L_SPARSE, L_ROWF,
-    L_DENSE, L_SC, L_COUNT
+    L_DENSE, L_SC, L_RBITS, L_RUNR, L_BORD, L_SBITS, L_COUNT
 };
 
 Layout layout_for(int W, int H, int* P_out, int* lb_stride_out) {
@@ -208,6 +211,11 @@ Layout layout_for(int W, int H, int* P_out, int* lb_stride_out) {
     sz[L_LB] = 8 * (size_t)LB_COUNT * lb_stride + 64;
     sz[L_SPARSE] = sz[L_ROWF] = sz[L_DENSE] = 2 * N + 64;
     sz[L_SC] = sizeof(DevScalars);
+    // bit-packed boundary stage (k_bnd.cu)
+    const size_t ctiles = (size_t)((W + 31) / 32) * ((H + 31) / 32);
+    sz[L_RBITS] = sz[L_SBITS] = (size_t)H * TX * 4 * 4 + 64;
+    sz[L_RUNR] = ctiles * 512 * 4 + 64;
+    sz[L_BORD] = ctiles * 128 * 4 + 64;
     Layout L;
     size_t o = 0;
     for (int i = 0; i < L_COUNT; ++i) {
@@ -262,6 +270,11 @@ stk_status ensure_slot(stk_ctx* ctx, Slot& s, int W, int H) {
     s.rowf = (int16_t*)(b + L.off[L_ROWF]);
     s.dense = (int16_t*)(b + L.off[L_DENSE]);
     s.sc = (DevScalars*)(b + L.off[L_SC]);
+    s.rbits = (uint32_t*)(b + L.off[L_RBITS]);
+    s.sbits = (uint32_t*)(b + L.off[L_SBITS]);
+    s.runroot = (int32_t*)(b + L.off[L_RUNR]);
+    s.bord = (int32_t*)(b + L.off[L_BORD]);
+    s.sbits_words = (int)(((size_t)W * H + 31) / 32);
     if (s.gexec) {
         cudaGraphExecDestroy(s.gexec);
         s.gexec = nullptr;
@@ -474,10 +487,11 @@ int enqueue_kernels(stk_ctx* ctx, Slot& s, const Frame& f, const BlurParams* bp,
         ++n;
     }
     rec(2);
-    launch_morph(f, MORPH_FUSED, &s.tm_morph.map, f.full ? f.mraw : nullptr, f.mref, st);
-    launch_ccl(f, st);
-    launch_prune(f, true, st);
-    n += 8;
+    // sparse starts all Unknown; the SAD kernels write the matchable pixels
+    cudaMemsetAsync(f.sparse, 0xff, (size_t)f.N * sizeof(int16_t), st);
+    const bool want_list = sad_uses_list(f, ctx->sad_kernel);
+    launch_boundary_bits(f, s.rbits, s.runroot, s.bord, s.sbits, s.sbits_words, true, want_list, st);
+    n += 9 + (want_list ? 1 : 0);
     rec(3);
     if (f.W >= f.window && f.H >= f.window) {
         launch_sad(f, ctx->sad_kernel, &s.tm_sadL.map, &s.tm_sadR.map, st);

@@ -115,6 +115,16 @@ void launch_morph(const Frame& f, int mode, const CUtensorMap* tmap, uint8_t* ou
                   uint8_t* out_b, cudaStream_t st);
 
 void launch_ccl(const Frame& f, cudaStream_t st);                 // K4a-c (+ roots, hist)
+void launch_ccl_compress(const Frame& f, cudaStream_t st);        // K4c alone
+void launch_prune_select(const Frame& f, cudaStream_t st);        // K4e alone
+// Bit-packed boundary stage of the frame path (k_bnd.cu): morphology from
+// gray, run-based CCL, prune, anchors, matchable bits and frame counts
+// (+ raw / pruned / anchored bytes in full mode; + the SAD list if asked).
+void launch_boundary_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
+                          uint32_t* sbits, int sbits_words, bool anchors, bool want_list,
+                          cudaStream_t st);
+// true when launch_sad will run the per-pixel list kernel (it needs f.list)
+bool sad_uses_list(const Frame& f, int kernel);
 void launch_prune(const Frame& f, bool anchors, cudaStream_t st); // K4e-g
 void launch_apply(const Frame& f, bool use_prune, bool anchors, cudaStream_t st);
 void launch_count_mask(const Frame& f, const uint8_t* mask, cudaStream_t st);
@@ -128,10 +138,10 @@ void launch_sad_cost(const Frame& f, int x, int y, int d, uint32_t* out, cudaStr
 enum SadKernel { SAD_AUTO = 0, SAD_LIST = 1, SAD_STRIP = 2, SAD_WS = 3 };
 // K5b column-sum strip kernel; returns false (nothing launched) when the
 // configuration is outside its register/shared-memory envelope.
-bool launch_sad_strip(const Frame& f, cudaStream_t st);
+bool launch_sad_strip(const Frame& f, cudaStream_t st, bool dry = false);
 // K5c warp-specialised column-sum kernel (windows 9/15/21/31); false when
 // outside its envelope.
-bool launch_sad_ws(const Frame& f, cudaStream_t st);
+bool launch_sad_ws(const Frame& f, cudaStream_t st, bool dry = false);
 void launch_sad(const Frame& f, int kernel, const CUtensorMap* tmL, const CUtensorMap* tmR,
                 cudaStream_t st);
 void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStream_t st);
