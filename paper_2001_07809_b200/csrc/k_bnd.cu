@@ -91,11 +91,13 @@ __device__ __forceinline__ void sunite(int* p, int a, int b) {
     }
 }
 
-__device__ __forceinline__ int gfind(const int* p, int x) {
+__device__ __forceinline__ int gfind(int* p, int x) {  // path halving
     int q = __ldcg(p + x);
     while (q != x) {
+        const int g = __ldcg(p + q);
+        if (g != q) p[x] = g;
         x = q;
-        q = __ldcg(p + x);
+        q = g;
     }
     return x;
 }
@@ -271,12 +273,48 @@ __device__ __forceinline__ unsigned long long budget_of(const Frame& f) {
 }
 
 // ------------------------------------------------------------------ B2 ----
+// Runs are numbered in (row, start) order within the tile (ridx); lanes work
+// on runs ridx = lane, lane + 32, ... so the union-find phases stay converged.
 // bord layout per tile: [top 32][bottom 32][left 32][right 32] root g or -1.
+struct RunSmem {
+    uint32_t rowm[CT], rows[CT];   // row masks, run starts
+    int rs[CT + 1];                // first ridx of each row
+    uint8_t rstart[kRunCap], rlen[kRunCap], rrow[kRunCap];
+    int par[kRunCap];
+    int sz[kRunCap];
+};
+
+__device__ __forceinline__ int rfind(int* p, int x) {  // with path halving
+    int q = p[x];
+    while (q != x) {
+        const int g = p[q];
+        if (g != q) p[x] = g;
+        x = q;
+        q = g;
+    }
+    return x;
+}
+
+__device__ __forceinline__ void runite(int* p, int a, int b) {
+    while (true) {
+        a = rfind(p, a);
+        b = rfind(p, b);
+        if (a == b) return;
+        if (a > b) {
+            const int t = a;
+            a = b;
+            b = t;
+        }
+        const int old = atomicMin(&p[b], a);
+        if (old == b) return;
+        b = old;
+    }
+}
+
 __global__ void __launch_bounds__(128) k_ccl_runs(Frame f, const uint32_t* __restrict__ rbits,
                                                   int32_t* __restrict__ runroot,
                                                   int32_t* __restrict__ bord) {
-    __shared__ int sp[4][CT * CT];
-    __shared__ int ssz[4][CT * CT];
+    __shared__ RunSmem sm_[4];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     {   // zero the size-histogram bins the prune will use (0..B+1)
         const unsigned long long B = budget_of(f);
@@ -288,43 +326,66 @@ __global__ void __launch_bounds__(128) k_ccl_runs(Frame f, const uint32_t* __res
     const int TXc = (f.W + CT - 1) / CT, TYc = (f.H + CT - 1) / CT;
     const int tile = blockIdx.x * 4 + wid;
     if (tile >= TXc * TYc) return;
+    RunSmem& S = sm_[wid];
     const int tx = tile % TXc, x0 = tx * CT, y0 = (tile / TXc) * CT;
-    int* p = sp[wid];
-    int* sz = ssz[wid];
     const uint32_t m = y0 + lane < f.H ? __ldg(rbits + (size_t)(y0 + lane) * f.bits_words + tx) : 0u;
     const uint32_t s = m & ~(m << 1);  // run starts
-    for (uint32_t t = s; t; t &= t - 1) {
-        const int node = lane * 32 + __ffs(t) - 1;
-        p[node] = node;
-        sz[node] = 0;
+    const int nr = __popc(s);
+    int rinc = nr;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, rinc, o);
+        if (lane >= o) rinc += v;
+    }
+    const int nruns = __shfl_sync(0xffffffffu, rinc, 31);
+    S.rowm[lane] = m;
+    S.rows[lane] = s;
+    S.rs[lane] = rinc - nr;
+    if (lane == 31) S.rs[CT] = rinc;
+    {
+        int k = rinc - nr;
+        for (uint32_t t = s; t; t &= t - 1, ++k) {
+            const int a = __ffs(t) - 1;
+            S.rstart[k] = (uint8_t)a;
+            S.rlen[k] = (uint8_t)run_len(m, a);
+            S.rrow[k] = (uint8_t)lane;
+        }
+    }
+    for (int i = lane; i < nruns; i += 32) {
+        S.par[i] = i;
+        S.sz[i] = 0;
     }
     __syncwarp();
-    uint32_t mu = __shfl_up_sync(0xffffffffu, m, 1), su = __shfl_up_sync(0xffffffffu, s, 1);
-    if (lane == 0) mu = su = 0;
-    for (uint32_t t = s; t; t &= t - 1) {
-        const int a = __ffs(t) - 1;
-        const int b = a + run_len(m, a) - 1;
+    // unions with the overlapping runs of the row above (8-connectivity)
+    for (int i = lane; i < nruns; i += 32) {
+        const int r = S.rrow[i];
+        if (r == 0) continue;
+        const int a = S.rstart[i], b = a + S.rlen[i] - 1;
         const int lo = a > 0 ? a - 1 : 0, hi = b < 31 ? b + 1 : 31;
+        const uint32_t mu = S.rowm[r - 1], su = S.rows[r - 1];
         uint32_t T = mu & upto_mask(hi) & ~((1u << lo) - 1u);
         while (T) {
             const int j = __ffs(T) - 1;
-            const int sa = 31 - __clz(su & upto_mask(j));
-            sunite(p, lane * 32 + a, (lane - 1) * 32 + sa);
+            const uint32_t below = su & upto_mask(j);
+            const int sa = 31 - __clz(below);
+            runite(S.par, i, S.rs[r - 1] + __popc(below) - 1);
             const int e = sa + run_len(mu, sa) - 1;
             T &= e >= 31 ? 0u : ~upto_mask(e);
         }
     }
     __syncwarp();
+    // flatten, sizes at the local roots
     int nroots = 0;
-    for (uint32_t t = s; t; t &= t - 1) {
-        const int a = __ffs(t) - 1, node = lane * 32 + a;
-        const int r = sfind(p, node);
-        p[node] = r;
-        atomicAdd(&sz[r], run_len(m, a));
-        nroots += r == node;
+    for (int i = lane; i < nruns; i += 32) {
+        const int rt = rfind(S.par, i);
+        S.par[i] = rt;
+        atomicAdd(&S.sz[rt], (int)S.rlen[i]);
+        nroots += rt == i;
     }
     __syncwarp();
-    // local roots -> list (unordered) with their sizes; par[g] = g, cnt[g] = 0
+    // local roots -> list (unordered) with sizes; par[g] = g, cnt[g] = 0.  The
+    // root run is the component's first run in (row, start) order, so its
+    // start is the component's minimum raster index g.
     int incl = nroots;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -337,45 +398,36 @@ __global__ void __launch_bounds__(128) k_ccl_runs(Frame f, const uint32_t* __res
     unsigned pos = base + incl - nroots;
     uint32_t* lr_idx = f.list;
     uint32_t* lr_size = reinterpret_cast<uint32_t*>(f.rank);
-    auto gof = [&](int node) { return (y0 + (node >> 5)) * f.W + x0 + (node & 31); };
-    for (uint32_t t = s; t; t &= t - 1) {
-        const int node = lane * 32 + __ffs(t) - 1;
-        if (p[node] == node) {
-            const int g = gof(node);
+    auto gof = [&](int ri) { return (y0 + S.rrow[ri]) * f.W + x0 + S.rstart[ri]; };
+    int32_t* rr = runroot + (size_t)tile * kRunCap;
+    for (int i = lane; i < nruns; i += 32) {
+        const int rt = S.par[i];
+        const int g = gof(rt);
+        rr[i] = g;
+        if (rt == i) {
             lr_idx[pos] = (uint32_t)g;
-            lr_size[pos] = (uint32_t)sz[node];
+            lr_size[pos] = (uint32_t)S.sz[i];
             f.par[g] = g;
             f.cnt[g] = 0;
             ++pos;
         }
     }
-    // runs -> root g, in (row, start) order
-    const int nr = __popc(s);
-    int rinc = nr;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, rinc, o);
-        if (lane >= o) rinc += v;
-    }
-    int ridx = rinc - nr;
-    int32_t* rr = runroot + (size_t)tile * kRunCap;
-    for (uint32_t t = s; t; t &= t - 1) rr[ridx++] = gof(p[lane * 32 + __ffs(t) - 1]);
     // borders: root g of every set pixel (-1 when unset)
     int32_t* bd = bord + (size_t)tile * 128;
-    auto root_at = [&](int row, int col) {  // pixel (row, col) of the tile, set
-        const uint32_t mr = __shfl_sync(0xffffffffu, m, row), sr = __shfl_sync(0xffffffffu, s, row);
-        const bool on = (mr >> col) & 1u;
-        const int st = on ? 31 - __clz(sr & upto_mask(col)) : 0;
-        return on ? gof(p[row * 32 + st]) : -1;
-    };
-    bd[lane] = root_at(0, lane);
-    bd[32 + lane] = root_at(31, lane);
-    const bool lon = m & 1u, ron = (m >> 31) & 1u;
-    bd[64 + lane] = lon ? gof(p[lane * 32]) : -1;  // column 0: run starting at 0
-    bd[96 + lane] = ron ? gof(p[lane * 32 + (31 - __clz(s))]) : -1;  // column 31: last run
+    {
+        const uint32_t m0 = S.rowm[0], s0 = S.rows[0];
+        const uint32_t m31 = S.rowm[31], s31 = S.rows[31];
+        bd[lane] = (m0 >> lane) & 1u ? gof(S.par[__popc(s0 & upto_mask(lane)) - 1]) : -1;
+        bd[32 + lane] = (m31 >> lane) & 1u ? gof(S.par[S.rs[31] + __popc(s31 & upto_mask(lane)) - 1]) : -1;
+        bd[64 + lane] = m & 1u ? gof(S.par[rinc - nr]) : -1;
+        bd[96 + lane] = (m >> 31) & 1u ? gof(S.par[rinc - 1]) : -1;
+    }
 }
 
 // ------------------------------------------------------------------ B3 ----
+// A lane whose predecessor has the same root and is a neighbour of the same
+// pixels only adds the one new neighbour: redundant unions of long border runs
+// (which serialise on one root's atomicMin) are skipped.
 __global__ void __launch_bounds__(128) k_ccl_borders(Frame f, const int32_t* __restrict__ bord) {
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int TXc = (f.W + CT - 1) / CT, TYc = (f.H + CT - 1) / CT;
@@ -385,6 +437,7 @@ __global__ void __launch_bounds__(128) k_ccl_borders(Frame f, const int32_t* __r
     const int32_t* bd = bord + (size_t)tile * 128;
     if (ty > 0) {
         const int a = bd[lane];  // top row pixel x0 + lane
+        const int ap = __shfl_up_sync(0xffffffffu, a, 1);
         if (a >= 0) {
             const int32_t* up = bord + (size_t)(tile - TXc) * 128 + 32;  // bottom row above
             const int u0 = lane > 0 ? up[lane - 1]
@@ -392,21 +445,24 @@ __global__ void __launch_bounds__(128) k_ccl_borders(Frame f, const int32_t* __r
             const int u1 = up[lane];
             const int u2 = lane < 31 ? up[lane + 1]
                                      : (tx + 1 < TXc ? bord[(size_t)(tile - TXc + 1) * 128 + 32] : -1);
-            if (u0 >= 0) gunite(f.par, a, u0);
-            if (u1 >= 0) gunite(f.par, a, u1);
-            if (u2 >= 0) gunite(f.par, a, u2);
+            const bool cont = lane > 0 && ap == a;  // u0, u1 were the predecessor's u1, u2
+            if (!cont && u0 >= 0) gunite(f.par, a, u0);
+            if (!cont && u1 >= 0 && u1 != u0) gunite(f.par, a, u1);
+            if (u2 >= 0 && u2 != u1) gunite(f.par, a, u2);
         }
     }
     if (tx > 0) {
         const int a = bd[64 + lane];  // left column pixel y0 + lane
+        const int ap = __shfl_up_sync(0xffffffffu, a, 1);
         if (a >= 0) {
             const int32_t* lf = bord + (size_t)(tile - 1) * 128 + 96;  // right column, left tile
             const int l0 = lane > 0 ? lf[lane - 1] : -1;  // y-1 across the tile top: done above
             const int l1 = lf[lane];
             const int l2 = lane < 31 ? lf[lane + 1] : -1;  // y+1 below: done by the tile below-left
-            if (l0 >= 0) gunite(f.par, a, l0);
-            if (l1 >= 0) gunite(f.par, a, l1);
-            if (l2 >= 0) gunite(f.par, a, l2);
+            const bool cont = lane > 0 && ap == a;
+            if (!cont && l0 >= 0) gunite(f.par, a, l0);
+            if (!cont && l1 >= 0 && l1 != l0) gunite(f.par, a, l1);
+            if (l2 >= 0 && l2 != l1) gunite(f.par, a, l2);
         }
     }
 }
