@@ -9,22 +9,23 @@
 //                   remove, one warp per 30 word-columns x 32 rows, rows
 //                   streamed with a 3-row halo; refined bits + raw/refined
 //                   counts (raw bytes too in full mode).
-//   B2 ccl_runs     warp per 32x32 tile, lane = row: runs are union-find nodes
-//                   (atomicMin unions in shared memory, 8-connectivity); every
-//                   local component goes to the root list with its size and
-//                   its minimum raster index g (par[g] = g, the global
-//                   union-find node); each run records its component's g, and
-//                   the tile's four borders record the g of their pixels.
-//   B3 ccl_borders  warp per tile: top-row pixels unite with the three
-//                   neighbours in the row above (tiles above-left / above /
-//                   above-right), left-column pixels with the left tile
-//                   (lock-free atomicMin union on raster indices).
-//   (K4c compress, shared with the per-stage path: global root = minimum
-//                   raster index of the component = the reference's discovery
-//                   order, sizes summed at the root.)
+//   B2 ccl_region   CTA per 128x64 region, warp per 32x32 tile: run-level
+//                   union-find per tile, then the region's inner tile borders
+//                   merged in shared memory; every region component goes to
+//                   the root list with its size and its minimum raster index g
+//                   (par[g] = g, the global union-find node); each run records
+//                   its component's g, the region's outer borders the g of
+//                   their pixels.
+//   B3 ccl_borders  CTA per region: top-border pixels unite with their three
+//                   neighbours in the regions above, left-border pixels with
+//                   the left region (lock-free union, hash-priority linking,
+//                   path halving).
+//   B4 compress     region roots (dense ids) -> global root; size and minimum
+//                   raster index (the reference's discovery order) summed /
+//                   min'ed at the global root.
 //   B5 root_stats   global roots (par[g] == g): size histogram for the prune.
 //   (K4e prune_select: s*, q.)
-//   B7 prune_roots  size < s* -> removed; size == s* -> bit g of a raster
+//   B7 prune_roots  size < s* -> removed; size == s* -> bit minkey of a raster
 //                   bitmap; B7b then removes the first q of them in raster
 //                   (= label) order with one ordered scan of the bitmap.
 //   B8 apply_runs   warp per tile: runs -> their root -> removed?  -> pruned
@@ -66,31 +67,6 @@ __device__ __forceinline__ void store_bits_as_bytes(uint8_t* dst, uint32_t v) { 
     reinterpret_cast<uint4*>(dst)[1] = b;
 }
 
-__device__ __forceinline__ int sfind(volatile int* p, int x) {
-    int q = p[x];
-    while (q != x) {
-        x = q;
-        q = p[x];
-    }
-    return x;
-}
-
-__device__ __forceinline__ void sunite(int* p, int a, int b) {
-    while (true) {
-        a = sfind(p, a);
-        b = sfind(p, b);
-        if (a == b) return;
-        if (a > b) {
-            const int t = a;
-            a = b;
-            b = t;
-        }
-        const int old = atomicMin(&p[b], a);
-        if (old == b) return;
-        b = old;
-    }
-}
-
 __device__ __forceinline__ int gfind(int* p, int x) {  // path halving
     int q = __ldcg(p + x);
     while (q != x) {
@@ -102,19 +78,30 @@ __device__ __forceinline__ int gfind(int* p, int x) {  // path halving
     return x;
 }
 
+// Global union-find over region roots: link by a hash priority of the node
+// (random-permutation order keeps the trees O(log n) deep even for one giant
+// component); the component's minimum raster index is tracked separately
+// (minkey) because the reference's label order needs it, not the root.
+__device__ __forceinline__ uint32_t prio(int x) {
+    uint32_t h = (uint32_t)x * 0x9E3779B1u;  // odd multiplier and xor-shift: bijective
+    h ^= h >> 15;
+    h *= 0x85EBCA77u;
+    h ^= h >> 13;
+    return h;
+}
+
 __device__ __forceinline__ void gunite(int* p, int a, int b) {
     while (true) {
         a = gfind(p, a);
         b = gfind(p, b);
         if (a == b) return;
-        if (a > b) {
+        if (prio(a) < prio(b)) {
             const int t = a;
             a = b;
             b = t;
         }
-        const int old = atomicMin(p + b, a);
-        if (old == b) return;
-        b = old;
+        // link b (lower priority) under a, if b is still a root
+        if (atomicCAS(p + b, b, a) == b) return;
     }
 }
 
@@ -273,15 +260,29 @@ __device__ __forceinline__ unsigned long long budget_of(const Frame& f) {
 }
 
 // ------------------------------------------------------------------ B2 ----
-// Runs are numbered in (row, start) order within the tile (ridx); lanes work
-// on runs ridx = lane, lane + 32, ... so the union-find phases stay converged.
-// bord layout per tile: [top 32][bottom 32][left 32][right 32] root g or -1.
+// One CTA per region of RGX x RGY tiles (one warp per 32x32 tile).
+//  1. tile-local CCL: runs are numbered in (row, start) order (ridx); lanes
+//     work on runs ridx = lane, lane + 32, ... so the union-find phases stay
+//     converged; 8-connected unions with the overlapping runs of the row
+//     above; min-linking makes a component's root its first run, i.e. its
+//     minimum raster index.
+//  2. region merge in shared memory: node = warp * kRunCap + ridx; the tiles'
+//     inner borders are united, and every region component gets the minimum
+//     raster index g of its tile components (its key) and their size sum.
+//  3. region components -> root list (g, size), par[g] = g; every run records
+//     its component's g; the region's outer borders record the g of their
+//     pixels for the global merge (B3).
+constexpr int RGX = 4, RGY = 2, NRW = RGX * RGY;  // 128 x 64-pixel regions
+constexpr int RW = RGX * CT, RH = RGY * CT;
+constexpr int RBORD = 2 * RW + 2 * RH;             // [top RW][bottom RW][left RH][right RH]
+
 struct RunSmem {
     uint32_t rowm[CT], rows[CT];   // row masks, run starts
     int rs[CT + 1];                // first ridx of each row
     uint8_t rstart[kRunCap], rlen[kRunCap], rrow[kRunCap];
-    int par[kRunCap];
+    int par[kRunCap];              // region node ids after step 1
     int sz[kRunCap];
+    int key[kRunCap];              // g of tile-local roots, INT_MAX otherwise
 };
 
 __device__ __forceinline__ int rfind(int* p, int x) {  // with path halving
@@ -311,10 +312,48 @@ __device__ __forceinline__ void runite(int* p, int a, int b) {
     }
 }
 
-__global__ void __launch_bounds__(128) k_ccl_runs(Frame f, const uint32_t* __restrict__ rbits,
-                                                  int32_t* __restrict__ runroot,
-                                                  int32_t* __restrict__ bord) {
-    __shared__ RunSmem sm_[4];
+// region-wide union-find over nodes w * kRunCap + ridx
+__device__ __forceinline__ int* cpar(RunSmem* R, int node) { return &R[node / kRunCap].par[node % kRunCap]; }
+
+__device__ __forceinline__ int cfind(RunSmem* R, int x) {
+    int q = *cpar(R, x);
+    while (q != x) {
+        const int g = *cpar(R, q);
+        if (g != q) *cpar(R, x) = g;
+        x = q;
+        q = g;
+    }
+    return x;
+}
+
+__device__ __forceinline__ void cunite(RunSmem* R, int a, int b) {
+    while (true) {
+        a = cfind(R, a);
+        b = cfind(R, b);
+        if (a == b) return;
+        if (a > b) {
+            const int t = a;
+            a = b;
+            b = t;
+        }
+        const int old = atomicMin(cpar(R, b), a);
+        if (old == b) return;
+        b = old;
+    }
+}
+
+// region node of pixel (row, col) of warp w's tile, -1 when unset
+__device__ __forceinline__ int node_at(const RunSmem* R, int w, int row, int col) {
+    const RunSmem& S = R[w];
+    if (!((S.rowm[row] >> col) & 1u)) return -1;
+    return w * kRunCap + S.rs[row] + __popc(S.rows[row] & upto_mask(col)) - 1;
+}
+
+__global__ void __launch_bounds__(32 * NRW) k_ccl_region(Frame f, const uint32_t* __restrict__ rbits,
+                                                         int32_t* __restrict__ runroot,
+                                                         int32_t* __restrict__ bord) {
+    extern __shared__ __align__(16) uint8_t smraw[];
+    RunSmem* R = reinterpret_cast<RunSmem*>(smraw);
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     {   // zero the size-histogram bins the prune will use (0..B+1)
         const unsigned long long B = budget_of(f);
@@ -324,11 +363,15 @@ __global__ void __launch_bounds__(128) k_ccl_runs(Frame f, const uint32_t* __res
         if (gt == 0) f.sc->budget = B;
     }
     const int TXc = (f.W + CT - 1) / CT, TYc = (f.H + CT - 1) / CT;
-    const int tile = blockIdx.x * 4 + wid;
-    if (tile >= TXc * TYc) return;
-    RunSmem& S = sm_[wid];
-    const int tx = tile % TXc, x0 = tx * CT, y0 = (tile / TXc) * CT;
-    const uint32_t m = y0 + lane < f.H ? __ldg(rbits + (size_t)(y0 + lane) * f.bits_words + tx) : 0u;
+    const int RXc = (f.W + RW - 1) / RW;
+    const int rx = blockIdx.x % RXc, ry = blockIdx.x / RXc;
+    const int tc = wid % RGX, tr = wid / RGX;
+    const int tx = rx * RGX + tc, ty = ry * RGY + tr;
+    const bool tile_ok = tx < TXc && ty < TYc;
+    const int tile = ty * TXc + tx;
+    const int x0 = tx * CT, y0 = ty * CT;
+    RunSmem& S = R[wid];
+    const uint32_t m = tile_ok && y0 + lane < f.H ? __ldg(rbits + (size_t)(y0 + lane) * f.bits_words + tx) : 0u;
     const uint32_t s = m & ~(m << 1);  // run starts
     const int nr = __popc(s);
     int rinc = nr;
@@ -356,7 +399,7 @@ __global__ void __launch_bounds__(128) k_ccl_runs(Frame f, const uint32_t* __res
         S.sz[i] = 0;
     }
     __syncwarp();
-    // unions with the overlapping runs of the row above (8-connectivity)
+    // 1. unions with the overlapping runs of the row above (8-connectivity)
     for (int i = lane; i < nruns; i += 32) {
         const int r = S.rrow[i];
         if (r == 0) continue;
@@ -374,18 +417,66 @@ __global__ void __launch_bounds__(128) k_ccl_runs(Frame f, const uint32_t* __res
         }
     }
     __syncwarp();
-    // flatten, sizes at the local roots
-    int nroots = 0;
+    // flatten, sizes at the tile-local roots; switch to region node ids
+    auto gof = [&](const RunSmem& Q, int ri, int qx0, int qy0) { return (qy0 + Q.rrow[ri]) * f.W + qx0 + Q.rstart[ri]; };
     for (int i = lane; i < nruns; i += 32) {
         const int rt = rfind(S.par, i);
         S.par[i] = rt;
         atomicAdd(&S.sz[rt], (int)S.rlen[i]);
-        nroots += rt == i;
     }
     __syncwarp();
-    // local roots -> list (unordered) with sizes; par[g] = g, cnt[g] = 0.  The
-    // root run is the component's first run in (row, start) order, so its
-    // start is the component's minimum raster index g.
+    for (int i = lane; i < nruns; i += 32) {
+        const int rt = S.par[i];
+        S.key[i] = rt == i ? gof(S, i, x0, y0) : 0x7fffffff;
+        S.par[i] = wid * kRunCap + rt;
+    }
+    __syncthreads();
+    // 2. inner borders of the region (the tile above / left, and the two
+    //    upper diagonals), duplicates of a long border run skipped
+    if (tr > 0) {
+        const int wa = wid - RGX;
+        const int a = node_at(R, wid, 0, lane);
+        const int ap = __shfl_up_sync(0xffffffffu, a, 1);
+        int u0 = lane > 0 ? node_at(R, wa, 31, lane - 1) : (tc > 0 ? node_at(R, wa - 1, 31, 31) : -1);
+        int u1 = node_at(R, wa, 31, lane);
+        int u2 = lane < 31 ? node_at(R, wa, 31, lane + 1) : (tc + 1 < RGX ? node_at(R, wa + 1, 31, 0) : -1);
+        if (a >= 0) {
+            const bool cont = lane > 0 && ap >= 0 && cfind(R, ap) == cfind(R, a);
+            if (!cont && u0 >= 0) cunite(R, a, u0);
+            if (!cont && u1 >= 0) cunite(R, a, u1);
+            if (u2 >= 0) cunite(R, a, u2);
+        }
+    }
+    if (tc > 0) {
+        const int wl = wid - 1;
+        const int a = node_at(R, wid, lane, 0);
+        if (a >= 0) {
+            const int l0 = lane > 0 ? node_at(R, wl, lane - 1, 31) : -1;
+            const int l1 = node_at(R, wl, lane, 31);
+            const int l2 = lane < 31 ? node_at(R, wl, lane + 1, 31) : -1;
+            if (l0 >= 0) cunite(R, a, l0);
+            if (l1 >= 0) cunite(R, a, l1);
+            if (l2 >= 0) cunite(R, a, l2);
+        }
+    }
+    __syncthreads();
+    // region roots: key = min g, size = sum over their tile components
+    for (int i = lane; i < nruns; i += 32) {
+        const int self = wid * kRunCap + i;
+        const int rt = cfind(R, self);
+        if (S.key[i] != 0x7fffffff && rt != self) {  // a tile root merged into another
+            RunSmem& Q = R[rt / kRunCap];
+            atomicAdd(&Q.sz[rt % kRunCap], S.sz[i]);
+            atomicMin(&Q.key[rt % kRunCap], S.key[i]);
+        }
+    }
+    __syncthreads();
+    // 3. region roots -> list; runs -> g; outer borders
+    int nroots = 0;
+    for (int i = lane; i < nruns; i += 32) {
+        const int self = wid * kRunCap + i;
+        nroots += cfind(R, self) == self;
+    }
     int incl = nroots;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -396,69 +487,81 @@ __global__ void __launch_bounds__(128) k_ccl_runs(Frame f, const uint32_t* __res
     if (lane == 31 && incl) base = atomicAdd(&f.sc->n_lroots, (unsigned)incl);
     base = __shfl_sync(0xffffffffu, base, 31);
     unsigned pos = base + incl - nroots;
-    uint32_t* lr_idx = f.list;
-    uint32_t* lr_size = reinterpret_cast<uint32_t*>(f.rank);
-    auto gof = [&](int ri) { return (y0 + S.rrow[ri]) * f.W + x0 + S.rstart[ri]; };
-    int32_t* rr = runroot + (size_t)tile * kRunCap;
+    // region roots get dense ids (global union-find node = id: cpar, ccnt and
+    // cmin = minimum raster index live in the first n_lroots entries of
+    // f.par / f.cnt / f.roots, small enough to stay in L2)
     for (int i = lane; i < nruns; i += 32) {
-        const int rt = S.par[i];
-        const int g = gof(rt);
-        rr[i] = g;
-        if (rt == i) {
-            lr_idx[pos] = (uint32_t)g;
-            lr_size[pos] = (uint32_t)S.sz[i];
-            f.par[g] = g;
-            f.cnt[g] = 0;
-            ++pos;
+        const int self = wid * kRunCap + i;
+        if (cfind(R, self) == self) {
+            const int id = (int)pos++;
+            f.par[id] = id;
+            f.cnt[id] = (uint32_t)S.sz[i];
+            f.roots[id] = S.key[i];
+            S.key[i] = id;
         }
     }
-    // borders: root g of every set pixel (-1 when unset)
-    int32_t* bd = bord + (size_t)tile * 128;
-    {
-        const uint32_t m0 = S.rowm[0], s0 = S.rows[0];
-        const uint32_t m31 = S.rowm[31], s31 = S.rows[31];
-        bd[lane] = (m0 >> lane) & 1u ? gof(S.par[__popc(s0 & upto_mask(lane)) - 1]) : -1;
-        bd[32 + lane] = (m31 >> lane) & 1u ? gof(S.par[S.rs[31] + __popc(s31 & upto_mask(lane)) - 1]) : -1;
-        bd[64 + lane] = m & 1u ? gof(S.par[rinc - nr]) : -1;
-        bd[96 + lane] = (m >> 31) & 1u ? gof(S.par[rinc - 1]) : -1;
+    __syncthreads();
+    auto gnode = [&](int node) {
+        const int rt = cfind(R, node);
+        return R[rt / kRunCap].key[rt % kRunCap];
+    };
+    if (tile_ok) {
+        int32_t* rr = runroot + (size_t)tile * kRunCap;
+        for (int i = lane; i < nruns; i += 32) rr[i] = gnode(wid * kRunCap + i);
+    }
+    int32_t* bd = bord + (size_t)blockIdx.x * RBORD;
+    if (tr == 0) {
+        const int a = node_at(R, wid, 0, lane);
+        bd[tc * CT + lane] = a >= 0 ? gnode(a) : -1;
+    }
+    if (tr == RGY - 1) {
+        const int a = node_at(R, wid, 31, lane);
+        bd[RW + tc * CT + lane] = a >= 0 ? gnode(a) : -1;
+    }
+    if (tc == 0) {
+        const int a = node_at(R, wid, lane, 0);
+        bd[2 * RW + tr * CT + lane] = a >= 0 ? gnode(a) : -1;
+    }
+    if (tc == RGX - 1) {
+        const int a = node_at(R, wid, lane, 31);
+        bd[2 * RW + RH + tr * CT + lane] = a >= 0 ? gnode(a) : -1;
     }
 }
 
 // ------------------------------------------------------------------ B3 ----
-// A lane whose predecessor has the same root and is a neighbour of the same
-// pixels only adds the one new neighbour: redundant unions of long border runs
-// (which serialise on one root's atomicMin) are skipped.
-__global__ void __launch_bounds__(128) k_ccl_borders(Frame f, const int32_t* __restrict__ bord) {
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int TXc = (f.W + CT - 1) / CT, TYc = (f.H + CT - 1) / CT;
-    const int tile = blockIdx.x * 4 + wid;
-    if (tile >= TXc * TYc) return;
-    const int tx = tile % TXc, ty = tile / TXc;
-    const int32_t* bd = bord + (size_t)tile * 128;
-    if (ty > 0) {
-        const int a = bd[lane];  // top row pixel x0 + lane
+// Region outer borders: thread t < RW takes top-border pixel t (its three
+// neighbours in the region above, corners from the regions above-left /
+// above-right), thread RW + r the left-border pixel r (the left region's right
+// column; the diagonals across region corners are covered by the top borders).
+// A lane whose predecessor has the same root only adds its one new neighbour.
+__global__ void __launch_bounds__(RW + RH) k_ccl_borders(Frame f, const int32_t* __restrict__ bord) {
+    const int t = threadIdx.x, lane = t & 31;
+    const int RXc = (f.W + RW - 1) / RW;
+    const int reg = blockIdx.x;
+    const int rx = reg % RXc, ry = reg / RXc;
+    const int32_t* bd = bord + (size_t)reg * RBORD;
+    if (t < RW) {
+        const int a = ry > 0 ? bd[t] : -1;
         const int ap = __shfl_up_sync(0xffffffffu, a, 1);
         if (a >= 0) {
-            const int32_t* up = bord + (size_t)(tile - TXc) * 128 + 32;  // bottom row above
-            const int u0 = lane > 0 ? up[lane - 1]
-                                    : (tx > 0 ? bord[(size_t)(tile - TXc - 1) * 128 + 32 + 31] : -1);
-            const int u1 = up[lane];
-            const int u2 = lane < 31 ? up[lane + 1]
-                                     : (tx + 1 < TXc ? bord[(size_t)(tile - TXc + 1) * 128 + 32] : -1);
+            const int32_t* up = bord + (size_t)(reg - RXc) * RBORD + RW;  // bottom row above
+            const int u0 = t > 0 ? up[t - 1] : (rx > 0 ? bord[(size_t)(reg - RXc - 1) * RBORD + RW + RW - 1] : -1);
+            const int u1 = up[t];
+            const int u2 = t < RW - 1 ? up[t + 1] : (rx + 1 < RXc ? bord[(size_t)(reg - RXc + 1) * RBORD + RW] : -1);
             const bool cont = lane > 0 && ap == a;  // u0, u1 were the predecessor's u1, u2
             if (!cont && u0 >= 0) gunite(f.par, a, u0);
             if (!cont && u1 >= 0 && u1 != u0) gunite(f.par, a, u1);
             if (u2 >= 0 && u2 != u1) gunite(f.par, a, u2);
         }
-    }
-    if (tx > 0) {
-        const int a = bd[64 + lane];  // left column pixel y0 + lane
+    } else {
+        const int r = t - RW;
+        const int a = rx > 0 ? bd[2 * RW + r] : -1;
         const int ap = __shfl_up_sync(0xffffffffu, a, 1);
         if (a >= 0) {
-            const int32_t* lf = bord + (size_t)(tile - 1) * 128 + 96;  // right column, left tile
-            const int l0 = lane > 0 ? lf[lane - 1] : -1;  // y-1 across the tile top: done above
-            const int l1 = lf[lane];
-            const int l2 = lane < 31 ? lf[lane + 1] : -1;  // y+1 below: done by the tile below-left
+            const int32_t* lf = bord + (size_t)(reg - 1) * RBORD + 2 * RW + RH;  // right column, left
+            const int l0 = r > 0 ? lf[r - 1] : -1;
+            const int l1 = lf[r];
+            const int l2 = r < RH - 1 ? lf[r + 1] : -1;
             const bool cont = lane > 0 && ap == a;
             if (!cont && l0 >= 0) gunite(f.par, a, l0);
             if (!cont && l1 >= 0 && l1 != l0) gunite(f.par, a, l1);
@@ -467,17 +570,30 @@ __global__ void __launch_bounds__(128) k_ccl_borders(Frame f, const int32_t* __r
     }
 }
 
+// ------------------------------------------------------------------ B4 ----
+// Region roots -> global root (path compression); size and minimum raster
+// index (cmin) accumulated at the global root.
+__global__ void __launch_bounds__(256) k_compress_roots(Frame f) {
+    const int n = (int)f.sc->n_lroots;
+    for (int id = blockIdx.x * blockDim.x + threadIdx.x; id < n; id += gridDim.x * blockDim.x) {
+        const int r = gfind(f.par, id);
+        if (r != id) {
+            f.par[id] = r;
+            atomicAdd(f.cnt + r, __ldcg(f.cnt + id));
+            atomicMin(f.roots + r, __ldcg(f.roots + id));
+        }
+    }
+}
+
 // ------------------------------------------------------------------ B5 ----
 __global__ void __launch_bounds__(256) k_root_stats(Frame f) {
-    const unsigned n = f.sc->n_lroots;
+    const int n = (int)f.sc->n_lroots;
     const unsigned long long B = f.sc->budget;
-    const uint32_t* lr_idx = f.list;
     unsigned nr = 0;
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int g = (int)lr_idx[i];
-        if (__ldcg(f.par + g) == g) {
+    for (int id = blockIdx.x * blockDim.x + threadIdx.x; id < n; id += gridDim.x * blockDim.x) {
+        if (__ldcg(f.par + id) == id) {
             ++nr;
-            const uint32_t sz = __ldcg(f.cnt + g);
+            const uint32_t sz = __ldcg(f.cnt + id);
             if (sz <= B + 1) atomicAdd(f.szhist + sz, 1u);
         }
     }
@@ -486,16 +602,21 @@ __global__ void __launch_bounds__(256) k_root_stats(Frame f) {
 }
 
 // ------------------------------------------------------------------ B7 ----
+// size < s* -> removed; size == s* -> bit cmin of the raster bitmap (and the
+// id behind it in idmap = f.rank)
 __global__ void __launch_bounds__(256) k_prune_roots(Frame f, uint32_t* __restrict__ sbits) {
-    const unsigned n = f.sc->n_lroots;
+    const int n = (int)f.sc->n_lroots;
     const unsigned long long sst = f.sc->s_star, q = f.sc->q;
-    const uint32_t* lr_idx = f.list;
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int g = (int)lr_idx[i];
-        if (__ldcg(f.par + g) != g) continue;
-        const uint32_t sz = __ldcg(f.cnt + g);
-        if (sz < sst) f.cnt[g] = sz | kRemoved;
-        else if (sz == sst && q > 0) atomicOr(sbits + (g >> 5), 1u << (g & 31));
+    for (int id = blockIdx.x * blockDim.x + threadIdx.x; id < n; id += gridDim.x * blockDim.x) {
+        if (__ldcg(f.par + id) != id) continue;
+        const uint32_t sz = __ldcg(f.cnt + id);
+        if (sz < sst) {
+            f.cnt[id] = sz | kRemoved;
+        } else if (sz == sst && q > 0) {
+            const int k = __ldcg(f.roots + id);
+            f.rank[k] = id;
+            atomicOr(sbits + (k >> 5), 1u << (k & 31));
+        }
     }
 }
 
@@ -554,8 +675,8 @@ __global__ void __launch_bounds__(256) k_prune_first_q(Frame f, const uint32_t* 
             uint32_t rk = run + inc2 - cj;
             const int base = (c * 1024 + wid * 128 + j * 32 + lane) * 32;
             for (uint32_t t = w[j]; t && rk < q; t &= t - 1, ++rk) {
-                const int g = base + __ffs(t) - 1;
-                f.cnt[g] |= kRemoved;
+                const int k = base + __ffs(t) - 1;  // a component's cmin
+                f.cnt[__ldcg(f.rank + k)] |= kRemoved;
             }
             run += __shfl_sync(0xffffffffu, inc2, 31);
         }
@@ -588,8 +709,8 @@ __global__ void __launch_bounds__(128) k_apply_runs(Frame f, const uint32_t* __r
         int k = 0;
         for (uint32_t t = s; t; t &= t - 1, ++k) {
             const int a = __ffs(t) - 1, len = run_len(m, a);
-            const int g = __ldg(rr + k);
-            const int r = __ldcg(f.par + g);
+            const int id = __ldg(rr + k);
+            const int r = __ldcg(f.par + id);
             if (!(__ldcg(f.cnt + r) & kRemoved))
                 pruned |= (len >= 32 ? 0xffffffffu : ((1u << len) - 1u)) << a;
         }
@@ -730,9 +851,12 @@ void launch_boundary_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int
     // B2, B3
     const int ntiles = ((f.W + CT - 1) / CT) * ((f.H + CT - 1) / CT);
     const int tb = (ntiles + 3) / 4;
-    k_ccl_runs<<<tb, 128, 0, st>>>(f, rbits, runroot, bord);
-    k_ccl_borders<<<tb, 128, 0, st>>>(f, bord);
-    launch_ccl_compress(f, st);
+    const int nreg = ((f.W + RW - 1) / RW) * ((f.H + RH - 1) / RH);
+    const size_t rsm = sizeof(RunSmem) * NRW;
+    cudaFuncSetAttribute(k_ccl_region, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
+    k_ccl_region<<<nreg, 32 * NRW, rsm, st>>>(f, rbits, runroot, bord);
+    k_ccl_borders<<<nreg, RW + RH, 0, st>>>(f, bord);
+    k_compress_roots<<<148 * 8, 256, 0, st>>>(f);
     k_root_stats<<<148 * 4, 256, 0, st>>>(f);
     launch_prune_select(f, st);
     cudaMemsetAsync(sbits, 0, (size_t)sbits_words * 4, st);
