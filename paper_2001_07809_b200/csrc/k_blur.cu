@@ -254,6 +254,405 @@ __global__ void __launch_bounds__(kThreads) k_blur_sep_k(Frame f, BlurParams bp,
     }
 }
 
+// v2 (default separable path): 128 x 32 output tile, 256 threads.
+//  stage   interior tiles: aligned 16-byte loads of each input row's byte run
+//          (replicate-clamped copy for edge tiles); the tile's blur decisions
+//          from the dense disparity and the per-disparity focus LUT;
+//  horiz   thread = (staged row, 4 outputs): 3 float planes in shared memory;
+//  vert    thread = (column, 16 output rows), taps slide in registers;
+//  output  sharp pixels keep their input bytes; the tile leaves through
+//          shared memory as coalesced 16-byte stores.
+constexpr int V2X = 128, V2Y = 32;
+
+template <int K>
+struct V2Geom {
+    static constexpr int h = K / 2;
+    static constexpr int IH = V2Y + 2 * h;
+    static constexpr int LB = (3 * h + 15) / 16 * 16;  // interior rows load from byte 3*x0 - LB
+    static constexpr int ROWB = ((3 * (V2X + 2 * h) + LB + 15) & ~15) + 16;  // staged row bytes
+    static constexpr int XOFF = LB - 3 * h;  // smem byte of input column x0 - h
+    static constexpr size_t SM_STAGE = (size_t)IH * ROWB;
+    static constexpr size_t SM_H = (size_t)3 * IH * V2X * sizeof(float);
+    static constexpr size_t SM_OUT = (size_t)V2Y * 3 * V2X;
+    static constexpr size_t SM = SM_STAGE + SM_H + SM_OUT + (size_t)V2X * V2Y + 16;
+};
+
+template <int K>
+__global__ void __launch_bounds__(kThreads) k_blur_v2(Frame f, BlurParams bp,
+                                                      const uint8_t* __restrict__ in,
+                                                      uint8_t* __restrict__ out,
+                                                      const int16_t* __restrict__ depth) {
+    using G = V2Geom<K>;
+    constexpr int h = G::h, IH = G::IH, ROWB = G::ROWB, XOFF = G::XOFF;
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint8_t* stage = smem;
+    float* hs = reinterpret_cast<float*>(smem + G::SM_STAGE);      // [3][IH][V2X]
+    uint8_t* otile = smem + G::SM_STAGE + G::SM_H;                  // [V2Y][3*V2X]
+    uint8_t* shf = otile + G::SM_OUT;                               // [V2Y][V2X] sharp flags
+    __shared__ uint8_t lut[1024];
+    const int W = f.W, H = f.H, tid = threadIdx.x;
+    const int x0 = blockIdx.x * V2X, y0 = blockIdx.y * V2Y;
+    const int nx = min(V2X, W - x0), ny = min(V2Y, H - y0);
+    for (int i = tid; i < bp.lut_len && i < 1024; i += kThreads) lut[i] = bp.sharp_lut[i];
+    __syncthreads();
+    {
+        int any = 0;
+        for (int i = tid; i < V2X * V2Y; i += kThreads) {
+            const int ox = i % V2X, oy = i / V2X;
+            uint8_t sh = 1;
+            if (ox < nx && oy < ny) {
+                const int d = depth[(size_t)(y0 + oy) * W + x0 + ox];
+                sh = d >= 0 && d < bp.lut_len && lut[d];
+                any |= !sh;
+            }
+            shf[i] = sh;
+        }
+        if (__syncthreads_or(any) == 0) {
+            // every pixel sharp: copy the tile
+            for (int r = tid / 32; r < ny; r += kThreads / 32) {
+                const uint8_t* src = in + ((size_t)(y0 + r) * W + x0) * 3;
+                uint8_t* dst = out + ((size_t)(y0 + r) * W + x0) * 3;
+                for (int b = tid % 32; b < 3 * nx; b += 32) dst[b] = src[b];
+            }
+            return;
+        }
+    }
+    // ---- stage rows y0-h .. y0+V2Y+h-1 (clamped), columns x0-h .. x0+V2X+h-1;
+    // input column x0 - h sits at smem byte XOFF of every staged row
+    // interior: the 16-byte run [3(x0) - LB, ...) lies inside the row and the image
+    const bool interior = 3 * x0 - G::LB >= 0 && x0 + V2X + h <= W && y0 - h >= 0 &&
+                          y0 + V2Y + h <= H && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
+                          (W * 3) % 16 == 0 &&
+                          3 * (x0 + V2X + h) + 16 <= 3 * W;  // last uint4 stays in the row
+    if (interior) {
+        constexpr int NV = (3 * (V2X + 2 * h) + G::LB + 15) / 16;  // uint4 per row
+        for (int i = tid; i < IH * NV; i += kThreads) {
+            const int r = i / NV, v = i % NV;
+            const uint4* src = reinterpret_cast<const uint4*>(in + ((size_t)(y0 - h + r) * W + x0) * 3 - G::LB);
+            *reinterpret_cast<uint4*>(stage + (size_t)r * ROWB + 16 * v) = __ldg(src + v);
+        }
+    } else {
+        for (int i = tid; i < IH * (V2X + 2 * h); i += kThreads) {
+            const int r = i / (V2X + 2 * h), c = i % (V2X + 2 * h);
+            const int sy = min(max(y0 - h + r, 0), H - 1), sx = min(max(x0 - h + c, 0), W - 1);
+            const uint8_t* p = in + ((size_t)sy * W + sx) * 3;
+            uint8_t* q = stage + (size_t)r * ROWB + XOFF + 3 * c;
+            q[0] = p[0];
+            q[1] = p[1];
+            q[2] = p[2];
+        }
+    }
+    __syncthreads();
+    float wk[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) wk[i] = __ldg(bp.g1 + i);
+    // ---- horizontal: item = (staged row, 4 outputs); bytes from aligned words
+    constexpr int SH = XOFF & 3;           // byte misalignment (3 * q4 % 4 == 0)
+    constexpr int NB = 3 * (K + 3);        // bytes of the 4 outputs' taps
+    constexpr int NWD = (SH + NB + 3) / 4;
+    for (int it = tid; it < IH * (V2X / 4); it += kThreads) {
+        const int r = it / (V2X / 4), q4 = (it % (V2X / 4)) * 4;
+        const uint32_t* wr = reinterpret_cast<const uint32_t*>(stage + (size_t)r * ROWB + ((XOFF + 3 * q4) & ~3));
+        uint32_t wv[NWD];
+#pragma unroll
+        for (int i = 0; i < NWD; ++i) wv[i] = wr[i];
+        float a[4][3];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) a[o][0] = a[o][1] = a[o][2] = 0.f;
+#pragma unroll
+        for (int p = 0; p < K + 3; ++p) {
+            float v[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int bi = SH + 3 * p + c;
+                v[c] = byte_f(wv[bi >> 2], bi & 3);
+            }
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                if (p - o >= 0 && p - o < K) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) a[o][c] = fmaf(wk[p - o], v[c], a[o][c]);
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            *reinterpret_cast<float4*>(hs + ((size_t)c * IH + r) * V2X + q4) =
+                make_float4(a[0][c], a[1][c], a[2][c], a[3][c]);
+    }
+    __syncthreads();
+    // ---- vertical: thread = (column, 16 rows)
+    {
+        const int ox = tid % V2X, oy0 = (tid / V2X) * 16;
+        float a[16][3];
+#pragma unroll
+        for (int o = 0; o < 16; ++o) a[o][0] = a[o][1] = a[o][2] = 0.f;
+#pragma unroll
+        for (int r = 0; r < 16 + K - 1; ++r) {
+            const float v0 = hs[((size_t)0 * IH + oy0 + r) * V2X + ox];
+            const float v1 = hs[((size_t)1 * IH + oy0 + r) * V2X + ox];
+            const float v2 = hs[((size_t)2 * IH + oy0 + r) * V2X + ox];
+#pragma unroll
+            for (int o = 0; o < 16; ++o) {
+                if (r - o >= 0 && r - o < K) {
+                    a[o][0] = fmaf(wk[r - o], v0, a[o][0]);
+                    a[o][1] = fmaf(wk[r - o], v1, a[o][1]);
+                    a[o][2] = fmaf(wk[r - o], v2, a[o][2]);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < 16; ++o) {
+            const int oy = oy0 + o;
+            uint8_t* dst = otile + (size_t)oy * 3 * V2X + 3 * ox;
+            if (shf[oy * V2X + ox]) {
+                const uint8_t* t = stage + (size_t)(oy + h) * ROWB + XOFF + 3 * (ox + h);
+                dst[0] = t[0];
+                dst[1] = t[1];
+                dst[2] = t[2];
+            } else {
+                dst[0] = (uint8_t)min(max((int)floorf(a[o][0] + 0.5f), 0), 255);
+                dst[1] = (uint8_t)min(max((int)floorf(a[o][1] + 0.5f), 0), 255);
+                dst[2] = (uint8_t)min(max((int)floorf(a[o][2] + 0.5f), 0), 255);
+            }
+        }
+    }
+    __syncthreads();
+    // ---- output rows
+    if (nx == V2X && (W * 3) % 16 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+        constexpr int NV = 3 * V2X / 16;  // 24 uint4 per row
+        for (int i = tid; i < ny * NV; i += kThreads) {
+            const int r = i / NV, v = i % NV;
+            reinterpret_cast<uint4*>(out + ((size_t)(y0 + r) * W + x0) * 3)[v] =
+                reinterpret_cast<const uint4*>(otile + (size_t)r * 3 * V2X)[v];
+        }
+    } else {
+        for (int i = tid; i < ny * 3 * V2X; i += kThreads) {
+            const int r = i / (3 * V2X), b = i % (3 * V2X);
+            if (b < 3 * nx) out[((size_t)(y0 + r) * W + x0) * 3 + b] = otile[(size_t)r * 3 * V2X + b];
+        }
+    }
+}
+
+// v3 (default separable path): vertical pass first, in registers.
+// Tile = 128 x 16 outputs; thread t < NC = 128 + 2h owns input column
+// x0 - h + t and walks the tile's 16 + 2h staged rows once: every converted
+// input value feeds its (up to) K pending vertical outputs through packed
+// FFMA2 (output pairs 2j, 2j+1 share the input, weights (w[k], w[k-1]) with
+// zero-padded ends).  The vertical results (3 float planes, 16 x NC) then go
+// through the horizontal pass (item = row x 4 outputs, FFMA2 over output
+// pairs); sharp pixels keep their staged input bytes and every item stores
+// its 12 output bytes directly (coalesced across the warp).
+__device__ __forceinline__ unsigned long long f2pack(float lo, float hi) {
+    return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ float f2lo(unsigned long long v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float f2hi(unsigned long long v) { return __uint_as_float((uint32_t)(v >> 32)); }
+
+template <int K>
+struct V3Geom {
+    static constexpr int h = K / 2, BX = 128, BY = 16;
+    static constexpr int NC = BX + 2 * h;               // staged / vertical columns
+    static constexpr int NCP = (NC + 3) & ~3;           // float plane row (16-byte rows)
+    static constexpr int IH = BY + 2 * h;
+    static constexpr int LB = (3 * h + 15) / 16 * 16;   // interior rows load from byte 3*x0 - LB
+    static constexpr int ROWB = ((3 * NC + LB + 15) & ~15) + 16;
+    static constexpr int XOFF = LB - 3 * h;             // smem byte of input column x0 - h
+    static constexpr int NT = (NC + 31) & ~31;           // threads
+    static constexpr size_t SM_STAGE = (size_t)IH * ROWB;
+    static constexpr size_t SM_V = (size_t)3 * BY * NCP * sizeof(float);
+    static constexpr size_t SM = SM_STAGE + SM_V + (size_t)BX * BY + 16;
+};
+
+template <int K>
+__global__ void __launch_bounds__(V3Geom<K>::NT) k_blur_v3(Frame f, BlurParams bp,
+                                                           const uint8_t* __restrict__ in,
+                                                           uint8_t* __restrict__ out,
+                                                           const int16_t* __restrict__ depth) {
+    using G = V3Geom<K>;
+    constexpr int h = G::h, BX = G::BX, BY = G::BY, NC = G::NC, NCP = G::NCP, IH = G::IH;
+    constexpr int ROWB = G::ROWB, XOFF = G::XOFF, NT = G::NT;
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint8_t* stage = smem;
+    float* vp = reinterpret_cast<float*>(smem + G::SM_STAGE);  // [3][BY][NCP]
+    uint8_t* shf = smem + G::SM_STAGE + G::SM_V;               // [BY][BX] sharp flags
+    __shared__ uint8_t lut[1024];
+    const int W = f.W, H = f.H, tid = threadIdx.x;
+    const int x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
+    const int nx = min(BX, W - x0), ny = min(BY, H - y0);
+    for (int i = tid; i < bp.lut_len && i < 1024; i += NT) lut[i] = bp.sharp_lut[i];
+    __syncthreads();
+    // ---- one latency exposure: the staged rows (rows y0-h .. y0+BY+h-1,
+    // columns x0-h .. x0+BX+h-1, replicate-clamped) and the tile's disparities
+    const bool interior = 3 * x0 - G::LB >= 0 && 3 * (x0 + BX + h) + 16 <= 3 * W && y0 - h >= 0 &&
+                          y0 + BY + h <= H && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
+                          (W * 3) % 16 == 0;
+    int any = 0;
+    if (interior) {
+        constexpr int NV = (3 * NC + G::LB + 15) / 16;
+        constexpr int PER = (IH * NV + NT - 1) / NT;
+        uint4 buf[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = tid + k * NT;
+            if (i < IH * NV) {
+                const int r = i / NV, v = i % NV;
+                buf[k] = __ldg(reinterpret_cast<const uint4*>(in + ((size_t)(y0 - h + r) * W + x0) * 3 - G::LB) + v);
+            }
+        }
+        constexpr int DPER = (BX * BY + NT - 1) / NT;
+        int16_t dv[DPER];
+#pragma unroll
+        for (int k = 0; k < DPER; ++k) {
+            const int i = tid + k * NT;
+            dv[k] = i < BX * BY ? depth[(size_t)(y0 + i / BX) * W + x0 + i % BX] : (int16_t)-1;
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = tid + k * NT;
+            if (i < IH * NV) *reinterpret_cast<uint4*>(stage + (size_t)(i / NV) * ROWB + 16 * (i % NV)) = buf[k];
+        }
+#pragma unroll
+        for (int k = 0; k < DPER; ++k) {
+            const int i = tid + k * NT;
+            if (i < BX * BY) {
+                const int d = dv[k];
+                const uint8_t sh = d >= 0 && d < bp.lut_len && lut[d];
+                shf[i] = sh;
+                any |= !sh;
+            }
+        }
+    } else {
+        for (int i = tid; i < IH * NC; i += NT) {
+            const int r = i / NC, c = i % NC;
+            const int sy = min(max(y0 - h + r, 0), H - 1), sx = min(max(x0 - h + c, 0), W - 1);
+            const uint8_t* p = in + ((size_t)sy * W + sx) * 3;
+            uint8_t* q = stage + (size_t)r * ROWB + XOFF + 3 * c;
+            q[0] = p[0];
+            q[1] = p[1];
+            q[2] = p[2];
+        }
+        for (int i = tid; i < BX * BY; i += NT) {
+            const int ox = i % BX, oy = i / BX;
+            uint8_t sh = 1;
+            if (ox < nx && oy < ny) {
+                const int d = depth[(size_t)(y0 + oy) * W + x0 + ox];
+                sh = d >= 0 && d < bp.lut_len && lut[d];
+                any |= !sh;
+            }
+            shf[i] = sh;
+        }
+    }
+    if (__syncthreads_or(any) == 0) {  // every pixel sharp: copy the staged input
+        for (int i = tid; i < ny * 3 * nx; i += NT) {
+            const int r = i / (3 * nx), b = i % (3 * nx);
+            out[((size_t)(y0 + r) * W + x0) * 3 + b] = stage[(size_t)(r + h) * ROWB + XOFF + 3 * h + b];
+        }
+        return;
+    }
+    // packed weight pairs wp[k] = (w[k], w[k-1]), w[-1] = w[K] = 0
+    unsigned long long wp[K + 1];
+    {
+        float w[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) w[i] = __ldg(bp.g1 + i);
+#pragma unroll
+        for (int k = 0; k <= K; ++k) wp[k] = f2pack(k < K ? w[k] : 0.f, k > 0 ? w[k - 1] : 0.f);
+    }
+    // ---- vertical: column tid, BY outputs in pairs (2j, 2j+1)
+    if (tid < NC) {
+        const uint8_t* colp = stage + XOFF + 3 * tid;
+        unsigned long long acc[BY / 2][3];
+#pragma unroll
+        for (int j = 0; j < BY / 2; ++j) acc[j][0] = acc[j][1] = acc[j][2] = 0ull;
+#pragma unroll
+        for (int r = 0; r < IH; ++r) {
+            const uint8_t* px = colp + (size_t)r * ROWB;
+            unsigned long long v2[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float v = (float)px[c];
+                v2[c] = f2pack(v, v);
+            }
+#pragma unroll
+            for (int j = 0; j < BY / 2; ++j) {
+                const int k = r - 2 * j;  // weight index of output 2j; output 2j+1 uses k-1
+                if (k >= 0 && k <= K) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) acc[j][c] = ffma2(wp[k], v2[c], acc[j][c]);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < BY / 2; ++j)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                vp[((size_t)c * BY + 2 * j) * NCP + tid] = f2lo(acc[j][c]);
+                vp[((size_t)c * BY + 2 * j + 1) * NCP + tid] = f2hi(acc[j][c]);
+            }
+    }
+    __syncthreads();
+    // ---- horizontal: item = (row, 4 outputs q4..q4+3); output pairs (0,1), (2,3)
+    for (int it = tid; it < BY * (BX / 4); it += NT) {
+        const int oy = it / (BX / 4), q4 = (it % (BX / 4)) * 4;
+        if (oy >= ny || q4 >= nx) continue;
+        unsigned long long a[2][3];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) a[j][0] = a[j][1] = a[j][2] = 0ull;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float* row = vp + ((size_t)c * BY + oy) * NCP + q4;
+            float v[K + 3 + 1];
+#pragma unroll
+            for (int i = 0; i < (K + 3 + 3) / 4; ++i) {
+                const float4 t = reinterpret_cast<const float4*>(row)[i];
+                v[4 * i] = t.x;
+                if (4 * i + 1 < K + 4) v[4 * i + 1] = t.y;
+                if (4 * i + 2 < K + 4) v[4 * i + 2] = t.z;
+                if (4 * i + 3 < K + 4) v[4 * i + 3] = t.w;
+            }
+#pragma unroll
+            for (int p = 0; p < K + 3; ++p) {
+                const unsigned long long v2 = f2pack(v[p], v[p]);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int k = p - 2 * j;
+                    if (k >= 0 && k <= K) a[j][c] = ffma2(wp[k], v2, a[j][c]);
+                }
+            }
+        }
+        // 4 pixels x 3 bytes
+        uint32_t ob[3] = {0, 0, 0};
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            const int ox = q4 + o;
+            const uint8_t* src = stage + (size_t)(oy + h) * ROWB + XOFF + 3 * (ox + h);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float af = (o & 1) ? f2hi(a[o >> 1][c]) : f2lo(a[o >> 1][c]);
+                const uint32_t b = shf[oy * BX + ox] ? (uint32_t)src[c]
+                                                     : (uint32_t)min(max((int)floorf(af + 0.5f), 0), 255);
+                const int bi = 3 * o + c;
+                ob[bi >> 2] |= b << (8 * (bi & 3));
+            }
+        }
+        uint8_t* dst = out + ((size_t)(y0 + oy) * W + x0 + q4) * 3;
+        if (q4 + 4 <= nx && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
+            reinterpret_cast<uint32_t*>(dst)[0] = ob[0];
+            reinterpret_cast<uint32_t*>(dst)[1] = ob[1];
+            reinterpret_cast<uint32_t*>(dst)[2] = ob[2];
+        } else {
+            for (int bi = 0; bi < 3 * min(4, nx - q4); ++bi) dst[bi] = (uint8_t)(ob[bi >> 2] >> (8 * (bi & 3)));
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) k_blur_exact(Frame f, BlurParams bp,
                                                          const uint8_t* __restrict__ in,
                                                          uint8_t* __restrict__ out,
@@ -330,6 +729,27 @@ void launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, ui
         k_blur_exact<<<grid, kThreads, sm, st>>>(f, bp, in_rgb, out_rgb, depth);
     } else {
         const int K = 2 * bp.hw + 1;
+        if (!bp.blur_map && bp.lut_len <= 1024) {
+            const dim3 g3((f.W + V3Geom<3>::BX - 1) / V3Geom<3>::BX, (f.H + V3Geom<3>::BY - 1) / V3Geom<3>::BY);
+#define STK_BLUR_V3(KK)                                                                         \
+    case KK:                                                                                    \
+        cudaFuncSetAttribute(k_blur_v3<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                             (int)V3Geom<KK>::SM);                                              \
+        k_blur_v3<KK><<<g3, V3Geom<KK>::NT, V3Geom<KK>::SM, st>>>(f, bp, in_rgb, out_rgb, depth); \
+        return;
+            switch (K) {
+                STK_BLUR_V3(3)
+                STK_BLUR_V3(5)
+                STK_BLUR_V3(7)
+                STK_BLUR_V3(9)
+                STK_BLUR_V3(11)
+                STK_BLUR_V3(13)
+                STK_BLUR_V3(17)
+                STK_BLUR_V3(25)
+                default: break;
+            }
+#undef STK_BLUR_V3
+        }
         // templated sizes: no weight array in shared memory
         const size_t smk = (size_t)(BY + 2 * bp.hw) * BX * sizeof(float4) + tile_bytes(bp.hw);
 #define STK_BLUR_K(KK)                                                                          \

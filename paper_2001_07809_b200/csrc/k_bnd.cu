@@ -24,7 +24,7 @@
 //                   raster index (the reference's discovery order) summed /
 //                   min'ed at the global root.
 //   B5 root_stats   global roots (par[g] == g): size histogram for the prune.
-//   (K4e prune_select: s*, q.)
+//   B6 prune_select s*, q from the size histogram (multi-block).
 //   B7 prune_roots  size < s* -> removed; size == s* -> bit minkey of a raster
 //                   bitmap; B7b then removes the first q of them in raster
 //                   (= label) order with one ordered scan of the bitmap.
@@ -41,7 +41,7 @@ namespace {
 
 constexpr int CT = 32;         // CCL tile side
 constexpr int kRunCap = 512;   // max runs in a 32x32 tile (16 per row)
-constexpr int MB_ROWS = 32;    // B1 output rows per warp
+constexpr int MB_ROWS = 16;    // B1 output rows per warp
 constexpr int MB_WPW = 30;     // B1 output words per warp (+1 halo word each side)
 
 __device__ __forceinline__ uint32_t upto_mask(int j) {  // bits 0..j
@@ -154,10 +154,15 @@ __global__ void __launch_bounds__(128) k_morph_bits(Frame f, uint32_t* __restric
             const uint32_t r = __shfl_down_sync(0xffffffffu, v, 1);
             return (v >> 1) | ((last ? (v >> 31) : (r & 1u)) << 31);
         };
-        auto planes_of = [&](int ri, uint32_t (&pl)[NPL]) {
+        // rows are fetched two iterations ahead of their use (load latency)
+        auto load_row = [&](int ri, uint4 (&g)[2]) {
             ri = min(max(ri, 0), H - 1);
             const uint4* src = reinterpret_cast<const uint4*>(f.grayL + (size_t)ri * f.P + 32 * wcl);
-            const uint4 g0 = __ldg(src), g1 = __ldg(src + 1);
+            g[0] = __ldg(src);
+            g[1] = __ldg(src + 1);
+        };
+        auto planes_of = [&](const uint4 (&gq)[2], uint32_t (&pl)[NPL]) {
+            const uint4 g0 = gq[0], g1 = gq[1];
             const uint32_t gw8[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
             for (int p = 0; p < NPL; ++p) pl[p] = 0;
@@ -184,6 +189,9 @@ __global__ void __launch_bounds__(128) k_morph_bits(Frame f, uint32_t* __restric
         // sliding windows: label planes (3 rows + shifted), raw (3 rows), fill (3 rows)
         uint32_t P0[NPL], P1[NPL], P2[NPL], L1[NPL], R1[NPL], L0[NPL], R0[NPL], L2[NPL], R2[NPL];
         uint32_t raw0 = 0, raw1 = 0, raw2 = 0, fil0 = 0, fil1 = 0, fil2 = 0;
+        uint4 qa[2], qb[2], qc[2];
+        load_row(yb - 3, qa);
+        load_row(yb - 2, qb);
         for (int i = 0; i < MB_ROWS + 6; ++i) {
             const int ri = yb - 3 + i;
             // shift the plane window: (P0, P1, P2) = rows ri-2, ri-1, ri
@@ -192,7 +200,9 @@ __global__ void __launch_bounds__(128) k_morph_bits(Frame f, uint32_t* __restric
                 P0[p] = P1[p], L0[p] = L1[p], R0[p] = R1[p];
                 P1[p] = P2[p], L1[p] = L2[p], R1[p] = R2[p];
             }
-            planes_of(ri, P2);
+            load_row(ri + 2, qc);
+            planes_of(qa, P2);
+            qa[0] = qb[0], qa[1] = qb[1], qb[0] = qc[0], qb[1] = qc[1];
 #pragma unroll
             for (int p = 0; p < NPL; ++p) {
                 L2[p] = shl(P2[p]);
@@ -620,6 +630,100 @@ __global__ void __launch_bounds__(256) k_prune_roots(Frame f, uint32_t* __restri
     }
 }
 
+// ------------------------------------------------------------------ B6 ----
+// s* = smallest size whose class-cumulative pixel count CS(s) exceeds
+// B = floor(budget), q = floor((B - CS(s*-1)) / s*) (see k_ccl.cu).  Sizes
+// 1..B+1 are split over kSelBlocks blocks; the last block to finish scans the
+// block sums and then the bins of the block where CS crosses B.
+constexpr int kSelBlocks = 128;
+
+__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v,
+                                                              unsigned long long* sh,
+                                                              unsigned long long* total) {
+    // 256 threads
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sh[wid] = x;
+    __syncthreads();
+    unsigned long long off = 0, tot = 0;
+    for (int i = 0; i < 8; ++i) {
+        if (i < wid) off += sh[i];
+        tot += sh[i];
+    }
+    __syncthreads();
+    *total = tot;
+    return off + x - v;
+}
+
+__global__ void __launch_bounds__(256) k_prune_select_mb(Frame f) {
+    __shared__ unsigned long long sh[8];
+    __shared__ unsigned int s_last;
+    __shared__ int s_blk;
+    __shared__ unsigned long long s_before;
+    DevScalars* sc = f.sc;
+    const unsigned long long B = sc->budget;
+    const long long L = (long long)B + 1;  // sizes 1..B+1
+    const long long per = (L + kSelBlocks - 1) / kSelBlocks;
+    auto range_sum = [&](long long a0, long long a1) {  // sum over [a0, a1) split by thread
+        const long long pt = (a1 - a0 + 255) / 256;
+        const long long t0 = a0 + threadIdx.x * pt, t1 = min(t0 + pt, a1);
+        unsigned long long sum = 0;
+        for (long long s = t0; s < t1; ++s) sum += (unsigned long long)s * __ldcg(f.szhist + s);
+        return sum;
+    };
+    {
+        const long long a0 = 1 + blockIdx.x * per, a1 = min(a0 + per, L + 1);
+        unsigned long long tot;
+        block_excl_scan(a0 < a1 ? range_sum(a0, a1) : 0ull, sh, &tot);
+        if (threadIdx.x == 0) {
+            sc->psel[blockIdx.x] = tot;
+            __threadfence();
+            s_last = atomicAdd(&sc->psel_done, 1u) == kSelBlocks - 1;
+        }
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+    }
+    // last block: which block's range crosses B?
+    if (threadIdx.x == 0) {
+        sc->s_star = B + 2;  // default: every size <= B+1 goes, q = 0
+        sc->q = 0;
+        s_blk = -1;
+    }
+    unsigned long long tot;
+    const unsigned long long v = threadIdx.x < kSelBlocks ? __ldcg(&sc->psel[threadIdx.x]) : 0ull;
+    const unsigned long long before = block_excl_scan(v, sh, &tot);
+    if (threadIdx.x < kSelBlocks && before <= B && before + v > B) {
+        s_blk = threadIdx.x;
+        s_before = before;
+    }
+    __syncthreads();
+    if (s_blk < 0) return;
+    const long long a0 = 1 + s_blk * per, a1 = min(a0 + per, L + 1);
+    const long long pt = (a1 - a0 + 255) / 256;
+    const long long t0 = a0 + threadIdx.x * pt, t1 = min(t0 + pt, a1);
+    unsigned long long mine = 0;
+    for (long long s = t0; s < t1; ++s) mine += (unsigned long long)s * __ldcg(f.szhist + s);
+    const unsigned long long tb = s_before + block_excl_scan(mine, sh, &tot);
+    if (tb <= B && tb + mine > B) {  // exactly one thread
+        unsigned long long cs = tb;
+        for (long long s = t0; s < t1; ++s) {
+            const unsigned long long add = (unsigned long long)s * __ldcg(f.szhist + s);
+            if (cs + add > B) {
+                sc->s_star = (unsigned long long)s;
+                sc->q = (B - cs) / (unsigned long long)s;
+                break;
+            }
+            cs += add;
+        }
+    }
+}
+
 // first q set bits of sbits in raster order -> removed.  Chunks of 1024 words
 // claimed in order; decoupled look-back on the per-chunk popcounts.
 __global__ void __launch_bounds__(256) k_prune_first_q(Frame f, const uint32_t* __restrict__ sbits,
@@ -858,7 +962,7 @@ void launch_boundary_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int
     k_ccl_borders<<<nreg, RW + RH, 0, st>>>(f, bord);
     k_compress_roots<<<148 * 8, 256, 0, st>>>(f);
     k_root_stats<<<148 * 4, 256, 0, st>>>(f);
-    launch_prune_select(f, st);
+    k_prune_select_mb<<<kSelBlocks, 256, 0, st>>>(f);
     cudaMemsetAsync(sbits, 0, (size_t)sbits_words * 4, st);
     k_prune_roots<<<148 * 4, 256, 0, st>>>(f, sbits);
     k_prune_first_q<<<148 * 2, 256, 0, st>>>(f, sbits, sbits_words);

@@ -96,6 +96,92 @@ __global__ void __launch_bounds__(kThreads) k_lstar(Frame f, const LstarTables* 
     }
 }
 
+// Both views in one streaming launch (blockIdx.y = view), 16 pixels per
+// thread-chunk (3 x 16-byte loads, one 16-byte store), two chunks in flight
+// per thread; W % 16 == 0 and 16-byte aligned planes.
+__global__ void __launch_bounds__(kThreads) k_lstar2(Frame f, const LstarTables* __restrict__ tab) {
+    __shared__ double pr[256], pg[256], pb[256];
+    for (int i = threadIdx.x; i < 256; i += kThreads) {
+        pr[i] = tab->prod[0][i];
+        pg[i] = tab->prod[1][i];
+        pb[i] = tab->prod[2][i];
+    }
+    __syncthreads();
+    // Y = (0.2126 lin[R] + 0.7152 lin[G]) + 0.0722 lin[B], products tabulated
+    auto lstar_p = [&](uint32_t r, uint32_t g, uint32_t b) {
+        const double y = __dadd_rn(__dadd_rn(pr[r], pg[g]), pb[b]);
+        const int bk = min((int)__dmul_rz(y, (double)kLstarBuckets), kLstarBuckets);
+        return (uint32_t)__ldg(&tab->base[bk]) + (y >= __ldg(&tab->tb[bk]) ? 1u : 0u);
+    };
+    const int view = blockIdx.y;
+    const uint8_t* __restrict__ rgb = view == 0 ? f.rgbL : f.rgbR;
+    uint8_t* __restrict__ gray = view == 0 ? f.grayL : f.grayR;
+    const int cpr = f.W / 16;
+    const long long nch = (long long)cpr * f.H;
+    const long long stride = (long long)gridDim.x * kThreads;
+    auto convert = [&](long long c, uint4 a, uint4 b, uint4 d) {
+        const int y = (int)(c / cpr), x = (int)(c - (long long)y * cpr) * 16;
+        const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
+        uint32_t out[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+            const int o = p * 3;
+            const uint32_t r = (w[o >> 2] >> ((o & 3) * 8)) & 0xffu;
+            const uint32_t g = (w[(o + 1) >> 2] >> (((o + 1) & 3) * 8)) & 0xffu;
+            const uint32_t bb = (w[(o + 2) >> 2] >> (((o + 2) & 3) * 8)) & 0xffu;
+            out[p >> 2] |= lstar_p(r, g, bb) << ((p & 3) * 8);
+        }
+        *reinterpret_cast<uint4*>(gray + (size_t)y * f.P + x) = make_uint4(out[0], out[1], out[2], out[3]);
+    };
+    long long c = blockIdx.x * (long long)kThreads + threadIdx.x;
+    for (; c + stride < nch; c += 2 * stride) {
+        const uint4* s0 = reinterpret_cast<const uint4*>(rgb + (size_t)c * 48);
+        const uint4* s1 = reinterpret_cast<const uint4*>(rgb + (size_t)(c + stride) * 48);
+        const uint4 a0 = __ldcs(s0), b0 = __ldcs(s0 + 1), d0 = __ldcs(s0 + 2);
+        const uint4 a1 = __ldcs(s1), b1 = __ldcs(s1 + 1), d1 = __ldcs(s1 + 2);
+        convert(c, a0, b0, d0);
+        convert(c + stride, a1, b1, d1);
+    }
+    if (c < nch) {
+        const uint4* s0 = reinterpret_cast<const uint4*>(rgb + (size_t)c * 48);
+        convert(c, __ldcs(s0), __ldcs(s0 + 1), __ldcs(s0 + 2));
+    }
+}
+
+// 256-bin histogram with warp-private shared counters (shared atomics), many
+// blocks, 16-byte loads two chunks deep; W % 16 == 0.
+__global__ void __launch_bounds__(kThreads) k_hist_warp(Frame f, const uint8_t* __restrict__ gray) {
+    __shared__ uint32_t wh[kThreads / 32][256];
+    const int tid = threadIdx.x, wid = tid >> 5;
+    for (int i = tid; i < (kThreads / 32) * 256; i += kThreads) (&wh[0][0])[i] = 0;
+    __syncthreads();
+    uint32_t* my = wh[wid];
+    const int cpr = f.W / 16;
+    const long long nch = (long long)cpr * f.H;
+    const long long stride = (long long)gridDim.x * kThreads;
+    auto count = [&](uint4 v) {
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int p = 0; p < 16; ++p) atomicAdd(&my[(w[p >> 2] >> ((p & 3) * 8)) & 0xffu], 1u);
+    };
+    auto load = [&](long long c) {
+        const int y = (int)(c / cpr), x = (int)(c - (long long)y * cpr) * 16;
+        return __ldcs(reinterpret_cast<const uint4*>(gray + (size_t)y * f.P + x));
+    };
+    long long c = blockIdx.x * (long long)kThreads + tid;
+    for (; c + stride < nch; c += 2 * stride) {
+        const uint4 a = load(c), b = load(c + stride);
+        count(a);
+        count(b);
+    }
+    if (c < nch) count(load(c));
+    __syncthreads();
+    uint32_t s = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) s += wh[w][tid];
+    if (s) atomicAdd(&f.sc->hist[tid], (unsigned long long)s);
+}
+
 // Histogram of an arbitrary pitched gray plane (stage entry build_histogram).
 __global__ void __launch_bounds__(kThreads) k_hist(Frame f, const uint8_t* __restrict__ gray) {
     __shared__ uint32_t hist[kThreads / 32][256];
@@ -132,6 +218,19 @@ __global__ void k_assign(Frame f, const uint8_t* __restrict__ gray, uint16_t* __
 void launch_lightness(const Frame& f, const LstarTables* dtab, bool left, bool right, bool hist,
                       cudaStream_t st) {
     if (f.N == 0) return;
+    const bool aligned = (reinterpret_cast<uintptr_t>(f.rgbL) & 15) == 0 &&
+                         (reinterpret_cast<uintptr_t>(f.rgbR) & 15) == 0;
+    if (left && right && f.W % 16 == 0 && aligned) {
+        // frame path: both views in one launch, then the histogram pass
+        const long long nch = (long long)(f.W / 16) * f.H;
+        const int bx = (int)std::min<long long>((nch + kThreads - 1) / kThreads, 148 * 4);
+        k_lstar2<<<dim3(bx, 2), kThreads, 0, st>>>(f, dtab);
+        if (hist) {
+            const int hb = (int)std::min<long long>((nch + kThreads - 1) / kThreads, 148 * 4);
+            k_hist_warp<<<hb, kThreads, 0, st>>>(f, f.grayL);
+        }
+        return;
+    }
     // byte counters: at most 240 pixels per thread per block
     const int per_row = f.W % 16 == 0 ? 16 * ((f.W + kThreads * 16 - 1) / (kThreads * 16))
                                       : (f.W + kThreads - 1) / kThreads;

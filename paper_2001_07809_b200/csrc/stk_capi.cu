@@ -143,6 +143,12 @@ int lstar_byte(double y) {
 
 void make_lstar_tables(LstarTables* t) {
     for (int v = 0; v < 256; ++v) t->linear[v] = srgb_to_linear(v);
+    for (int v = 0; v < 256; ++v) {
+        volatile double l = t->linear[v];  // plain IEEE products, no contraction
+        t->prod[0][v] = 0.2126 * l;
+        t->prod[1][v] = 0.7152 * l;
+        t->prod[2][v] = 0.0722 * l;
+    }
     t->thr[0] = -1.0;
     uint64_t hi_bits;
     const double two = 2.0;

@@ -47,6 +47,9 @@ struct DevScalars {
     unsigned int n_lroots;             // tile-local roots (K4a -> K4c)
     unsigned int pad1;
     unsigned int ctr[LB_COUNT];        // dynamic chunk counters
+    unsigned int psel_done;            // prune select: finished blocks
+    unsigned int pad2;
+    unsigned long long psel[128];      // prune select: per-block pixel sums
 };
 
 // Everything a kernel needs to know about one frame, passed by value.
@@ -98,6 +101,9 @@ struct LstarTables {
     // (checked on the host; the minimum threshold spacing is 4.3e-4 > 1/4096).
     double tb[4097];
     unsigned char base[4097];
+    // prod[c][v] = coefficient_c * linear[v] (lightness.cpp:41-43 products,
+    // IEEE round-to-nearest on the host == __dmul_rn on the device)
+    double prod[3][256];
 };
 constexpr int kLstarBuckets = 4096;
 
