@@ -130,20 +130,25 @@ __device__ __forceinline__ void window_sum(const char* __restrict__ cq, const ui
     uint2 t[2 + NT];
 #pragma unroll
     for (int i = 0; i < 2 + NT; ++i) t[i] = *reinterpret_cast<const uint2*>(cq + o[i]);
+    // per word: X = sum(terms) - S in 32 bits (lanes mixed), Y = the exact sum
+    // of the high lanes, low lanes = X - (Y << 16) (the true low sum is in
+    // [0, 2^32), so the modular result is exact)
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
         const bool y = NW == 2 ? w == 1 : sel_y;
-        uint32_t l = 0, hh = 0;
+        uint32_t X = 0, Y = 0;
 #pragma unroll
         for (int i = 0; i < 2 + NT; ++i) {
             if (i == 1) continue;  // the subtracted term
             const uint32_t x = y ? t[i].y : t[i].x;
-            l += lo16(x);
-            hh += hi16(x);
+            X += x;
+            Y += hi16(x);
         }
         const uint32_t xs = y ? t[1].y : t[1].x;
-        lo[w] = l - lo16(xs);
-        hi[w] = hh - hi16(xs);
+        X -= xs;
+        Y -= hi16(xs);
+        lo[w] = X - (Y << 16);
+        hi[w] = Y;
     }
 }
 
@@ -223,6 +228,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
             for (int k = 0; k < K; ++k) A[j][k] = B[j][k] = 0u;
         uint2* csq = cs + (size_t)(g * G) * p.CSW + ch * (K + 1);
         const size_t bufstride = (size_t)p.QP * p.CSW;
+        int rs_n = WIN % p.RS, ph_n = (WIN / p.RS) & 1, rs_o = 0;
         for (int t = 0; t < T; ++t) {
             if (t == 0) {
                 for (int i = 0; i < WIN; ++i) {
@@ -233,9 +239,11 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                     if (act) v_rows<WIN, G, K, true>(Ls + lw0, Rs + rw0, nullptr, nullptr, A, B);
                 }
             } else {
-                const int in = t + WIN - 1, io = t - 1;
-                const int sn = in % p.RS, so = io % p.RS;
-                mbar_wait(&fullb[sn], (uint32_t)((in / p.RS) & 1));
+                // slot / phase of the entering row t+WIN-1 and the leaving row t-1
+                const int sn = rs_n, so = rs_o;
+                mbar_wait(&fullb[sn], (uint32_t)ph_n);
+                if (++rs_n == p.RS) rs_n = 0, ph_n ^= 1;
+                if (++rs_o == p.RS) rs_o = 0;
                 const uint8_t* bn = ring + (size_t)sn * (p.LP + p.RP);
                 const uint8_t* bo = ring + (size_t)so * (p.LP + p.RP);
                 if (act)
@@ -337,7 +345,6 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
             const int x = pos_of(lane);
             uint32_t* bp = best + (b ^ 1) * p.SW;
             f.sparse[(size_t)(y - 1) * f.W + x0 + x] = (int16_t)(bp[x] & 1023u);
-            bp[x] = 0xffffffffu;
         }
         if (m) {
             const uint2* cb = cs + b * bufstride;
@@ -380,15 +387,17 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                     uint32_t k1 = keyof(x1), k2 = keyof(x2);
                     k1 = __reduce_min_sync(0xffffffffu, k1);
                     k2 = __reduce_min_sync(0xffffffffu, k2);
+                    // this warp owns the pixel and covers every main quad
                     if (lane == 0) {
-                        atomicMin(&bp[x1], k1);
-                        atomicMin(&bp[x2], k2);
+                        bp[x1] = k1;
+                        bp[x2] = k2;
                     }
                 }
             };
             if (fast) pixels(std::true_type{});
             else pixels(std::false_type{});
             // quads beyond the main blocks: lane r takes the pixel of mask bit r
+            __syncwarp();
             if (p.QMAIN < p.Q && ((m >> lane) & 1u)) {
                 const int x = pos_of(lane);
                 const int lim = min(p.D, x0 + x - h);
@@ -404,7 +413,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                         if (d <= lim) key = min(key, c[jj] * 1024u + (uint32_t)d);
                     }
                 }
-                atomicMin(&bp[x], key);
+                bp[x] = min(bp[x], key);
             }
         }
         if (t + 2 < T) named_arrive(BAR_EMPTY0 + b, NVH);
