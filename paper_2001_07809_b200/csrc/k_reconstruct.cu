@@ -1,11 +1,13 @@
 // K6 fill_rows + K7 peek_cols -- dense reconstruction from the sparse map
 // (reference: reconstruct.cpp:11-109, the paper's Algorithms 1 and 2).
 //
-// K6: one CTA per row; the row is staged in shared memory, every thread owns a
-//     contiguous chunk, and two block scans give each chunk the nearest known
-//     (x, d) on either side.  A run of unknowns between consecutive knowns of
-//     equal disparity is filled; knowns never change (reconstruct.cpp:11-33).
-// K7: one CTA per 32 columns x 16 row segments.  Phase 1 summarises each
+// K6: one CTA per row; every thread owns a contiguous chunk (16 pixels in
+//     registers when W % 16 == 0, else a shared-memory row), and two block
+//     scans give each chunk the nearest known (x, d) on either side.  A run of
+//     unknowns between consecutive knowns of equal disparity is filled; knowns
+//     never change (reconstruct.cpp:11-33).
+// K7: one CTA per 16 columns x 32 row segments (a warp = 16 columns x 2
+//     segments: 32-byte row accesses).  Phase 1 summarises each
 //     segment (known count, first/last known); phase 2 derives, per segment,
 //     the nearest known above/below and, per column, the first two / last two
 //     knowns; phase 3 walks the segment again and resolves each run of
@@ -91,8 +93,92 @@ __global__ void __launch_bounds__(kFillThreads) k_fill_rows(Frame f, const int16
     for (int x = tid; x < W; x += kFillThreads) dst[x] = row[x];
 }
 
+// K6 v2: one CTA per row, thread = 16 consecutive pixels held in registers
+// (2 x 16-byte loads / stores; W % 16 == 0, W <= 16384).  Block scans give
+// every chunk the nearest known to its left (max-scan of (x+1) << 16 | d) and
+// right (min-scan of x << 16 | d); the chunk is then filled in registers.
+__global__ void __launch_bounds__(1024) k_fill_rows16(Frame f, const int16_t* __restrict__ in,
+                                                      int16_t* __restrict__ out) {
+    __shared__ uint32_t wl[32], wf[32];
+    const int W = f.W, y = blockIdx.x, tid = threadIdx.x;
+    const int nchunk = W / 16;
+    const bool act = tid < nchunk;
+    const int x0 = tid * 16;
+    int16_t v[16];
+    {
+        uint4 a = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu), b = a;
+        if (act) {
+            const uint4* src = reinterpret_cast<const uint4*>(in + (size_t)y * W + x0);
+            a = __ldcs(src);
+            b = __ldcs(src + 1);
+        }
+        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = (int16_t)(w[i >> 1] >> (16 * (i & 1)));
+    }
+    uint32_t klast = 0, kfirst = 0xffffffffu;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+        if (v[i] >= 0) klast = ((uint32_t)(x0 + i + 1) << 16) | (uint16_t)v[i];
+#pragma unroll
+    for (int i = 15; i >= 0; --i)
+        if (v[i] >= 0) kfirst = ((uint32_t)(x0 + i) << 16) | (uint16_t)v[i];
+    const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    uint32_t incl_l = klast;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl_l, o);
+        if (lane >= o) incl_l = max(incl_l, t);
+    }
+    uint32_t incl_f = kfirst;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_down_sync(0xffffffffu, incl_f, o);
+        if (lane + o < 32) incl_f = min(incl_f, t);
+    }
+    if (lane == 31) wl[wid] = incl_l;
+    if (lane == 0) wf[wid] = incl_f;
+    __syncthreads();
+    uint32_t prev = __shfl_up_sync(0xffffffffu, incl_l, 1);
+    if (lane == 0) prev = 0;
+    for (int i = 0; i < wid; ++i) prev = max(prev, wl[i]);
+    uint32_t next = __shfl_down_sync(0xffffffffu, incl_f, 1);
+    if (lane == 31) next = 0xffffffffu;
+    for (int i = wid + 1; i < nw; ++i) next = min(next, wf[i]);
+    if (!act) return;
+    // fill: a run of unknowns between knowns of equal disparity (the input
+    // snapshot, reconstruct.cpp:11-33).  Left context: pd; right: the next known
+    // inside the chunk or `next`.
+    int pd = prev ? (int)(prev & 0xffffu) : -1;
+    int nd[16];  // disparity of the nearest known at or right of i
+    {
+        int cur = next != 0xffffffffu ? (int)(next & 0xffffu) : -2;
+#pragma unroll
+        for (int i = 15; i >= 0; --i) {
+            if (v[i] >= 0) cur = v[i];
+            nd[i] = cur;
+        }
+    }
+    int16_t o[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        if (v[i] >= 0) {
+            o[i] = v[i];
+            pd = v[i];
+        } else {
+            o[i] = (pd >= 0 && nd[i] == pd) ? (int16_t)pd : (int16_t)-1;
+        }
+    }
+    uint32_t w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = (uint16_t)o[2 * i] | ((uint32_t)(uint16_t)o[2 * i + 1] << 16);
+    uint4* dst = reinterpret_cast<uint4*>(out + (size_t)y * W + x0);
+    dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
 // ------------------------------------------------------------------ K7 ----
-constexpr int PC = 32;  // columns per CTA
+constexpr int PC = 16;  // columns per CTA (a warp = 16 columns x 2 segments)
 constexpr int PS = 32;  // row segments per column
 constexpr int PB = 8;   // rows loaded per batch (independent loads in flight)
 
@@ -107,7 +193,7 @@ __global__ void __launch_bounds__(PC * PS) k_peek_cols(Frame f, const int16_t* _
     __shared__ SegSum seg[PS][PC];
     __shared__ unsigned long long red[PS];
     const int W = f.W, H = f.H, thr = f.thr;
-    const int cx = threadIdx.x, s = threadIdx.y;
+    const int cx = threadIdx.x % PC, s = threadIdx.x / PC;
     const int x = blockIdx.x * PC + cx;
     const int sr = (H + PS - 1) / PS;
     const int ya = min(H, s * sr), yb = min(H, ya + sr);
@@ -201,11 +287,11 @@ __global__ void __launch_bounds__(PC * PS) k_peek_cols(Frame f, const int16_t* _
     }
     // known count for DepthStats::known_fraction
     for (int o = 16; o > 0; o >>= 1) known += __shfl_xor_sync(0xffffffffu, known, o);
-    if (cx == 0) red[s] = known;
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = known;
     __syncthreads();
-    if (s == 0 && cx == 0) {
+    if (threadIdx.x == 0) {
         unsigned long long t = 0;
-        for (int i = 0; i < PS; ++i) t += red[i];
+        for (int i = 0; i < PC * PS / 32; ++i) t += red[i];
         if (t) atomicAdd(&f.sc->known, t);
     }
 }
@@ -214,6 +300,11 @@ __global__ void __launch_bounds__(PC * PS) k_peek_cols(Frame f, const int16_t* _
 
 void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStream_t st) {
     if (f.N == 0) return;
+    if (f.W % 16 == 0 && f.W <= 16384) {
+        const int nt = ((f.W / 16) + 31) / 32 * 32;
+        k_fill_rows16<<<f.H, nt, 0, st>>>(f, in, out);
+        return;
+    }
     const size_t sm = (size_t)f.W * sizeof(int16_t);
     if (sm > 48 * 1024)
         cudaFuncSetAttribute(k_fill_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -222,7 +313,7 @@ void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStrea
 
 void launch_peek_cols(const Frame& f, const int16_t* in, int16_t* out, int16_t*, cudaStream_t st) {
     if (f.N == 0) return;
-    k_peek_cols<<<(f.W + PC - 1) / PC, dim3(PC, PS), 0, st>>>(f, in, out);
+    k_peek_cols<<<(f.W + PC - 1) / PC, PC * PS, 0, st>>>(f, in, out);
 }
 
 size_t peek_scratch_bytes(int, int) { return 0; }
