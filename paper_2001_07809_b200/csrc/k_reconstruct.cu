@@ -6,7 +6,7 @@
 //     scans give each chunk the nearest known (x, d) on either side.  A run of
 //     unknowns between consecutive knowns of equal disparity is filled; knowns
 //     never change (reconstruct.cpp:11-33).
-// K7: one CTA per 16 columns x 32 row segments (a warp = 16 columns x 2
+// K7: one CTA per 16 columns x 64 row segments (a warp = 16 columns x 2
 //     segments: 32-byte row accesses).  Phase 1 summarises each
 //     segment (known count, first/last known); phase 2 derives, per segment,
 //     the nearest known above/below and, per column, the first two / last two
@@ -179,8 +179,8 @@ __global__ void __launch_bounds__(1024) k_fill_rows16(Frame f, const int16_t* __
 
 // ------------------------------------------------------------------ K7 ----
 constexpr int PC = 16;  // columns per CTA (a warp = 16 columns x 2 segments)
-constexpr int PS = 32;  // row segments per column
-constexpr int PB = 8;   // rows loaded per batch (independent loads in flight)
+constexpr int PS = 64;  // row segments per column
+constexpr int PB = 12;  // rows loaded per batch (independent loads in flight)
 
 struct SegSum {
     int count;     // knowns in the segment
@@ -296,6 +296,131 @@ __global__ void __launch_bounds__(PC * PS) k_peek_cols(Frame f, const int16_t* _
     }
 }
 
+// K7 v2: the same segments, branch-free.  Pass 1 (top-down) builds the
+// segment summary and stores, per pixel, the nearest known above it inside the
+// segment (or -1) into `out` as scratch; after the cross-segment context
+// (phase 2) pass 2 walks the segment bottom-up carrying the nearest known
+// below and resolves every pixel with selects.
+__global__ void __launch_bounds__(PC * PS) k_peek_cols2(Frame f, const int16_t* __restrict__ in,
+                                                        int16_t* __restrict__ out) {
+    __shared__ SegSum seg[PS][PC];
+    __shared__ int16_t ctx_ab[PS][PC], ctx_bl[PS][PC];  // nearest known above / below a segment
+    __shared__ int col_total[PC], col_top[PC], col_bot[PC];
+    __shared__ unsigned long long red[PC * PS / 32];
+    const int W = f.W, H = f.H, thr = f.thr;
+    const int cx = threadIdx.x % PC, s = threadIdx.x / PC;
+    const int x = blockIdx.x * PC + cx;
+    const int sr = (H + PS - 1) / PS;
+    const int ya = min(H, s * sr), yb = min(H, ya + sr);
+    const bool col = x < W;
+    // pass 1 (top-down): segment summary; nearest known above inside the
+    // segment (or -1) parked in `out`
+    SegSum m{0, -1, -1, -1, -1};
+    if (col) {
+        int cur = -1;
+        const int16_t* ip = in + (size_t)ya * W + x;
+        int16_t* op = out + (size_t)ya * W + x;
+        for (int yy = ya; yy < yb; yy += PB, ip += (size_t)PB * W, op += (size_t)PB * W) {
+            const int n = min(PB, yb - yy);
+            int16_t v[PB];
+#pragma unroll
+            for (int k = 0; k < PB; ++k) v[k] = k < n ? __ldg(ip + (size_t)k * W) : (int16_t)-1;
+#pragma unroll
+            for (int k = 0; k < PB; ++k) {
+                if (k < n) op[(size_t)k * W] = (int16_t)cur;
+                const int d = v[k];
+                const bool kn = d >= 0;
+                m.f2 = (kn && m.count == 1) ? (int16_t)d : m.f2;
+                m.f1 = (kn && m.count == 0) ? (int16_t)d : m.f1;
+                m.l2 = kn ? m.l1 : m.l2;
+                m.l1 = kn ? (int16_t)d : m.l1;
+                m.count += kn;
+                cur = kn ? d : cur;
+            }
+        }
+    }
+    seg[s][cx] = m;
+    __syncthreads();
+    // phase 2: one thread per column scans the segments once
+    if (s == 0) {
+        int total = 0, last = -1;
+        int cf1 = -1, cf2 = -1;
+        for (int i = 0; i < PS; ++i) {
+            const SegSum g = seg[i][cx];
+            ctx_ab[i][cx] = (int16_t)last;
+            if (g.count) {
+                last = g.l1;
+                if (cf1 < 0) {
+                    cf1 = g.f1;
+                    if (g.count > 1) cf2 = g.f2;
+                } else if (cf2 < 0) {
+                    cf2 = g.f1;
+                }
+            }
+            total += g.count;
+        }
+        int first = -1, cl1 = -1, cl2 = -1;
+        for (int i = PS - 1; i >= 0; --i) {
+            const SegSum g = seg[i][cx];
+            ctx_bl[i][cx] = (int16_t)first;
+            if (g.count) {
+                first = g.f1;
+                if (cl1 < 0) {
+                    cl1 = g.l1;
+                    if (g.count > 1) cl2 = g.l2;
+                } else if (cl2 < 0) {
+                    cl2 = g.l1;
+                }
+            }
+        }
+        col_total[cx] = total;
+        col_top[cx] = total >= 2 ? peek_estimate(cf1, cf2, thr) : -1;
+        col_bot[cx] = total >= 2 ? peek_estimate(cl2, cl1, thr) : -1;
+    }
+    __syncthreads();
+    const int total = col_total[cx], est_top = col_top[cx], est_bot = col_bot[cx];
+    const int above = ctx_ab[s][cx];
+    // pass 2 (bottom-up): nearest known below carried, every pixel resolved
+    unsigned long long known = 0;
+    if (col) {
+        int nb = ctx_bl[s][cx];
+        for (int yy = yb - 1; yy >= ya; yy -= PB) {
+            const int n = min(PB, yy - ya + 1);
+            int16_t v[PB], a[PB];
+            const int16_t* ip = in + (size_t)yy * W + x;
+            int16_t* op = out + (size_t)yy * W + x;
+#pragma unroll
+            for (int k = 0; k < PB; ++k) {
+                v[k] = k < n ? __ldg(ip - (size_t)k * W) : (int16_t)-1;
+                a[k] = k < n ? op[-(long long)k * W] : (int16_t)-1;
+            }
+#pragma unroll
+            for (int k = 0; k < PB; ++k) {
+                if (k >= n) break;
+                const int d = v[k];
+                const int ab = a[k] >= 0 ? a[k] : above;  // nearest known above
+                int r;
+                if (d >= 0) r = d;
+                else if (total == 0) r = -1;
+                else if (total == 1) r = ab >= 0 ? ab : nb;
+                else if (ab >= 0 && nb >= 0) r = peek_estimate(ab, nb, thr);
+                else r = ab < 0 ? est_top : est_bot;
+                op[-(long long)k * W] = (int16_t)r;
+                known += r >= 0;
+                nb = d >= 0 ? d : nb;
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) known += __shfl_xor_sync(0xffffffffu, known, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = known;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int i = 0; i < PC * PS / 32; ++i) t += red[i];
+        if (t) atomicAdd(&f.sc->known, t);
+    }
+}
+
 }  // namespace
 
 void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStream_t st) {
@@ -313,7 +438,7 @@ void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStrea
 
 void launch_peek_cols(const Frame& f, const int16_t* in, int16_t* out, int16_t*, cudaStream_t st) {
     if (f.N == 0) return;
-    k_peek_cols<<<(f.W + PC - 1) / PC, PC * PS, 0, st>>>(f, in, out);
+    k_peek_cols2<<<(f.W + PC - 1) / PC, PC * PS, 0, st>>>(f, in, out);
 }
 
 size_t peek_scratch_bytes(int, int) { return 0; }
