@@ -6,7 +6,7 @@ iS, iE, iW = h.index("Source"), h.index("Instructions Executed"), h.index("Warp 
 tot = 0; ops = collections.Counter(); stall = collections.Counter()
 recs = []
 for r in rows[2:]:
-    if len(r) < len(h): continue
+    if len(r) < len(h) or not (r[iE] or "0").isdigit(): continue
     n = int(r[iE] or 0); s = int(r[iW] or 0)
     op = r[iS].split()[0] if r[iS].split() else ""
     if op.startswith("@"): op = r[iS].split()[1]
