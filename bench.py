@@ -46,7 +46,7 @@ METRIC = "4096x2304 stereo frames/sec end-to-end (per-stage HBM GB/s in roofline
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=60)
+    p.add_argument("--steps", type=int, default=250)  # the paper's 250-frame video
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--config", default="C", choices=sorted(CONFIGS))
@@ -84,7 +84,7 @@ class ClockSampler:
                         self.samples.append(f)
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(0.05)
 
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
