@@ -932,7 +932,53 @@ __global__ void __launch_bounds__(128) k_list_bits(Frame f) {
         }
 }
 
+// Stage entry prune_components: a byte mask (pitched) -> bit rows + count.
+__global__ void __launch_bounds__(256) k_mask_to_bits(Frame f, const uint8_t* __restrict__ mask,
+                                                      uint32_t* __restrict__ rbits) {
+    const int BW = (f.W + 31) / 32;
+    const long long nw = (long long)BW * f.H;
+    unsigned long long cnt = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nw;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(i / BW), wc = (int)(i - (long long)y * BW);
+        const uint8_t* row = mask + (size_t)y * f.P + 32 * wc;
+        uint32_t m = 0;
+        for (int b = 0; b < 32 && 32 * wc + b < f.W; ++b) m |= (row[b] ? 1u : 0u) << b;
+        rbits[(size_t)y * f.bits_words + wc] = m;
+        cnt += __popc(m);
+    }
+    cnt = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&f.sc->refined_count, cnt);
+}
+
 }  // namespace
+
+void launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
+                           uint32_t* sbits, int sbits_words, bool anchors, cudaStream_t st) {
+    // B2 - B8
+    const int ntiles = ((f.W + CT - 1) / CT) * ((f.H + CT - 1) / CT);
+    const int tb = (ntiles + 3) / 4;
+    const int nreg = ((f.W + RW - 1) / RW) * ((f.H + RH - 1) / RH);
+    const size_t rsm = sizeof(RunSmem) * NRW;
+    cudaFuncSetAttribute(k_ccl_region, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
+    k_ccl_region<<<nreg, 32 * NRW, rsm, st>>>(f, rbits, runroot, bord);
+    k_ccl_borders<<<nreg, RW + RH, 0, st>>>(f, bord);
+    k_compress_roots<<<148 * 8, 256, 0, st>>>(f);
+    k_root_stats<<<148 * 4, 256, 0, st>>>(f);
+    k_prune_select_mb<<<kSelBlocks, 256, 0, st>>>(f);
+    cudaMemsetAsync(sbits, 0, (size_t)sbits_words * 4, st);
+    k_prune_roots<<<148 * 4, 256, 0, st>>>(f, sbits);
+    k_prune_first_q<<<148 * 2, 256, 0, st>>>(f, sbits, sbits_words);
+    k_apply_runs<<<tb, 128, 0, st>>>(f, rbits, runroot, anchors ? 1 : 0);
+}
+
+void launch_prune_mask_bits(const Frame& f, const uint8_t* mask, uint32_t* rbits, int32_t* runroot,
+                            int32_t* bord, uint32_t* sbits, int sbits_words, cudaStream_t st) {
+    if (f.N == 0) return;
+    const long long nw = (long long)((f.W + 31) / 32) * f.H;
+    k_mask_to_bits<<<(int)std::min<long long>((nw + 255) / 256, 148 * 8), 256, 0, st>>>(f, mask, rbits);
+    launch_ccl_prune_bits(f, rbits, runroot, bord, sbits, sbits_words, false, st);
+}
 
 void launch_boundary_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
                           uint32_t* sbits, int sbits_words, bool anchors, bool want_list,
@@ -952,21 +998,7 @@ void launch_boundary_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int
         case 4: k_morph_bits<4><<<gb, 128, 0, st>>>(f, rbits); break;
         default: k_morph_bits<8><<<gb, 128, 0, st>>>(f, rbits); break;
     }
-    // B2, B3
-    const int ntiles = ((f.W + CT - 1) / CT) * ((f.H + CT - 1) / CT);
-    const int tb = (ntiles + 3) / 4;
-    const int nreg = ((f.W + RW - 1) / RW) * ((f.H + RH - 1) / RH);
-    const size_t rsm = sizeof(RunSmem) * NRW;
-    cudaFuncSetAttribute(k_ccl_region, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
-    k_ccl_region<<<nreg, 32 * NRW, rsm, st>>>(f, rbits, runroot, bord);
-    k_ccl_borders<<<nreg, RW + RH, 0, st>>>(f, bord);
-    k_compress_roots<<<148 * 8, 256, 0, st>>>(f);
-    k_root_stats<<<148 * 4, 256, 0, st>>>(f);
-    k_prune_select_mb<<<kSelBlocks, 256, 0, st>>>(f);
-    cudaMemsetAsync(sbits, 0, (size_t)sbits_words * 4, st);
-    k_prune_roots<<<148 * 4, 256, 0, st>>>(f, sbits);
-    k_prune_first_q<<<148 * 2, 256, 0, st>>>(f, sbits, sbits_words);
-    k_apply_runs<<<tb, 128, 0, st>>>(f, rbits, runroot, anchors ? 1 : 0);
+    launch_ccl_prune_bits(f, rbits, runroot, bord, sbits, sbits_words, anchors, st);
     if (want_list) k_list_bits<<<f.n_chunks, 128, 0, st>>>(f);
 }
 

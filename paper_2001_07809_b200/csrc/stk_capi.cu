@@ -1051,9 +1051,9 @@ stk_status stk_prune_components(stk_ctx* ctx, const uint8_t* mask, int w, int h,
     f.window = 1;
     f.hw = 0;
     f.mprn = s.mprn;
-    launch_count_mask(f, s.mref, st);
-    launch_ccl(f, st);
-    launch_prune(f, false, st);
+    f.manc = s.manc;
+    // the frame path's bit-packed run CCL + prune (k_bnd.cu)
+    launch_prune_mask_bits(f, s.mref, s.rbits, s.runroot, s.bord, s.sbits, s.sbits_words, st);
     D2H_PLANE(out, s.mprn, 1);
     FINISH();
 }

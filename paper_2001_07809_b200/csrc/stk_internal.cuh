@@ -129,6 +129,12 @@ void launch_prune_select(const Frame& f, cudaStream_t st);        // K4e alone
 void launch_boundary_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
                           uint32_t* sbits, int sbits_words, bool anchors, bool want_list,
                           cudaStream_t st);
+// B2-B8 alone on refined bits already in rbits (refined_count set)
+void launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
+                           uint32_t* sbits, int sbits_words, bool anchors, cudaStream_t st);
+// stage entry prune_components on a pitched byte mask (writes f.mprn / f.manc)
+void launch_prune_mask_bits(const Frame& f, const uint8_t* mask, uint32_t* rbits, int32_t* runroot,
+                            int32_t* bord, uint32_t* sbits, int sbits_words, cudaStream_t st);
 // true when launch_sad will run the per-pixel list kernel (it needs f.list)
 bool sad_uses_list(const Frame& f, int kernel);
 void launch_prune(const Frame& f, bool anchors, cudaStream_t st); // K4e-g

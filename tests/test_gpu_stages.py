@@ -165,6 +165,33 @@ def test_prune_many_equal_sizes_partial_class(dev, stk, port):
         eq(stk.prune_components(m, frac, device=dev), port.prune(m, frac))
 
 
+@pytest.mark.parametrize("w,h,seed,pct", [(300, 200, 1, 15), (517, 331, 2, 30), (1024, 256, 3, 8),
+                                         (129, 65, 4, 45), (700, 140, 5, 22)])
+def test_prune_bitpacked_vs_oracle(dev, stk, port, synth, w, h, seed, pct):
+    """prune_components runs the frame path's bit-packed run CCL (region merge
+    across 128x64 regions, global union-find, s*/q select, first-q bitmap scan):
+    random masks with many small components, crossing tile and region borders,
+    at fractions that cut inside a size class (q > 0) and beyond."""
+    m = synth.random_mask(w, h, seed, pct)
+    for frac in (0.0, 0.01, 0.04, 0.1, 0.3, 0.6):
+        eq(stk.prune_components(m, frac, device=dev), port.prune(m, frac))
+
+
+def test_prune_bitpacked_giant_and_lines(dev, stk, port):
+    """One component spanning every region (a comb) next to many singletons and
+    2-pixel dominoes, plus long runs along tile / region borders."""
+    m = np.zeros((300, 700), np.uint8)
+    m[5, :] = 1                      # spine across all regions
+    m[5:290:1, ::31] = 1             # teeth down tile borders (x = 0, 31, 62, ...)
+    m[63:65, :600] = 1               # a run pair straddling the 64-row region seam
+    m[100:300:4, 3:700:5] = 1        # singletons
+    m[102:300:8, 1:690:7] = 1
+    m[102:300:8, 2:690:7] = 1        # dominoes
+    m[31:33, 127:129] = 1            # 2x2 block on a region corner
+    for frac in (0.0, 0.02, 0.05, 0.2):
+        eq(stk.prune_components(m, frac, device=dev), port.prune(m, frac))
+
+
 def test_anchors(dev, stk, golden, synth):
     eq(stk.add_border_anchors(np.zeros((10, 10), np.uint8), 4, device=dev), golden["anch_10_4"])
     eq(stk.add_border_anchors(np.zeros((5, 7), np.uint8), 0, device=dev), golden["anch_7_0"])
