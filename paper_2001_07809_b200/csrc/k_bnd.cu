@@ -20,14 +20,15 @@
 //                   neighbours in the regions above, left-border pixels with
 //                   the left region (lock-free union, hash-priority linking,
 //                   path halving).
-//   B4 compress     region roots (dense ids) -> global root; size and minimum
-//                   raster index (the reference's discovery order) summed /
-//                   min'ed at the global root.
-//   B5 root_stats   global roots (par[g] == g): size histogram for the prune.
-//   B6 prune_select s*, q from the size histogram (multi-block).
-//   B7 prune_roots  size < s* -> removed; size == s* -> bit minkey of a raster
-//                   bitmap; B7b then removes the first q of them in raster
-//                   (= label) order with one ordered scan of the bitmap.
+//   B4-B7 prune_fused  one cooperative launch, grid barriers between:
+//                   compress region roots (dense ids) to global roots with
+//                   size and minimum raster index (the reference's discovery
+//                   order) summed / min'ed at the root; size histogram;
+//                   s* = smallest size whose class-cumulative pixel count
+//                   exceeds B = floor(budget), q = floor((B - CS(s*-1)) / s*);
+//                   size < s* removed; size == s* -> bit (min raster index) of
+//                   a bitmap whose first q set bits in raster (= label) order
+//                   are removed by one ordered scan.
 //   B8 apply_runs   warp per tile: runs -> their root -> removed?  -> pruned
 //                   bits, border anchors, window filter -> matchable bits and
 //                   the frame counts (bytes in full mode).
@@ -580,62 +581,7 @@ __global__ void __launch_bounds__(RW + RH) k_ccl_borders(Frame f, const int32_t*
     }
 }
 
-// ------------------------------------------------------------------ B4 ----
-// Region roots -> global root (path compression); size and minimum raster
-// index (cmin) accumulated at the global root.
-__global__ void __launch_bounds__(256) k_compress_roots(Frame f) {
-    const int n = (int)f.sc->n_lroots;
-    for (int id = blockIdx.x * blockDim.x + threadIdx.x; id < n; id += gridDim.x * blockDim.x) {
-        const int r = gfind(f.par, id);
-        if (r != id) {
-            f.par[id] = r;
-            atomicAdd(f.cnt + r, __ldcg(f.cnt + id));
-            atomicMin(f.roots + r, __ldcg(f.roots + id));
-        }
-    }
-}
-
-// ------------------------------------------------------------------ B5 ----
-__global__ void __launch_bounds__(256) k_root_stats(Frame f) {
-    const int n = (int)f.sc->n_lroots;
-    const unsigned long long B = f.sc->budget;
-    unsigned nr = 0;
-    for (int id = blockIdx.x * blockDim.x + threadIdx.x; id < n; id += gridDim.x * blockDim.x) {
-        if (__ldcg(f.par + id) == id) {
-            ++nr;
-            const uint32_t sz = __ldcg(f.cnt + id);
-            if (sz <= B + 1) atomicAdd(f.szhist + sz, 1u);
-        }
-    }
-    nr = __reduce_add_sync(0xffffffffu, nr);
-    if ((threadIdx.x & 31) == 0 && nr) atomicAdd(&f.sc->n_roots, nr);
-}
-
-// ------------------------------------------------------------------ B7 ----
-// size < s* -> removed; size == s* -> bit cmin of the raster bitmap (and the
-// id behind it in idmap = f.rank)
-__global__ void __launch_bounds__(256) k_prune_roots(Frame f, uint32_t* __restrict__ sbits) {
-    const int n = (int)f.sc->n_lroots;
-    const unsigned long long sst = f.sc->s_star, q = f.sc->q;
-    for (int id = blockIdx.x * blockDim.x + threadIdx.x; id < n; id += gridDim.x * blockDim.x) {
-        if (__ldcg(f.par + id) != id) continue;
-        const uint32_t sz = __ldcg(f.cnt + id);
-        if (sz < sst) {
-            f.cnt[id] = sz | kRemoved;
-        } else if (sz == sst && q > 0) {
-            const int k = __ldcg(f.roots + id);
-            f.rank[k] = id;
-            atomicOr(sbits + (k >> 5), 1u << (k & 31));
-        }
-    }
-}
-
-// ------------------------------------------------------------------ B6 ----
-// s* = smallest size whose class-cumulative pixel count CS(s) exceeds
-// B = floor(budget), q = floor((B - CS(s*-1)) / s*) (see k_ccl.cu).  Sizes
-// 1..B+1 are split over kSelBlocks blocks; the last block to finish scans the
-// block sums and then the bins of the block where CS crosses B.
-constexpr int kSelBlocks = 128;
+// 256-thread exclusive block scan (u64) used by the prune select.
 
 __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v,
                                                               unsigned long long* sh,
@@ -658,133 +604,6 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
     __syncthreads();
     *total = tot;
     return off + x - v;
-}
-
-__global__ void __launch_bounds__(256) k_prune_select_mb(Frame f) {
-    __shared__ unsigned long long sh[8];
-    __shared__ unsigned int s_last;
-    __shared__ int s_blk;
-    __shared__ unsigned long long s_before;
-    DevScalars* sc = f.sc;
-    const unsigned long long B = sc->budget;
-    const long long L = (long long)B + 1;  // sizes 1..B+1
-    const long long per = (L + kSelBlocks - 1) / kSelBlocks;
-    auto range_sum = [&](long long a0, long long a1) {  // sum over [a0, a1) split by thread
-        const long long pt = (a1 - a0 + 255) / 256;
-        const long long t0 = a0 + threadIdx.x * pt, t1 = min(t0 + pt, a1);
-        unsigned long long sum = 0;
-        for (long long s = t0; s < t1; ++s) sum += (unsigned long long)s * __ldcg(f.szhist + s);
-        return sum;
-    };
-    {
-        const long long a0 = 1 + blockIdx.x * per, a1 = min(a0 + per, L + 1);
-        unsigned long long tot;
-        block_excl_scan(a0 < a1 ? range_sum(a0, a1) : 0ull, sh, &tot);
-        if (threadIdx.x == 0) {
-            sc->psel[blockIdx.x] = tot;
-            __threadfence();
-            s_last = atomicAdd(&sc->psel_done, 1u) == kSelBlocks - 1;
-        }
-        __syncthreads();
-        if (!s_last) return;
-        __threadfence();
-    }
-    // last block: which block's range crosses B?
-    if (threadIdx.x == 0) {
-        sc->s_star = B + 2;  // default: every size <= B+1 goes, q = 0
-        sc->q = 0;
-        s_blk = -1;
-    }
-    unsigned long long tot;
-    const unsigned long long v = threadIdx.x < kSelBlocks ? __ldcg(&sc->psel[threadIdx.x]) : 0ull;
-    const unsigned long long before = block_excl_scan(v, sh, &tot);
-    if (threadIdx.x < kSelBlocks && before <= B && before + v > B) {
-        s_blk = threadIdx.x;
-        s_before = before;
-    }
-    __syncthreads();
-    if (s_blk < 0) return;
-    const long long a0 = 1 + s_blk * per, a1 = min(a0 + per, L + 1);
-    const long long pt = (a1 - a0 + 255) / 256;
-    const long long t0 = a0 + threadIdx.x * pt, t1 = min(t0 + pt, a1);
-    unsigned long long mine = 0;
-    for (long long s = t0; s < t1; ++s) mine += (unsigned long long)s * __ldcg(f.szhist + s);
-    const unsigned long long tb = s_before + block_excl_scan(mine, sh, &tot);
-    if (tb <= B && tb + mine > B) {  // exactly one thread
-        unsigned long long cs = tb;
-        for (long long s = t0; s < t1; ++s) {
-            const unsigned long long add = (unsigned long long)s * __ldcg(f.szhist + s);
-            if (cs + add > B) {
-                sc->s_star = (unsigned long long)s;
-                sc->q = (B - cs) / (unsigned long long)s;
-                break;
-            }
-            cs += add;
-        }
-    }
-}
-
-// first q set bits of sbits in raster order -> removed.  Chunks of 1024 words
-// claimed in order; decoupled look-back on the per-chunk popcounts.
-__global__ void __launch_bounds__(256) k_prune_first_q(Frame f, const uint32_t* __restrict__ sbits,
-                                                       int nwords) {
-    __shared__ uint32_t s_chunk, s_excl;
-    __shared__ uint32_t wcount[8];
-    const unsigned long long q = f.sc->q;
-    if (q == 0) return;
-    unsigned long long* status = f.lb + LB_RANK * f.lb_stride;
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    while (true) {
-        __syncthreads();
-        if (threadIdx.x == 0) s_chunk = atomicAdd(&f.sc->ctr[LB_RANK], 1u);
-        __syncthreads();
-        const int c = (int)s_chunk;
-        if (c * 1024 >= nwords) return;
-        uint32_t w[4], cnt = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int idx = c * 1024 + wid * 128 + j * 32 + lane;
-            w[j] = idx < nwords ? __ldcg(sbits + idx) : 0u;
-            cnt += __popc(w[j]);
-        }
-        // per-lane exclusive prefix within the warp, warp totals across the block
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
-        }
-        if (lane == 31) wcount[wid] = incl;
-        __syncthreads();
-        if (wid == 0) {
-            const uint32_t agg = __reduce_add_sync(0xffffffffu, lane < 8 ? wcount[lane] : 0u);
-            const uint32_t excl = lb_exclusive_warp(status, c, agg);
-            if (lane == 0) s_excl = excl;
-        }
-        __syncthreads();
-        // words are j-major (index c*1024 + wid*128 + j*32 + lane): rank the
-        // bits in raster order with one lane scan per j
-        uint32_t run = s_excl;
-        for (int i = 0; i < wid; ++i) run += wcount[i];
-        if (run >= q) continue;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t cj = __popc(w[j]);
-            uint32_t inc2 = cj;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, inc2, o);
-                if (lane >= o) inc2 += v;
-            }
-            uint32_t rk = run + inc2 - cj;
-            const int base = (c * 1024 + wid * 128 + j * 32 + lane) * 32;
-            for (uint32_t t = w[j]; t && rk < q; t &= t - 1, ++rk) {
-                const int k = base + __ffs(t) - 1;  // a component's cmin
-                f.cnt[__ldcg(f.rank + k)] |= kRemoved;
-            }
-            run += __shfl_sync(0xffffffffu, inc2, 31);
-        }
-    }
 }
 
 // ------------------------------------------------------------------ B8 ----
@@ -932,6 +751,178 @@ __global__ void __launch_bounds__(128) k_list_bits(Frame f) {
         }
 }
 
+// ------------------------------------------------------------- B4-B7 fused --
+// One cooperative launch (all blocks co-resident) runs compress, root stats,
+// the s*/q select, the size classes and the first-q raster scan, separated by
+// grid barriers instead of five kernel boundaries.
+__device__ __forceinline__ void grid_barrier(DevScalars* sc, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* vgen = &sc->gbar_gen;
+        const unsigned gen = *vgen;
+        __threadfence();
+        if (atomicAdd(&sc->gbar_count, 1u) == nblocks - 1) {
+            sc->gbar_count = 0;
+            __threadfence();
+            atomicAdd(&sc->gbar_gen, 1u);
+        } else {
+            while (*vgen == gen) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_prune_fused(Frame f, uint32_t* __restrict__ sbits,
+                                                     int nwords) {
+    __shared__ unsigned long long sh[8];
+    __shared__ int s_blk;
+    __shared__ unsigned long long s_before;
+    __shared__ uint32_t s_wsum[8];
+    DevScalars* sc = f.sc;
+    const unsigned G = gridDim.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int gt = blockIdx.x * 256 + tid, gs = G * 256;
+    const int n = (int)sc->n_lroots;
+    // B4 compress
+    for (int id = gt; id < n; id += gs) {
+        const int r = gfind(f.par, id);
+        if (r != id) {
+            f.par[id] = r;
+            atomicAdd(f.cnt + r, __ldcg(f.cnt + id));
+            atomicMin(f.roots + r, __ldcg(f.roots + id));
+        }
+    }
+    grid_barrier(sc, G);
+    // B5 root stats
+    const unsigned long long B = sc->budget;
+    {
+        unsigned nr = 0;
+        for (int id = gt; id < n; id += gs) {
+            if (__ldcg(f.par + id) == id) {
+                ++nr;
+                const uint32_t sz = __ldcg(f.cnt + id);
+                if (sz <= B + 1) atomicAdd(f.szhist + sz, 1u);
+            }
+        }
+        nr = __reduce_add_sync(0xffffffffu, nr);
+        if (lane == 0 && nr) atomicAdd(&sc->n_roots, nr);
+    }
+    grid_barrier(sc, G);
+    // B6 select: block sums over sizes 1..B+1, then block 0 finds s*, q
+    const long long L = (long long)B + 1;
+    const long long per = (L + G - 1) / G;
+    auto bin_sum = [&](long long a0, long long a1) {
+        const long long pt = (a1 - a0 + 255) / 256;
+        const long long t0 = a0 + tid * pt, t1 = min(t0 + pt, a1);
+        unsigned long long sum = 0;
+        for (long long s = t0; s < t1; ++s) sum += (unsigned long long)s * __ldcg(f.szhist + s);
+        return sum;
+    };
+    {
+        const long long a0 = 1 + blockIdx.x * per, a1 = min(a0 + per, L + 1);
+        unsigned long long tot;
+        block_excl_scan(a0 < a1 ? bin_sum(a0, a1) : 0ull, sh, &tot);
+        if (tid == 0) sc->gsum[blockIdx.x] = tot;
+    }
+    grid_barrier(sc, G);
+    if (blockIdx.x == 0) {
+        if (tid == 0) {
+            sc->s_star = B + 2;
+            sc->q = 0;
+            s_blk = -1;
+        }
+        // scan the G block sums (G <= 256 * ... handled in chunks of 256)
+        unsigned long long base = 0;
+        for (int c0 = 0; c0 < (int)G; c0 += 256) {
+            const int i = c0 + tid;
+            const unsigned long long v = i < (int)G ? __ldcg(&sc->gsum[i]) : 0ull;
+            unsigned long long tot;
+            const unsigned long long before = base + block_excl_scan(v, sh, &tot);
+            if (i < (int)G && before <= B && before + v > B) {
+                s_blk = i;
+                s_before = before;
+            }
+            base += tot;
+        }
+        __syncthreads();
+        if (s_blk >= 0) {
+            const long long a0 = 1 + s_blk * per, a1 = min(a0 + per, L + 1);
+            const long long pt = (a1 - a0 + 255) / 256;
+            const long long t0 = a0 + tid * pt, t1 = min(t0 + pt, a1);
+            unsigned long long mine = 0;
+            for (long long s = t0; s < t1; ++s) mine += (unsigned long long)s * __ldcg(f.szhist + s);
+            unsigned long long tot;
+            const unsigned long long tb = s_before + block_excl_scan(mine, sh, &tot);
+            if (tb <= B && tb + mine > B) {
+                unsigned long long cs = tb;
+                for (long long s = t0; s < t1; ++s) {
+                    const unsigned long long add = (unsigned long long)s * __ldcg(f.szhist + s);
+                    if (cs + add > B) {
+                        sc->s_star = (unsigned long long)s;
+                        sc->q = (B - cs) / (unsigned long long)s;
+                        break;
+                    }
+                    cs += add;
+                }
+            }
+        }
+    }
+    grid_barrier(sc, G);
+    // B7 size classes
+    const unsigned long long sst = sc->s_star, q = sc->q;
+    for (int id = gt; id < n; id += gs) {
+        if (__ldcg(f.par + id) != id) continue;
+        const uint32_t sz = __ldcg(f.cnt + id);
+        if (sz < sst) {
+            f.cnt[id] = sz | kRemoved;
+        } else if (sz == sst && q > 0) {
+            const int k = __ldcg(f.roots + id);
+            f.rank[k] = id;
+            atomicOr(sbits + (k >> 5), 1u << (k & 31));
+        }
+    }
+    if (q == 0) return;  // uniform: no barrier is pending
+    grid_barrier(sc, G);
+    // B7b: the first q size-s* components in raster order.  Block b owns words
+    // [b * per_w, (b + 1) * per_w); counts, barrier, prefix over earlier blocks.
+    const int per_w = (nwords + G - 1) / G;
+    const int w0 = blockIdx.x * per_w, w1 = min(w0 + per_w, nwords);
+    uint32_t mycnt = 0;
+    for (int i = w0 + tid; i < w1; i += 256) mycnt += __popc(__ldcg(sbits + i));
+    mycnt = __reduce_add_sync(0xffffffffu, mycnt);
+    if (lane == 0) s_wsum[wid] = mycnt;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t t = 0;
+        for (int i = 0; i < 8; ++i) t += s_wsum[i];
+        sc->gcnt[blockIdx.x] = t;
+    }
+    grid_barrier(sc, G);
+    uint32_t before = 0;
+    for (int i = tid; i < (int)blockIdx.x; i += 256) before += __ldcg(&sc->gcnt[i]);
+    before = __reduce_add_sync(0xffffffffu, before);
+    if (lane == 0) s_wsum[wid] = before;
+    __syncthreads();
+    uint32_t run = 0;
+    for (int i = 0; i < 8; ++i) run += s_wsum[i];
+    if (run >= q) return;
+    // walk the block's words in order, 256 at a time, warp-then-block scan
+    for (int c0 = w0; c0 < w1 && run < q; c0 += 256) {
+        const int i = c0 + tid;
+        const uint32_t wd = i < w1 ? __ldcg(sbits + i) : 0u;
+        const uint32_t cnt = __popc(wd);
+        unsigned long long tot;
+        const uint32_t ex = (uint32_t)block_excl_scan(cnt, sh, &tot);
+        uint32_t rk = run + ex;
+        for (uint32_t t = wd; t && rk < q; t &= t - 1, ++rk) {
+            const int k = i * 32 + __ffs(t) - 1;
+            f.cnt[__ldcg(f.rank + k)] |= kRemoved;
+        }
+        run += (uint32_t)tot;
+    }
+}
+
 // Stage entry prune_components: a byte mask (pitched) -> bit rows + count.
 __global__ void __launch_bounds__(256) k_mask_to_bits(Frame f, const uint8_t* __restrict__ mask,
                                                       uint32_t* __restrict__ rbits) {
@@ -963,12 +954,20 @@ void launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, in
     cudaFuncSetAttribute(k_ccl_region, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
     k_ccl_region<<<nreg, 32 * NRW, rsm, st>>>(f, rbits, runroot, bord);
     k_ccl_borders<<<nreg, RW + RH, 0, st>>>(f, bord);
-    k_compress_roots<<<148 * 8, 256, 0, st>>>(f);
-    k_root_stats<<<148 * 4, 256, 0, st>>>(f);
-    k_prune_select_mb<<<kSelBlocks, 256, 0, st>>>(f);
     cudaMemsetAsync(sbits, 0, (size_t)sbits_words * 4, st);
-    k_prune_roots<<<148 * 4, 256, 0, st>>>(f, sbits);
-    k_prune_first_q<<<148 * 2, 256, 0, st>>>(f, sbits, sbits_words);
+    {   // B4-B7 in one cooperative launch (co-resident blocks, grid barriers)
+        static int g_blocks = 0;
+        if (!g_blocks) {
+            int per_sm = 0, sms = 148, dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_prune_fused, 256, 0);
+            g_blocks = std::min(512, std::max(1, std::min(per_sm, 2)) * sms);  // <= gsum/gcnt slots
+        }
+        int nw = sbits_words;
+        void* args[] = {(void*)&f, (void*)&sbits, (void*)&nw};
+        cudaLaunchCooperativeKernel((const void*)k_prune_fused, dim3(g_blocks), dim3(256), args, 0, st);
+    }
     k_apply_runs<<<tb, 128, 0, st>>>(f, rbits, runroot, anchors ? 1 : 0);
 }
 

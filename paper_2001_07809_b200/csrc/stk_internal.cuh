@@ -48,8 +48,12 @@ struct DevScalars {
     unsigned int pad1;
     unsigned int ctr[LB_COUNT];        // dynamic chunk counters
     unsigned int psel_done;            // prune select: finished blocks
+    unsigned int gbar_count;           // grid barrier (cooperative prune kernel)
+    unsigned int gbar_gen;
     unsigned int pad2;
     unsigned long long psel[128];      // prune select: per-block pixel sums
+    unsigned long long gsum[512];      // cooperative prune: per-block pixel sums
+    unsigned int gcnt[512];            // cooperative prune: per-block size-s* root counts
 };
 
 // Everything a kernel needs to know about one frame, passed by value.
