@@ -51,10 +51,13 @@ def parse():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--config", default="C", choices=sorted(CONFIGS))
     p.add_argument("--pool", type=int, default=8, help="distinct synthetic frames cycled")
-    p.add_argument("--slots", type=int, default=3, help="frames in flight per GPU")
+    p.add_argument("--slots", type=int, default=4, help="frames in flight per GPU")
     p.add_argument("--sad", default="auto", choices=["auto", "list", "strip"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-s", type=float, default=20.0)
+    p.add_argument("--e2e-dense", action="store_true",
+                   help="also read the dense disparity back in the e2e leg (run_refocus_pipeline "
+                        "returns only the refocused image; DepthResult is optional)")
     return p.parse_args()
 
 
@@ -309,7 +312,7 @@ def main():
     outs = [_lib.StkFrameOut() for _ in range(S)]
     for s in range(S):
         outs[s].refocused = ho[s][0].ctypes.data
-        outs[s].dense = ho[s][1].ctypes.data
+        outs[s].dense = ho[s][1].ctypes.data if args.e2e_dense else None
 
     def submit_host(i):
         slot = i % S
@@ -404,7 +407,8 @@ def main():
                    "parallelism": f"frame-sharded x{world} (frame f -> rank f % {world}, no NCCL)",
                    "sad_kernel": args.sad, "matched_fraction": round(matched_frac, 4)},
         "e2e": {"value": round(fps_e2e, 3), "unit": "frames/s",
-                "h2d_bytes_per_step": 2 * 3 * N, "d2h_bytes_per_step": 3 * N + 2 * N,
+                "h2d_bytes_per_step": 2 * 3 * N,
+                "d2h_bytes_per_step": 3 * N + (2 * N if args.e2e_dense else 0),
                 "path": "stk_frame_submit (C-ABI, pinned host buffers)"},
         "gpu_launches": int(kernels_per_frame * args.steps * 2),
         "kernels_per_frame": int(kernels_per_frame),

@@ -34,6 +34,7 @@
 // EMPTY[b] (horizontal arrive, vertical sync) on the double-buffered colsum
 // rows, so row t's horizontal pass overlaps row t+1's vertical pass.  Only
 // pixels whose matchable bit is set (K4g) are evaluated and written.
+#include <cstdlib>
 #include <type_traits>
 
 #include "stk_device.cuh"
@@ -528,8 +529,14 @@ bool launch_sad_ws(const Frame& f, cudaStream_t st, bool dry) {
     if (!sm) return false;
     const int strips = (f.W + p.SW - 1) / p.SW;
     const int rows = f.H - 2 * h;
-    // one wave of one CTA per SM when possible; bands of >= 32 rows
-    int bands = std::max(1, sms / strips);
+    // one wave of one CTA per SM when possible; bands of >= 32 rows.
+    // STK_SAD_SMS (experiment knob) caps the SMs the kernel takes so other
+    // frames' kernels can run beside it.
+    static const int sms_cap = [] {
+        const char* e = getenv("STK_SAD_SMS");
+        return e ? atoi(e) : 0;
+    }();
+    int bands = std::max(1, (sms_cap > 0 ? std::min(sms, sms_cap) : sms) / strips);
     bands = std::min(bands, std::max(1, rows / 32));
     p.TH = (rows + bands - 1) / bands;
     bands = (rows + p.TH - 1) / p.TH;
