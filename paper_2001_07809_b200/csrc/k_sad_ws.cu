@@ -295,18 +295,15 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
     const int hw = wp - p.NVW;
     const int htid = tid - 32 * p.NVW;
     const int NW32 = p.SW / 32;                 // mask words per strip row
-    const int NPW = 8 / p.NHW;                  // nibbles per word per warp (1, 2, 4)
-    const int lnpw = NPW == 1 ? 0 : (NPW == 2 ? 1 : 2);
-    // position (strip column) of bit r of this warp's mask
-    auto pos_of = [&](int r) {
-        const int j = r >> (2 + lnpw), k = (r >> 2) & (NPW - 1);
-        return 32 * j + 4 * (hw + p.NHW * k) + (r & 3);
-    };
-    // warp mask of row y: lane gi < 8 fetches nibble group gi (word gi >> lnpw,
-    // nibble hw + NHW * (gi & (NPW-1))) and the warp OR-reduces the groups
+    // warp hw owns the 4-column groups gi = NHW*k + hw, k = 0..7 (SW = 32*NHW);
+    // bit r of its mask is column 4*(NHW*(r>>2) + hw) + (r&3)
+    auto pos_of = [&](int r) { return 4 * (p.NHW * (r >> 2) + hw) + (r & 3); };
+    // warp mask of row y: lane k < 8 fetches group NHW*k + hw (word gi>>3,
+    // nibble gi&7) and the warp OR-reduces the groups
     const uint32_t* mcol = f.mbits + (x0 >> 5);
-    const int mj = (lane & 7) >> lnpw;
-    const int mshift = 4 * (hw + p.NHW * ((lane & 7) & (NPW - 1)));
+    const int mgi = p.NHW * (lane & 7) + hw;
+    const int mj = mgi >> 3;
+    const int mshift = 4 * (mgi & 7);
     const bool mload = lane < 8 && x0 + 32 * mj < f.W;
     auto load_mask = [&](int y) {
         const uint32_t wd = mload ? __ldg(mcol + (size_t)y * f.bits_words + mj) : 0u;
@@ -442,7 +439,7 @@ void run_ws(const Frame& f, const WP& p, size_t sm, int bands, cudaStream_t st) 
 template <int WIN>
 struct Shape {
     static constexpr int K = WIN <= 21 ? 12 : 8;
-    static constexpr int G = WIN <= 21 ? 3 : 4;
+    static constexpr int G = WIN <= 21 ? 3 : 5;  // 33 / 65 quads at D = 128 / 256
 };
 
 template <int WIN>
@@ -481,7 +478,7 @@ bool launch_sad_ws(const Frame& f, cudaStream_t st, bool dry) {
     // strip width: as wide as shared memory allows (fewer halo columns)
     const int sms = 148;
     size_t sm = 0;
-    for (int SW : {256, 128, 64}) {
+    for (int SW : {256, 192, 128, 96, 64}) {
         p.SW = SW;
         p.CW = SW + w - 1;
         p.NCH = (p.CW + K - 1) / K;
@@ -489,23 +486,23 @@ bool launch_sad_ws(const Frame& f, cudaStream_t st, bool dry) {
         // bank pairs), residue chosen to minimise the vertical warps' 8-byte
         // store conflicts (a half-warp = 16 lanes per shared-memory wavefront)
         {
-            const int base = (p.NCH * (K + 1) + 1 + 15) & ~15;
-            int bestc = 1, bestcost = 1 << 30;
-            for (int c = 1; c < 16; c += 2) {
+            const int base = p.NCH * (K + 1) + 1;  // skewed columns + the zero slot
+            int bestc = base | 1, bestcost = 1 << 30;
+            for (int c = base | 1; c < base + 16; c += 2) {
                 int cost = 0;
                 for (int t0 = 0; t0 < p.NG * p.NCH; t0 += 16) {
                     int cnt[16] = {0};
                     int mx = 0;
                     for (int l = t0; l < std::min(t0 + 16, p.NG * p.NCH); ++l) {
                         const int ch = l % p.NCH, g = l / p.NCH;
-                        const int sl = ((g * G) * (base + c) + ch * (K + 1)) & 15;
+                        const int sl = ((g * G) * c + ch * (K + 1)) & 15;
                         mx = std::max(mx, ++cnt[sl]);
                     }
                     cost += mx;
                 }
                 if (cost < bestcost) bestcost = cost, bestc = c;
             }
-            p.CSW = base + bestc;
+            p.CSW = bestc;
         }
         p.NSEG = SW / kSegW;
         p.NHW = p.NSEG;
@@ -523,7 +520,7 @@ bool launch_sad_ws(const Frame& f, cudaStream_t st, bool dry) {
         const int NE = w <= 21 ? (w == 21 ? WinTab<21, 12>::NE : WinTab<15, 12>::NE) : WinTab<31, 8>::NE;
         sm = (size_t)2 * p.QP * p.CSW * 8 + (size_t)p.RS * (p.LP + p.RP) + p.RS * 8 +
              2 * SW * 4 + (size_t)SW * NE * 4;
-        if (sm <= 220 * 1024 && p.nthreads <= kMaxThreads) break;
+        if (sm <= 226 * 1024 && p.nthreads <= kMaxThreads) break;
         sm = 0;
     }
     if (!sm) return false;
