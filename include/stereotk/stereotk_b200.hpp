@@ -163,6 +163,21 @@ DisparityMap match_boundary_pixels(const GrayImage& left, const GrayImage& right
                                    const BoundaryMask& mask, const MatchConfig& config,
                                    int workers = 1);
 
+// ---------------------------------------------------------- evaluate ----
+// evaluate.hpp:10-36, 57-58 (file I/O entry points are not part of this
+// library).
+struct EvalResult {
+    double bad_pixel_rate = 0.0;
+    std::uint64_t compared = 0;
+    std::uint64_t excluded = 0;
+    double delta_d = 0.0;
+};
+EvalResult bad_pixel_rate(const DisparityMap& computed, const DisparityMap& truth, double delta_d,
+                          int workers = 1);
+DisparityMap dense_sad_baseline(const GrayImage& left, const GrayImage& right,
+                                const MatchConfig& config, int workers = 1);
+std::string eval_report_json(const EvalResult& result);
+
 // -------------------------------------------------------- reconstruct ----
 DisparityMap fill_scanlines(const DisparityMap& sparse, int workers = 1);
 DisparityMap peek_columns(const DisparityMap& map, int threshold, int workers = 1);

@@ -192,6 +192,19 @@ stk_status stk_selective_blur(stk_ctx* ctx, const uint8_t* rgb, const uint8_t* m
 stk_status stk_selective_blur_weights(stk_ctx* ctx, const uint8_t* rgb, const uint8_t* map, int w,
                                       int h, const double* weights, int size, uint8_t* out);
 
+/* ------------------------------------------------------ evaluation -- */
+/* dense_sad_baseline (evaluate.hpp:35-36, evaluate.cpp:92-135): winner-takes-
+ * all SAD over every pixel with a valid window (match_boundary_pixels with a
+ * full mask). */
+stk_status stk_dense_sad_baseline(stk_ctx* ctx, const uint8_t* left, const uint8_t* right, int w,
+                                  int h, int window, int max_disparity, int16_t* out);
+/* bad_pixel_rate (evaluate.hpp:22-24, evaluate.cpp:17-74): pixels known in
+ * both maps are compared, bad iff |computed - truth| > delta_d; rate = bad /
+ * compared (0 when nothing compared), excluded = w*h - compared. */
+stk_status stk_bad_pixel_rate(stk_ctx* ctx, const int16_t* computed, const int16_t* truth, int w,
+                              int h, double delta_d, double* rate, uint64_t* compared,
+                              uint64_t* excluded);
+
 /* ----------------------------------------------------------- frames -- */
 /* run_depth_pipeline (focus == NULL) / run_refocus_pipeline
  * (pipeline.hpp:78-89): synchronous, host buffers. */

@@ -95,6 +95,11 @@ class Oracle:
             L.ref_selective_blur.argtypes = [_u8p, _u8p, C.c_int, C.c_int, C.c_double,
                                              C.c_int, C.c_int, _u8p]
             L.ref_hardware_workers.restype = C.c_int
+            L.ref_dense_sad_baseline.argtypes = [_u8p, _u8p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                                 C.c_int, _i16p]
+            L.ref_bad_pixel_rate.argtypes = [_i16p, _i16p, C.c_int, C.c_int, C.c_double, C.c_int,
+                                             C.POINTER(C.c_double), C.POINTER(C.c_uint64),
+                                             C.POINTER(C.c_uint64), C.c_char_p, C.c_int]
         else:
             L.orc_lightness.argtypes = [_u8p, C.c_int, C.c_int, _u8p]
             L.orc_histogram.argtypes = [_u8p, C.c_size_t, _u64p]
@@ -217,6 +222,41 @@ class Oracle:
             self._check(self.lib.orc_match(left.reshape(-1), right.reshape(-1), mask.reshape(-1),
                                            w, h, window, max_disparity, out.reshape(-1)))
         return out
+
+    def dense_sad_baseline(self, left, right, window, max_disparity, workers: int = 1):
+        """evaluate.cpp:92-135 -- the port restates it as match() with a full mask
+        (every pixel with a valid window; test_evaluate.cpp:125-143 asserts the
+        equality)."""
+        left = np.ascontiguousarray(left, np.uint8)
+        right = np.ascontiguousarray(right, np.uint8)
+        h, w = left.shape
+        if self.kind == "reference":
+            out = np.empty((h, w), np.int16)
+            self._check(self.lib.ref_dense_sad_baseline(left.reshape(-1), right.reshape(-1), w, h,
+                                                        window, max_disparity, workers,
+                                                        out.reshape(-1)))
+            return out
+        return self.match(left, right, np.ones((h, w), np.uint8), window, max_disparity)
+
+    def bad_pixel_rate(self, computed, truth, delta_d, workers: int = 1):
+        """evaluate.cpp:17-74 -> (rate, compared, excluded, report json or None)."""
+        computed = np.ascontiguousarray(computed, np.int16)
+        truth = np.ascontiguousarray(truth, np.int16)
+        h, w = computed.shape
+        if self.kind == "reference":
+            rate, cmp_, exc = C.c_double(), C.c_uint64(), C.c_uint64()
+            buf = C.create_string_buffer(512)
+            self._check(self.lib.ref_bad_pixel_rate(computed.reshape(-1), truth.reshape(-1), w, h,
+                                                     float(delta_d), workers, C.byref(rate),
+                                                     C.byref(cmp_), C.byref(exc), buf, 512))
+            return rate.value, cmp_.value, exc.value, buf.value.decode()
+        if delta_d < 0:
+            raise OracleParamError("bad_pixel_rate: delta_d must be >= 0")
+        known = (computed >= 0) & (truth >= 0)
+        compared = int(known.sum())
+        diff = np.abs(computed.astype(np.int32) - truth.astype(np.int32))
+        bad = int((known & (diff > delta_d)).sum())
+        return (0.0 if compared == 0 else bad / compared), compared, w * h - compared, None
 
     def sad_cost(self, left, right, x, y, d, window):
         assert self.kind == "port"

@@ -6,6 +6,7 @@
 // Python tests and bench.py's reference arm load it through ctypes to obtain
 // the reference's exact outputs and timings.  Nothing here is product code.
 #include <chrono>
+#include <cstdio>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -14,6 +15,7 @@
 
 #include "stereotk/boundary.hpp"
 #include "stereotk/error.hpp"
+#include "stereotk/evaluate.hpp"
 #include "stereotk/image.hpp"
 #include "stereotk/parallel.hpp"
 #include "stereotk/pipeline.hpp"
@@ -64,9 +66,44 @@ int guard(Fn&& fn) {
 }
 }  // namespace
 
+// image_io.cpp needs libpng, absent here: the file entry points evaluate.cpp
+// references are stubbed (the tests never call them).
+namespace stereotk {
+GrayImage load_gray(const std::string& path, std::vector<std::string>*) {
+    throw IoError(path + ": image I/O is not built into the test oracle");
+}
+void save_gray(const GrayImage&, const std::string& path, const std::vector<std::string>&) {
+    throw IoError(path + ": image I/O is not built into the test oracle");
+}
+}  // namespace stereotk
+
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_dense_sad_baseline(const uint8_t* l, const uint8_t* r, int w, int h, int window, int max_d,
+                           int workers, int16_t* out) {
+    return guard([&] {
+        MatchConfig c;
+        c.window = window;
+        c.max_disparity = max_d;
+        const DisparityMap m = dense_sad_baseline(gray_in(l, w, h), gray_in(r, w, h), c, workers);
+        std::memcpy(out, m.values.data(), m.values.size() * 2);
+    });
+}
+
+int ref_bad_pixel_rate(const int16_t* comp, const int16_t* truth, int w, int h, double delta,
+                       int workers, double* rate, uint64_t* compared, uint64_t* excluded,
+                       char* json, int json_cap) {
+    return guard([&] {
+        const EvalResult e = bad_pixel_rate(disp_in(comp, w, h), disp_in(truth, w, h), delta, workers);
+        *rate = e.bad_pixel_rate;
+        *compared = e.compared;
+        *excluded = e.excluded;
+        const std::string js = eval_report_json(e);
+        std::snprintf(json, json_cap, "%s", js.c_str());
+    });
+}
 
 int ref_lightness(const uint8_t* rgb, int w, int h, int workers, uint8_t* gray) {
     return guard([&] {

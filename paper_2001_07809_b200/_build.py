@@ -38,6 +38,7 @@ CU_SOURCES = [
     "k_sad_ws.cu",
     "k_reconstruct.cu",
     "k_blur.cu",
+    "k_eval.cu",
     "stk_capi.cu",
 ]
 CXX_SOURCES = ["stereotk_shim.cpp"]  # the C++ stereotk:: drop-in over the C-ABI

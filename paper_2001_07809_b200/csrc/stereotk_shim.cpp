@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <cstdio>
 #include <string>
 
 #include "stereotk/stereotk_b200.hpp"
@@ -192,6 +193,53 @@ DisparityMap match_boundary_pixels(const GrayImage& left, const GrayImage& right
                                     left.height, config.window, config.max_disparity, out.values.data()),
           c);
     return out;
+}
+
+EvalResult bad_pixel_rate(const DisparityMap& computed, const DisparityMap& truth, double delta_d,
+                          int workers) {
+    check_workers(workers);
+    if (computed.width != truth.width || computed.height != truth.height)  // evaluate.cpp:20-26
+        throw ParamError("bad_pixel_rate: computed " + dims(computed.width, computed.height) +
+                         " vs truth " + dims(truth.width, truth.height));
+    EvalResult r;
+    r.delta_d = delta_d;
+    stk_ctx* c = ctx();
+    check(stk_bad_pixel_rate(c, computed.values.data(), truth.values.data(), computed.width,
+                             computed.height, delta_d, &r.bad_pixel_rate, &r.compared, &r.excluded),
+          c);
+    return r;
+}
+
+DisparityMap dense_sad_baseline(const GrayImage& left, const GrayImage& right,
+                                const MatchConfig& config, int workers) {
+    check_workers(workers);
+    if (left.width != right.width || left.height != right.height)  // evaluate.cpp:95-101
+        throw ParamError("dense_sad_baseline: image sizes differ, left " + dims(left.width, left.height) +
+                         " vs right " + dims(right.width, right.height));
+    DisparityMap out(left.width, left.height);
+    stk_ctx* c = ctx();
+    check(stk_dense_sad_baseline(c, left.data.data(), right.data.data(), left.width, left.height,
+                                 config.window, config.max_disparity, out.values.data()),
+          c);
+    return out;
+}
+
+// evaluate.cpp:220-227: nlohmann::json dump -- keys in sorted order, compact,
+// doubles in the shortest form that round-trips.
+std::string eval_report_json(const EvalResult& r) {
+    auto num = [](double v) {
+        char buf[40];
+        for (int p = 1; p <= 17; ++p) {
+            std::snprintf(buf, sizeof buf, "%.*g", p, v);
+            if (std::strtod(buf, nullptr) == v) break;
+        }
+        std::string t = buf;
+        if (t.find_first_of(".eEn") == std::string::npos) t += ".0";
+        return t;
+    };
+    return "{\"bad_pixel_rate\":" + num(r.bad_pixel_rate) + ",\"compared\":" +
+           std::to_string(r.compared) + ",\"delta_d\":" + num(r.delta_d) + ",\"excluded\":" +
+           std::to_string(r.excluded) + "}";
 }
 
 DisparityMap fill_scanlines(const DisparityMap& sparse, int workers) {

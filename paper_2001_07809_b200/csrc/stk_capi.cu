@@ -1113,6 +1113,61 @@ stk_status stk_match_boundary_pixels(stk_ctx* ctx, const uint8_t* left, const ui
     FINISH();
 }
 
+// dense_sad_baseline (evaluate.cpp:92-135): match_boundary_pixels with every
+// pixel in the mask -- the mask plane is filled on the device.
+stk_status stk_dense_sad_baseline(stk_ctx* ctx, const uint8_t* left, const uint8_t* right, int w,
+                                  int h, int window, int max_disparity, int16_t* out) {
+    if (window < 1 || window % 2 == 0)
+        return fail(ctx, STK_EPARAM, "dense_sad_baseline: window must be odd and positive, got " +
+                                         std::to_string(window));
+    if (max_disparity < 0)
+        return fail(ctx, STK_EPARAM, "dense_sad_baseline: max_disparity must be >= 0, got " +
+                                         std::to_string(max_disparity));
+    TRY(check_gpu_limits(ctx, window, max_disparity));
+    STAGE_BEGIN(w, h);
+    if (N == 0) return STK_OK;
+    H2D_PLANE(s.grayL, left, 1);
+    H2D_PLANE(s.grayR, right, 1);
+    CK(cudaMemsetAsync(s.mref, 1, (size_t)s.P * h, st));
+    CK(cudaMemsetAsync(s.sc, 0, sizeof(DevScalars), st));
+    CK(cudaMemsetAsync(s.lb, 0, sizeof(unsigned long long) * LB_COUNT * s.lb_stride, st));
+    f.window = window;
+    f.hw = window / 2;
+    f.D = max_disparity;
+    TRY(encode(ctx, s.tm_sadL, s.grayL, 1, w, h, s.P, 128, window));
+    TRY(encode(ctx, s.tm_sadR, s.grayR, 1, w, h, s.P, 128, window));
+    launch_apply(f, false, false, st);
+    if (w >= window && h >= window) launch_sad(f, ctx->sad_kernel, &s.tm_sadL.map, &s.tm_sadR.map, st);
+    CK(cudaMemcpyAsync(out, s.sparse, 2 * N, cudaMemcpyDeviceToHost, st));
+    FINISH();
+}
+
+// bad_pixel_rate (evaluate.cpp:17-74)
+stk_status stk_bad_pixel_rate(stk_ctx* ctx, const int16_t* computed, const int16_t* truth, int w,
+                              int h, double delta_d, double* rate, uint64_t* compared,
+                              uint64_t* excluded) {
+    if (!(delta_d >= 0.0))
+        return fail(ctx, STK_EPARAM, "bad_pixel_rate: delta_d must be >= 0, got " + std::to_string(delta_d));
+    STAGE_BEGIN(w, h);
+    unsigned long long counts[2] = {0, 0};
+    if (N) {
+        int16_t* d_c = s.sparse;
+        int16_t* d_t = s.rowf;
+        unsigned long long* d_out = &s.sc->raw_count;  // two adjacent u64 counters
+        CK(cudaMemsetAsync(d_out, 0, 2 * sizeof(unsigned long long), st));
+        CK(cudaMemcpyAsync(d_c, computed, 2 * N, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d_t, truth, 2 * N, cudaMemcpyHostToDevice, st));
+        launch_bad_pixel(d_c, d_t, (long long)N, delta_d, d_out, st);
+        CK(cudaMemcpyAsync(counts, d_out, sizeof(counts), cudaMemcpyDeviceToHost, st));
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st));
+    }
+    if (compared) *compared = counts[0];
+    if (excluded) *excluded = (uint64_t)N - counts[0];
+    if (rate) *rate = counts[0] == 0 ? 0.0 : (double)counts[1] / (double)counts[0];
+    return STK_OK;
+}
+
 stk_status stk_fill_scanlines(stk_ctx* ctx, const int16_t* sparse, int w, int h, int16_t* out) {
     STAGE_BEGIN(w, h);
     if (N == 0) return STK_OK;

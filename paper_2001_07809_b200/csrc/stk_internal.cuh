@@ -139,6 +139,9 @@ void launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, in
 // stage entry prune_components on a pitched byte mask (writes f.mprn / f.manc)
 void launch_prune_mask_bits(const Frame& f, const uint8_t* mask, uint32_t* rbits, int32_t* runroot,
                             int32_t* bord, uint32_t* sbits, int sbits_words, cudaStream_t st);
+// K9 evaluation: out[0] += compared, out[1] += bad (evaluate.cpp:17-74)
+void launch_bad_pixel(const int16_t* comp, const int16_t* truth, long long n, double delta,
+                      unsigned long long* out, cudaStream_t st);
 // true when launch_sad will run the per-pixel list kernel (it needs f.list)
 bool sad_uses_list(const Frame& f, int kernel);
 void launch_prune(const Frame& f, bool anchors, cudaStream_t st); // K4e-g

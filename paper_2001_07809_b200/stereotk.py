@@ -92,6 +92,15 @@ class MatchConfig:
 
 
 @dataclass
+class EvalResult:
+    """stereotk::EvalResult (evaluate.hpp:10-16)."""
+    bad_pixel_rate: float = 0.0
+    compared: int = 0
+    excluded: int = 0
+    delta_d: float = 0.0
+
+
+@dataclass
 class Clustering:
     """stereotk::Clustering (segmentation.hpp:27-33)."""
     centers: np.ndarray
@@ -337,6 +346,43 @@ def match_boundary_pixels(left, right, mask, config: MatchConfig = MatchConfig()
     _dev(device)._call("stk_match_boundary_pixels", _p(left), _p(right), _p(mask), w, h,
                        config.window, config.max_disparity, _p(out))
     return out
+
+
+def dense_sad_baseline(left, right, config: MatchConfig = MatchConfig(), workers: int = 1, *,
+                       device=None) -> np.ndarray:
+    """evaluate.hpp:35-36: winner-takes-all SAD over every pixel with a valid window."""
+    left, right = _c8(left), _c8(right)
+    if left.shape != right.shape:
+        raise ParamError("dense_sad_baseline: image sizes differ, left %dx%d vs right %dx%d"
+                         % (left.shape[1], left.shape[0], right.shape[1], right.shape[0]))
+    h, w = left.shape
+    out = np.empty((h, w), np.int16)
+    _dev(device)._call("stk_dense_sad_baseline", _p(left), _p(right), w, h, config.window,
+                       config.max_disparity, _p(out))
+    return out
+
+
+def bad_pixel_rate(computed, truth, delta_d: float, workers: int = 1, *, device=None) -> EvalResult:
+    """evaluate.hpp:22-24."""
+    computed = np.ascontiguousarray(computed, np.int16)
+    truth = np.ascontiguousarray(truth, np.int16)
+    if computed.shape != truth.shape:
+        raise ParamError("bad_pixel_rate: computed %dx%d vs truth %dx%d"
+                         % (computed.shape[1], computed.shape[0], truth.shape[1], truth.shape[0]))
+    h, w = computed.shape
+    rate, cmp_, exc = C.c_double(0.0), C.c_uint64(0), C.c_uint64(0)
+    _dev(device)._call("stk_bad_pixel_rate", _p(computed), _p(truth), w, h, float(delta_d),
+                       C.byref(rate), C.byref(cmp_), C.byref(exc))
+    return EvalResult(rate.value, cmp_.value, exc.value, float(delta_d))
+
+
+def eval_report_json(result: EvalResult) -> str:
+    """evaluate.cpp:220-227 (nlohmann::json::dump: keys sorted, compact)."""
+    import json
+
+    return json.dumps({"bad_pixel_rate": result.bad_pixel_rate, "compared": result.compared,
+                       "delta_d": result.delta_d, "excluded": result.excluded},
+                      separators=(",", ":"))
 
 
 def fill_scanlines(sparse, workers: int = 1, *, device=None) -> np.ndarray:

@@ -123,6 +123,35 @@ int main(int argc, char** argv) {
     for (auto& v : all.data) v = 1;
     RgbImage b = selective_blur(p.left, all, box);
     CHECK(b.width == 96);
+    {  // evaluate.hpp (test_evaluate.cpp:38-50, 125-143, 205-227)
+        DisparityMap c(2, 2), t(2, 2);
+        c.values = {5, 5, 7, 2};
+        t.values = {5, 6, 9, 2};
+        EvalResult r = bad_pixel_rate(c, t, 1.0);
+        CHECK(r.bad_pixel_rate == 0.25 && r.compared == 4 && r.excluded == 0 && r.delta_d == 1.0);
+        CHECK(bad_pixel_rate(c, t, 0.0).bad_pixel_rate == 0.5);
+        bool threw = false;
+        try {
+            bad_pixel_rate(c, DisparityMap(2, 3), 1.0);
+        } catch (const ParamError&) {
+            threw = true;
+        }
+        CHECK(threw);
+        EvalResult e;
+        e.bad_pixel_rate = 0.25;
+        e.compared = 4;
+        e.excluded = 0;
+        e.delta_d = 1.0;
+        CHECK(eval_report_json(e) == "{\"bad_pixel_rate\":0.25,\"compared\":4,\"delta_d\":1.0,\"excluded\":0}");
+        StereoPair tn = rectangle_scene_pair(24, 20, 3, 55);
+        GrayImage gl = rgb_to_lightness(tn.left), gr = rgb_to_lightness(tn.right);
+        MatchConfig mc;
+        mc.window = 3;
+        mc.max_disparity = 6;
+        BoundaryMask every(24, 20);
+        for (auto& v : every.mask) v = 1;
+        CHECK(dense_sad_baseline(gl, gr, mc).values == match_boundary_pixels(gl, gr, every, mc).values);
+    }
     if (argc > 1) {  // dump the rect(96,72,4,63) frame for the byte comparison
         StereoPair q = rectangle_scene_pair(96, 72, 4, 63);
         PipelineConfig c2;

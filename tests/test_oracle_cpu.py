@@ -246,3 +246,19 @@ def test_no_gpu_fails_loudly(stk):
         pytest.skip("a GPU is present")
     with pytest.raises(stk.CudaError, match="no CUDA device"):
         stk.Device(0)
+
+
+def test_port_evaluation_matches_reference(ref, port):
+    """The port's bad_pixel_rate / dense_sad_baseline restatements equal the
+    compiled reference (evaluate.cpp)."""
+    rng = np.random.default_rng(77)
+    for (w, h) in ((16, 12), (50, 40), (97, 33)):
+        a = rng.integers(-1, 30, (h, w)).astype(np.int16)
+        b = rng.integers(-1, 30, (h, w)).astype(np.int16)
+        for d in (0.0, 1.0, 2.5):
+            assert port.bad_pixel_rate(a, b, d)[:3] == ref.bad_pixel_rate(a, b, d)[:3]
+        l = rng.integers(0, 255, (h, w), dtype=np.uint8)
+        r = np.roll(l, -2, axis=1)
+        for win, D in ((3, 6), (5, 16), (9, 4)):
+            np.testing.assert_array_equal(port.dense_sad_baseline(l, r, win, D),
+                                          ref.dense_sad_baseline(l, r, win, D))
