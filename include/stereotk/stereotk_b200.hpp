@@ -259,6 +259,23 @@ RgbImage run_refocus_pipeline(const RgbImage& left, const RgbImage& right,
 void validate_config(const PipelineConfig& config);
 
 // ------------------------------------------------------ B200 controls ----
+// ------------------------------------------------------------- bench ----
+// bench.hpp:13-34: per-stage timing of run_depth_pipeline over a batch of
+// frames, once per worker count (the serial plan first).  Stage times come
+// from CUDA events; worker counts are validated as the reference does and
+// otherwise do not change the GPU work (results are identical for any count).
+struct BenchReport {
+    int workers = 0;
+    int frames = 0;
+    StageTimes times;
+    StageTimes serial;
+    double speedup = 0.0;
+};
+std::vector<BenchReport> run_benchmark(const std::vector<StereoPair>& frames,
+                                       const std::vector<int>& worker_counts,
+                                       const PipelineConfig& config);
+std::string benchmark_csv(const std::vector<BenchReport>& reports);
+
 namespace b200 {
 // Device used by this thread's implicit context (default: $STK_DEVICE or 0).
 void set_device(int device);

@@ -3,6 +3,8 @@
 // per host thread (device from stereotk::b200::set_device or $STK_DEVICE).
 // STK_EPARAM becomes stereotk::ParamError with the C-ABI's message (which
 // mirrors the reference's text); any other failure becomes std::runtime_error.
+#include <algorithm>
+#include <sstream>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -222,6 +224,78 @@ DisparityMap dense_sad_baseline(const GrayImage& left, const GrayImage& right,
                                  config.window, config.max_disparity, out.values.data()),
           c);
     return out;
+}
+
+// bench.cpp:13-108 over the GPU pipeline.
+namespace {
+StageTimes measure_batch(const std::vector<StereoPair>& frames, const PipelineConfig& config) {
+    StageTimes scratch;  // warm-up (bench.cpp:15-20)
+    run_depth_pipeline(frames.front().left, frames.front().right, config, &scratch);
+    StageTimes total;
+    for (const StereoPair& frame : frames) {
+        StageTimes t;
+        run_depth_pipeline(frame.left, frame.right, config, &t);
+        total.convert += t.convert;
+        total.segment += t.segment;
+        total.boundary += t.boundary;
+        total.match += t.match;
+        total.fill += t.fill;
+        total.peek += t.peek;
+    }
+    return total;
+}
+}  // namespace
+
+std::vector<BenchReport> run_benchmark(const std::vector<StereoPair>& frames,
+                                       const std::vector<int>& worker_counts,
+                                       const PipelineConfig& config) {
+    if (frames.empty()) throw ParamError("benchmark: no frames given");
+    if (worker_counts.empty()) throw ParamError("benchmark: no worker counts given");
+    if (std::find(worker_counts.begin(), worker_counts.end(), 1) == worker_counts.end())
+        throw ParamError("benchmark: worker counts must include 1, the serial baseline");
+    for (int w : worker_counts)
+        if (w < 1) throw ParamError("benchmark: worker count must be >= 1, got " + std::to_string(w));
+    PipelineConfig serial_config = config;
+    serial_config.workers = 1;
+    const StageTimes serial = measure_batch(frames, serial_config);
+    std::vector<BenchReport> reports;
+    for (int workers : worker_counts) {
+        BenchReport r;
+        r.workers = workers;
+        r.frames = static_cast<int>(frames.size());
+        r.serial = serial;
+        if (workers == 1) {
+            r.times = serial;
+        } else {
+            PipelineConfig run_config = config;
+            run_config.workers = workers;
+            r.times = measure_batch(frames, run_config);
+        }
+        r.speedup = r.times.total() > 0.0 ? serial.total() / r.times.total() : 0.0;
+        reports.push_back(r);
+    }
+    return reports;
+}
+
+std::string benchmark_csv(const std::vector<BenchReport>& reports) {
+    std::ostringstream out;
+    out << "frames,workers,stage,serial_ms,parallel_ms,speedup\n";
+    auto row = [&](int f, int w, const char* stage, double s, double p) {
+        out << f << ',' << w << ',' << stage << ',' << s << ',' << p << ',' << (p > 0.0 ? s / p : 0.0)
+            << '\n';
+    };
+    for (const BenchReport& r : reports) {
+        const StageTimes& s = r.serial;
+        const StageTimes& t = r.times;
+        row(r.frames, r.workers, "convert", s.convert, t.convert);
+        row(r.frames, r.workers, "segment", s.segment, t.segment);
+        row(r.frames, r.workers, "boundary", s.boundary, t.boundary);
+        row(r.frames, r.workers, "match", s.match, t.match);
+        row(r.frames, r.workers, "fill", s.fill, t.fill);
+        row(r.frames, r.workers, "peek", s.peek, t.peek);
+        row(r.frames, r.workers, "total", s.total(), t.total());
+    }
+    return out.str();
 }
 
 // evaluate.cpp:220-227: nlohmann::json dump -- keys in sorted order, compact,

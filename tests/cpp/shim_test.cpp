@@ -152,6 +152,36 @@ int main(int argc, char** argv) {
         for (auto& v : every.mask) v = 1;
         CHECK(dense_sad_baseline(gl, gr, mc).values == match_boundary_pixels(gl, gr, every, mc).values);
     }
+    {  // bench.hpp (test_parallel.cpp:78-117): validation and the CSV layout
+        std::vector<StereoPair> frames;
+        PipelineConfig bc;
+        bc.max_disparity = 8;
+        auto throws = [&](const std::vector<int>& wc) {
+            try {
+                run_benchmark(frames, wc, bc);
+            } catch (const ParamError&) {
+                return true;
+            }
+            return false;
+        };
+        CHECK(throws({1}));  // no frames
+        frames.push_back(rectangle_scene_pair(96, 72, 4, 4));
+        CHECK(throws({}));
+        CHECK(throws({2, 4}));
+        CHECK(throws({1, 0}));
+        auto reports = run_benchmark(frames, {1, 2}, bc);
+        const std::string csv = benchmark_csv(reports);
+        CHECK(csv.rfind("frames,workers,stage,serial_ms,parallel_ms,speedup\n", 0) == 0);
+        int lines = 0;
+        for (char ch : csv) lines += ch == '\n';
+        CHECK(lines == 1 + 7 * 2);
+        CHECK(csv.find(",total,") != std::string::npos && csv.find(",match,") != std::string::npos);
+        const auto pos = csv.find("1,1,total,");
+        CHECK(pos != std::string::npos);
+        const std::string row = csv.substr(pos, csv.find('\n', pos) - pos);
+        CHECK(row.substr(row.rfind(',') + 1) == "1");
+        CHECK(reports[0].times.match > 0.0 && reports[1].speedup > 0.0);
+    }
     if (argc > 1) {  // dump the rect(96,72,4,63) frame for the byte comparison
         StereoPair q = rectangle_scene_pair(96, 72, 4, 63);
         PipelineConfig c2;
