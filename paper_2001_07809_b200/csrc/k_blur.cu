@@ -452,6 +452,19 @@ __device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsign
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
     return d;
 }
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long fadd2_rm(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+constexpr unsigned long long kMagicNeg2 = 0xcb000000cb000000ull;  // (-2^23, -2^23)
+constexpr unsigned long long kMagic2 = 0x4b0000004b000000ull;     // (2^23, 2^23)
+constexpr unsigned long long kHalf2 = 0x3f0000003f000000ull;      // (0.5, 0.5)
 __device__ __forceinline__ float f2lo(unsigned long long v) { return __uint_as_float((uint32_t)v); }
 __device__ __forceinline__ float f2hi(unsigned long long v) { return __uint_as_float((uint32_t)(v >> 32)); }
 
@@ -459,6 +472,7 @@ template <int K>
 struct V3Geom {
     static constexpr int h = K / 2, BX = 128, BY = 16;
     static constexpr int NC = BX + 2 * h;               // staged / vertical columns
+    static constexpr int NCH = NC / 2;                  // vertical column pairs
     static constexpr int NCP = (NC + 3) & ~3;           // float plane row (16-byte rows)
     static constexpr int IH = BY + 2 * h;
     static constexpr int LB = (3 * h + 15) / 16 * 16;   // interior rows load from byte 3*x0 - LB
@@ -477,7 +491,7 @@ __global__ void __launch_bounds__(V3Geom<K>::NT) k_blur_v3(Frame f, BlurParams b
                                                            const int16_t* __restrict__ depth) {
     using G = V3Geom<K>;
     constexpr int h = G::h, BX = G::BX, BY = G::BY, NC = G::NC, NCP = G::NCP, IH = G::IH;
-    constexpr int ROWB = G::ROWB, XOFF = G::XOFF, NT = G::NT;
+    constexpr int ROWB = G::ROWB, XOFF = G::XOFF, NT = G::NT, NCH = G::NCH;
     extern __shared__ __align__(16) unsigned char smem[];
     uint8_t* stage = smem;
     float* vp = reinterpret_cast<float*>(smem + G::SM_STAGE);  // [3][BY][NCP]
@@ -556,92 +570,102 @@ __global__ void __launch_bounds__(V3Geom<K>::NT) k_blur_v3(Frame f, BlurParams b
         }
         return;
     }
-    // packed weight pairs wp[k] = (w[k], w[k-1]), w[-1] = w[K] = 0
-    unsigned long long wp[K + 1];
-    {
-        float w[K];
+    float w[K];
 #pragma unroll
-        for (int i = 0; i < K; ++i) w[i] = __ldg(bp.g1 + i);
-#pragma unroll
-        for (int k = 0; k <= K; ++k) wp[k] = f2pack(k < K ? w[k] : 0.f, k > 0 ? w[k - 1] : 0.f);
-    }
-    // ---- vertical: column tid, BY outputs in pairs (2j, 2j+1)
-    if (tid < NC) {
-        const uint8_t* colp = stage + XOFF + 3 * tid;
+    for (int i = 0; i < K; ++i) w[i] = __ldg(bp.g1 + i);
+    // ---- vertical: thread = (column pair cp, row half); 8 outputs of both
+    // columns, FFMA2 over the column pair with broadcast weights (w[k], w[k])
+    if (tid < 2 * NCH) {
+        const int cp = tid % NCH, half = tid / NCH;
+        const uint8_t* colp = stage + (size_t)(half * (BY / 2)) * ROWB + XOFF + 6 * cp;
         unsigned long long acc[BY / 2][3];
 #pragma unroll
         for (int j = 0; j < BY / 2; ++j) acc[j][0] = acc[j][1] = acc[j][2] = 0ull;
 #pragma unroll
-        for (int r = 0; r < IH; ++r) {
+        for (int r = 0; r < BY / 2 + K - 1; ++r) {
             const uint8_t* px = colp + (size_t)r * ROWB;
             unsigned long long v2[3];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const float v = (float)px[c];
-                v2[c] = f2pack(v, v);
-            }
+            for (int c = 0; c < 3; ++c)
+                v2[c] = fadd2(f2pack(__uint_as_float(px[c] | 0x4b000000u), __uint_as_float(px[3 + c] | 0x4b000000u)),
+                              kMagicNeg2);
 #pragma unroll
             for (int j = 0; j < BY / 2; ++j) {
-                const int k = r - 2 * j;  // weight index of output 2j; output 2j+1 uses k-1
-                if (k >= 0 && k <= K) {
+                const int k = r - j;
+                if (k >= 0 && k < K) {
+                    const unsigned long long wk = f2pack(w[k], w[k]);
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) acc[j][c] = ffma2(wp[k], v2[c], acc[j][c]);
+                    for (int c = 0; c < 3; ++c) acc[j][c] = ffma2(wk, v2[c], acc[j][c]);
                 }
             }
         }
 #pragma unroll
         for (int j = 0; j < BY / 2; ++j)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                vp[((size_t)c * BY + 2 * j) * NCP + tid] = f2lo(acc[j][c]);
-                vp[((size_t)c * BY + 2 * j + 1) * NCP + tid] = f2hi(acc[j][c]);
-            }
+            for (int c = 0; c < 3; ++c)
+                *reinterpret_cast<unsigned long long*>(vp + ((size_t)c * BY + half * (BY / 2) + j) * NCP + 2 * cp) =
+                    acc[j][c];
+    }
+    // tap pairs: even outputs use (w[2i], w[2i+1]), odd ones (w[2i-1], w[2i])
+    constexpr int NPR = (K + 1) / 2;
+    unsigned long long we[NPR], wo[NPR];
+#pragma unroll
+    for (int i = 0; i < NPR; ++i) {
+        we[i] = f2pack(w[2 * i], 2 * i + 1 < K ? w[2 * i + 1] : 0.f);
+        wo[i] = f2pack(i > 0 ? w[2 * i - 1] : 0.f, w[2 * i]);
     }
     __syncthreads();
-    // ---- horizontal: item = (row, 4 outputs q4..q4+3); output pairs (0,1), (2,3)
+    // ---- horizontal: item = (row, 4 outputs q4..q4+3); each output sums its
+    // even and odd taps in the two lanes of an FFMA2 over aligned input pairs
     for (int it = tid; it < BY * (BX / 4); it += NT) {
         const int oy = it / (BX / 4), q4 = (it % (BX / 4)) * 4;
         if (oy >= ny || q4 >= nx) continue;
-        unsigned long long a[2][3];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) a[j][0] = a[j][1] = a[j][2] = 0ull;
+        float o4[3][4];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const float* row = vp + ((size_t)c * BY + oy) * NCP + q4;
-            float v[K + 3 + 1];
+            const unsigned long long* row =
+                reinterpret_cast<const unsigned long long*>(vp + ((size_t)c * BY + oy) * NCP + q4);
+            unsigned long long pr[NPR + 1];  // (v[2i], v[2i+1])
 #pragma unroll
-            for (int i = 0; i < (K + 3 + 3) / 4; ++i) {
-                const float4 t = reinterpret_cast<const float4*>(row)[i];
-                v[4 * i] = t.x;
-                if (4 * i + 1 < K + 4) v[4 * i + 1] = t.y;
-                if (4 * i + 2 < K + 4) v[4 * i + 2] = t.z;
-                if (4 * i + 3 < K + 4) v[4 * i + 3] = t.w;
+            for (int i = 0; i < (NPR + 2) / 2; ++i) {
+                const ulonglong2 t = reinterpret_cast<const ulonglong2*>(row)[i];
+                pr[2 * i] = t.x;
+                if (2 * i + 1 <= NPR) pr[2 * i + 1] = t.y;
             }
+            unsigned long long a0 = 0ull, a1 = 0ull, a2 = 0ull, a3 = 0ull;
 #pragma unroll
-            for (int p = 0; p < K + 3; ++p) {
-                const unsigned long long v2 = f2pack(v[p], v[p]);
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    const int k = p - 2 * j;
-                    if (k >= 0 && k <= K) a[j][c] = ffma2(wp[k], v2, a[j][c]);
-                }
+            for (int i = 0; i < NPR; ++i) {
+                a0 = ffma2(we[i], pr[i], a0);
+                a1 = ffma2(wo[i], pr[i], a1);
+                a2 = ffma2(we[i], pr[i + 1], a2);
+                a3 = ffma2(wo[i], pr[i + 1], a3);
             }
+            o4[c][0] = f2lo(a0) + f2hi(a0);
+            o4[c][1] = f2lo(a1) + f2hi(a1);
+            o4[c][2] = f2lo(a2) + f2hi(a2);
+            o4[c][3] = f2lo(a3) + f2hi(a3);
         }
-        // 4 pixels x 3 bytes
-        uint32_t ob[3] = {0, 0, 0};
+        // floor(x + 0.5) in the low mantissa byte: (x + 0.5) + 2^23 rounded down
+        // (x in [0, 255 (1 + eps)]: non-negative normalised weights and 8-bit inputs)
+        uint32_t z[12];
 #pragma unroll
-        for (int o = 0; o < 4; ++o) {
-            const int ox = q4 + o;
-            const uint8_t* src = stage + (size_t)(oy + h) * ROWB + XOFF + 3 * (ox + h);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const float af = (o & 1) ? f2hi(a[o >> 1][c]) : f2lo(a[o >> 1][c]);
-                const uint32_t b = shf[oy * BX + ox] ? (uint32_t)src[c]
-                                                     : (uint32_t)min(max((int)floorf(af + 0.5f), 0), 255);
-                const int bi = 3 * o + c;
-                ob[bi >> 2] |= b << (8 * (bi & 3));
-            }
+        for (int bi = 0; bi < 12; bi += 2) {
+            const unsigned long long q = fadd2_rm(
+                fadd2(f2pack(o4[bi % 3][bi / 3], o4[(bi + 1) % 3][(bi + 1) / 3]), kHalf2), kMagic2);
+            z[bi] = (uint32_t)q;
+            z[bi + 1] = (uint32_t)(q >> 32);
         }
+        uint32_t ob[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            ob[k] = __byte_perm(__byte_perm(z[4 * k], z[4 * k + 1], 0x0040), __byte_perm(z[4 * k + 2], z[4 * k + 3], 0x0040),
+                                0x5410);
+        // sharp pixels keep their input bytes
+        const uint32_t m = *reinterpret_cast<const uint32_t*>(shf + oy * BX + q4) * 0xffu;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(stage + (size_t)(oy + h) * ROWB + G::LB + 3 * q4);
+        const uint32_t mw[3] = {__byte_perm(m, 0, 0x1000), __byte_perm(m, 0, 0x2211), __byte_perm(m, 0, 0x3332)};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) ob[k] = (ob[k] & ~mw[k]) | (src[k] & mw[k]);
         uint8_t* dst = out + ((size_t)(y0 + oy) * W + x0 + q4) * 3;
         if (q4 + 4 <= nx && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
             reinterpret_cast<uint32_t*>(dst)[0] = ob[0];
