@@ -497,16 +497,18 @@ __global__ void __launch_bounds__(V3Geom<K>::NT) k_blur_v3(Frame f, BlurParams b
     float* vp = reinterpret_cast<float*>(smem + G::SM_STAGE);  // [3][BY][NCP]
     uint8_t* shf = smem + G::SM_STAGE + G::SM_V;               // [BY][BX] sharp flags
     __shared__ uint8_t lut[1024];
+    __shared__ unsigned long long wpair[K + 1];
     const int W = f.W, H = f.H, tid = threadIdx.x;
     const int x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
     const int nx = min(BX, W - x0), ny = min(BY, H - y0);
     for (int i = tid; i < bp.lut_len && i < 1024; i += NT) lut[i] = bp.sharp_lut[i];
+    if (tid <= K) wpair[tid] = f2pack(tid < K ? __ldg(bp.g1 + tid) : 0.f, tid > 0 ? __ldg(bp.g1 + tid - 1) : 0.f);
     __syncthreads();
     // ---- one latency exposure: the staged rows (rows y0-h .. y0+BY+h-1,
     // columns x0-h .. x0+BX+h-1, replicate-clamped) and the tile's disparities
     const bool interior = 3 * x0 - G::LB >= 0 && 3 * (x0 + BX + h) + 16 <= 3 * W && y0 - h >= 0 &&
                           y0 + BY + h <= H && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
-                          (W * 3) % 16 == 0;
+                          (reinterpret_cast<uintptr_t>(depth) & 15) == 0 && (W * 3) % 16 == 0;
     int any = 0;
     if (interior) {
         constexpr int NV = (3 * NC + G::LB + 15) / 16;
@@ -520,12 +522,14 @@ __global__ void __launch_bounds__(V3Geom<K>::NT) k_blur_v3(Frame f, BlurParams b
                 buf[k] = __ldg(reinterpret_cast<const uint4*>(in + ((size_t)(y0 - h + r) * W + x0) * 3 - G::LB) + v);
             }
         }
-        constexpr int DPER = (BX * BY + NT - 1) / NT;
-        int16_t dv[DPER];
+        constexpr int DV = BX * BY / 8, DPER = (DV + NT - 1) / NT;  // 8 disparities per vector
+        uint4 dv[DPER];
 #pragma unroll
         for (int k = 0; k < DPER; ++k) {
             const int i = tid + k * NT;
-            dv[k] = i < BX * BY ? depth[(size_t)(y0 + i / BX) * W + x0 + i % BX] : (int16_t)-1;
+            if (i < DV)
+                dv[k] = __ldg(reinterpret_cast<const uint4*>(depth + (size_t)(y0 + i / (BX / 8)) * W + x0) +
+                              i % (BX / 8));
         }
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
@@ -535,11 +539,17 @@ __global__ void __launch_bounds__(V3Geom<K>::NT) k_blur_v3(Frame f, BlurParams b
 #pragma unroll
         for (int k = 0; k < DPER; ++k) {
             const int i = tid + k * NT;
-            if (i < BX * BY) {
-                const int d = dv[k];
-                const uint8_t sh = d >= 0 && d < bp.lut_len && lut[d];
-                shf[i] = sh;
-                any |= !sh;
+            if (i < DV) {
+                const uint32_t dw[4] = {dv[k].x, dv[k].y, dv[k].z, dv[k].w};
+                uint32_t sh[2] = {0, 0};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int d = (int16_t)(dw[e >> 1] >> (16 * (e & 1)));
+                    const uint32_t b = (uint32_t)d < (uint32_t)bp.lut_len && lut[d];
+                    sh[e >> 2] |= b << (8 * (e & 3));
+                }
+                *reinterpret_cast<uint2*>(shf + 8 * i) = make_uint2(sh[0], sh[1]);
+                any |= (sh[0] & sh[1]) != 0x01010101u;
             }
         }
     } else {
@@ -570,12 +580,12 @@ __global__ void __launch_bounds__(V3Geom<K>::NT) k_blur_v3(Frame f, BlurParams b
         }
         return;
     }
-    float w[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) w[i] = __ldg(bp.g1 + i);
     // ---- vertical: thread = (column pair cp, row half); 8 outputs of both
-    // columns, FFMA2 over the column pair with broadcast weights (w[k], w[k])
+    // columns, FFMA2 over the column pair with the weight broadcast
     if (tid < 2 * NCH) {
+        float w[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) w[i] = __ldg(bp.g1 + i);
         const int cp = tid % NCH, half = tid / NCH;
         const uint8_t* colp = stage + (size_t)(half * (BY / 2)) * ROWB + XOFF + 6 * cp;
         unsigned long long acc[BY / 2][3];
@@ -584,10 +594,26 @@ __global__ void __launch_bounds__(V3Geom<K>::NT) k_blur_v3(Frame f, BlurParams b
 #pragma unroll
         for (int r = 0; r < BY / 2 + K - 1; ++r) {
             const uint8_t* px = colp + (size_t)r * ROWB;
+            uint32_t t[6];  // byte j of the column pair's 6 staged bytes sits in byte sel[j] of t[j]
+            int sel[6];
+            if constexpr (XOFF % 2 == 0) {
+#pragma unroll
+                for (int j = 0; j < 6; ++j) {
+                    t[j] = reinterpret_cast<const uint16_t*>(px)[j >> 1];
+                    sel[j] = j & 1;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 6; ++j) {
+                    t[j] = px[j];
+                    sel[j] = 0;
+                }
+            }
             unsigned long long v2[3];
 #pragma unroll
-            for (int c = 0; c < 3; ++c)
-                v2[c] = fadd2(f2pack(__uint_as_float(px[c] | 0x4b000000u), __uint_as_float(px[3 + c] | 0x4b000000u)),
+            for (int c = 0; c < 3; ++c)  // (col 2cp, col 2cp+1) of channel c, exact via 2^23 + byte
+                v2[c] = fadd2(f2pack(__uint_as_float(__byte_perm(t[c], 0x4b000000u, 0x7540 | sel[c])),
+                                     __uint_as_float(__byte_perm(t[3 + c], 0x4b000000u, 0x7540 | sel[3 + c]))),
                               kMagicNeg2);
 #pragma unroll
             for (int j = 0; j < BY / 2; ++j) {
@@ -606,54 +632,44 @@ __global__ void __launch_bounds__(V3Geom<K>::NT) k_blur_v3(Frame f, BlurParams b
                 *reinterpret_cast<unsigned long long*>(vp + ((size_t)c * BY + half * (BY / 2) + j) * NCP + 2 * cp) =
                     acc[j][c];
     }
-    // tap pairs: even outputs use (w[2i], w[2i+1]), odd ones (w[2i-1], w[2i])
-    constexpr int NPR = (K + 1) / 2;
-    unsigned long long we[NPR], wo[NPR];
+    // horizontal tap pairs wp[k] = (w[k], w[k-1]) (w[-1] = w[K] = 0), from shared memory
+    unsigned long long wp[K + 1];
 #pragma unroll
-    for (int i = 0; i < NPR; ++i) {
-        we[i] = f2pack(w[2 * i], 2 * i + 1 < K ? w[2 * i + 1] : 0.f);
-        wo[i] = f2pack(i > 0 ? w[2 * i - 1] : 0.f, w[2 * i]);
-    }
+    for (int k = 0; k <= K; ++k) wp[k] = wpair[k];
     __syncthreads();
-    // ---- horizontal: item = (row, 4 outputs q4..q4+3); each output sums its
-    // even and odd taps in the two lanes of an FFMA2 over aligned input pairs
+    // ---- horizontal: item = (row, 4 outputs q4..q4+3); output pairs (0,1),
+    // (2,3) with the input value broadcast, taps in the reference's order
     for (int it = tid; it < BY * (BX / 4); it += NT) {
         const int oy = it / (BX / 4), q4 = (it % (BX / 4)) * 4;
         if (oy >= ny || q4 >= nx) continue;
-        float o4[3][4];
+        uint32_t z[12];  // byte 3*o + c: output o, channel c
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const unsigned long long* row =
-                reinterpret_cast<const unsigned long long*>(vp + ((size_t)c * BY + oy) * NCP + q4);
-            unsigned long long pr[NPR + 1];  // (v[2i], v[2i+1])
+            const float* row = vp + ((size_t)c * BY + oy) * NCP + q4;
+            float v[K + 3 + 1];
 #pragma unroll
-            for (int i = 0; i < (NPR + 2) / 2; ++i) {
-                const ulonglong2 t = reinterpret_cast<const ulonglong2*>(row)[i];
-                pr[2 * i] = t.x;
-                if (2 * i + 1 <= NPR) pr[2 * i + 1] = t.y;
+            for (int i = 0; i < (K + 3 + 3) / 4; ++i) {
+                const float4 t4 = reinterpret_cast<const float4*>(row)[i];
+                v[4 * i] = t4.x;
+                if (4 * i + 1 < K + 4) v[4 * i + 1] = t4.y;
+                if (4 * i + 2 < K + 4) v[4 * i + 2] = t4.z;
+                if (4 * i + 3 < K + 4) v[4 * i + 3] = t4.w;
             }
-            unsigned long long a0 = 0ull, a1 = 0ull, a2 = 0ull, a3 = 0ull;
+            unsigned long long a01 = 0ull, a23 = 0ull;
 #pragma unroll
-            for (int i = 0; i < NPR; ++i) {
-                a0 = ffma2(we[i], pr[i], a0);
-                a1 = ffma2(wo[i], pr[i], a1);
-                a2 = ffma2(we[i], pr[i + 1], a2);
-                a3 = ffma2(wo[i], pr[i + 1], a3);
+            for (int p = 0; p < K + 3; ++p) {
+                const unsigned long long vv = f2pack(v[p], v[p]);
+                if (p <= K) a01 = ffma2(vv, wp[p], a01);
+                if (p >= 2) a23 = ffma2(vv, wp[p - 2], a23);
             }
-            o4[c][0] = f2lo(a0) + f2hi(a0);
-            o4[c][1] = f2lo(a1) + f2hi(a1);
-            o4[c][2] = f2lo(a2) + f2hi(a2);
-            o4[c][3] = f2lo(a3) + f2hi(a3);
-        }
-        // floor(x + 0.5) in the low mantissa byte: (x + 0.5) + 2^23 rounded down
-        // (x in [0, 255 (1 + eps)]: non-negative normalised weights and 8-bit inputs)
-        uint32_t z[12];
-#pragma unroll
-        for (int bi = 0; bi < 12; bi += 2) {
-            const unsigned long long q = fadd2_rm(
-                fadd2(f2pack(o4[bi % 3][bi / 3], o4[(bi + 1) % 3][(bi + 1) / 3]), kHalf2), kMagic2);
-            z[bi] = (uint32_t)q;
-            z[bi + 1] = (uint32_t)(q >> 32);
+            // floor(x + 0.5) in the low mantissa byte: (x + 0.5) + 2^23 rounded down
+            // (x in [0, 255 (1 + eps)]: non-negative normalised weights, 8-bit inputs)
+            const unsigned long long q01 = fadd2_rm(fadd2(a01, kHalf2), kMagic2);
+            const unsigned long long q23 = fadd2_rm(fadd2(a23, kHalf2), kMagic2);
+            z[c] = (uint32_t)q01;
+            z[3 + c] = (uint32_t)(q01 >> 32);
+            z[6 + c] = (uint32_t)q23;
+            z[9 + c] = (uint32_t)(q23 >> 32);
         }
         uint32_t ob[3];
 #pragma unroll
