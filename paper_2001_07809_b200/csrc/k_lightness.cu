@@ -96,55 +96,136 @@ __global__ void __launch_bounds__(kThreads) k_lstar(Frame f, const LstarTables* 
     }
 }
 
-// Both views in one streaming launch (blockIdx.y = view), 16 pixels per
-// thread-chunk (3 x 16-byte loads, one 16-byte store), two chunks in flight
-// per thread; W % 16 == 0 and 16-byte aligned planes.
-__global__ void __launch_bounds__(kThreads) k_lstar2(Frame f, const LstarTables* __restrict__ tab) {
-    __shared__ double pr[256], pg[256], pb[256];
-    for (int i = threadIdx.x; i < 256; i += kThreads) {
-        pr[i] = tab->prod[0][i];
-        pg[i] = tab->prod[1][i];
-        pb[i] = tab->prod[2][i];
+// floor(2^36 y) for 0 <= y <= 1 without a (slow, XU-pipe) F64->int
+// conversion: y + 2^16 rounded toward zero is 2^16 + floor(2^36 y) 2^-36, so
+// the low 52 bits of its pattern are floor(2^36 y) = bucket << 24 | position.
+__device__ __forceinline__ void split36(double y, uint32_t& bk, uint32_t& yq) {
+    const double t = __dadd_rz(y, 65536.0);
+    const uint32_t lo = __double2loint(t), hi = __double2hiint(t);
+    bk = __funnelshift_r(lo, hi, 24) & 0x1fffu;
+    yq = lo & 0xffffffu;
+}
+
+// Both views in one streaming launch (blockIdx.y = view); W % 16 == 0 and
+// 16-byte aligned planes.  One 1024-thread CTA per SM.  A warp takes 32
+// consecutive 16-pixel chunks (1536 contiguous bytes, coalesced 16-byte loads
+// into shared memory) and lane l converts the pixel pairs 2l, 2l+1 (+ 64p).
+// The three product tables are held in 16 copies, entry e of copy c at
+// (16 e + c) * 8 bytes: lane l reads copy l % 16, so each half-warp's 64-bit
+// lookups land in 16 distinct bank pairs whatever the pixel values (a 64-bit
+// warp access is two half-warp wavefronts).  The 512 output bytes go back
+// through shared memory as one 16-byte store per chunk.
+constexpr int kL2Threads = 1024, kL2Copies = 16;
+constexpr size_t kL2TabBytes = 3 * 256 * kL2Copies * sizeof(double);          // 96 KB
+constexpr size_t kL2Smem = kL2TabBytes + (kLstarBuckets + 4) * sizeof(uint32_t) +  // + 16 KB
+                           (size_t)(kL2Threads / 32) * (97 + 32) * sizeof(uint4);    // + 64.5 KB
+
+__global__ void __launch_bounds__(kL2Threads, 1) k_lstar2(Frame f, const LstarTables* __restrict__ tab) {
+    extern __shared__ __align__(16) unsigned char l2s[];
+    double* tabs = reinterpret_cast<double*>(l2s);  // [3][256][16]
+    uint32_t* bw = reinterpret_cast<uint32_t*>(l2s + kL2TabBytes);
+    uint4* xin_all = reinterpret_cast<uint4*>(bw + kLstarBuckets + 4);  // [32 warps][97]
+    uint4* xout_all = xin_all + (kL2Threads / 32) * 97;                 // [32 warps][32]
+    {  // all loads in flight before the stores
+        constexpr int NT = 3 * 256 * kL2Copies / kL2Threads;  // 12 table entries per thread
+        double t[NT];
+#pragma unroll
+        for (int k = 0; k < NT; ++k) {
+            const int i = threadIdx.x + k * kL2Threads;  // = (table * 256 + e) * 16 + c
+            t[k] = __ldg(&tab->prod[0][0] + (i >> 4));
+        }
+        constexpr int NV = kLstarBuckets / 4 / kL2Threads;
+        uint4 v[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) v[k] = __ldg(reinterpret_cast<const uint4*>(tab->bw) + threadIdx.x + k * kL2Threads);
+#pragma unroll
+        for (int k = 0; k < NT; ++k) tabs[threadIdx.x + k * kL2Threads] = t[k];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) reinterpret_cast<uint4*>(bw)[threadIdx.x + k * kL2Threads] = v[k];
+        if (threadIdx.x == 0) bw[kLstarBuckets] = tab->bw[kLstarBuckets];
     }
     __syncthreads();
     // Y = (0.2126 lin[R] + 0.7152 lin[G]) + 0.0722 lin[B], products tabulated
-    auto lstar_p = [&](uint32_t r, uint32_t g, uint32_t b) {
-        const double y = __dadd_rn(__dadd_rn(pr[r], pg[g]), pb[b]);
-        const int bk = min((int)__dmul_rz(y, (double)kLstarBuckets), kLstarBuckets);
-        return (uint32_t)__ldg(&tab->base[bk]) + (y >= __ldg(&tab->tb[bk]) ? 1u : 0u);
+    // (byte v of channel c at copy-base + 128 v); floor(2^36 Y) = bucket << 24
+    // | position in the bucket in 2^-24 steps (exact, see split36).
+    // Y <= 1 (coefficients sum to 1, linear[] <= 1), so the bucket is <= 4096.
+    const char* prb = reinterpret_cast<const char*>(tabs) + (threadIdx.x & (kL2Copies - 1)) * 8;
+    const char* pgb = prb + 256 * kL2Copies * 8;
+    const char* pbb = pgb + 256 * kL2Copies * 8;
+    auto y_of = [&](uint32_t v) {  // v = R | G << 8 | B << 16
+        return __dadd_rn(__dadd_rn(*reinterpret_cast<const double*>(prb + ((v << 7) & 0x7f80u)),
+                                   *reinterpret_cast<const double*>(pgb + ((v >> 1) & 0x7f80u))),
+                         *reinterpret_cast<const double*>(pbb + ((v >> 9) & 0x7f80u)));
     };
-    const int view = blockIdx.y;
+    const int view = blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint8_t* __restrict__ rgb = view == 0 ? f.rgbL : f.rgbR;
     uint8_t* __restrict__ gray = view == 0 ? f.grayL : f.grayR;
     const int cpr = f.W / 16;
     const long long nch = (long long)cpr * f.H;
-    const long long stride = (long long)gridDim.x * kThreads;
-    auto convert = [&](long long c, uint4 a, uint4 b, uint4 d) {
-        const int y = (int)(c / cpr), x = (int)(c - (long long)y * cpr) * 16;
-        const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
-        uint32_t out[4] = {0, 0, 0, 0};
+    const long long stride = (long long)gridDim.x * kL2Threads;
+    uint4* xin = xin_all + wid * 97;
+    uint4* xout = xout_all + wid * 32;
+    const uint32_t* xw = reinterpret_cast<const uint32_t*>(xin);
+    uint8_t* xo = reinterpret_cast<uint8_t*>(xout);
+    // lane l converts the pixel pairs (2l, 2l+1) + 64p: bytes 6l + 192p .. +5,
+    // in words 48p + (3l >> 1) and the next one, starting at byte 2 (l & 1)
+    const int sh = (lane & 1) * 16, wb = (3 * lane) >> 1;
+    uint16_t* xo2 = reinterpret_cast<uint16_t*>(xo);
+    // software pipelined: the next group's 48 bytes per lane are in flight
+    // while this group converts
+    auto load_group = [&](long long cw, uint4* t) {
+        const int nc = (int)min(32ll, nch - cw);
+        const uint4* src = reinterpret_cast<const uint4*>(rgb + (size_t)cw * 48);
 #pragma unroll
-        for (int p = 0; p < 16; ++p) {
-            const int o = p * 3;
-            const uint32_t r = (w[o >> 2] >> ((o & 3) * 8)) & 0xffu;
-            const uint32_t g = (w[(o + 1) >> 2] >> (((o + 1) & 3) * 8)) & 0xffu;
-            const uint32_t bb = (w[(o + 2) >> 2] >> (((o + 2) & 3) * 8)) & 0xffu;
-            out[p >> 2] |= lstar_p(r, g, bb) << ((p & 3) * 8);
-        }
-        *reinterpret_cast<uint4*>(gray + (size_t)y * f.P + x) = make_uint4(out[0], out[1], out[2], out[3]);
+        for (int k = 0; k < 3; ++k)
+            if (lane + 32 * k < 3 * nc) t[k] = __ldcs(src + lane + 32 * k);
     };
-    long long c = blockIdx.x * (long long)kThreads + threadIdx.x;
-    for (; c + stride < nch; c += 2 * stride) {
-        const uint4* s0 = reinterpret_cast<const uint4*>(rgb + (size_t)c * 48);
-        const uint4* s1 = reinterpret_cast<const uint4*>(rgb + (size_t)(c + stride) * 48);
-        const uint4 a0 = __ldcs(s0), b0 = __ldcs(s0 + 1), d0 = __ldcs(s0 + 2);
-        const uint4 a1 = __ldcs(s1), b1 = __ldcs(s1 + 1), d1 = __ldcs(s1 + 2);
-        convert(c, a0, b0, d0);
-        convert(c + stride, a1, b1, d1);
-    }
-    if (c < nch) {
-        const uint4* s0 = reinterpret_cast<const uint4*>(rgb + (size_t)c * 48);
-        convert(c, __ldcs(s0), __ldcs(s0 + 1), __ldcs(s0 + 2));
+    long long cw = blockIdx.x * (long long)kL2Threads + wid * 32;
+    uint4 t[3];
+    if (cw < nch) load_group(cw, t);
+    for (; cw < nch; cw += stride) {
+        const int nc = (int)min(32ll, nch - cw);
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (lane + 32 * k < 3 * nc) xin[lane + 32 * k] = t[k];
+        __syncwarp();
+        if (cw + stride < nch) load_group(cw + stride, t);
+        uint32_t ties = 0;
+        auto pair_of = [&](int p) {
+            return ((unsigned long long)xw[48 * p + wb + 1] << 32 | xw[48 * p + wb]) >> sh;
+        };
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            const unsigned long long x = pair_of(p);
+            uint32_t g2 = 0;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                uint32_t bk, yq;
+                split36(y_of((uint32_t)(x >> (24 * e))), bk, yq);
+                const uint32_t w = bw[bk], q = w & 0xffffffu;
+                g2 |= ((w >> 24) + (yq > q ? 1u : 0u)) << (8 * e);
+                ties |= (yq == q ? 1u : 0u) << (2 * p + e);
+            }
+            xo2[lane + 32 * p] = (uint16_t)g2;
+        }
+        if (ties) {  // rare: Y's position equals the threshold's 2^-24 step, read tb[b]
+#pragma unroll 1
+            for (int i = 0; i < 16; ++i) {
+                if ((ties >> i) & 1u) {
+                    const double y = y_of((uint32_t)(pair_of(i >> 1) >> (24 * (i & 1))));
+                    uint32_t bk, yq;
+                    split36(y, bk, yq);
+                    if (y >= __ldg(&tab->tb[bk])) xo[2 * (lane + 32 * (i >> 1)) + (i & 1)] += 1;
+                }
+            }
+        }
+        __syncwarp();
+        if (lane < nc) {
+            const long long c = cw + lane;
+            const int y = (int)(c / cpr), x = (int)(c - (long long)y * cpr) * 16;
+            *reinterpret_cast<uint4*>(gray + (size_t)y * f.P + x) = xout[lane];
+        }
+        __syncwarp();
     }
 }
 
@@ -223,8 +304,9 @@ void launch_lightness(const Frame& f, const LstarTables* dtab, bool left, bool r
     if (left && right && f.W % 16 == 0 && aligned) {
         // frame path: both views in one launch, then the histogram pass
         const long long nch = (long long)(f.W / 16) * f.H;
-        const int bx = (int)std::min<long long>((nch + kThreads - 1) / kThreads, 148 * 4);
-        k_lstar2<<<dim3(bx, 2), kThreads, 0, st>>>(f, dtab);
+        const int bx = (int)std::min<long long>((nch + kL2Threads - 1) / kL2Threads, 74);
+        cudaFuncSetAttribute(k_lstar2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kL2Smem);
+        k_lstar2<<<dim3(bx, 2), kL2Threads, kL2Smem, st>>>(f, dtab);
         if (hist) {
             const int hb = (int)std::min<long long>((nch + kThreads - 1) / kThreads, 148 * 4);
             k_hist_warp<<<hb, kThreads, 0, st>>>(f, f.grayL);

@@ -176,6 +176,9 @@ void make_lstar_tables(LstarTables* t) {
         t->base[b] = (unsigned char)(v - 1);
         t->tb[b] = (v < 256 && t->thr[v] < hi) ? t->thr[v] : INFINITY;
         if (v + 1 < 256 && t->thr[v + 1] < hi && t->thr[v] < hi) t->tb[b] = -INFINITY;  // flagged
+        uint32_t q = 0xffffffu;
+        if (std::isfinite(t->tb[b])) q = (uint32_t)((t->tb[b] * NB - b) * 16777216.0);  // exact, < 2^24
+        t->bw[b] = (uint32_t)t->base[b] << 24 | q;
     }
 }
 

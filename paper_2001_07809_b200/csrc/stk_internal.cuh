@@ -108,6 +108,11 @@ struct LstarTables {
     // prod[c][v] = coefficient_c * linear[v] (lightness.cpp:41-43 products,
     // IEEE round-to-nearest on the host == __dmul_rn on the device)
     double prod[3][256];
+    // packed bucket words for K1's shared-memory lookup: base[b] << 24 | q[b],
+    // q[b] = floor(2^24 * (4096 * tb[b] - b)) (0xffffff without a threshold);
+    // a Y in bucket b with floor(2^24 * (4096 * Y - b)) != q[b] decides
+    // Y >= tb[b] from the integers alone (all steps exact), ties read tb[b].
+    alignas(16) uint32_t bw[4097];
 };
 constexpr int kLstarBuckets = 4096;
 
