@@ -389,11 +389,23 @@ def main():
         "shared_wavefronts_pct": sad_prof.get("lsu_shared_wavefronts_pct"),
         "traffic_source": "profiles/r01_ncu_kernels.json (ncu --set full, one 4K launch)" if traffic else None,
     }
+    # the brute-force SAD ceiling (VABSDIFF4 issue rate,
+    # microbenchmarked here) and the frame roofline 1 / (bytes/BW + SAD/peak)
+    sad_peak = C.c_double(0.0)
+    if L.stk_probe_sad_peak(dev.h, C.byref(sad_peak)) == 0 and sad_peak.value > 0:
+        roofline["sad_ceiling_byte_ad_per_s"] = sad_peak.value
+        roofline["byte_sad_vs_ceiling"] = round(sad_ops / t_match / sad_peak.value, 3)
+        roofline["ceiling_note"] = ("ceiling = measured VABSDIFF4 rate x 4 (brute-force w^2 per "
+                                    "(pixel, d)); the box-filter formulation exceeds it")
     roofline_frame = {
         "bound": "hbm", "kernel": "frame (all launches, algorithmic 41N+8M bytes)",
         "achieved": round(total_alg / (frame_ms_dev * 1e-3) / 1e9, 1), "peak": hbm_peak, "unit": "GB/s",
         "frac": round(total_alg / (frame_ms_dev * 1e-3) / 1e9 / hbm_peak, 4), "dominant_stage": dominant,
     }
+    if sad_peak.value > 0:
+        model_fps = 1.0 / (total_alg / 8.0e12 + sad_ops / sad_peak.value)
+        roofline_frame["survey_model_fps"] = round(model_fps, 1)
+        roofline_frame["fps_vs_survey_model"] = round(fps_dev / model_fps, 3)
 
     line = {
         "metric": METRIC, "value": round(fps_dev, 3), "unit": "frames/s", "n_gpus": world,

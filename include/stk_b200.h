@@ -205,6 +205,12 @@ stk_status stk_bad_pixel_rate(stk_ctx* ctx, const int16_t* computed, const int16
                               int h, double delta_d, double* rate, uint64_t* compared,
                               uint64_t* excluded);
 
+/* Diagnostics: VABSDIFF4 throughput of this device in byte absolute
+ * differences per second (4 per instruction), from a register-only probe
+ * kernel -- the brute-force SAD ceiling the match stage is reported against
+ * (SURVEY.md 8(d)); no reference counterpart. */
+stk_status stk_probe_sad_peak(stk_ctx* ctx, double* byte_ad_per_s);
+
 /* ----------------------------------------------------------- frames -- */
 /* run_depth_pipeline (focus == NULL) / run_refocus_pipeline
  * (pipeline.hpp:78-89): synchronous, host buffers. */

@@ -81,6 +81,7 @@ SIGNATURES = {
     "stk_sad_cost": (I, [VP, VP, VP, I, I, I, I, I, I, C.POINTER(C.c_uint32)]),
     "stk_match_boundary_pixels": (I, [VP, VP, VP, VP, I, I, I, I, VP]),
     "stk_dense_sad_baseline": (I, [VP, VP, VP, I, I, I, I, VP]),
+    "stk_probe_sad_peak": (I, [VP, C.POINTER(C.c_double)]),
     "stk_bad_pixel_rate": (I, [VP, VP, VP, I, I, D, C.POINTER(C.c_double), C.POINTER(C.c_uint64),
                                C.POINTER(C.c_uint64)]),
     "stk_fill_scanlines": (I, [VP, VP, I, I, VP]),

@@ -56,7 +56,48 @@ __global__ void __launch_bounds__(256) k_bad_pixel(const int16_t* __restrict__ c
     }
 }
 
+// VABSDIFF4 issue-rate probe (the match stage's brute-force
+// ALU ceiling is microbenchmarked on the box): 8 independent chains per
+// thread, 32 VABSDIFF4 per loop trip, no memory traffic.
+__global__ void __launch_bounds__(256) k_vabsdiff4_probe(uint32_t seed, int iters, uint32_t* out) {
+    uint32_t a[8], b[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        a[i] = seed * (2 * i + 1) + threadIdx.x;
+        b[i] = (seed ^ 0x9e3779b9u) * (i + 3) + blockIdx.x;
+    }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = __vabsdiffu4(a[i], b[i]);
+    }
+    uint32_t x = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x ^= a[i];
+    if (x == seed) out[0] = x;  // keeps the chains alive; practically never taken
+}
+
 }  // namespace
+
+double probe_vabsdiff4_rate(int sms, uint32_t* scratch, cudaStream_t st) {
+    const int blocks = sms * 8, iters = 8192;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_vabsdiff4_probe<<<blocks, 256, 0, st>>>(12345u, 64, scratch);  // warm-up
+    cudaEventRecord(e0, st);
+    k_vabsdiff4_probe<<<blocks, 256, 0, st>>>(12345u, iters, scratch);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (cudaGetLastError() != cudaSuccess || ms <= 0.f) return 0.0;
+    const double ops = (double)blocks * 256 * iters * 32;  // VABSDIFF4 instructions (4 byte-ADs each)
+    return ops / (ms * 1e-3);
+}
 
 void launch_bad_pixel(const int16_t* comp, const int16_t* truth, long long n, double delta,
                       unsigned long long* out, cudaStream_t st) {

@@ -1171,6 +1171,19 @@ stk_status stk_bad_pixel_rate(stk_ctx* ctx, const int16_t* computed, const int16
     return STK_OK;
 }
 
+// the match stage's brute-force ALU ceiling, microbenchmarked
+stk_status stk_probe_sad_peak(stk_ctx* ctx, double* byte_ad_per_s) {
+    if (!byte_ad_per_s) return fail(ctx, STK_EPARAM, "probe_sad_peak: null output");
+    STAGE_BEGIN(1, 1);
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    const double rate = probe_vabsdiff4_rate(sms, reinterpret_cast<uint32_t*>(s.sc), st);
+    CK(cudaGetLastError());
+    if (rate <= 0.0) return fail(ctx, STK_ECUDA, "probe_sad_peak: probe kernel failed");
+    *byte_ad_per_s = 4.0 * rate;
+    return STK_OK;
+}
+
 stk_status stk_fill_scanlines(stk_ctx* ctx, const int16_t* sparse, int w, int h, int16_t* out) {
     STAGE_BEGIN(w, h);
     if (N == 0) return STK_OK;

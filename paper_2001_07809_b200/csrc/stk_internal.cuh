@@ -145,6 +145,8 @@ void launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, in
 void launch_prune_mask_bits(const Frame& f, const uint8_t* mask, uint32_t* rbits, int32_t* runroot,
                             int32_t* bord, uint32_t* sbits, int sbits_words, cudaStream_t st);
 // K9 evaluation: out[0] += compared, out[1] += bad (evaluate.cpp:17-74)
+// VABSDIFF4 instructions per second on this device (probe kernel, blocking)
+double probe_vabsdiff4_rate(int sms, uint32_t* scratch, cudaStream_t st);
 void launch_bad_pixel(const int16_t* comp, const int16_t* truth, long long n, double delta,
                       unsigned long long* out, cudaStream_t st);
 // true when launch_sad will run the per-pixel list kernel (it needs f.list)

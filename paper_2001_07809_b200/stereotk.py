@@ -385,6 +385,14 @@ def eval_report_json(result: EvalResult) -> str:
                       separators=(",", ":"))
 
 
+def probe_sad_peak(*, device=None) -> float:
+    """Brute-force SAD ceiling of this device: VABSDIFF4 byte absolute
+    differences per second from a register-only probe kernel."""
+    out = C.c_double(0.0)
+    _dev(device)._call("stk_probe_sad_peak", C.byref(out))
+    return out.value
+
+
 def fill_scanlines(sparse, workers: int = 1, *, device=None) -> np.ndarray:
     sparse = np.ascontiguousarray(sparse, np.int16)
     h, w = sparse.shape

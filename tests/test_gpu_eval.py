@@ -73,3 +73,10 @@ def test_dense_sad_baseline_validation(dev, stk):
         stk.dense_sad_baseline(g, g, stk.MatchConfig(3, -1), device=dev)
     with pytest.raises(stk.ParamError, match="image sizes differ"):
         stk.dense_sad_baseline(g, np.zeros((10, 11), np.uint8), stk.MatchConfig(3, 2), device=dev)
+
+
+@pytest.mark.gpu
+def test_probe_sad_peak_plausible(dev, stk):
+    # 148 SMs x 64 lanes/clk x 4 byte-ADs at ~1.9 GHz is ~7e13; accept a wide band
+    peak = stk.probe_sad_peak()
+    assert 1e12 < peak < 1e15, peak
