@@ -226,3 +226,15 @@ def test_async_slots_match_sync(dev, stk, synth):
         stk._raise(L.stk_frame_wait(dev.h, s, None, None, None), dev.h)
     for a, b in zip(outs, want):
         eq(a, b, "async")
+
+
+def test_frame_lightness_all_2pow24_triples(dev, stk, port):
+    """The frame path's K1 (both views in one launch, bucket words + exact tie
+    reads) on every RGB triple, left and right, against the pinned oracle."""
+    v = np.arange(256, dtype=np.uint8)
+    rgb = np.stack(np.meshgrid(v, v, v, indexing="ij"), -1).reshape(4096, 4096, 3)
+    rgb_r = np.ascontiguousarray(rgb[::-1])
+    res, _ = run(stk, dev, rgb, rgb_r, k=4, window=9, D=8)
+    want = port.lightness(rgb)
+    eq(res.left_lightness, want, "left_lightness")
+    eq(res.right_lightness, want[::-1], "right_lightness")
