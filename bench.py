@@ -327,6 +327,9 @@ def main():
         submit_host(i)
     ms_e2e = timed_region(submit_host, args.steps)
     fps_e2e = world * args.steps / (ms_e2e / 1e3)
+    for s in range(S):
+        wait(s)
+    pcie = _pcie_probe(local)
 
     # ---- per-stage device times (separate, event-instrumented frames)
     stage_ms = {}
@@ -421,7 +424,9 @@ def main():
         "e2e": {"value": round(fps_e2e, 3), "unit": "frames/s",
                 "h2d_bytes_per_step": 2 * 3 * N,
                 "d2h_bytes_per_step": 3 * N + (2 * N if args.e2e_dense else 0),
-                "path": "stk_frame_submit (C-ABI, pinned host buffers)"},
+                "path": "stk_frame_submit (C-ABI, pinned host buffers)",
+                "pcie": _pcie_model(pcie, 2 * 3 * N, 3 * N + (2 * N if args.e2e_dense else 0),
+                                    fps_e2e / world, frame_ms_dev)},
         "gpu_launches": int(kernels_per_frame * args.steps * 2),
         "kernels_per_frame": int(kernels_per_frame),
         "roofline": roofline,
@@ -453,6 +458,72 @@ def _pinned(L, nbytes):
         raise RuntimeError("pinned alloc failed")
     _pinned_keep.append(p)
     return p.value
+
+
+def _pcie_probe(dev_index, mb=128, reps=5):
+    """Pinned host <-> device copy bandwidth on this box (GB/s): H2D alone,
+    D2H alone, and both directions at once on two streams (the e2e leg's
+    ceiling: a frame's inputs go up while an earlier frame's result comes down)."""
+    import torch
+
+    n = mb << 20
+    h_a = torch.empty(n, dtype=torch.uint8).pin_memory()
+    h_b = torch.empty(n, dtype=torch.uint8).pin_memory()
+    d_a = torch.empty(n, dtype=torch.uint8, device=f"cuda:{dev_index}")
+    d_b = torch.empty(n, dtype=torch.uint8, device=f"cuda:{dev_index}")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fn()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            fn()
+        # the copies run on s1/s2: join them into the current stream before e1
+        torch.cuda.current_stream().wait_stream(s1)
+        torch.cuda.current_stream().wait_stream(s2)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e-3
+
+    def h2d():
+        with torch.cuda.stream(s1):
+            d_a.copy_(h_a, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s1)
+
+    def d2h():
+        with torch.cuda.stream(s2):
+            h_b.copy_(d_b, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s2)
+
+    def both():
+        with torch.cuda.stream(s1):
+            d_a.copy_(h_a, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_b.copy_(d_b, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s1)
+        torch.cuda.current_stream().wait_stream(s2)
+
+    t_h = timed(h2d)
+    t_d = timed(d2h)
+    t_b = timed(both)
+    gb = reps * n / 1e9
+    return {"h2d_GBps": round(gb / t_h, 1), "d2h_GBps": round(gb / t_d, 1),
+            "duplex_GBps_each_way": round(gb / t_b, 1), "probe": f"{reps} x {mb} MiB pinned copies"}
+
+
+def _pcie_model(pcie, h2d_bytes, d2h_bytes, fps_e2e, frame_ms_dev):
+    """e2e ceiling: per frame max(H2D time, D2H time, device time) with the
+    copies overlapping each other (duplex bandwidth) and the kernels."""
+    bw = pcie["duplex_GBps_each_way"] * 1e9
+    t = max(h2d_bytes / bw, d2h_bytes / bw, frame_ms_dev * 1e-3)
+    out = dict(pcie)
+    out["achieved_h2d_GBps"] = round(h2d_bytes * fps_e2e / 1e9, 1)
+    out["model_fps"] = round(1.0 / t, 1)
+    out["frac"] = round(fps_e2e * t, 3)
+    return out
 
 
 def _ncu_profile():
