@@ -238,3 +238,25 @@ def test_frame_lightness_all_2pow24_triples(dev, stk, port):
     want = port.lightness(rgb)
     eq(res.left_lightness, want, "left_lightness")
     eq(res.right_lightness, want[::-1], "right_lightness")
+
+
+def test_pipeline_8k_config_e(dev, stk, synth):
+    """Config E (7680x4320, D=256, w=31, K=8, sigma=8 -> 49-tap blur): the
+    warp-specialised SAD (G=5 lanes per column group for w=31) equals the
+    list kernel on every pixel; reconstruction and blur invariants hold."""
+    W, H, D, win, K = 7680, 4320, 256, 31, 8
+    l, r = synth.dead_leaves(W, H, D, frame=0)
+    dev.set_sad_kernel("ws")
+    a, img = run(stk, dev, l, r, k=K, window=win, D=D, focus=[(128, 256)], sigma=8.0)
+    dev.set_sad_kernel("list")
+    b, _ = run(stk, dev, l, r, k=K, window=win, D=D)
+    dev.set_sad_kernel("auto")
+    eq(a.sparse, b.sparse, "ws vs list")
+    assert 0.1 < a.stats.matched_fraction < 0.3
+    k = a.sparse >= 0
+    assert (a.row_filled[k] == a.sparse[k]).all()
+    k = a.row_filled >= 0
+    assert (a.dense[k] == a.row_filled[k]).all()
+    sharp = (a.dense >= 128) & (a.dense <= 256)
+    assert (img[sharp] == l[sharp]).all()
+    assert (img[~sharp] != l[~sharp]).any()
