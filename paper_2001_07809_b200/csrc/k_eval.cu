@@ -85,18 +85,22 @@ double probe_vabsdiff4_rate(int sms, uint32_t* scratch, cudaStream_t st) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    k_vabsdiff4_probe<<<blocks, 256, 0, st>>>(12345u, 64, scratch);  // warm-up
-    cudaEventRecord(e0, st);
-    k_vabsdiff4_probe<<<blocks, 256, 0, st>>>(12345u, iters, scratch);
-    cudaEventRecord(e1, st);
-    cudaEventSynchronize(e1);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
+    k_vabsdiff4_probe<<<blocks, 256, 0, st>>>(12345u, iters, scratch);  // warm-up (clocks up)
+    float best = 0.f;
+    for (int rep = 0; rep < 3; ++rep) {  // best of 3
+        cudaEventRecord(e0, st);
+        k_vabsdiff4_probe<<<blocks, 256, 0, st>>>(12345u, iters, scratch);
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms > 0.f && (best == 0.f || ms < best)) best = ms;
+    }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    if (cudaGetLastError() != cudaSuccess || ms <= 0.f) return 0.0;
+    if (cudaGetLastError() != cudaSuccess || best <= 0.f) return 0.0;
     const double ops = (double)blocks * 256 * iters * 32;  // VABSDIFF4 instructions (4 byte-ADs each)
-    return ops / (ms * 1e-3);
+    return ops / (best * 1e-3);
 }
 
 void launch_bad_pixel(const int16_t* comp, const int16_t* truth, long long n, double delta,
