@@ -421,6 +421,173 @@ __global__ void __launch_bounds__(PC * PS) k_peek_cols2(Frame f, const int16_t* 
     }
 }
 
+// K7 v4: k_peek_cols2's algorithm with two adjacent columns per thread
+// (32-bit loads/stores of int16 pairs: a warp's 8 column pairs x 4 segments
+// move 32 contiguous bytes per row each) and unchecked full batches.
+constexpr int P4C = 8;   // column pairs per CTA (16 columns)
+constexpr int P4S = 64;  // row segments per column
+constexpr int P4B = 8;   // rows per batch
+
+struct ColSeg {  // segment summary of one column while walking down
+    int count, f1, f2, l1, l2;
+};
+__device__ __forceinline__ void seg_add(ColSeg& m, int d) {
+    const bool kn = d >= 0;
+    m.f2 = (kn && m.count == 1) ? d : m.f2;
+    m.f1 = (kn && m.count == 0) ? d : m.f1;
+    m.l2 = kn ? m.l1 : m.l2;
+    m.l1 = kn ? d : m.l1;
+    m.count += kn;
+}
+__device__ __forceinline__ uint32_t pack2(int a, int b) { return (uint32_t)(uint16_t)a | (uint32_t)b << 16; }
+__device__ __forceinline__ int lo16(uint32_t v) { return (int16_t)(v & 0xffffu); }
+__device__ __forceinline__ int hi16s(uint32_t v) { return (int16_t)(v >> 16); }
+
+__global__ void __launch_bounds__(P4C * P4S, 2) k_peek_cols4(Frame f, const int16_t* __restrict__ in,
+                                                          int16_t* __restrict__ out) {
+    __shared__ SegSum seg[P4S][2 * P4C];
+    __shared__ int16_t ctx_ab[P4S][2 * P4C], ctx_bl[P4S][2 * P4C];
+    __shared__ int col_total[2 * P4C], col_top[2 * P4C], col_bot[2 * P4C];
+    __shared__ unsigned long long red[P4C * P4S / 32];
+    const int W = f.W, H = f.H, thr = f.thr;
+    const int cp = threadIdx.x % P4C, s = threadIdx.x / P4C;
+    const int x = 2 * (blockIdx.x * P4C + cp);  // W even
+    const int sr = (H + P4S - 1) / P4S;
+    const int ya = min(H, s * sr), yb = min(H, ya + sr);
+    const bool col = x < W;
+    const uint32_t* __restrict__ in2 = reinterpret_cast<const uint32_t*>(in);
+    uint32_t* __restrict__ out2 = reinterpret_cast<uint32_t*>(out);
+    const size_t W2 = (size_t)W / 2;  // row stride in pairs
+    // pass 1 (top-down)
+    ColSeg m0{0, -1, -1, -1, -1}, m1{0, -1, -1, -1, -1};
+    if (col) {
+        int c0 = -1, c1 = -1;
+        size_t o = (size_t)ya * W2 + x / 2;
+        for (int yy = ya; yy < yb; yy += P4B, o += P4B * W2) {
+            const int n = min(P4B, yb - yy);
+            uint32_t v[P4B];
+            if (n == P4B) {
+#pragma unroll
+                for (int k = 0; k < P4B; ++k) v[k] = __ldg(in2 + o + k * W2);
+#pragma unroll
+                for (int k = 0; k < P4B; ++k) {
+                    out2[o + k * W2] = pack2(c0, c1);
+                    const int d0 = lo16(v[k]), d1 = hi16s(v[k]);
+                    seg_add(m0, d0);
+                    seg_add(m1, d1);
+                    c0 = d0 >= 0 ? d0 : c0;
+                    c1 = d1 >= 0 ? d1 : c1;
+                }
+            } else {
+                for (int k = 0; k < n; ++k) {
+                    const uint32_t vk = __ldg(in2 + o + k * W2);
+                    out2[o + k * W2] = pack2(c0, c1);
+                    const int d0 = lo16(vk), d1 = hi16s(vk);
+                    seg_add(m0, d0);
+                    seg_add(m1, d1);
+                    c0 = d0 >= 0 ? d0 : c0;
+                    c1 = d1 >= 0 ? d1 : c1;
+                }
+            }
+        }
+    }
+    seg[s][2 * cp] = SegSum{m0.count, (int16_t)m0.f1, (int16_t)m0.f2, (int16_t)m0.l1, (int16_t)m0.l2};
+    seg[s][2 * cp + 1] = SegSum{m1.count, (int16_t)m1.f1, (int16_t)m1.f2, (int16_t)m1.l1, (int16_t)m1.l2};
+    __syncthreads();
+    // phase 2: one thread per column scans the segments once
+    if (threadIdx.x < 2 * P4C) {
+        const int cx = threadIdx.x;
+        int total = 0, last = -1, cf1 = -1, cf2 = -1;
+        for (int i = 0; i < P4S; ++i) {
+            const SegSum g = seg[i][cx];
+            ctx_ab[i][cx] = (int16_t)last;
+            if (g.count) {
+                last = g.l1;
+                if (cf1 < 0) {
+                    cf1 = g.f1;
+                    if (g.count > 1) cf2 = g.f2;
+                } else if (cf2 < 0) {
+                    cf2 = g.f1;
+                }
+            }
+            total += g.count;
+        }
+        int first = -1, cl1 = -1, cl2 = -1;
+        for (int i = P4S - 1; i >= 0; --i) {
+            const SegSum g = seg[i][cx];
+            ctx_bl[i][cx] = (int16_t)first;
+            if (g.count) {
+                first = g.f1;
+                if (cl1 < 0) {
+                    cl1 = g.l1;
+                    if (g.count > 1) cl2 = g.l2;
+                } else if (cl2 < 0) {
+                    cl2 = g.l1;
+                }
+            }
+        }
+        col_total[cx] = total;
+        col_top[cx] = total >= 2 ? peek_estimate(cf1, cf2, thr) : -1;
+        col_bot[cx] = total >= 2 ? peek_estimate(cl2, cl1, thr) : -1;
+    }
+    __syncthreads();
+    // pass 2 (bottom-up)
+    unsigned long long known = 0;
+    if (col) {
+        const int t0 = col_total[2 * cp], t1 = col_total[2 * cp + 1];
+        const int et0 = col_top[2 * cp], et1 = col_top[2 * cp + 1];
+        const int eb0 = col_bot[2 * cp], eb1 = col_bot[2 * cp + 1];
+        const int ab0 = ctx_ab[s][2 * cp], ab1 = ctx_ab[s][2 * cp + 1];
+        int nb0 = ctx_bl[s][2 * cp], nb1 = ctx_bl[s][2 * cp + 1];
+        auto resolve = [&](int d, int a, int above, int& nb, int total, int et, int eb) {
+            const int ab = a >= 0 ? a : above;  // nearest known above
+            int r;
+            if (d >= 0) r = d;
+            else if (total == 0) r = -1;
+            else if (total == 1) r = ab >= 0 ? ab : nb;
+            else if (ab >= 0 && nb >= 0) r = peek_estimate(ab, nb, thr);
+            else r = ab < 0 ? et : eb;
+            nb = d >= 0 ? d : nb;
+            return r;
+        };
+        for (int yy = yb - 1; yy >= ya; yy -= P4B) {
+            const int n = min(P4B, yy - ya + 1);
+            const size_t o = (size_t)yy * W2 + x / 2;
+            if (n == P4B) {
+                uint32_t v[P4B], a[P4B];
+#pragma unroll
+                for (int k = 0; k < P4B; ++k) {
+                    v[k] = __ldg(in2 + o - k * W2);
+                    a[k] = out2[o - k * W2];
+                }
+#pragma unroll
+                for (int k = 0; k < P4B; ++k) {
+                    const int r0 = resolve(lo16(v[k]), lo16(a[k]), ab0, nb0, t0, et0, eb0);
+                    const int r1 = resolve(hi16s(v[k]), hi16s(a[k]), ab1, nb1, t1, et1, eb1);
+                    out2[o - k * W2] = pack2(r0, r1);
+                    known += (r0 >= 0) + (r1 >= 0);
+                }
+            } else {
+                for (int k = 0; k < n; ++k) {
+                    const uint32_t vk = __ldg(in2 + o - k * W2), ak = out2[o - k * W2];
+                    const int r0 = resolve(lo16(vk), lo16(ak), ab0, nb0, t0, et0, eb0);
+                    const int r1 = resolve(hi16s(vk), hi16s(ak), ab1, nb1, t1, et1, eb1);
+                    out2[o - k * W2] = pack2(r0, r1);
+                    known += (r0 >= 0) + (r1 >= 0);
+                }
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) known += __shfl_xor_sync(0xffffffffu, known, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = known;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int i = 0; i < P4C * P4S / 32; ++i) t += red[i];
+        if (t) atomicAdd(&f.sc->known, t);
+    }
+}
+
 }  // namespace
 
 void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStream_t st) {
@@ -438,6 +605,10 @@ void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStrea
 
 void launch_peek_cols(const Frame& f, const int16_t* in, int16_t* out, int16_t*, cudaStream_t st) {
     if (f.N == 0) return;
+    if (f.W % 2 == 0 && (reinterpret_cast<uintptr_t>(in) & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 3) == 0) {
+        k_peek_cols4<<<(f.W + 2 * P4C - 1) / (2 * P4C), P4C * P4S, 0, st>>>(f, in, out);
+        return;
+    }
     k_peek_cols2<<<(f.W + PC - 1) / PC, PC * PS, 0, st>>>(f, in, out);
 }
 
