@@ -106,6 +106,52 @@ __device__ __forceinline__ void gunite(int* p, int a, int b) {
     }
 }
 
+// a united with up to 3 nodes b[0..nb): the 1 + nb root walks (path halving)
+// advance in lockstep, so their dependent L2 loads overlap instead of running
+// one chain after another; then the roots are linked by priority (CAS), a
+// lost race falls back to gunite.
+__device__ __forceinline__ void gunite_n(int* p, int a, const int (&b)[3], int nb) {
+    int x[4] = {a, b[0], b[1], b[2]};
+    bool act[4] = {true, nb > 0, nb > 1, nb > 2};
+    while (act[0] | act[1] | act[2] | act[3]) {
+        int q[4], g[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (act[i]) q[i] = __ldcg(p + x[i]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (!act[i]) continue;
+            if (q[i] == x[i]) act[i] = false;
+            else g[i] = __ldcg(p + q[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (!act[i]) continue;
+            if (g[i] == q[i]) {
+                x[i] = q[i];
+                act[i] = false;
+            } else {
+                p[x[i]] = g[i];
+                x[i] = g[i];
+            }
+        }
+    }
+    int r = x[0];
+#pragma unroll
+    for (int i = 1; i < 4; ++i) {
+        if (i > nb) break;
+        const int rb = x[i];
+        if (rb == r || (i > 1 && rb == x[1]) || (i > 2 && rb == x[2])) continue;
+        const int hi = prio(r) > prio(rb) ? r : rb, lo = r ^ rb ^ hi;
+        if (atomicCAS(p + lo, lo, hi) == lo) {
+            r = hi;
+        } else {
+            gunite(p, r, rb);
+            r = gfind(p, r);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ B1 ----
 // NPL label bit-planes.  lutp[v] holds bit p of lut[v] at bit 8p (p < 4), so
 // 8 pixels combine with shift-adds into one word whose byte p is plane p's
@@ -560,9 +606,11 @@ __global__ void __launch_bounds__(RW + RH) k_ccl_borders(Frame f, const int32_t*
             const int u1 = up[t];
             const int u2 = t < RW - 1 ? up[t + 1] : (rx + 1 < RXc ? bord[(size_t)(reg - RXc + 1) * RBORD + RW] : -1);
             const bool cont = lane > 0 && ap == a;  // u0, u1 were the predecessor's u1, u2
-            if (!cont && u0 >= 0) gunite(f.par, a, u0);
-            if (!cont && u1 >= 0 && u1 != u0) gunite(f.par, a, u1);
-            if (u2 >= 0 && u2 != u1) gunite(f.par, a, u2);
+            int nb = 0, b[3] = {-1, -1, -1};
+            if (!cont && u0 >= 0) b[nb++] = u0;
+            if (!cont && u1 >= 0 && u1 != u0) b[nb++] = u1;
+            if (u2 >= 0 && u2 != u1) b[nb++] = u2;
+            if (nb) gunite_n(f.par, a, b, nb);
         }
     } else {
         const int r = t - RW;
@@ -574,9 +622,11 @@ __global__ void __launch_bounds__(RW + RH) k_ccl_borders(Frame f, const int32_t*
             const int l1 = lf[r];
             const int l2 = r < RH - 1 ? lf[r + 1] : -1;
             const bool cont = lane > 0 && ap == a;
-            if (!cont && l0 >= 0) gunite(f.par, a, l0);
-            if (!cont && l1 >= 0 && l1 != l0) gunite(f.par, a, l1);
-            if (l2 >= 0 && l2 != l1) gunite(f.par, a, l2);
+            int nb = 0, b[3] = {-1, -1, -1};
+            if (!cont && l0 >= 0) b[nb++] = l0;
+            if (!cont && l1 >= 0 && l1 != l0) b[nb++] = l1;
+            if (l2 >= 0 && l2 != l1) b[nb++] = l2;
+            if (nb) gunite_n(f.par, a, b, nb);
         }
     }
 }
