@@ -14,7 +14,8 @@
 //     when the weights are exactly gaussian_kernel(sigma, size) and
 //     stereotk::b200::fast_blur() is on (default), the separable FP32 kernel
 //     (<= 1 LSB) runs instead.
-//   * Image file I/O (load_image / save_rgb ...) is not part of this library.
+//   * File I/O: binary PGM/PPM exactly as the reference; PNG is coded over
+//     zlib instead of libpng (stk_io.cpp).
 // The per-header forwarding files (image.hpp, pipeline.hpp, ...) include this
 // file, so `#include "stereotk/pipeline.hpp"` keeps working.
 #pragma once
@@ -69,6 +70,12 @@ struct GrayImage {
 };
 
 GrayImage rgb_to_lightness(const RgbImage& image, int workers = 1);
+
+// image.hpp:55-79 (stk_io.cpp)
+RgbImage load_image(const std::string& path);
+GrayImage load_gray(const std::string& path, std::vector<std::string>* comments = nullptr);
+void save_gray(const GrayImage& image, const std::string& path, const std::vector<std::string>& comments = {});
+void save_rgb(const RgbImage& image, const std::string& path);
 
 // ------------------------------------------------------- segmentation ----
 struct Histogram {
@@ -164,8 +171,7 @@ DisparityMap match_boundary_pixels(const GrayImage& left, const GrayImage& right
                                    int workers = 1);
 
 // ---------------------------------------------------------- evaluate ----
-// evaluate.hpp:10-36, 57-58 (file I/O entry points are not part of this
-// library).
+// evaluate.hpp:10-72 (file entry points in stk_io.cpp).
 struct EvalResult {
     double bad_pixel_rate = 0.0;
     std::uint64_t compared = 0;
@@ -177,6 +183,10 @@ EvalResult bad_pixel_rate(const DisparityMap& computed, const DisparityMap& trut
 DisparityMap dense_sad_baseline(const GrayImage& left, const GrayImage& right,
                                 const MatchConfig& config, int workers = 1);
 std::string eval_report_json(const EvalResult& result);
+DisparityMap load_ground_truth(const std::string& path, double scale);
+void save_disparity(const DisparityMap& map, const std::string& path, double output_scale);
+std::string disparity_mask_path(const std::string& path);
+DisparityMap load_disparity(const std::string& path, double fallback_scale = 0.0);
 
 // -------------------------------------------------------- reconstruct ----
 DisparityMap fill_scanlines(const DisparityMap& sparse, int workers = 1);
@@ -275,6 +285,12 @@ std::vector<BenchReport> run_benchmark(const std::vector<StereoPair>& frames,
                                        const std::vector<int>& worker_counts,
                                        const PipelineConfig& config);
 std::string benchmark_csv(const std::vector<BenchReport>& reports);
+
+// Frame-pair discovery of the reference CLI (tools/main.cpp:247-284): every
+// <stem>_L.<ext> with a sibling <stem>_R.<ext> (.png/.ppm/.pgm), by stem.
+// IoError if `dir` is not a directory, ParamError if no pair is found.
+std::vector<std::pair<std::string, std::string>> list_frame_pairs(const std::string& dir);
+std::vector<StereoPair> load_frames(const std::string& dir);
 
 namespace b200 {
 // Device used by this thread's implicit context (default: $STK_DEVICE or 0).

@@ -234,6 +234,41 @@ stk_status stk_frame_wait(stk_ctx* ctx, int slot, stk_stats* stats, stk_times* t
 /* The slot's cudaStream_t (as void*), for callers that time with events. */
 void* stk_slot_stream(stk_ctx* ctx, int slot);
 
+/* ------------------------------------------------------- file I/O -- */
+/* Host-side file formats (no GPU needed).  Errors:
+ * STK_EIO (cannot open / read / write, reference IoError) and STK_EFORMAT
+ * (malformed or unsupported contents, reference FormatError), message via
+ * stk_last_error(NULL).  Binary PGM/PPM exactly as image_io.cpp:29-241; PNG
+ * decoded/encoded over zlib (the reference uses libpng, absent here).
+ * Callers size buffers with stk_image_probe first; the load entries check
+ * that w/h match the file (STK_EPARAM otherwise). */
+/* width, height and channels (1 = P5 / grey PNG types, 3 = colour) */
+stk_status stk_image_probe(const char* path, int* w, int* h, int* channels);
+/* load_image (image.hpp:55-60, image_io.cpp:160-184): any supported file as
+ * w*h*3 RGB; a P5 plane is replicated into the three channels. */
+stk_status stk_load_image(const char* path, uint8_t* rgb, int w, int h);
+/* load_gray (image.hpp:62-67, image_io.cpp:186-214): P5, or a PNG whose
+ * pixels are grey.  The header comment lines (without "# ") are written to
+ * `comments` joined by '\n' (may be NULL; *need = bytes required incl. NUL). */
+stk_status stk_load_gray(const char* path, uint8_t* gray, int w, int h, char* comments, size_t cap,
+                         size_t* need);
+/* save_gray (image.hpp:69-72): P5; `comments` = '\n'-separated lines or NULL */
+stk_status stk_save_gray(const char* path, const uint8_t* gray, int w, int h, const char* comments);
+/* save_rgb (image.hpp:74-76): PNG when the extension is .png, else P6 */
+stk_status stk_save_rgb(const char* path, const uint8_t* rgb, int w, int h);
+/* save_disparity / load_disparity / load_ground_truth / disparity_mask_path
+ * (evaluate.hpp:27-67, evaluate.cpp:76-90, 136-229) */
+stk_status stk_save_disparity(const char* path, const int16_t* disparity, int w, int h,
+                              double output_scale);
+stk_status stk_load_disparity(const char* path, int16_t* disparity, int w, int h,
+                              double fallback_scale);
+stk_status stk_load_ground_truth(const char* path, int16_t* disparity, int w, int h, double scale);
+stk_status stk_disparity_mask_path(const char* path, char* out, size_t cap, size_t* need);
+/* Frame-pair discovery of the CLI (tools/main.cpp:247-284): every
+ * <stem>_L.<ext> with a <stem>_R.<ext> beside it (ext .png/.ppm/.pgm), sorted
+ * by stem, written as "left\tright\n" lines. */
+stk_status stk_list_frame_pairs(const char* dir, char* out, size_t cap, size_t* need, int* count);
+
 #ifdef __cplusplus
 }
 #endif

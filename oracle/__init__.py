@@ -473,3 +473,70 @@ def ref_synth(name: str, *args):
                                   C.c_int(dmax), out.ctypes.data_as(C.c_void_p))
         return out
     raise ValueError(name)
+
+
+# ------------------------------------------------------------------ file I/O --
+class RefIOError(Exception):
+    """An exception the reference's file entry points threw: .kind is
+    "ParamError" / "IoError" / "FormatError" / "other", .msg its what()."""
+
+    def __init__(self, kind: str, msg: str):
+        super().__init__(f"{kind}: {msg}")
+        self.kind, self.msg = kind, msg
+
+
+_IO_KINDS = {-1: "ParamError", -2: "other", -3: "IoError", -4: "FormatError"}
+
+
+def _ref_io_call(L, rc):
+    if rc != 0:
+        raise RefIOError(_IO_KINDS.get(rc, "other"), L.ref_last_error().decode(errors="replace"))
+
+
+def ref_io(name: str, *args):
+    """The reference's own image_io.cpp / evaluate.cpp file entry points
+    (compiled against oracle/pngstub/png.h: PGM/PPM only).  Raises RefIOError
+    with the reference's exception class and message; None without oracle/_ref."""
+    r = reference()
+    if r is None:
+        return None
+    L = r.lib
+    L.ref_last_error.restype = C.c_char_p
+    w, h = C.c_int(), C.c_int()
+    if name in ("load_image", "load_gray", "load_disparity", "load_ground_truth"):
+        path = str(args[0]).encode()
+        if name == "load_image":
+            _ref_io_call(L, L.ref_load_image(path, C.byref(w), C.byref(h), None))
+            out = np.empty((h.value, w.value, 3), np.uint8)
+            _ref_io_call(L, L.ref_load_image(path, C.byref(w), C.byref(h), out.ctypes.data_as(C.c_void_p)))
+            return out
+        if name == "load_gray":
+            _ref_io_call(L, L.ref_load_gray(path, C.byref(w), C.byref(h), None, None, 0))
+            out = np.empty((h.value, w.value), np.uint8)
+            buf = C.create_string_buffer(1 << 16)
+            _ref_io_call(L, L.ref_load_gray(path, C.byref(w), C.byref(h), out.ctypes.data_as(C.c_void_p),
+                                            buf, C.c_int(len(buf))))
+            return out, buf.value.decode(errors="replace").splitlines()
+        fn = L.ref_load_disparity if name == "load_disparity" else L.ref_load_ground_truth
+        scale = C.c_double(float(args[1]) if len(args) > 1 else 0.0)
+        _ref_io_call(L, fn(path, scale, C.byref(w), C.byref(h), None))
+        out = np.empty((h.value, w.value), np.int16)
+        _ref_io_call(L, fn(path, scale, C.byref(w), C.byref(h), out.ctypes.data_as(C.c_void_p)))
+        return out
+    if name == "save_gray":
+        img, path = np.ascontiguousarray(args[0], np.uint8), str(args[1]).encode()
+        comment = args[2].encode() if len(args) > 2 and args[2] else None
+        _ref_io_call(L, L.ref_save_gray(path, img.ctypes.data_as(C.c_void_p), C.c_int(img.shape[1]),
+                                        C.c_int(img.shape[0]), comment))
+        return None
+    if name == "save_rgb":
+        img, path = np.ascontiguousarray(args[0], np.uint8), str(args[1]).encode()
+        _ref_io_call(L, L.ref_save_rgb(path, img.ctypes.data_as(C.c_void_p), C.c_int(img.shape[1]),
+                                       C.c_int(img.shape[0])))
+        return None
+    if name == "save_disparity":
+        d, path = np.ascontiguousarray(args[0], np.int16), str(args[1]).encode()
+        _ref_io_call(L, L.ref_save_disparity(path, d.ctypes.data_as(C.c_void_p), C.c_int(d.shape[1]),
+                                             C.c_int(d.shape[0]), C.c_double(float(args[2]))))
+        return None
+    raise ValueError(name)

@@ -66,20 +66,78 @@ int guard(Fn&& fn) {
 }
 }  // namespace
 
-// image_io.cpp needs libpng, absent here: the file entry points evaluate.cpp
-// references are stubbed (the tests never call them).
-namespace stereotk {
-GrayImage load_gray(const std::string& path, std::vector<std::string>*) {
-    throw IoError(path + ": image I/O is not built into the test oracle");
+// image_io.cpp is compiled from the reference sources against
+// oracle/pngstub/png.h (libpng is absent): its PGM/PPM code runs unmodified,
+// PNG entries throw.  File entry points report the exception class:
+// 0 ok, -1 ParamError, -3 IoError, -4 FormatError, -2 anything else.
+namespace {
+const void* im_data(const RgbImage& i) { return i.data.data(); }
+const void* im_data(const GrayImage& i) { return i.data.data(); }
+const void* im_data(const DisparityMap& i) { return i.values.data(); }
+
+template <typename Fn>
+int io_guard(Fn&& fn) {
+    try {
+        fn();
+        return 0;
+    } catch (const ParamError& e) {
+        g_err = e.what();
+        return -1;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return -3;
+    } catch (const FormatError& e) {
+        g_err = e.what();
+        return -4;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -2;
+    }
 }
-void save_gray(const GrayImage&, const std::string& path, const std::vector<std::string>&) {
-    throw IoError(path + ": image I/O is not built into the test oracle");
+// Two-call pattern: buf == nullptr -> only *w/*h are reported.
+template <typename Img>
+void copy_out(const Img& im, int* w, int* h, void* buf, std::size_t elem_bytes) {
+    *w = im.width;
+    *h = im.height;
+    if (buf) std::memcpy(buf, im_data(im), static_cast<std::size_t>(im.width) * im.height * elem_bytes);
 }
-}  // namespace stereotk
+}  // namespace
 
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_load_image(const char* path, int* w, int* h, uint8_t* rgb) {
+    return io_guard([&] { copy_out(load_image(path), w, h, rgb, 3); });
+}
+int ref_load_gray(const char* path, int* w, int* h, uint8_t* gray, char* comments, int cap) {
+    return io_guard([&] {
+        std::vector<std::string> c;
+        copy_out(load_gray(path, &c), w, h, gray, 1);
+        std::string j;
+        for (const auto& s : c) j += s + "\n";
+        if (comments && cap > 0) std::snprintf(comments, cap, "%s", j.c_str());
+    });
+}
+int ref_save_gray(const char* path, const uint8_t* gray, int w, int h, const char* comment) {
+    return io_guard([&] {
+        std::vector<std::string> c;
+        if (comment && *comment) c.push_back(comment);
+        save_gray(gray_in(gray, w, h), path, c);
+    });
+}
+int ref_save_rgb(const char* path, const uint8_t* rgb, int w, int h) {
+    return io_guard([&] { save_rgb(rgb_in(rgb, w, h), path); });
+}
+int ref_save_disparity(const char* path, const int16_t* d, int w, int h, double scale) {
+    return io_guard([&] { save_disparity(disp_in(d, w, h), path, scale); });
+}
+int ref_load_disparity(const char* path, double fallback, int* w, int* h, int16_t* d) {
+    return io_guard([&] { copy_out(load_disparity(path, fallback), w, h, d, 2); });
+}
+int ref_load_ground_truth(const char* path, double scale, int* w, int* h, int16_t* d) {
+    return io_guard([&] { copy_out(load_ground_truth(path, scale), w, h, d, 2); });
+}
 
 int ref_dense_sad_baseline(const uint8_t* l, const uint8_t* r, int w, int h, int window, int max_d,
                            int workers, int16_t* out) {

@@ -41,7 +41,7 @@ CU_SOURCES = [
     "k_eval.cu",
     "stk_capi.cu",
 ]
-CXX_SOURCES = ["stereotk_shim.cpp"]  # the C++ stereotk:: drop-in over the C-ABI
+CXX_SOURCES = ["stereotk_shim.cpp", "stk_io.cpp"]  # C++ stereotk:: drop-in over the C-ABI; file I/O
 HEADERS = ["stk_internal.cuh", "stk_device.cuh"]
 
 
@@ -83,7 +83,7 @@ def build(verbose: bool = False, force: bool = False) -> None:
             _run(["/usr/bin/g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-I", INCLUDE,
                   "-c", s, "-o", o], verbose)
     if force or _newer(objs, LIB):
-        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt",
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lz", "-lrt",
               "-ldl", "-lpthread"], verbose)
     if force or _newer([CSRC / "synth.c"], SYNTH):
         _run(["/usr/bin/gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-Wall", "-o", SYNTH,

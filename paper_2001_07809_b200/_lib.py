@@ -98,6 +98,17 @@ SIGNATURES = {
     "stk_frame_wait": (I, [VP, I, C.POINTER(StkStats), C.POINTER(StkTimes),
                            C.POINTER(StkFrameInfo)]),
     "stk_slot_stream": (VP, [VP, I]),
+    # file I/O (host only)
+    "stk_image_probe": (I, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "stk_load_image": (I, [C.c_char_p, VP, I, I]),
+    "stk_load_gray": (I, [C.c_char_p, VP, I, I, C.c_char_p, SZ, C.POINTER(SZ)]),
+    "stk_save_gray": (I, [C.c_char_p, VP, I, I, C.c_char_p]),
+    "stk_save_rgb": (I, [C.c_char_p, VP, I, I]),
+    "stk_save_disparity": (I, [C.c_char_p, VP, I, I, D]),
+    "stk_load_disparity": (I, [C.c_char_p, VP, I, I, D]),
+    "stk_load_ground_truth": (I, [C.c_char_p, VP, I, I, D]),
+    "stk_disparity_mask_path": (I, [C.c_char_p, C.c_char_p, SZ, C.POINTER(SZ)]),
+    "stk_list_frame_pairs": (I, [C.c_char_p, C.c_char_p, SZ, C.POINTER(SZ), C.POINTER(C.c_int)]),
 }
 
 _lib = None

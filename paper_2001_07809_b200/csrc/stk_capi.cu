@@ -660,6 +660,10 @@ stk_status submit(stk_ctx* ctx, int slot, const uint8_t* rgbL, const uint8_t* rg
 }  // namespace
 
 // =================================================================== ABI ===
+namespace stk {
+void set_thread_error(const std::string& msg) { t_err = msg; }  // host I/O entries (stk_io.cpp)
+}
+
 extern "C" {
 
 int stk_abi_version(void) { return STK_ABI_VERSION; }

@@ -541,3 +541,100 @@ def run_refocus_pipeline(left, right, config: PipelineConfig, focus: FocusSpec,
     if depth_out is not None:
         depth_out.append(r)
     return out
+
+
+# ------------------------------------------------------------- file I/O --
+# image.hpp:55-79, evaluate.hpp:27-67, tools/main.cpp:247-284 -- host code in
+# libstk_b200.so (csrc/stk_io.cpp); no GPU needed.
+def _b(path) -> bytes:
+    return str(path).encode()
+
+
+def _probe(path):
+    w, h, c = C.c_int(), C.c_int(), C.c_int()
+    _raise(_lib.lib().stk_image_probe(_b(path), C.byref(w), C.byref(h), C.byref(c)))
+    return w.value, h.value, c.value
+
+
+def load_image(path) -> np.ndarray:
+    """image.hpp:55-60: PNG / P6 / P5 (replicated) as (h, w, 3) uint8."""
+    w, h, _ = _probe(path)
+    out = np.empty((h, w, 3), np.uint8)
+    _raise(_lib.lib().stk_load_image(_b(path), _p(out), w, h))
+    return out
+
+
+def load_gray(path, comments: Optional[list] = None) -> np.ndarray:
+    """image.hpp:62-67: P5 or grey PNG as (h, w) uint8; header comments appended to ``comments``."""
+    w, h, _ = _probe(path)
+    out = np.empty((h, w), np.uint8)
+    need = C.c_size_t()
+    buf = C.create_string_buffer(4096)
+    L = _lib.lib()
+    _raise(L.stk_load_gray(_b(path), _p(out), w, h, buf, 4096, C.byref(need)))
+    if need.value > 4096:
+        buf = C.create_string_buffer(need.value)
+        _raise(L.stk_load_gray(_b(path), _p(out), w, h, buf, need.value, C.byref(need)))
+    if comments is not None:
+        comments.extend(buf.value.decode(errors="replace").splitlines())
+    return out
+
+
+def save_gray(image: np.ndarray, path, comments: Sequence[str] = ()) -> None:
+    """image.hpp:69-72 (binary PGM, comments after the magic number)."""
+    img = _c8(image)
+    text = "".join(c + "\n" for c in comments).encode() if comments else None
+    _raise(_lib.lib().stk_save_gray(_b(path), _p(img), img.shape[1], img.shape[0], text))
+
+
+def save_rgb(image: np.ndarray, path) -> None:
+    """image.hpp:74-76 (.png -> PNG, anything else -> binary PPM)."""
+    img = _c8(image)
+    _raise(_lib.lib().stk_save_rgb(_b(path), _p(img), img.shape[1], img.shape[0]))
+
+
+def save_disparity(m: np.ndarray, path, output_scale: float) -> None:
+    """evaluate.hpp:53-58: PGM of round(d * scale) + '# scale' comment + sibling mask."""
+    d = np.ascontiguousarray(m, dtype=np.int16)
+    _raise(_lib.lib().stk_save_disparity(_b(path), _p(d), d.shape[1], d.shape[0], float(output_scale)))
+
+
+def load_disparity(path, fallback_scale: float = 0.0) -> np.ndarray:
+    """evaluate.hpp:63-67."""
+    w, h, _ = _probe(path)
+    out = np.empty((h, w), np.int16)
+    _raise(_lib.lib().stk_load_disparity(_b(path), _p(out), w, h, float(fallback_scale)))
+    return out
+
+
+def load_ground_truth(path, scale: float) -> np.ndarray:
+    """evaluate.hpp:27-30: value / scale rounded, 0 -> unknown."""
+    if not scale > 0.0:  # checked before the file is touched, as evaluate.cpp:76-80
+        _raise(_lib.lib().stk_load_ground_truth(_b(path), None, 0, 0, float(scale)))
+    w, h, _ = _probe(path)
+    out = np.empty((h, w), np.int16)
+    _raise(_lib.lib().stk_load_ground_truth(_b(path), _p(out), w, h, float(scale)))
+    return out
+
+
+def disparity_mask_path(path) -> str:
+    """evaluate.hpp:60-61."""
+    need = C.c_size_t()
+    buf = C.create_string_buffer(len(str(path).encode()) + 64)
+    _raise(_lib.lib().stk_disparity_mask_path(_b(path), buf, len(buf), C.byref(need)))
+    return buf.value.decode()
+
+
+def list_frame_pairs(directory) -> list:
+    """tools/main.cpp:247-284: [(left, right)] for every <stem>_L/_R pair, by stem."""
+    need, n = C.c_size_t(), C.c_int()
+    L = _lib.lib()
+    _raise(L.stk_list_frame_pairs(_b(directory), None, 0, C.byref(need), C.byref(n)))
+    buf = C.create_string_buffer(need.value)
+    _raise(L.stk_list_frame_pairs(_b(directory), buf, need.value, C.byref(need), C.byref(n)))
+    return [tuple(line.split("\t")) for line in buf.value.decode().splitlines()]
+
+
+def load_frames(directory) -> list:
+    """The CLI's load_frames: [(left_rgb, right_rgb)] in stem order."""
+    return [(load_image(l), load_image(r)) for l, r in list_frame_pairs(directory)]

@@ -1,0 +1,428 @@
+"""CPU tests of the frame / disparity file I/O, host code
+in libstk_b200.so (csrc/stk_io.cpp) reached through the C-ABI -- no GPU.
+
+* PGM/PPM reader and writers vs the reference's own image_io.cpp /
+  evaluate.cpp (compiled into oracle/_ref against oracle/pngstub/png.h) and vs
+  tests/golden/io_golden.json made from it: same pixels, same comments, same
+  exception class and message text, byte-identical files.
+* The reference's own I/O known-answer tests (test_imaging.cpp:29-147,
+  test_evaluate.cpp:113-211) re-expressed.
+* PNG (the reference uses libpng, absent here): round trips, every colour type
+  and bit depth against PIL / OpenCV decoders, Adam7 against an independent
+  interlaced encoder written in this file, and our encoder's output decoded
+  by PIL and OpenCV.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import struct
+import zlib
+
+import numpy as np
+import pytest
+
+import io_cases
+from conftest import ROOT
+
+GOLD = json.load(open(os.path.join(ROOT, "tests", "golden", "io_golden.json")))
+
+KINDS = {"ParamError": "ParamError", "IoError": "IoError", "FormatError": "FormatError"}
+
+
+def sha(b: bytes) -> str:
+    return hashlib.sha256(b).hexdigest()
+
+
+def ours(stk, fn, path):
+    try:
+        r = fn()
+    except (stk.ParamError, stk.IoError, stk.FormatError) as e:
+        return {"kind": type(e).__name__, "msg": str(e).replace(str(path), "{path}")}
+    if isinstance(r, tuple):
+        return {"kind": "ok", "shape": list(r[0].shape), "sha": sha(r[0].tobytes()), "comments": r[1]}
+    return {"kind": "ok", "shape": list(r.shape), "sha": sha(r.tobytes())}
+
+
+def _load_gray_c(stk, p):
+    c = []
+    g = stk.load_gray(p, c)
+    return g, c
+
+
+# ------------------------------------------------------------- PNM reader --
+@pytest.mark.parametrize("name,blob", io_cases.pnm_cases(), ids=[n for n, _ in io_cases.pnm_cases()])
+def test_pnm_reader_matches_reference_golden(stk, tmp_path, name, blob):
+    p = tmp_path / (name + ".pnm")
+    p.write_bytes(blob)
+    want = GOLD["read"][name]
+    assert ours(stk, lambda: stk.load_image(p), p) == want["load_image"]
+    assert ours(stk, lambda: _load_gray_c(stk, p), p) == want["load_gray"]
+    assert ours(stk, lambda: stk.load_ground_truth(p, 16.0), p) == want["load_ground_truth_16"]
+    assert ours(stk, lambda: stk.load_disparity(p, 8.0), p) == want["load_disparity_fb8"]
+
+
+def test_pnm_reader_matches_compiled_reference_live(stk, ref, tmp_path):
+    """Same cases, against the reference library itself (not the stored golden)."""
+    import oracle
+
+    def refo(fn, p):
+        try:
+            r = fn()
+        except oracle.RefIOError as e:
+            return {"kind": e.kind, "msg": e.msg.replace(str(p), "{path}")}
+        if isinstance(r, tuple):
+            return {"kind": "ok", "shape": list(r[0].shape), "sha": sha(r[0].tobytes()), "comments": r[1]}
+        return {"kind": "ok", "shape": list(r.shape), "sha": sha(r.tobytes())}
+
+    for name, blob in io_cases.pnm_cases():
+        p = tmp_path / (name + ".pnm")
+        p.write_bytes(blob)
+        assert ours(stk, lambda: stk.load_image(p), p) == refo(lambda: oracle.ref_io("load_image", p), p), name
+        assert ours(stk, lambda: _load_gray_c(stk, p), p) == refo(lambda: oracle.ref_io("load_gray", p), p), name
+
+
+def test_missing_file_is_io_error(stk, tmp_path):
+    """test_imaging.cpp:108-112"""
+    for fn in (stk.load_image, stk.load_gray, lambda p: stk.load_disparity(p),
+               lambda p: stk.load_ground_truth(p, 8.0)):
+        with pytest.raises(stk.IoError, match="cannot open"):
+            fn(tmp_path / "no_such_file.ppm")
+
+
+# ------------------------------------------------------------- PNM writers --
+def test_writers_byte_identical_to_reference(stk, tmp_path):
+    for name, img, comment in io_cases.gray_inputs():
+        p = tmp_path / (name + ".pgm")
+        stk.save_gray(img, p, [comment] if comment else ())
+        assert sha(p.read_bytes()) == GOLD["save_gray"][name], name
+    for name, img in io_cases.rgb_inputs():
+        p = tmp_path / (name + ".ppm")
+        stk.save_rgb(img, p)
+        assert sha(p.read_bytes()) == GOLD["save_rgb"][name], name
+
+
+def test_save_disparity_byte_identical_to_reference(stk, tmp_path):
+    for name, d, scale in io_cases.disparity_inputs():
+        p = tmp_path / (name + ".pgm")
+        want = GOLD["save_disparity"][name]
+        if want["kind"] != "ok":
+            with pytest.raises(getattr(stk, want["kind"])) as ei:
+                stk.save_disparity(d, p, scale)
+            assert str(ei.value) == want["msg"]
+            continue
+        stk.save_disparity(d, p, scale)
+        assert sha(p.read_bytes()) == want["values"], name
+        m = tmp_path / (name + ".mask.pgm")
+        assert stk.disparity_mask_path(p) == str(m)
+        assert sha(m.read_bytes()) == want["mask"], name
+        assert sha(stk.load_disparity(p).tobytes()) == GOLD["load_disparity"][name], name
+        os.remove(m)
+        assert sha(stk.load_disparity(p, 999.0).tobytes()) == GOLD["load_disparity"][name + "_nomask"]
+
+
+# ------------------------------------- the reference's I/O known answers --
+def test_pgm_writer_exact_bytes_1x1_white(stk, tmp_path):
+    """test_imaging.cpp:29-41"""
+    p = tmp_path / "one_white.pgm"
+    stk.save_gray(np.array([[255]], np.uint8), p)
+    assert p.read_bytes() == b"P5\n1 1\n255\n\xff"
+
+
+def test_pgm_comments_between_magic_and_dims(stk, tmp_path):
+    """test_imaging.cpp:43-57"""
+    p = tmp_path / "commented.pgm"
+    stk.save_gray(np.array([[7, 9]], np.uint8), p, ["scale 8"])
+    assert p.read_bytes().startswith(b"P5\n# scale 8\n2 1\n255\n")
+    c = []
+    back = stk.load_gray(p, c)
+    assert c == ["scale 8"] and back.tolist() == [[7, 9]]
+
+
+def test_pnm_round_trips(stk, synth, tmp_path):
+    """test_imaging.cpp:59-79 (seeds 1-5, random_gray 37x21 / random_rgb 19x33)"""
+    for seed in range(1, 6):
+        g = synth.random_gray(37, 21, seed)
+        stk.save_gray(g, tmp_path / "rt.pgm")
+        assert np.array_equal(stk.load_gray(tmp_path / "rt.pgm"), g)
+        rgb = synth.random_rgb(19, 33, seed + 100)
+        stk.save_rgb(rgb, tmp_path / "rt.ppm")
+        assert np.array_equal(stk.load_image(tmp_path / "rt.ppm"), rgb)
+
+
+def test_grey_pnm_replicates_into_rgb(stk, synth, tmp_path):
+    """test_imaging.cpp:91-104"""
+    g = synth.random_gray(9, 7, 11)
+    stk.save_gray(g, tmp_path / "rep.pgm")
+    rgb = stk.load_image(tmp_path / "rep.pgm")
+    assert rgb.shape == (7, 9, 3) and all(np.array_equal(rgb[..., c], g) for c in range(3))
+
+
+def test_malformed_files_are_format_errors(stk, tmp_path):
+    """test_imaging.cpp:106-124"""
+    (tmp_path / "garbage.ppm").write_bytes(b"this is not an image at all\n")
+    (tmp_path / "truncated.ppm").write_bytes(b"P6\n2 2\n255\nabcde")
+    (tmp_path / "deep.pgm").write_bytes(b"P5\n1 1\n65535\n\0\0")
+    with pytest.raises(stk.FormatError):
+        stk.load_image(tmp_path / "garbage.ppm")
+    with pytest.raises(stk.FormatError):
+        stk.load_image(tmp_path / "truncated.ppm")
+    with pytest.raises(stk.FormatError):
+        stk.load_gray(tmp_path / "deep.pgm")
+
+
+def test_ground_truth_divides_and_excludes_zeros(stk, tmp_path):
+    """test_evaluate.cpp:113-123"""
+    p = tmp_path / "truth.pgm"
+    stk.save_gray(np.array([[80, 0, 81, 88]], np.uint8), p)
+    assert stk.load_ground_truth(p, 16.0).tolist() == [[5, -1, 5, 6]]
+    for s in (0.0, -2.0):
+        with pytest.raises(stk.ParamError):
+            stk.load_ground_truth(p, s)
+
+
+def test_disparity_round_trip_through_mask(stk, synth, tmp_path):
+    """test_evaluate.cpp:145-156"""
+    m = synth.random_sparse(20, 14, 56, 60, 14)
+    m[3, 3] = 0
+    p = tmp_path / "disp.pgm"
+    stk.save_disparity(m, p, 8.0)
+    assert os.path.exists(stk.disparity_mask_path(p))
+    assert np.array_equal(stk.load_disparity(p), m)
+
+
+def test_zero_without_mask_reads_unknown(stk, synth, tmp_path):
+    """test_evaluate.cpp:158-177"""
+    m = synth.random_sparse(12, 9, 57, 60, 10)
+    m[2, 2] = 0
+    m[5, 5] = 3
+    p = tmp_path / "nomask.pgm"
+    stk.save_disparity(m, p, 8.0)
+    os.remove(stk.disparity_mask_path(p))
+    back = stk.load_disparity(p)
+    assert np.array_equal(back[m >= 1], m[m >= 1]) and (back[m < 1] == -1).all()
+
+
+def test_scale_comment_and_fallback(stk, tmp_path):
+    """test_evaluate.cpp:179-203"""
+    p = tmp_path / "scaled.pgm"
+    stk.save_disparity(np.array([[4, 10]], np.int16), p, 8.0)
+    assert b"# scale 8\n" in p.read_bytes()
+    assert stk.load_disparity(p, 999.0).tolist() == [[4, 10]]
+    q = tmp_path / "plain.pgm"
+    stk.save_gray(np.array([[0, 8, 16]], np.uint8), q)
+    assert stk.load_disparity(q, 8.0).tolist() == [[-1, 1, 2]]
+    assert stk.load_disparity(q).tolist() == [[-1, 8, 16]]
+
+
+def test_save_rejects_overflowing_scales(stk, tmp_path):
+    """test_evaluate.cpp:205-211"""
+    p = tmp_path / "overflow.pgm"
+    one = np.array([[40]], np.int16)
+    with pytest.raises(stk.ParamError):
+        stk.save_disparity(one, p, 8.0)
+    with pytest.raises(stk.ParamError):
+        stk.save_disparity(one, p, 0.0)
+    stk.save_disparity(one, p, 6.0)
+
+
+def test_mask_path_rule(stk):
+    """evaluate.cpp:136-143"""
+    assert stk.disparity_mask_path("a/b.pgm") == "a/b.mask.pgm"
+    assert stk.disparity_mask_path("a.b/c") == "a.b/c.mask.pgm"
+    assert stk.disparity_mask_path("noext") == "noext.mask.pgm"
+    assert stk.disparity_mask_path("x.y.z") == "x.y.mask.z"
+
+
+# --------------------------------------------------------------------- PNG --
+def test_png_round_trip(stk, synth, tmp_path):
+    """test_imaging.cpp:81-89 (random_rgb 24x17 seed 42) plus larger/odd sizes"""
+    for (w, h, seed) in ((24, 17, 42), (1, 1, 3), (257, 131, 5)):
+        rgb = synth.random_rgb(w, h, seed)
+        stk.save_rgb(rgb, tmp_path / "rt.png")
+        assert np.array_equal(stk.load_image(tmp_path / "rt.png"), rgb)
+    rgb = synth.random_rgb(8, 8, 1)
+    stk.save_rgb(rgb, tmp_path / "UPPER.PNG")  # extension test is case-insensitive
+    assert (tmp_path / "UPPER.PNG").read_bytes()[:8] == b"\x89PNG\r\n\x1a\n"
+
+
+def test_png_colour_refuses_gray_and_grey_loads(stk, synth, tmp_path):
+    """test_imaging.cpp:126-147"""
+    c = np.zeros((4, 4, 3), np.uint8)
+    c[...] = (200, 10, 10)
+    stk.save_rgb(c, tmp_path / "colour.png")
+    with pytest.raises(stk.FormatError):
+        stk.load_gray(tmp_path / "colour.png")
+    rgb = synth.random_rgb(6, 5, 3)
+    rgb[..., 1] = rgb[..., 0]
+    rgb[..., 2] = rgb[..., 0]
+    stk.save_rgb(rgb, tmp_path / "grey.png")
+    assert np.array_equal(stk.load_gray(tmp_path / "grey.png"), rgb[..., 0])
+
+
+def test_png_encoder_output_decodes_in_pil_and_opencv(stk, synth, tmp_path):
+    PIL = pytest.importorskip("PIL.Image")
+    cv2 = pytest.importorskip("cv2")
+    rgb = synth.random_rgb(61, 47, 9)
+    rgb[10:30, 5:40] = 77  # flat area exercises the filters
+    p = tmp_path / "enc.png"
+    stk.save_rgb(rgb, p)
+    assert np.array_equal(np.asarray(PIL.open(p).convert("RGB")), rgb)
+    assert np.array_equal(cv2.imread(str(p), cv2.IMREAD_UNCHANGED)[..., ::-1], rgb)
+
+
+def _pil_variants(tmp_path):
+    PIL = pytest.importorskip("PIL.Image")
+    rng = np.random.default_rng(5)
+    g8 = rng.integers(0, 256, (23, 29), dtype=np.uint8)
+    rgb = rng.integers(0, 256, (23, 29, 3), dtype=np.uint8)
+    out = []
+    p = tmp_path / "l8.png"
+    PIL.fromarray(g8, "L").save(p)
+    out.append((p, np.repeat(g8[..., None], 3, 2)))
+    p = tmp_path / "rgb8.png"
+    PIL.fromarray(rgb, "RGB").save(p)
+    out.append((p, rgb))
+    bw = (g8 > 127)
+    p = tmp_path / "bw1.png"
+    PIL.fromarray(bw).save(p)  # mode "1": 1-bit grey
+    out.append((p, np.repeat((bw * 255).astype(np.uint8)[..., None], 3, 2)))
+    for bits in (1, 2, 4, 8):
+        n = 1 << bits
+        pal = rng.integers(0, 256, (n, 3), dtype=np.uint8)
+        idx = rng.integers(0, n, (23, 29), dtype=np.uint8)
+        im = PIL.fromarray(idx, "P")
+        im.putpalette(pal.flatten().tolist())
+        p = tmp_path / f"pal{bits}.png"
+        im.save(p, bits=bits)
+        out.append((p, pal[idx]))
+    im = PIL.fromarray(np.dstack([rgb, np.full((23, 29), 255, np.uint8)]), "RGBA")
+    p = tmp_path / "rgba_opaque.png"
+    im.save(p)
+    out.append((p, rgb))
+    a = np.zeros((23, 29), np.uint8)
+    im = PIL.fromarray(np.dstack([rgb, a]), "RGBA")
+    p = tmp_path / "rgba_clear.png"
+    im.save(p)
+    out.append((p, np.zeros_like(rgb)))
+    return out
+
+
+def test_png_variants_vs_pil(stk, tmp_path):
+    for p, want in _pil_variants(tmp_path):
+        got = stk.load_image(p)
+        assert np.array_equal(got, want), p.name
+
+
+def _png_chunk(t: bytes, d: bytes) -> bytes:
+    return struct.pack(">I", len(d)) + t + d + struct.pack(">I", zlib.crc32(t + d) & 0xFFFFFFFF)
+
+
+def _encode_png(samples: np.ndarray, ctype: int, depth: int, interlace: bool, extra=b"") -> bytes:
+    """Independent minimal PNG encoder for tests: samples (h, w, ch) ints,
+    filter 'Up' on every row (exercises unfiltering), optional Adam7."""
+    h, w = samples.shape[:2]
+
+    def pack_rows(img):
+        rows = []
+        for r in img:
+            if depth == 16:
+                b = r.astype(">u2").tobytes()
+            elif depth == 8:
+                b = r.astype(np.uint8).tobytes()
+            else:
+                bits = "".join(format(int(v), f"0{depth}b") for v in r.flatten())
+                bits += "0" * (-len(bits) % 8)
+                b = bytes(int(bits[i:i + 8], 2) for i in range(0, len(bits), 8))
+            rows.append(b)
+        out, prev = b"", None
+        for b in rows:
+            f = bytes((x - (prev[i] if prev else 0)) & 255 for i, x in enumerate(b))
+            out += b"\x02" + f
+            prev = b
+        return out
+
+    if interlace:
+        raw = b""
+        for x0, y0, dx, dy in ((0, 0, 8, 8), (4, 0, 8, 8), (0, 4, 4, 8), (2, 0, 4, 4), (0, 2, 2, 4),
+                               (1, 0, 2, 2), (0, 1, 1, 2)):
+            sub = samples[y0::dy, x0::dx]
+            if sub.shape[0] and sub.shape[1]:
+                raw += pack_rows(sub)
+    else:
+        raw = pack_rows(samples)
+    ihdr = struct.pack(">IIBBBBB", w, h, depth, ctype, 0, 0, 1 if interlace else 0)
+    return (b"\x89PNG\r\n\x1a\n" + _png_chunk(b"IHDR", ihdr) + extra +
+            _png_chunk(b"IDAT", zlib.compress(raw)) + _png_chunk(b"IEND", b""))
+
+
+def test_png_adam7_and_low_depths(stk, tmp_path):
+    rng = np.random.default_rng(17)
+    for (w, h) in ((1, 1), (3, 2), (9, 9), (33, 17)):
+        rgb = rng.integers(0, 256, (h, w, 3))
+        for inter in (False, True):
+            p = tmp_path / f"rgb_{w}x{h}_{inter}.png"
+            p.write_bytes(_encode_png(rgb, 2, 8, inter))
+            assert np.array_equal(stk.load_image(p), rgb.astype(np.uint8)), p.name
+        for depth in (1, 2, 4):
+            g = rng.integers(0, 1 << depth, (h, w, 1))
+            want = (g * 255 // ((1 << depth) - 1)).astype(np.uint8)
+            for inter in (False, True):
+                p = tmp_path / f"g{depth}_{w}x{h}_{inter}.png"
+                p.write_bytes(_encode_png(g, 0, depth, inter))
+                assert np.array_equal(stk.load_gray(p), want[..., 0]), p.name
+
+
+def test_png_16bit_and_gamma(stk, tmp_path):
+    rng = np.random.default_rng(19)
+    g = rng.integers(0, 65536, (5, 7, 1))
+    # with an sRGB chunk: plain 16 -> 8 scaling
+    p = tmp_path / "g16_srgb.png"
+    p.write_bytes(_encode_png(g, 0, 16, False, _png_chunk(b"sRGB", b"\x00")))
+    assert np.array_equal(stk.load_gray(p), ((g[..., 0] * 255 + 32895) >> 16).astype(np.uint8))
+    # no colour information: 16-bit samples are linear light -> sRGB-encoded
+    p = tmp_path / "g16_lin.png"
+    p.write_bytes(_encode_png(g, 0, 16, False))
+    lin = g[..., 0] / 65535.0
+    enc = np.where(lin <= 0.0031308, 12.92 * lin, 1.055 * lin ** (1 / 2.4) - 0.055)
+    assert np.array_equal(stk.load_gray(p), np.clip(np.rint(enc * 255), 0, 255).astype(np.uint8))
+
+
+def test_png_rejects_corruption(stk, synth, tmp_path):
+    rgb = synth.random_rgb(16, 16, 2)
+    p = tmp_path / "ok.png"
+    stk.save_rgb(rgb, p)
+    b = bytearray(p.read_bytes())
+    for i, (pos, val) in enumerate(((20, 0x55), (len(b) - 20, 0x00), (12, ord("X")))):
+        c = bytearray(b)
+        c[pos] ^= val or 0xFF
+        q = tmp_path / f"bad{i}.png"
+        q.write_bytes(bytes(c))
+        with pytest.raises(stk.FormatError):
+            stk.load_image(q)
+    q = tmp_path / "short.png"
+    q.write_bytes(bytes(b[:40]))
+    with pytest.raises(stk.FormatError):
+        stk.load_image(q)
+
+
+# ------------------------------------------------------- frame discovery --
+def test_list_frame_pairs(stk, tmp_path):
+    """tools/main.cpp:247-284: <stem>_L/_R pairs by stem; strays ignored."""
+    img = np.zeros((2, 3, 3), np.uint8)
+    for name in ("b_L.ppm", "b_R.ppm", "a_L.png", "a_R.png", "c_L.pgm", "lonely_L.ppm", "x_R.ppm"):
+        if name.endswith(".pgm"):
+            stk.save_gray(img[..., 0], tmp_path / name)
+        else:
+            stk.save_rgb(img, tmp_path / name)
+    pairs = stk.list_frame_pairs(tmp_path)
+    assert [os.path.basename(l) for l, _ in pairs] == ["a_L.png", "b_L.ppm"]
+    assert [os.path.basename(r) for _, r in pairs] == ["a_R.png", "b_R.ppm"]
+    frames = stk.load_frames(tmp_path)
+    assert len(frames) == 2 and frames[0][0].shape == (2, 3, 3)
+    with pytest.raises(stk.IoError, match="not a directory"):
+        stk.list_frame_pairs(tmp_path / "nope")
+    (tmp_path / "empty").mkdir()
+    with pytest.raises(stk.ParamError, match="no \\*_L/_R frame pairs"):
+        stk.list_frame_pairs(tmp_path / "empty")
