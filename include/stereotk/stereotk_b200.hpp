@@ -298,6 +298,9 @@ void set_device(int device);
 // Separable FP32 blur (<= 1 LSB, default on) vs bit-exact FP64 2-D blur.
 void set_fast_blur(bool on);
 bool fast_blur();
+// A double as nlohmann::json::dump() prints it (the reference CLI's and
+// eval_report_json's number format).
+std::string json_number(double v);
 }  // namespace b200
 
 }  // namespace stereotk

@@ -21,6 +21,7 @@ CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 
 LIB = PKG / "libstk_b200.so"
+CLI = PKG / "stereotk"  # the reference CLI (tools/main.cpp) on libstk_b200.so
 SYNTH = PKG / "libstk_synth.so"
 
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
@@ -85,6 +86,9 @@ def build(verbose: bool = False, force: bool = False) -> None:
     if force or _newer(objs, LIB):
         _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lz", "-lrt",
               "-ldl", "-lpthread"], verbose)
+    if force or _newer([CSRC / "stereotk_cli.cpp", LIB] + deps, CLI):
+        _run(["/usr/bin/g++", "-O2", "-std=c++17", "-Wall", "-I", INCLUDE, CSRC / "stereotk_cli.cpp",
+              "-o", CLI, "-L", PKG, "-lstk_b200", "-Wl,-rpath,$ORIGIN"], verbose)
     if force or _newer([CSRC / "synth.c"], SYNTH):
         _run(["/usr/bin/gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-Wall", "-o", SYNTH,
               CSRC / "synth.c"], verbose)

@@ -298,22 +298,55 @@ std::string benchmark_csv(const std::vector<BenchReport>& reports) {
     return out.str();
 }
 
-// evaluate.cpp:220-227: nlohmann::json dump -- keys in sorted order, compact,
-// doubles in the shortest form that round-trips.
+// evaluate.cpp:220-227: nlohmann::json dump -- keys in sorted order, compact.
 std::string eval_report_json(const EvalResult& r) {
-    auto num = [](double v) {
-        char buf[40];
-        for (int p = 1; p <= 17; ++p) {
-            std::snprintf(buf, sizeof buf, "%.*g", p, v);
-            if (std::strtod(buf, nullptr) == v) break;
-        }
-        std::string t = buf;
-        if (t.find_first_of(".eEn") == std::string::npos) t += ".0";
-        return t;
-    };
-    return "{\"bad_pixel_rate\":" + num(r.bad_pixel_rate) + ",\"compared\":" +
-           std::to_string(r.compared) + ",\"delta_d\":" + num(r.delta_d) + ",\"excluded\":" +
-           std::to_string(r.excluded) + "}";
+    return "{\"bad_pixel_rate\":" + b200::json_number(r.bad_pixel_rate) + ",\"compared\":" +
+           std::to_string(r.compared) + ",\"delta_d\":" + b200::json_number(r.delta_d) +
+           ",\"excluded\":" + std::to_string(r.excluded) + "}";
+}
+
+// nlohmann::json's double serialisation: the shortest digit string that
+// round-trips, laid out as its format_buffer does (decimal point kept for
+// integral values, plain notation for decimal exponents in (-4, 15], else
+// d.ddde+XX with at least two exponent digits).
+std::string b200::json_number(double v) {
+    if (!std::isfinite(v)) return "null";
+    if (v == 0.0) return std::signbit(v) ? "-0.0" : "0.0";
+    char buf[64];
+    int p = 1;
+    for (; p <= 17; ++p) {
+        std::snprintf(buf, sizeof buf, "%.*e", p - 1, v);
+        if (std::strtod(buf, nullptr) == v) break;
+    }
+    std::string s = buf, sign;
+    if (s[0] == '-') {
+        sign = "-";
+        s.erase(0, 1);
+    }
+    const std::size_t e = s.find('e');
+    const int exp10 = std::atoi(s.c_str() + e + 1);
+    std::string digits;
+    for (std::size_t i = 0; i < e; ++i)
+        if (s[i] != '.') digits += s[i];
+    while (digits.size() > 1 && digits.back() == '0') digits.pop_back();
+    const int k = static_cast<int>(digits.size());
+    const int n = exp10 + 1;  // position of the decimal point
+    std::string out;
+    if (k <= n && n <= 15) {
+        out = digits + std::string(n - k, '0') + ".0";
+    } else if (0 < n && n <= 15) {
+        out = digits.substr(0, n) + "." + digits.substr(n);
+    } else if (-4 < n && n <= 0) {
+        out = "0." + std::string(-n, '0') + digits;
+    } else {
+        out = digits.substr(0, 1);
+        if (k > 1) out += "." + digits.substr(1);
+        const int x = n - 1;
+        char eb[16];
+        std::snprintf(eb, sizeof eb, "e%c%02d", x < 0 ? '-' : '+', x < 0 ? -x : x);
+        out += eb;
+    }
+    return sign + out;
 }
 
 DisparityMap fill_scanlines(const DisparityMap& sparse, int workers) {
