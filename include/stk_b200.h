@@ -269,6 +269,34 @@ stk_status stk_disparity_mask_path(const char* path, char* out, size_t cap, size
  * by stem, written as "left\tright\n" lines. */
 stk_status stk_list_frame_pairs(const char* dir, char* out, size_t cap, size_t* need, int* count);
 
+/* -------------------------------------------------- streamed frame I/O -- */
+/* A directory of <stem>_L/_R pairs (stk_list_frame_pairs) refocused to
+ * <out_dir>/<stem>.ppm|.png (and <stem>_disp.pgm when disparity_scale > 0):
+ * decoder threads fill pinned host buffers ahead of the GPU, frames run on
+ * `slots` GPU slots of `ctx` (stk_create with at least that many), writer
+ * threads encode the results -- file decode, H2D, kernels, D2H and encode all
+ * overlap.  Frames shard across processes by index:
+ * this call handles frames f with f % shard_count == shard_index.  No
+ * reference counterpart (its CLI runs one pair per process,
+ * tools/main.cpp:327-379); each output equals run_refocus_pipeline's. */
+typedef struct stk_video_opts {
+    int slots;            /* GPU frames in flight (<= the context's slots) */
+    int decode_threads;   /* host decoder threads */
+    int write_threads;    /* host encoder threads */
+    int png;              /* 1: write .png, 0: .ppm */
+    double disparity_scale; /* > 0: also save_disparity(dense, <stem>_disp.pgm, scale) */
+    int shard_index, shard_count;
+} stk_video_opts;
+typedef struct stk_video_report {
+    int frames;           /* frames this call processed */
+    int frames_total;     /* pairs in the directory */
+    double wall_s, frames_per_s;
+    double decode_s, write_s, gpu_wait_s; /* summed thread time per phase */
+    double matched_fraction;
+} stk_video_report;
+stk_status stk_video_refocus(stk_ctx* ctx, const char* in_dir, const char* out_dir, const stk_config* cfg,
+                             const stk_focus* focus, const stk_video_opts* opts, stk_video_report* report);
+
 #ifdef __cplusplus
 }
 #endif

@@ -42,7 +42,7 @@ CU_SOURCES = [
     "k_eval.cu",
     "stk_capi.cu",
 ]
-CXX_SOURCES = ["stereotk_shim.cpp", "stk_io.cpp"]  # C++ stereotk:: drop-in over the C-ABI; file I/O
+CXX_SOURCES = ["stereotk_shim.cpp", "stk_io.cpp", "stk_video.cpp"]  # C++ stereotk:: drop-in over the C-ABI; file I/O
 HEADERS = ["stk_internal.cuh", "stk_device.cuh"]
 
 
@@ -81,7 +81,7 @@ def build(verbose: bool = False, force: bool = False) -> None:
         o = objdir / (src + ".o")
         objs.append(o)
         if force or _newer([s] + deps, o):
-            _run(["/usr/bin/g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-I", INCLUDE,
+            _run(["/usr/bin/g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-pthread", "-I", INCLUDE,
                   "-c", s, "-o", o], verbose)
     if force or _newer(objs, LIB):
         _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lz", "-lrt",

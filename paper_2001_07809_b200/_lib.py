@@ -52,6 +52,18 @@ class StkFrameOut(C.Structure):
                 ("row_filled", C.c_void_p)]
 
 
+class StkVideoOpts(C.Structure):
+    _fields_ = [("slots", C.c_int), ("decode_threads", C.c_int), ("write_threads", C.c_int),
+                ("png", C.c_int), ("disparity_scale", C.c_double), ("shard_index", C.c_int),
+                ("shard_count", C.c_int)]
+
+
+class StkVideoReport(C.Structure):
+    _fields_ = [("frames", C.c_int), ("frames_total", C.c_int), ("wall_s", C.c_double),
+                ("frames_per_s", C.c_double), ("decode_s", C.c_double), ("write_s", C.c_double),
+                ("gpu_wait_s", C.c_double), ("matched_fraction", C.c_double)]
+
+
 # name -> (restype, argtypes); every symbol include/stk_b200.h declares.
 VP, I, D, SZ = C.c_void_p, C.c_int, C.c_double, C.c_size_t
 SIGNATURES = {
@@ -108,6 +120,8 @@ SIGNATURES = {
     "stk_load_disparity": (I, [C.c_char_p, VP, I, I, D]),
     "stk_load_ground_truth": (I, [C.c_char_p, VP, I, I, D]),
     "stk_disparity_mask_path": (I, [C.c_char_p, C.c_char_p, SZ, C.POINTER(SZ)]),
+    "stk_video_refocus": (I, [VP, C.c_char_p, C.c_char_p, C.POINTER(StkConfig), C.POINTER(StkFocus),
+                              C.POINTER(StkVideoOpts), C.POINTER(StkVideoReport)]),
     "stk_list_frame_pairs": (I, [C.c_char_p, C.c_char_p, SZ, C.POINTER(SZ), C.POINTER(C.c_int)]),
 }
 

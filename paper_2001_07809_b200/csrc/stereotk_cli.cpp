@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "stereotk/stereotk_b200.hpp"
+#include "stk_b200.h"
 
 namespace fs = std::filesystem;
 using namespace stereotk;
@@ -666,6 +667,70 @@ int run_bench(BenchOpts& o) {  // main.cpp:412-440
     return 0;
 }
 
+// B200 extension (no reference counterpart): a directory of frame pairs
+// refocused with file decode, PCIe copies, kernels and encode overlapped
+// (stk_video_refocus), optionally one shard of the frames per GPU.
+struct VideoOpts {
+    std::string in_dir, out_dir, focus_text;
+    double sigma = 2.0, disparity_scale = 0.0;
+    int kernel_size = 0, slots = 3, decode_threads = 4, write_threads = 2, device = -1;
+    int shard_index = 0, shard_count = 1;
+    std::string png = "0";
+    PipelineFlags pipeline;
+};
+
+int run_video(VideoOpts& o) {
+    if (!o.pipeline.config_path.empty()) apply_config_file(o.pipeline.config_path, o.pipeline.bindings());
+    if (!(o.sigma > 0.0)) throw ParamError("sigma must be positive, got " + std::to_string(o.sigma));
+    if (o.kernel_size != 0 && (o.kernel_size < 1 || o.kernel_size % 2 == 0))
+        throw ParamError("kernel size must be odd and positive, got " + std::to_string(o.kernel_size));
+    if (o.slots < 1) throw ParamError("slots must be >= 1, got " + std::to_string(o.slots));
+    auto ranges = parse_focus(o.focus_text);
+    std::vector<int> lo, hi;
+    for (auto& [a, b] : ranges) {
+        lo.push_back(std::min(a, o.pipeline.config.max_disparity));
+        hi.push_back(std::min(b, o.pipeline.config.max_disparity));
+    }
+    const PipelineConfig& c = o.pipeline.config;
+    const stk_config cfg{c.k, c.window, c.max_disparity, c.threshold, c.prune_fraction, c.workers};
+    const stk_focus fo{lo.data(), hi.data(), static_cast<int>(lo.size()), o.sigma, o.kernel_size,
+                       b200::fast_blur() ? 0 : 1};
+    const stk_video_opts vo{o.slots, o.decode_threads, o.write_threads, o.png == "1" || o.png == "true",
+                            o.disparity_scale, o.shard_index, o.shard_count};
+    int device = o.device;
+    if (device < 0) {
+        const char* e = std::getenv("STK_DEVICE");
+        device = e ? std::atoi(e) : 0;
+    }
+    auto check = [](stk_status s, const stk_ctx* ctx) {
+        if (s == STK_OK) return;
+        const std::string m = stk_last_error(ctx);
+        if (s == STK_EPARAM) throw ParamError(m);
+        if (s == STK_EIO) throw IoError(m);
+        if (s == STK_EFORMAT) throw FormatError(m);
+        throw std::runtime_error(m);
+    };
+    check(stk_validate_config(&cfg), nullptr);
+    stk_ctx* ctx = nullptr;
+    check(stk_create(device, 0, 0, o.slots, &ctx), nullptr);
+    stk_video_report rep{};
+    const stk_status st = stk_video_refocus(ctx, o.in_dir.c_str(), o.out_dir.c_str(), &cfg, &fo, &vo, &rep);
+    stk_destroy(ctx);
+    check(st, nullptr);
+    JsonOut j;
+    j.integer("frames", rep.frames);
+    j.integer("frames_total", rep.frames_total);
+    j.num("wall_s", rep.wall_s);
+    j.num("frames_per_s", rep.frames_per_s);
+    j.num("decode_s", rep.decode_s);
+    j.num("write_s", rep.write_s);
+    j.num("gpu_wait_s", rep.gpu_wait_s);
+    j.num("matched_fraction", rep.matched_fraction);
+    j.str("out_dir", o.out_dir);
+    std::cout << j.dump() << "\n";
+    return 0;
+}
+
 const char* kAppHelp =
     "Boundary-driven stereo depth estimation and selective refocus (B200)\n"
     "Usage: stereotk [OPTIONS] SUBCOMMAND\n\n"
@@ -674,7 +739,8 @@ const char* kAppHelp =
     "  depth                       Estimate a dense disparity map from a rectified pair\n"
     "  refocus                     Blur everything outside the in-focus disparity ranges\n"
     "  eval                        Compare a computed disparity map against ground truth\n"
-    "  bench                       Time the pipeline serial vs parallel over a frame batch\n";
+    "  bench                       Time the pipeline serial vs parallel over a frame batch\n"
+    "  video                       Refocus a directory of frame pairs, decode/GPU/encode overlapped\n";
 
 }  // namespace
 
@@ -715,7 +781,24 @@ int main(int argc, char** argv) {
     bench.text("--csv", bench_opts.csv_path, "Write the CSV here instead of stdout");
     bench_opts.pipeline.add(bench, /*with_workers=*/false);
 
-    Command* cmds[] = {&depth, &refocus, &eval, &bench};
+    VideoOpts video_opts;
+    Command video{"video", "Refocus a directory of <stem>_L/_R frame pairs (B200 extension)", {}};
+    video.text("frames", video_opts.in_dir, "Directory of <stem>_L/<stem>_R frame pairs");
+    video.text("--out-dir", video_opts.out_dir, "Output directory (<stem>.ppm|.png)", true);
+    video.text("--focus", video_opts.focus_text, "In-focus disparity ranges lo:hi[,lo:hi...]", true);
+    video.num("--sigma", video_opts.sigma, "Gaussian blur strength");
+    video.num("--kernel-size", video_opts.kernel_size, "Odd kernel side (default: derived from sigma)");
+    video.text("--png", video_opts.png, "1: write PNG instead of PPM");
+    video.num("--disparity-scale", video_opts.disparity_scale, "> 0: also write <stem>_disp.pgm at this scale");
+    video.num("--slots", video_opts.slots, "GPU frames in flight");
+    video.num("--decode-threads", video_opts.decode_threads, "Host decoder threads");
+    video.num("--write-threads", video_opts.write_threads, "Host encoder threads");
+    video.num("--device", video_opts.device, "CUDA device (default $STK_DEVICE or 0)");
+    video.num("--shard-index", video_opts.shard_index, "Process frames f with f % shard-count == shard-index");
+    video.num("--shard-count", video_opts.shard_count, "Number of shards (one per GPU)");
+    video_opts.pipeline.add(video);
+
+    Command* cmds[] = {&depth, &refocus, &eval, &bench, &video};
     std::vector<std::string> args(argv + 1, argv + argc);
     Command* chosen = nullptr;
     try {
@@ -742,6 +825,7 @@ int main(int argc, char** argv) {
         if (chosen == &refocus) return run_refocus(refocus_opts);
         if (chosen == &eval) return run_eval(eval_opts);
         if (chosen == &bench) return run_bench(bench_opts);
+        if (chosen == &video) return run_video(video_opts);
     } catch (const ParamError& e) {
         std::cerr << "error: " << e.what() << "\n";
         return 2;

@@ -638,3 +638,38 @@ def list_frame_pairs(directory) -> list:
 def load_frames(directory) -> list:
     """The CLI's load_frames: [(left_rgb, right_rgb)] in stem order."""
     return [(load_image(l), load_image(r)) for l, r in list_frame_pairs(directory)]
+
+
+@dataclass
+class VideoReport:
+    """stk_video_report: what one refocus_video call did and how fast."""
+    frames: int
+    frames_total: int
+    wall_s: float
+    frames_per_s: float
+    decode_s: float
+    write_s: float
+    gpu_wait_s: float
+    matched_fraction: float
+
+
+def refocus_video(in_dir, out_dir, config: PipelineConfig, focus: FocusSpec, kernel_size: int = 0, *,
+                  slots: int = 0, decode_threads: int = 4, write_threads: int = 2, png: bool = False,
+                  disparity_scale: float = 0.0, shard_index: int = 0, shard_count: int = 1,
+                  device: Optional[Device] = None) -> VideoReport:
+    """Every <stem>_L/_R pair of ``in_dir`` refocused into ``out_dir`` with
+    decode, copies, kernels and encode overlapped (stk_video_refocus).
+    ``slots`` = GPU frames in flight (default: all of the device's)."""
+    from ._lib import StkVideoOpts, StkVideoReport
+
+    dev = _dev(device)
+    slots = slots or dev.slots
+    cfg = config.c()
+    fc, keep = _focus_c(focus, kernel_size)
+    opts = StkVideoOpts(slots, decode_threads, write_threads, 1 if png else 0, float(disparity_scale),
+                        shard_index, shard_count)
+    rep = StkVideoReport()
+    _raise(_lib.lib().stk_video_refocus(dev.h, _b(in_dir), _b(out_dir), C.byref(cfg), C.byref(fc),
+                                        C.byref(opts), C.byref(rep)), None)
+    return VideoReport(rep.frames, rep.frames_total, rep.wall_s, rep.frames_per_s, rep.decode_s,
+                       rep.write_s, rep.gpu_wait_s, rep.matched_fraction)
