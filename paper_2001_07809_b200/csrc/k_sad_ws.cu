@@ -13,10 +13,11 @@
 //   vertical  (NVW warps) thread = (G disparity quads, K consecutive colsum
 //             columns).  colsum(c, d) = sum over the w window rows of
 //             |L(c) - R(c-d)|, kept in registers as u16x2 words
-//             A = (4q, 4q+1), B = (4q+2, 4q+3).  One VABSDIFF4 of the
-//             replicated L byte against R(c-4q-3 .. c-4q) gives 4 disparities;
-//             each row step adds the entering row and subtracts the leaving
-//             one in a single IADD3 per word.  All byte alignments are
+//             A = (4q, 4q+1), B = (4q+2, 4q+3).  One VABSDIFF4 of the spread
+//             L byte (L, 0, L, 0) against a spread R pair (R(x), 0, R(x-1), 0)
+//             gives two disparities directly in u16x2 lanes; each row step
+//             adds the entering row and subtracts the leaving one in a single
+//             IADD3 per word.  All byte alignments are
 //             compile-time (K % 4 == 0, strip origin % 16 == 0, WIN fixed), so
 //             every shift/permute has an immediate selector.  The row's
 //             colsums go to shared memory buffer (row & 1).
@@ -57,6 +58,15 @@ struct WP {
 __device__ __forceinline__ uint32_t lo16(uint32_t v) { return v & 0xffffu; }
 __device__ __forceinline__ uint32_t hi16(uint32_t v) { return v >> 16; }
 
+// (byte p, 0, byte p-1, 0) of a run of words (p compile-time after unrolling).
+template <int N>
+__device__ __forceinline__ uint32_t r_pair(const uint32_t (&w)[N], int p) {
+    const int i = p >> 2, s = p & 3;
+    if (s) return __byte_perm(w[i], 0u, (uint32_t)s | 0x40u | (uint32_t)(s - 1) << 8 | 0x4000u);
+    // byte p = byte 0 of w[i], byte p-1 = byte 3 of w[i-1]
+    return __byte_perm(w[i - 1], w[i], 0x0304u) & 0x00ff00ffu;
+}
+
 // Vertical update of the G x K colsum units of one thread for one row pair.
 // INIT: add the new row only.  Rw/Lw: R and L words of the row(s).
 template <int WIN, int G, int K, bool INIT>
@@ -79,28 +89,33 @@ __device__ __forceinline__ void v_rows(const uint32_t* __restrict__ Ln, const ui
 #pragma unroll
         for (int i = 0; i < NWR; ++i) ro[i] = Ro[i];
     }
+    // Spread words: the L byte as (L, 0, L, 0) and R byte pairs as
+    // (R(x), 0, R(x-1), 0), so one VABSDIFF4 yields two disparities already
+    // in u16x2 lanes (no per-result unpacking).  R(c - 4q - m) sits at byte
+    // o + 3 - m of the run, o = rR + k - 4j + 4(G-1); word A (d = 4q, 4q+1)
+    // takes the pair at p = o + 3, word B (d = 4q+2, 4q+3) the pair at
+    // p = o + 1.  Pairs are pure functions of compile-time p, so each is
+    // built once per row and shared by every (k, j) that uses it.
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const int lb = rL + k;
-        const uint32_t repn = __byte_perm(ln[lb >> 2], 0u, (lb & 3) * 0x1111);
-        uint32_t repo = 0;
-        if (!INIT) repo = __byte_perm(lo[lb >> 2], 0u, (lb & 3) * 0x1111);
+        const uint32_t lsel = (uint32_t)(lb & 3) * 0x0101u | 0x4040u;  // bytes 1, 3 <- zero
+        const uint32_t spn = __byte_perm(ln[lb >> 2], 0u, lsel);
+        uint32_t spo = 0;
+        if (!INIT) spo = __byte_perm(lo[lb >> 2], 0u, lsel);
 #pragma unroll
         for (int j = 0; j < G; ++j) {
-            // R window bytes for (k, quad j): offset o = rR + k - 4j relative to
-            // word index (G-1) of the loaded run
             const int o = rR + k - 4 * j + 4 * (G - 1);
-            const int wi = o >> 2, sh = o & 3;
-            const uint32_t wn = sh ? __funnelshift_r(rn[wi], rn[wi + 1], sh * 8) : rn[wi];
-            const uint32_t vn = __vabsdiffu4(repn, wn);
+            const uint32_t an = __vabsdiffu4(spn, r_pair<NWR>(rn, o + 3));
+            const uint32_t bn = __vabsdiffu4(spn, r_pair<NWR>(rn, o + 1));
             if (INIT) {
-                A[j][k] += __byte_perm(vn, 0u, 0x4243);
-                B[j][k] += __byte_perm(vn, 0u, 0x4041);
+                A[j][k] += an;
+                B[j][k] += bn;
             } else {
-                const uint32_t wo = sh ? __funnelshift_r(ro[wi], ro[wi + 1], sh * 8) : ro[wi];
-                const uint32_t vo = __vabsdiffu4(repo, wo);
-                A[j][k] = A[j][k] + __byte_perm(vn, 0u, 0x4243) - __byte_perm(vo, 0u, 0x4243);
-                B[j][k] = B[j][k] + __byte_perm(vn, 0u, 0x4041) - __byte_perm(vo, 0u, 0x4041);
+                const uint32_t ao = __vabsdiffu4(spo, r_pair<NWR>(ro, o + 3));
+                const uint32_t bo = __vabsdiffu4(spo, r_pair<NWR>(ro, o + 1));
+                A[j][k] = A[j][k] + an - ao;
+                B[j][k] = B[j][k] + bn - bo;
             }
         }
     }
