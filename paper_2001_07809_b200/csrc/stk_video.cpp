@@ -52,8 +52,6 @@ struct HostSet {
     std::size_t cap_px = 0;
     std::uint8_t *left = nullptr, *right = nullptr, *out = nullptr;
     std::int16_t* dense = nullptr;
-    std::string error;  // decode/encode failure of this frame
-    stk_stats stats{};
 };
 
 struct Pipeline {

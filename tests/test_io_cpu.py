@@ -426,3 +426,17 @@ def test_list_frame_pairs(stk, tmp_path):
     (tmp_path / "empty").mkdir()
     with pytest.raises(stk.ParamError, match="no \\*_L/_R frame pairs"):
         stk.list_frame_pairs(tmp_path / "empty")
+
+
+def test_cpp_dropin_file_io(tmp_path):
+    """The C++ drop-in's file entry points, from a program written against the
+    reference headers (tests/cpp/io_test.cpp); host code only, no GPU."""
+    import subprocess
+
+    exe = str(tmp_path / "io_test")
+    lib = os.path.join(ROOT, "paper_2001_07809_b200")
+    subprocess.run(["/usr/bin/g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "io_test.cpp"), "-L", lib, "-lstk_b200",
+                    f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+    r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
