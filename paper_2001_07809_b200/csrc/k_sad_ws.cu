@@ -391,8 +391,27 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                     }
                     return key;
                 };
-                // two matchable pixels per iteration (independent chains)
-                for (uint32_t mm = m; mm;) {
+                // four (then two) matchable pixels per iteration: independent
+                // load -> sum -> min chains overlap on dense rows
+                uint32_t mm = m;
+                while (__popc(mm) >= 4) {
+                    int xs[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        xs[i] = pos_of(__ffs(mm) - 1);
+                        mm &= mm - 1;
+                    }
+                    uint32_t ks[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) ks[i] = keyof(xs[i]);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) ks[i] = __reduce_min_sync(0xffffffffu, ks[i]);
+                    if (lane == 0) {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) bp[xs[i]] = ks[i];
+                    }
+                }
+                for (; mm;) {
                     const int x1 = pos_of(__ffs(mm) - 1);
                     mm &= mm - 1;
                     const int x2 = mm ? pos_of(__ffs(mm) - 1) : x1;
