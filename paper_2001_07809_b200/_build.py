@@ -73,7 +73,8 @@ def build(verbose: bool = False, force: bool = False) -> None:
         o = objdir / (src + ".o")
         objs.append(o)
         if force or _newer([s] + deps, o):
-            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+            _run([NVCC, *ARCH, *os.environ.get("STK_NVCC_EXTRA", "").split(), "-O3", "-lineinfo",
+                  "-std=c++17", "-Xcompiler", "-fPIC",
                   "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr",
                   "-I", INCLUDE, "-I", CSRC, "-rdc=false", "-c", s, "-o", o], verbose)
     for src in CXX_SOURCES:

@@ -46,6 +46,10 @@ namespace {
 
 constexpr int kMaxThreads = 512;  // 4 warps per SMSP: 128 registers
 constexpr int kSegW = 32;  // output columns per horizontal segment
+#ifndef STK_SAD_HB
+#define STK_SAD_HB 6
+#endif
+constexpr int HB = STK_SAD_HB;  // matchable pixels per horizontal batch
 enum { BAR_FULL0 = 1, BAR_FULL1 = 2, BAR_EMPTY0 = 3, BAR_EMPTY1 = 4, BAR_H = 5 };
 
 struct WP {
@@ -394,23 +398,26 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                 // four (then two) matchable pixels per iteration: independent
                 // load -> sum -> min chains overlap on dense rows
                 uint32_t mm = m;
-                while (__popc(mm) >= 4) {
-                    int xs[4];
+                auto batch = [&](auto n_tag) {
+                    constexpr int NB = decltype(n_tag)::value;
+                    int xs[NB];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
+                    for (int i = 0; i < NB; ++i) {
                         xs[i] = pos_of(__ffs(mm) - 1);
                         mm &= mm - 1;
                     }
-                    uint32_t ks[4];
+                    uint32_t ks[NB];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) ks[i] = keyof(xs[i]);
+                    for (int i = 0; i < NB; ++i) ks[i] = keyof(xs[i]);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) ks[i] = __reduce_min_sync(0xffffffffu, ks[i]);
+                    for (int i = 0; i < NB; ++i) ks[i] = __reduce_min_sync(0xffffffffu, ks[i]);
                     if (lane == 0) {
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) bp[xs[i]] = ks[i];
+                        for (int i = 0; i < NB; ++i) bp[xs[i]] = ks[i];
                     }
-                }
+                };
+                while (__popc(mm) >= HB) batch(std::integral_constant<int, HB>{});
+                if (HB > 4 && __popc(mm) >= 4) batch(std::integral_constant<int, 4>{});
                 for (; mm;) {
                     const int x1 = pos_of(__ffs(mm) - 1);
                     mm &= mm - 1;
