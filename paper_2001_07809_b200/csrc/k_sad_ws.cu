@@ -317,6 +317,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
     // warp hw owns the 4-column groups gi = NHW*k + hw, k = 0..7 (SW = 32*NHW);
     // bit r of its mask is column 4*(NHW*(r>>2) + hw) + (r&3)
     auto pos_of = [&](int r) { return 4 * (p.NHW * (r >> 2) + hw) + (r & 3); };
+    // the window-term table and the best keys are indexed by (warp, mask bit):
+    // entry hwb + r is strip position pos_of(r), so a matchable pixel's table
+    // address comes straight from its bit index
+    const int hwb = 32 * hw;
     // warp mask of row y: lane k < 8 fetches group NHW*k + hw (word gi>>3,
     // nibble gi&7) and the warp OR-reduces the groups
     const uint32_t* mcol = f.mbits + (x0 >> 5);
@@ -340,7 +344,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
         constexpr int NT = WinTab<WIN, K>::NT;
         for (int a = htid; a < p.SW; a += 32 * p.NHW) {
             const int e = a + WIN - 1, ca = a / K, ce = e / K;
-            uint32_t* en = tab + a * NE;
+            const int g4 = a >> 2;  // a = pos_of(r) of warp g4 % NHW, r = 4 (g4 / NHW) + a % 4
+            uint32_t* en = tab + (32 * (g4 % p.NHW) + 4 * (g4 / p.NHW) + (a & 3)) * NE;
             auto slot = [&](int cc) { return (uint32_t)(cc + cc / K) * 8u; };
             en[0] = slot(e);
             en[1] = a % K ? slot(a - 1) : (uint32_t)ZC * 8u;
@@ -361,16 +366,16 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
         if ((mprev >> lane) & 1u) {
             const int x = pos_of(lane);
             uint32_t* bp = best + (b ^ 1) * p.SW;
-            f.sparse[(size_t)(y - 1) * f.W + x0 + x] = (int16_t)(bp[x] & 1023u);
+            f.sparse[(size_t)(y - 1) * f.W + x0 + x] = (int16_t)(bp[hwb + lane] & 1023u);
         }
         if (m) {
             const uint2* cb = cs + b * bufstride;
             uint32_t* bp = best + b * p.SW;
             auto pixels = [&](auto fast_tag) {
                 constexpr bool FAST = decltype(fast_tag)::value;
-                // in-lane min key of the main quads at strip position x
-                auto keyof = [&](int x) {
-                    const int lim = min(p.D, x0 + x - h);
+                // in-lane min key of the main quads at mask bit r
+                auto keyof = [&](int r) {
+                    const int lim = FAST ? p.D : min(p.D, x0 + pos_of(r) - h);
                     uint32_t key = 0xffffffffu;
 #pragma unroll
                     for (int qb = 0; qb < NQB; ++qb) {
@@ -379,7 +384,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                         const char* cq = reinterpret_cast<const char*>(cb + (size_t)(qok ? q : 0) * p.CSW);
                         const uint32_t dbase = 4 * q + 2 * region;
                         uint32_t lo[HQ], hi[HQ];
-                        window_sum<WIN, K, HQ>(cq, tab + x * NE, region != 0, lo, hi);
+                        window_sum<WIN, K, HQ>(cq, tab + (hwb + r) * NE, region != 0, lo, hi);
 #pragma unroll
                         for (int w = 0; w < HQ; ++w) {
                             // word w: d = dbase + 2w (lo lane), dbase + 2w + 1 (hi lane)
@@ -400,10 +405,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                 uint32_t mm = m;
                 auto batch = [&](auto n_tag) {
                     constexpr int NB = decltype(n_tag)::value;
-                    int xs[NB];
+                    int xs[NB];  // mask bits
 #pragma unroll
                     for (int i = 0; i < NB; ++i) {
-                        xs[i] = pos_of(__ffs(mm) - 1);
+                        xs[i] = __ffs(mm) - 1;
                         mm &= mm - 1;
                     }
                     uint32_t ks[NB];
@@ -413,23 +418,23 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                     for (int i = 0; i < NB; ++i) ks[i] = __reduce_min_sync(0xffffffffu, ks[i]);
                     if (lane == 0) {
 #pragma unroll
-                        for (int i = 0; i < NB; ++i) bp[xs[i]] = ks[i];
+                        for (int i = 0; i < NB; ++i) bp[hwb + xs[i]] = ks[i];
                     }
                 };
                 while (__popc(mm) >= HB) batch(std::integral_constant<int, HB>{});
                 if (HB > 4 && __popc(mm) >= 4) batch(std::integral_constant<int, 4>{});
                 for (; mm;) {
-                    const int x1 = pos_of(__ffs(mm) - 1);
+                    const int x1 = __ffs(mm) - 1;
                     mm &= mm - 1;
-                    const int x2 = mm ? pos_of(__ffs(mm) - 1) : x1;
+                    const int x2 = mm ? __ffs(mm) - 1 : x1;
                     mm &= mm - 1;
                     uint32_t k1 = keyof(x1), k2 = keyof(x2);
                     k1 = __reduce_min_sync(0xffffffffu, k1);
                     k2 = __reduce_min_sync(0xffffffffu, k2);
                     // this warp owns the pixel and covers every main quad
                     if (lane == 0) {
-                        bp[x1] = k1;
-                        bp[x2] = k2;
+                        bp[hwb + x1] = k1;
+                        bp[hwb + x2] = k2;
                     }
                 }
             };
@@ -444,7 +449,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                 for (int qx = p.QMAIN; qx < p.Q; ++qx) {
                     uint32_t lo[2], hi[2];
                     window_sum<WIN, K, 2>(reinterpret_cast<const char*>(cb + (size_t)qx * p.CSW),
-                                          tab + x * NE, false, lo, hi);
+                                          tab + (hwb + lane) * NE, false, lo, hi);
                     const uint32_t c[4] = {lo[0], hi[0], lo[1], hi[1]};
 #pragma unroll
                     for (int jj = 0; jj < 4; ++jj) {
@@ -452,7 +457,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                         if (d <= lim) key = min(key, c[jj] * 1024u + (uint32_t)d);
                     }
                 }
-                bp[x] = min(bp[x], key);
+                bp[hwb + lane] = min(bp[hwb + lane], key);
             }
         }
         if (t + 2 < T) named_arrive(BAR_EMPTY0 + b, NVH);
@@ -463,7 +468,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
     named_sync(BAR_H, 32 * p.NHW);
     if ((mprev >> lane) & 1u) {
         const int x = pos_of(lane), y = yb1 - 1, b = (T - 1) & 1;
-        f.sparse[(size_t)y * f.W + x0 + x] = (int16_t)(best[b * p.SW + x] & 1023u);
+        f.sparse[(size_t)y * f.W + x0 + x] = (int16_t)(best[b * p.SW + hwb + lane] & 1023u);
     }
 }
 
