@@ -55,6 +55,7 @@ def parse():
     p.add_argument("--sad", default="auto", choices=["auto", "list", "strip"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-s", type=float, default=20.0)
+    p.add_argument("--cpu-serial", type=int, default=1, help="also time one reference frame at workers = 1")
     p.add_argument("--e2e-dense", action="store_true",
                    help="also read the dense disparity back in the e2e leg (run_refocus_pipeline "
                         "returns only the refocused image; DepthResult is optional)")
@@ -441,13 +442,31 @@ def main():
         fps, cores, kind, sample, _ = cpu_reference(args.config, args.cpu_sample_s, warmup=0,
                                                     pool=args.pool)
         line["cpu_baseline"] = {"value": fps, "unit": "frames/s", "cores": cores, "kind": kind,
-                                "sample": sample}
+                                "sample": sample, "cpu_model": _cpu_model(), "nproc": os.cpu_count()}
+        if kind == "reference" and args.cpu_serial:
+            # the reference at workers = 1 as well (one frame, bounded)
+            ref = __import__("oracle").reference()
+            frame = reference_frames(args.config, 1, 1)[0]
+            dt, _ = run_reference_frame(ref, frame, args.config, 1)
+            line["cpu_baseline"]["serial"] = {"value": 1.0 / dt, "unit": "frames/s", "cores": 1,
+                                              "sample": "1 frame, workers = 1"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     dev.close()
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 _pinned_keep = []
