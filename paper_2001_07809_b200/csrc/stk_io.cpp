@@ -692,9 +692,20 @@ stk_status stk_image_probe(const char* path, int* w, int* h, int* channels) {
             H = static_cast<int>(ph);
             C = png_channels(b[25]) >= 3 || b[25] == 3 ? 3 : 1;
         } else {
-            // headers may carry long comments: parse the whole file's header
-            const Bytes all = stereotk::read_file(path);
-            const auto hd = stereotk::pnm_header(all, path, nullptr);
+            // the header from the first MiB (the whole file if the header --
+            // which may carry long comment lines -- does not fit)
+            Bytes head(1 << 20);
+            in.clear();
+            in.seekg(0);
+            in.read(reinterpret_cast<char*>(head.data()), static_cast<std::streamsize>(head.size()));
+            head.resize(static_cast<size_t>(in.gcount()));
+            stereotk::Pnm hd;
+            try {
+                hd = stereotk::pnm_header(head, path, nullptr);
+            } catch (const stereotk::FormatError&) {
+                if (head.size() < (1u << 20)) throw;
+                hd = stereotk::pnm_header(stereotk::read_file(path), path, nullptr);
+            }
             W = hd.width;
             H = hd.height;
             C = hd.channels;
