@@ -14,6 +14,9 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+#include <nvtx3/nvToolsExtCudaRt.h>
+
 #include "stk_b200.h"
 #include "stk_internal.cuh"
 
@@ -476,12 +479,23 @@ stk_status upload_focus(stk_ctx* ctx, Slot& s, const int* lo, const int* hi, int
 }
 
 // --------------------------------------------------------- frame enqueue ---
+// NVTX range for the host-side enqueue of one stage (SURVEY.md §5 tracing;
+// free when no tool is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 int enqueue_kernels(stk_ctx* ctx, Slot& s, const Frame& f, const BlurParams* bp, bool timed,
                     bool want_labels) {
+    NvtxRange frame_range("stk enqueue frame");
     cudaStream_t st = s.st;
     int n = 0;
+    static const char* kStage[8] = {"convert", "segment", "boundary", "match", "fill", "peek", "blur", "end"};
     auto rec = [&](int i) {
         if (timed) cudaEventRecord(s.ev[i], st);
+        if (i > 0) nvtxRangePop();
+        if (i < 7) nvtxRangePushA(kStage[i]);
     };
     cudaMemsetAsync(f.sc, 0, sizeof(DevScalars), st);
     cudaMemsetAsync(f.lb, 0, sizeof(unsigned long long) * LB_COUNT * f.lb_stride, st);
@@ -554,6 +568,7 @@ stk_status submit(stk_ctx* ctx, int slot, const uint8_t* rgbL, const uint8_t* rg
                   int w, int h, const stk_config* cfg, const stk_focus* focus,
                   const stk_frame_out* out, bool host_out, uint8_t* d_refocused, int16_t* d_dense,
                   bool timed) {
+    NvtxRange range("stk_frame_submit");
     int ksize = 0;
     TRY(check_frame_args(ctx, slot, w, h, cfg, focus, &ksize));
     CK(cudaSetDevice(ctx->device));
@@ -729,6 +744,9 @@ stk_status stk_create(int device, int max_width, int max_height, int slots, stk_
                 break;
             }
             for (auto& e : s.ev) cudaEventCreate(&e);
+            const std::string nm = "stk dev" + std::to_string(device) + " slot " +
+                                   std::to_string(&s - ctx->slots.data());
+            nvtxNameCudaStreamA(s.st, nm.c_str());
         }
         if (rc != STK_OK) break;
         if (max_width > 0 && max_height > 0) rc = ensure_slot(ctx, ctx->slots[0], max_width, max_height);
