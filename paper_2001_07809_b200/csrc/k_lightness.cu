@@ -296,17 +296,80 @@ __global__ void k_assign(Frame f, const uint8_t* __restrict__ gray, uint16_t* __
 
 }  // namespace
 
+// ---- exact 2^24-entry L* table (K1 LUT path) --------------------------------
+// lut[r << 16 | g << 8 | b] = lstar_of(r, g, b), built once per context by the
+// same exact per-triple rule as every other K1 variant (so the table is
+// bit-exact by construction; the exhaustive 2^24 GPU test checks the frame
+// path against the oracle).  16 MB, kept L2-resident through an access-policy
+// window on the slot streams: per pixel the frame path then reads 3 RGB bytes
+// and gathers one table byte instead of three FP64 products, two DADDs and a
+// bucket compare.
+__global__ void __launch_bounds__(256) k_lut_build(const LstarTables* __restrict__ tab, uint8_t* __restrict__ lut) {
+    __shared__ double lin[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) lin[i] = tab->linear[i];
+    __syncthreads();
+    const uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
+    if (i0 >= (1u << 24)) return;
+    uint32_t packed = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t i = i0 + k;
+        packed |= lstar_of(lin, tab, i >> 16, (i >> 8) & 0xffu, i & 0xffu) << (8 * k);
+    }
+    reinterpret_cast<uint32_t*>(lut)[i0 >> 2] = packed;
+}
+
+// Both views in one launch (blockIdx.y = view); thread = 16 consecutive
+// pixels of a row (3 streaming 16-byte loads, 16 table gathers, one 16-byte
+// store into the pitched gray plane).
+__global__ void __launch_bounds__(256) k_lstar_lut(Frame f, const uint8_t* __restrict__ lut) {
+    const int view = blockIdx.y;
+    const uint8_t* __restrict__ rgb = view == 0 ? f.rgbL : f.rgbR;
+    uint8_t* __restrict__ gray = view == 0 ? f.grayL : f.grayR;
+    const int cpr = f.W >> 4;  // 16-pixel chunks per row
+    const long long nch = (long long)cpr * f.H;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < nch;
+         c += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(c / cpr), x = (int)(c - (long long)y * cpr) * 16;
+        const uint4* s4 = reinterpret_cast<const uint4*>(rgb + ((size_t)y * f.W + x) * 3);
+        const uint4 a = __ldcs(s4), b = __ldcs(s4 + 1), d = __ldcs(s4 + 2);
+        const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
+        uint32_t v[16];
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+            const int o = p * 3;
+            const uint32_t r = (w[o >> 2] >> ((o & 3) * 8)) & 0xffu;
+            const uint32_t g = (w[(o + 1) >> 2] >> (((o + 1) & 3) * 8)) & 0xffu;
+            const uint32_t bb = (w[(o + 2) >> 2] >> (((o + 2) & 3) * 8)) & 0xffu;
+            v[p] = __ldg(lut + (r << 16 | g << 8 | bb));
+        }
+        uint32_t out[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) out[q] = v[4 * q] | v[4 * q + 1] << 8 | v[4 * q + 2] << 16 | v[4 * q + 3] << 24;
+        *reinterpret_cast<uint4*>(gray + (size_t)y * f.P + x) = make_uint4(out[0], out[1], out[2], out[3]);
+    }
+}
+
+void build_lstar_lut(const LstarTables* dtab, uint8_t* lut, cudaStream_t st) {
+    k_lut_build<<<(1 << 22) / 256, 256, 0, st>>>(dtab, lut);
+}
+
 void launch_lightness(const Frame& f, const LstarTables* dtab, bool left, bool right, bool hist,
-                      cudaStream_t st) {
+                      cudaStream_t st, const uint8_t* lut) {
     if (f.N == 0) return;
     const bool aligned = (reinterpret_cast<uintptr_t>(f.rgbL) & 15) == 0 &&
                          (reinterpret_cast<uintptr_t>(f.rgbR) & 15) == 0;
     if (left && right && f.W % 16 == 0 && aligned) {
         // frame path: both views in one launch, then the histogram pass
         const long long nch = (long long)(f.W / 16) * f.H;
-        const int bx = (int)std::min<long long>((nch + kL2Threads - 1) / kL2Threads, 74);
-        cudaFuncSetAttribute(k_lstar2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kL2Smem);
-        k_lstar2<<<dim3(bx, 2), kL2Threads, kL2Smem, st>>>(f, dtab);
+        if (lut) {
+            const int bx = (int)std::min<long long>((nch + 255) / 256, 148 * 4);
+            k_lstar_lut<<<dim3(bx, 2), 256, 0, st>>>(f, lut);
+        } else {
+            const int bx = (int)std::min<long long>((nch + kL2Threads - 1) / kL2Threads, 74);
+            cudaFuncSetAttribute(k_lstar2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kL2Smem);
+            k_lstar2<<<dim3(bx, 2), kL2Threads, kL2Smem, st>>>(f, dtab);
+        }
         if (hist) {
             const int hb = (int)std::min<long long>((nch + kThreads - 1) / kThreads, 148 * 4);
             k_hist_warp<<<hb, kThreads, 0, st>>>(f, f.grayL);

@@ -105,6 +105,7 @@ struct stk_ctx {
     int device = 0;
     std::string err;
     LstarTables* d_tab = nullptr;
+    uint8_t* d_lut = nullptr;  // exact 2^24-entry L* table (frame path), null = K1 arithmetic path
     std::vector<Slot> slots;
     int sad_kernel = SAD_AUTO;
     int use_graphs = 1;
@@ -500,7 +501,7 @@ int enqueue_kernels(stk_ctx* ctx, Slot& s, const Frame& f, const BlurParams* bp,
     cudaMemsetAsync(f.sc, 0, sizeof(DevScalars), st);
     cudaMemsetAsync(f.lb, 0, sizeof(unsigned long long) * LB_COUNT * f.lb_stride, st);
     rec(0);
-    launch_lightness(f, ctx->d_tab, true, true, true, st);  // left (+histogram), right
+    launch_lightness(f, ctx->d_tab, true, true, true, st, ctx->d_lut);  // left (+histogram), right
     n += 2;
     rec(1);
     launch_kmeans(f, 0, 100, 0.5, st);
@@ -735,6 +736,33 @@ stk_status stk_create(int device, int max_width, int max_height, int slots, stk_
             rc = fail(ctx, STK_ECUDA, "stk_create: table upload failed");
             break;
         }
+        // K1's exact 2^24-entry table, opt-in ($STK_LSTAR_LUT=1), persisting in
+        // L2 for the slot streams below.  Measured at 4K: convert 52 -> 40 us on
+        // the grey benchmark frames but 55 -> 93 us on uniformly random RGB
+        // (L2 gathers), so the arithmetic kernel, flat across inputs, stays the
+        // default.
+        static const bool lut_on = [] {
+            const char* e = getenv("STK_LSTAR_LUT");
+            return e ? atoi(e) != 0 : false;
+        }();
+        if (lut_on) {
+            if (cudaMalloc(&ctx->d_lut, size_t(1) << 24) != cudaSuccess) {
+                rc = fail(ctx, STK_ECUDA, "stk_create: L* table allocation failed");
+                break;
+            }
+            build_lstar_lut(ctx->d_tab, ctx->d_lut, 0);
+            if (cudaDeviceSynchronize() != cudaSuccess) {
+                rc = fail(ctx, STK_ECUDA, "stk_create: L* table build failed");
+                break;
+            }
+            int max_persist = 0;
+            cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+            size_t cur = 0;
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            const size_t want = std::min<size_t>(size_t(1) << 24, (size_t)max_persist);
+            if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+            cudaGetLastError();
+        }
         ctx->slots.resize(std::max(slots, 1));
         for (Slot& s : ctx->slots) {
             if (cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking) != cudaSuccess ||
@@ -747,6 +775,16 @@ stk_status stk_create(int device, int max_width, int max_height, int slots, stk_
             const std::string nm = "stk dev" + std::to_string(device) + " slot " +
                                    std::to_string(&s - ctx->slots.data());
             nvtxNameCudaStreamA(s.st, nm.c_str());
+            if (ctx->d_lut) {
+                cudaStreamAttrValue av = {};
+                av.accessPolicyWindow.base_ptr = ctx->d_lut;
+                av.accessPolicyWindow.num_bytes = size_t(1) << 24;
+                av.accessPolicyWindow.hitRatio = 1.0f;
+                av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+                cudaStreamSetAttribute(s.st, cudaStreamAttributeAccessPolicyWindow, &av);
+                cudaGetLastError();  // best effort: without persistence the table still works
+            }
         }
         if (rc != STK_OK) break;
         if (max_width > 0 && max_height > 0) rc = ensure_slot(ctx, ctx->slots[0], max_width, max_height);
@@ -777,6 +815,7 @@ void stk_destroy(stk_ctx* ctx) {
         if (s.st) cudaStreamDestroy(s.st);
     }
     if (ctx->d_tab) cudaFree(ctx->d_tab);
+    if (ctx->d_lut) cudaFree(ctx->d_lut);
     delete ctx;
 }
 
