@@ -4,9 +4,12 @@ compiled reference's golden frames and the oracle, the refocused image within
 1 LSB (bit-exact in exact-blur mode), plus size-independent properties at the
 benchmark's full 4096x2304 size, determinism and the async frame slots."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
+
+from conftest import ROOT
 
 pytestmark = pytest.mark.gpu
 
@@ -260,3 +263,31 @@ def test_pipeline_8k_config_e(dev, stk, synth):
     sharp = (a.dense >= 128) & (a.dense <= 256)
     assert (img[sharp] == l[sharp]).all()
     assert (img[~sharp] != l[~sharp]).any()
+
+
+def test_frame_lightness_lut_option_all_2pow24_triples(tmp_path, port):
+    """The opt-in exact L* table (STK_LSTAR_LUT=1, read once per process, so a
+    subprocess): every RGB triple through the frame path, both views, equals
+    the pinned oracle."""
+    import subprocess
+    import sys
+
+    v = np.arange(256, dtype=np.uint8)
+    rgb = np.stack(np.meshgrid(v, v, v, indexing="ij"), -1).reshape(4096, 4096, 3)
+    np.save(tmp_path / "rgb.npy", rgb)
+    code = f"""
+import sys, numpy as np
+sys.path.insert(0, {ROOT!r})
+from paper_2001_07809_b200 import stereotk as stk
+rgb = np.load({str(tmp_path / 'rgb.npy')!r})
+res = stk.run_depth_pipeline(rgb, np.ascontiguousarray(rgb[::-1]),
+                             stk.PipelineConfig(k=4, window=9, max_disparity=8))
+np.save({str(tmp_path / 'l.npy')!r}, res.left_lightness)
+np.save({str(tmp_path / 'r.npy')!r}, res.right_lightness)
+"""
+    env = dict(os.environ, STK_LSTAR_LUT="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    want = port.lightness(rgb)
+    eq(np.load(tmp_path / "l.npy"), want, "lut left_lightness")
+    eq(np.load(tmp_path / "r.npy"), want[::-1], "lut right_lightness")
