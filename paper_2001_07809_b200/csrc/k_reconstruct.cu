@@ -15,6 +15,8 @@
 //       0 knowns -> stays unknown, 1 known -> copy,
 //       above & below -> est(above, below),
 //       nothing above -> est(first two), nothing below -> est(last two).
+#include <cstdlib>
+
 #include "stk_device.cuh"
 
 namespace stk {
@@ -421,169 +423,208 @@ __global__ void __launch_bounds__(PC * PS) k_peek_cols2(Frame f, const int16_t* 
     }
 }
 
-// K7 v4: k_peek_cols2's algorithm with two adjacent columns per thread
-// (32-bit loads/stores of int16 pairs: a warp's 8 column pairs x 4 segments
-// move 32 contiguous bytes per row each) and unchecked full batches.
-constexpr int P4C = 8;   // column pairs per CTA (16 columns)
-constexpr int P4S = 64;  // row segments per column
-constexpr int P4B = 8;   // rows per batch
+// K7 helpers for the two-columns-per-thread kernel (int16 pairs in 32-bit
+// loads/stores: a warp's 8 column pairs x 4 segments move 32 contiguous bytes
+// per row each).
+constexpr int P4B = 8;   // rows per load batch
 
-struct ColSeg {  // segment summary of one column while walking down
-    int count, f1, f2, l1, l2;
-};
-__device__ __forceinline__ void seg_add(ColSeg& m, int d) {
-    const bool kn = d >= 0;
-    m.f2 = (kn && m.count == 1) ? d : m.f2;
-    m.f1 = (kn && m.count == 0) ? d : m.f1;
-    m.l2 = kn ? m.l1 : m.l2;
-    m.l1 = kn ? d : m.l1;
-    m.count += kn;
-}
 __device__ __forceinline__ uint32_t pack2(int a, int b) { return (uint32_t)(uint16_t)a | (uint32_t)b << 16; }
 __device__ __forceinline__ int lo16(uint32_t v) { return (int16_t)(v & 0xffffu); }
 __device__ __forceinline__ int hi16s(uint32_t v) { return (int16_t)(v >> 16); }
 
-__global__ void __launch_bounds__(P4C * P4S, 2) k_peek_cols4(Frame f, const int16_t* __restrict__ in,
+// K7 v5 (even W; k_peek_cols2 otherwise): 16 columns x 64 row segments per
+// CTA, two adjacent columns per thread, lean passes:
+//   pass 1 (bottom-up): the nearest known strictly below within the segment
+//     goes to `out` as scratch, and the segment summary (count, first two,
+//     last two knowns) to shared memory;
+//   phase 2: warp w = column w; lanes hold 2 segments each and warp shuffles
+//     give every segment its nearest known above / below (ordered scans) and
+//     the column its first two / last two knowns (ordered tree reductions) --
+//     no serial per-column loop;
+//   pass 2 (top-down): each pixel resolved from (input, nearest above carried
+//     in a register, nearest below from the scratch or the segment context).
+constexpr int P5C = 8;   // column pairs per CTA (16 columns)
+constexpr int P5S = 64;  // row segments per column (= 2 x 32 lanes in phase 2)
+
+__device__ __forceinline__ int peek_resolve(int d, int a, int b, int total, int et, int eb, int thr) {
+    if (d >= 0) return d;
+    if (total == 0) return -1;
+    if (total == 1) return a >= 0 ? a : b;
+    if (a >= 0 && b >= 0) return peek_estimate(a, b, thr);
+    return a < 0 ? et : eb;
+}
+
+__global__ void __launch_bounds__(P5C * P5S, 2) k_peek_cols5(Frame f, const int16_t* __restrict__ in,
                                                           int16_t* __restrict__ out) {
-    __shared__ SegSum seg[P4S][2 * P4C];
-    __shared__ int16_t ctx_ab[P4S][2 * P4C], ctx_bl[P4S][2 * P4C];
-    __shared__ int col_total[2 * P4C], col_top[2 * P4C], col_bot[2 * P4C];
-    __shared__ unsigned long long red[P4C * P4S / 32];
+    __shared__ int s_cnt[P5S][2 * P5C];
+    __shared__ uint32_t s_first[P5S][2 * P5C];  // f1 | f2 << 16 (int16 each, -1 = none)
+    __shared__ uint32_t s_last[P5S][2 * P5C];   // l1 | l2 << 16 (last, second last)
+    __shared__ int16_t ctx_ab[P5S][2 * P5C], ctx_bl[P5S][2 * P5C];
+    __shared__ int col_total[2 * P5C], col_top[2 * P5C], col_bot[2 * P5C];
+    __shared__ unsigned long long red[P5C * P5S / 32];
     const int W = f.W, H = f.H, thr = f.thr;
-    const int cp = threadIdx.x % P4C, s = threadIdx.x / P4C;
-    const int x = 2 * (blockIdx.x * P4C + cp);  // W even
-    const int sr = (H + P4S - 1) / P4S;
+    const int cp = threadIdx.x % P5C, s = threadIdx.x / P5C;
+    const int x = 2 * (blockIdx.x * P5C + cp);  // W even
+    const int sr = (H + P5S - 1) / P5S;
     const int ya = min(H, s * sr), yb = min(H, ya + sr);
     const bool col = x < W;
     const uint32_t* __restrict__ in2 = reinterpret_cast<const uint32_t*>(in);
     uint32_t* __restrict__ out2 = reinterpret_cast<uint32_t*>(out);
-    const size_t W2 = (size_t)W / 2;  // row stride in pairs
-    // pass 1 (top-down)
-    ColSeg m0{0, -1, -1, -1, -1}, m1{0, -1, -1, -1, -1};
+    const size_t W2 = (size_t)W / 2;
+    // ---- pass 1 (bottom-up)
+    int n0 = 0, n1 = 0, b0 = -1, b1 = -1;
+    int f10 = -1, f20 = -1, l10 = -1, l20 = -1, f11 = -1, f21 = -1, l11 = -1, l21 = -1;
     if (col) {
-        int c0 = -1, c1 = -1;
-        size_t o = (size_t)ya * W2 + x / 2;
-        for (int yy = ya; yy < yb; yy += P4B, o += P4B * W2) {
-            const int n = min(P4B, yb - yy);
+        const uint32_t* ip = in2 + x / 2;
+        uint32_t* op = out2 + x / 2;
+        auto row = [&](uint32_t v, size_t o) {
+            op[o] = pack2(b0, b1);
+            const int d0 = lo16(v), d1 = hi16s(v);
+            if (d0 >= 0) {
+                l20 = n0 == 1 ? d0 : l20;
+                l10 = n0 == 0 ? d0 : l10;
+                f20 = f10;
+                f10 = d0;
+                b0 = d0;
+                ++n0;
+            }
+            if (d1 >= 0) {
+                l21 = n1 == 1 ? d1 : l21;
+                l11 = n1 == 0 ? d1 : l11;
+                f21 = f11;
+                f11 = d1;
+                b1 = d1;
+                ++n1;
+            }
+        };
+        int y = yb - 1;
+        for (; y - P4B + 1 >= ya; y -= P4B) {
             uint32_t v[P4B];
-            if (n == P4B) {
 #pragma unroll
-                for (int k = 0; k < P4B; ++k) v[k] = __ldg(in2 + o + k * W2);
+            for (int k = 0; k < P4B; ++k) v[k] = __ldg(ip + (size_t)(y - k) * W2);
 #pragma unroll
-                for (int k = 0; k < P4B; ++k) {
-                    out2[o + k * W2] = pack2(c0, c1);
-                    const int d0 = lo16(v[k]), d1 = hi16s(v[k]);
-                    seg_add(m0, d0);
-                    seg_add(m1, d1);
-                    c0 = d0 >= 0 ? d0 : c0;
-                    c1 = d1 >= 0 ? d1 : c1;
+            for (int k = 0; k < P4B; ++k) row(v[k], (size_t)(y - k) * W2);
+        }
+        for (; y >= ya; --y) row(__ldg(ip + (size_t)y * W2), (size_t)y * W2);
+    }
+    s_cnt[s][2 * cp] = n0;
+    s_cnt[s][2 * cp + 1] = n1;
+    s_first[s][2 * cp] = pack2(f10, f20);
+    s_first[s][2 * cp + 1] = pack2(f11, f21);
+    s_last[s][2 * cp] = pack2(l10, l20);
+    s_last[s][2 * cp + 1] = pack2(l11, l21);
+    __syncthreads();
+    // ---- phase 2: warp = column, lane = segments (2 lane, 2 lane + 1)
+    {
+        const unsigned full = 0xffffffffu;
+        const int cx = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int i0 = 2 * lane, i1 = i0 + 1;
+        const int c0 = s_cnt[i0][cx], c1 = s_cnt[i1][cx];
+        const uint32_t F0 = s_first[i0][cx], F1 = s_first[i1][cx];
+        const uint32_t L0 = s_last[i0][cx], L1 = s_last[i1][cx];
+        // nearest known above each segment: "latest known" exclusive scan
+        int inc = c1 ? lo16(L1) : (c0 ? lo16(L0) : -1);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(full, inc, o);
+            if (lane >= o && inc < 0) inc = t;
+        }
+        int ex = __shfl_up_sync(full, inc, 1);
+        if (lane == 0) ex = -1;
+        ctx_ab[i0][cx] = (int16_t)ex;
+        ctx_ab[i1][cx] = (int16_t)(c0 ? lo16(L0) : ex);
+        // nearest known below each segment: "earliest known" suffix scan
+        int sinc = c0 ? lo16(F0) : (c1 ? lo16(F1) : -1);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_down_sync(full, sinc, o);
+            if (lane + o < 32 && sinc < 0) sinc = t;
+        }
+        int sx = __shfl_down_sync(full, sinc, 1);
+        if (lane == 31) sx = -1;
+        ctx_bl[i1][cx] = (int16_t)sx;
+        ctx_bl[i0][cx] = (int16_t)(c1 ? lo16(F1) : sx);
+        const int total = __reduce_add_sync(full, c0 + c1);
+        // first two knowns of the column: ordered combine of (k1, k2)
+        auto comb_first = [](int a1, int a2, int b1, int& r1, int& r2) {
+            if (a2 >= 0) { r1 = a1; r2 = a2; }
+            else if (a1 >= 0) { r1 = a1; r2 = b1; }
+            else { r1 = b1; r2 = -2; }  // -2: take b's second below
+        };
+        int k1, k2;
+        {
+            int r1, r2;
+            comb_first(lo16(F0), hi16s(F0), lo16(F1), r1, r2);
+            k1 = r1;
+            k2 = r2 == -2 ? hi16s(F1) : r2;
+        }
+        // last two: (m1 = last, m2 = second last), ordered combine, later wins
+        int m1, m2;
+        if (hi16s(L1) >= 0) { m1 = lo16(L1); m2 = hi16s(L1); }
+        else if (lo16(L1) >= 0) { m1 = lo16(L1); m2 = lo16(L0); }
+        else { m1 = lo16(L0); m2 = hi16s(L0); }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int ok1 = __shfl_down_sync(full, k1, o), ok2 = __shfl_down_sync(full, k2, o);
+            const int om1 = __shfl_down_sync(full, m1, o), om2 = __shfl_down_sync(full, m2, o);
+            if ((lane & (2 * o - 1)) == 0 && lane + o < 32) {
+                // this lane's range precedes the other's
+                if (k2 < 0) {
+                    if (k1 >= 0) k2 = ok1;
+                    else { k1 = ok1; k2 = ok2; }
                 }
-            } else {
-                for (int k = 0; k < n; ++k) {
-                    const uint32_t vk = __ldg(in2 + o + k * W2);
-                    out2[o + k * W2] = pack2(c0, c1);
-                    const int d0 = lo16(vk), d1 = hi16s(vk);
-                    seg_add(m0, d0);
-                    seg_add(m1, d1);
-                    c0 = d0 >= 0 ? d0 : c0;
-                    c1 = d1 >= 0 ? d1 : c1;
-                }
+                if (om2 >= 0) { m1 = om1; m2 = om2; }
+                else if (om1 >= 0) { m2 = m1; m1 = om1; }
             }
+        }
+        if (lane == 0) {
+            col_total[cx] = total;
+            col_top[cx] = total >= 2 ? peek_estimate(k1, k2, thr) : -1;
+            col_bot[cx] = total >= 2 ? peek_estimate(m2, m1, thr) : -1;
         }
     }
-    seg[s][2 * cp] = SegSum{m0.count, (int16_t)m0.f1, (int16_t)m0.f2, (int16_t)m0.l1, (int16_t)m0.l2};
-    seg[s][2 * cp + 1] = SegSum{m1.count, (int16_t)m1.f1, (int16_t)m1.f2, (int16_t)m1.l1, (int16_t)m1.l2};
     __syncthreads();
-    // phase 2: one thread per column scans the segments once
-    if (threadIdx.x < 2 * P4C) {
-        const int cx = threadIdx.x;
-        int total = 0, last = -1, cf1 = -1, cf2 = -1;
-        for (int i = 0; i < P4S; ++i) {
-            const SegSum g = seg[i][cx];
-            ctx_ab[i][cx] = (int16_t)last;
-            if (g.count) {
-                last = g.l1;
-                if (cf1 < 0) {
-                    cf1 = g.f1;
-                    if (g.count > 1) cf2 = g.f2;
-                } else if (cf2 < 0) {
-                    cf2 = g.f1;
-                }
-            }
-            total += g.count;
-        }
-        int first = -1, cl1 = -1, cl2 = -1;
-        for (int i = P4S - 1; i >= 0; --i) {
-            const SegSum g = seg[i][cx];
-            ctx_bl[i][cx] = (int16_t)first;
-            if (g.count) {
-                first = g.f1;
-                if (cl1 < 0) {
-                    cl1 = g.l1;
-                    if (g.count > 1) cl2 = g.l2;
-                } else if (cl2 < 0) {
-                    cl2 = g.l1;
-                }
-            }
-        }
-        col_total[cx] = total;
-        col_top[cx] = total >= 2 ? peek_estimate(cf1, cf2, thr) : -1;
-        col_bot[cx] = total >= 2 ? peek_estimate(cl2, cl1, thr) : -1;
-    }
-    __syncthreads();
-    // pass 2 (bottom-up)
+    // ---- pass 2 (top-down)
     unsigned long long known = 0;
     if (col) {
         const int t0 = col_total[2 * cp], t1 = col_total[2 * cp + 1];
         const int et0 = col_top[2 * cp], et1 = col_top[2 * cp + 1];
         const int eb0 = col_bot[2 * cp], eb1 = col_bot[2 * cp + 1];
-        const int ab0 = ctx_ab[s][2 * cp], ab1 = ctx_ab[s][2 * cp + 1];
-        int nb0 = ctx_bl[s][2 * cp], nb1 = ctx_bl[s][2 * cp + 1];
-        auto resolve = [&](int d, int a, int above, int& nb, int total, int et, int eb) {
-            const int ab = a >= 0 ? a : above;  // nearest known above
-            int r;
-            if (d >= 0) r = d;
-            else if (total == 0) r = -1;
-            else if (total == 1) r = ab >= 0 ? ab : nb;
-            else if (ab >= 0 && nb >= 0) r = peek_estimate(ab, nb, thr);
-            else r = ab < 0 ? et : eb;
-            nb = d >= 0 ? d : nb;
-            return r;
+        int a0 = ctx_ab[s][2 * cp], a1 = ctx_ab[s][2 * cp + 1];
+        const int bl0 = ctx_bl[s][2 * cp], bl1 = ctx_bl[s][2 * cp + 1];
+        const uint32_t* ip = in2 + x / 2;
+        uint32_t* op = out2 + x / 2;
+        auto row = [&](uint32_t v, uint32_t bw, size_t o) {
+            const int d0 = lo16(v), d1 = hi16s(v);
+            const int s0 = lo16(bw), s1 = hi16s(bw);
+            const int r0 = peek_resolve(d0, a0, s0 >= 0 ? s0 : bl0, t0, et0, eb0, thr);
+            const int r1 = peek_resolve(d1, a1, s1 >= 0 ? s1 : bl1, t1, et1, eb1, thr);
+            a0 = d0 >= 0 ? d0 : a0;
+            a1 = d1 >= 0 ? d1 : a1;
+            op[o] = pack2(r0, r1);
+            known += (r0 >= 0) + (r1 >= 0);
         };
-        for (int yy = yb - 1; yy >= ya; yy -= P4B) {
-            const int n = min(P4B, yy - ya + 1);
-            const size_t o = (size_t)yy * W2 + x / 2;
-            if (n == P4B) {
-                uint32_t v[P4B], a[P4B];
+        // batches: all loads of P4B rows (input and scratch) issue before the
+        // stores (the scratch loads would otherwise wait behind them)
+        int y = ya;
+        for (; y + P4B <= yb; y += P4B) {
+            uint32_t v[P4B], bw[P4B];
 #pragma unroll
-                for (int k = 0; k < P4B; ++k) {
-                    v[k] = __ldg(in2 + o - k * W2);
-                    a[k] = out2[o - k * W2];
-                }
-#pragma unroll
-                for (int k = 0; k < P4B; ++k) {
-                    const int r0 = resolve(lo16(v[k]), lo16(a[k]), ab0, nb0, t0, et0, eb0);
-                    const int r1 = resolve(hi16s(v[k]), hi16s(a[k]), ab1, nb1, t1, et1, eb1);
-                    out2[o - k * W2] = pack2(r0, r1);
-                    known += (r0 >= 0) + (r1 >= 0);
-                }
-            } else {
-                for (int k = 0; k < n; ++k) {
-                    const uint32_t vk = __ldg(in2 + o - k * W2), ak = out2[o - k * W2];
-                    const int r0 = resolve(lo16(vk), lo16(ak), ab0, nb0, t0, et0, eb0);
-                    const int r1 = resolve(hi16s(vk), hi16s(ak), ab1, nb1, t1, et1, eb1);
-                    out2[o - k * W2] = pack2(r0, r1);
-                    known += (r0 >= 0) + (r1 >= 0);
-                }
+            for (int k = 0; k < P4B; ++k) {
+                v[k] = __ldg(ip + (size_t)(y + k) * W2);
+                bw[k] = op[(size_t)(y + k) * W2];
             }
+#pragma unroll
+            for (int k = 0; k < P4B; ++k) row(v[k], bw[k], (size_t)(y + k) * W2);
         }
+        for (; y < yb; ++y) row(__ldg(ip + (size_t)y * W2), op[(size_t)y * W2], (size_t)y * W2);
     }
     for (int o = 16; o > 0; o >>= 1) known += __shfl_xor_sync(0xffffffffu, known, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = known;
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long t = 0;
-        for (int i = 0; i < P4C * P4S / 32; ++i) t += red[i];
+        for (int i = 0; i < P5C * P5S / 32; ++i) t += red[i];
         if (t) atomicAdd(&f.sc->known, t);
     }
 }
@@ -606,7 +647,7 @@ void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStrea
 void launch_peek_cols(const Frame& f, const int16_t* in, int16_t* out, int16_t*, cudaStream_t st) {
     if (f.N == 0) return;
     if (f.W % 2 == 0 && (reinterpret_cast<uintptr_t>(in) & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 3) == 0) {
-        k_peek_cols4<<<(f.W + 2 * P4C - 1) / (2 * P4C), P4C * P4S, 0, st>>>(f, in, out);
+        k_peek_cols5<<<(f.W + 2 * P5C - 1) / (2 * P5C), P5C * P5S, 0, st>>>(f, in, out);
         return;
     }
     k_peek_cols2<<<(f.W + PC - 1) / PC, PC * PS, 0, st>>>(f, in, out);
