@@ -95,88 +95,83 @@ __global__ void __launch_bounds__(kFillThreads) k_fill_rows(Frame f, const int16
     for (int x = tid; x < W; x += kFillThreads) dst[x] = row[x];
 }
 
-// K6 v2: one CTA per row, thread = 16 consecutive pixels held in registers
-// (2 x 16-byte loads / stores; W % 16 == 0, W <= 16384).  Block scans give
-// every chunk the nearest known to its left (max-scan of (x+1) << 16 | d) and
-// right (min-scan of x << 16 | d); the chunk is then filled in registers.
-__global__ void __launch_bounds__(1024) k_fill_rows16(Frame f, const int16_t* __restrict__ in,
-                                                      int16_t* __restrict__ out) {
-    __shared__ uint32_t wl[32], wf[32];
+// K6 v3 (W % 16 == 0): CTA per row, 16 pixels per thread in registers
+// (2 x 16-byte loads / stores), value-only scans: a pixel is filled iff its nearest known
+// on the left and on the right both exist and are equal, so the chunk only
+// publishes its last / first known value (-1 = none) and the block scans use
+// "latest / earliest known" operators -- no positions, no int16 arrays.
+__global__ void __launch_bounds__(1024) k_fill_rows16v(Frame f, const int16_t* __restrict__ in,
+                                                       int16_t* __restrict__ out) {
+    __shared__ int wl[32], wf[32];
+    const unsigned full = 0xffffffffu;
     const int W = f.W, y = blockIdx.x, tid = threadIdx.x;
-    const int nchunk = W / 16;
-    const bool act = tid < nchunk;
+    const bool act = tid < W / 16;
     const int x0 = tid * 16;
-    int16_t v[16];
+    uint32_t w[8];
     {
-        uint4 a = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu), b = a;
+        uint4 a = make_uint4(full, full, full, full), b = a;
         if (act) {
             const uint4* src = reinterpret_cast<const uint4*>(in + (size_t)y * W + x0);
             a = __ldcs(src);
             b = __ldcs(src + 1);
         }
-        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = (int16_t)(w[i >> 1] >> (16 * (i & 1)));
+        w[0] = a.x, w[1] = a.y, w[2] = a.z, w[3] = a.w, w[4] = b.x, w[5] = b.y, w[6] = b.z, w[7] = b.w;
     }
-    uint32_t klast = 0, kfirst = 0xffffffffu;
+    int v[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i)
-        if (v[i] >= 0) klast = ((uint32_t)(x0 + i + 1) << 16) | (uint16_t)v[i];
+    for (int i = 0; i < 8; ++i) {
+        v[2 * i] = (int)(w[i] << 16) >> 16;
+        v[2 * i + 1] = (int)w[i] >> 16;
+    }
+    int lastv = -1, firstv = -1;
 #pragma unroll
-    for (int i = 15; i >= 0; --i)
-        if (v[i] >= 0) kfirst = ((uint32_t)(x0 + i) << 16) | (uint16_t)v[i];
+    for (int i = 0; i < 16; ++i) lastv = v[i] >= 0 ? v[i] : lastv;
+#pragma unroll
+    for (int i = 15; i >= 0; --i) firstv = v[i] >= 0 ? v[i] : firstv;
     const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-    uint32_t incl_l = klast;
+    int inc = lastv;  // latest known over lanes <= lane
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, incl_l, o);
-        if (lane >= o) incl_l = max(incl_l, t);
+        const int t = __shfl_up_sync(full, inc, o);
+        if (lane >= o && inc < 0) inc = t;
     }
-    uint32_t incl_f = kfirst;
+    int sinc = firstv;  // earliest known over lanes >= lane
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_down_sync(0xffffffffu, incl_f, o);
-        if (lane + o < 32) incl_f = min(incl_f, t);
+        const int t = __shfl_down_sync(full, sinc, o);
+        if (lane + o < 32 && sinc < 0) sinc = t;
     }
-    if (lane == 31) wl[wid] = incl_l;
-    if (lane == 0) wf[wid] = incl_f;
+    if (lane == 31) wl[wid] = inc;
+    if (lane == 0) wf[wid] = sinc;
     __syncthreads();
-    uint32_t prev = __shfl_up_sync(0xffffffffu, incl_l, 1);
-    if (lane == 0) prev = 0;
-    for (int i = 0; i < wid; ++i) prev = max(prev, wl[i]);
-    uint32_t next = __shfl_down_sync(0xffffffffu, incl_f, 1);
-    if (lane == 31) next = 0xffffffffu;
-    for (int i = wid + 1; i < nw; ++i) next = min(next, wf[i]);
+    int pd = __shfl_up_sync(full, inc, 1);
+    if (lane == 0) pd = -1;
+    if (pd < 0)
+        for (int i = wid - 1; i >= 0 && pd < 0; --i) pd = wl[i];
+    int nd = __shfl_down_sync(full, sinc, 1);
+    if (lane == 31) nd = -1;
+    if (nd < 0)
+        for (int i = wid + 1; i < nw && nd < 0; ++i) nd = wf[i];
     if (!act) return;
-    // fill: a run of unknowns between knowns of equal disparity (the input
-    // snapshot, reconstruct.cpp:11-33).  Left context: pd; right: the next known
-    // inside the chunk or `next`.
-    int pd = prev ? (int)(prev & 0xffffu) : -1;
-    int nd[16];  // disparity of the nearest known at or right of i
-    {
-        int cur = next != 0xffffffffu ? (int)(next & 0xffffu) : -2;
+    // right context of each pixel: the nearest known at or right of it
+    int r[16];
 #pragma unroll
-        for (int i = 15; i >= 0; --i) {
-            if (v[i] >= 0) cur = v[i];
-            nd[i] = cur;
-        }
+    for (int i = 15; i >= 0; --i) {
+        r[i] = nd;
+        nd = v[i] >= 0 ? v[i] : nd;
     }
-    int16_t o[16];
+    uint32_t o[8];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-        if (v[i] >= 0) {
-            o[i] = v[i];
-            pd = v[i];
-        } else {
-            o[i] = (pd >= 0 && nd[i] == pd) ? (int16_t)pd : (int16_t)-1;
-        }
+        // unknown: filled iff nearest left == nearest right (both -1 -> stays -1)
+        const int val = v[i] >= 0 ? v[i] : (pd == r[i] ? pd : -1);
+        pd = v[i] >= 0 ? v[i] : pd;
+        if (i & 1) o[i >> 1] |= (uint32_t)val << 16;
+        else o[i >> 1] = (uint32_t)val & 0xffffu;
     }
-    uint32_t w[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) w[i] = (uint16_t)o[2 * i] | ((uint32_t)(uint16_t)o[2 * i + 1] << 16);
     uint4* dst = reinterpret_cast<uint4*>(out + (size_t)y * W + x0);
-    dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-    dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+    dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
 }
 
 // ------------------------------------------------------------------ K7 ----
@@ -635,7 +630,7 @@ void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStrea
     if (f.N == 0) return;
     if (f.W % 16 == 0 && f.W <= 16384) {
         const int nt = ((f.W / 16) + 31) / 32 * 32;
-        k_fill_rows16<<<f.H, nt, 0, st>>>(f, in, out);
+        k_fill_rows16v<<<f.H, nt, 0, st>>>(f, in, out);
         return;
     }
     const size_t sm = (size_t)f.W * sizeof(int16_t);
