@@ -441,12 +441,18 @@ __device__ __forceinline__ int hi16s(uint32_t v) { return (int16_t)(v >> 16); }
 constexpr int P5C = 8;   // column pairs per CTA (16 columns)
 constexpr int P5S = 64;  // row segments per column (= 2 x 32 lanes in phase 2)
 
-__device__ __forceinline__ int peek_resolve(int d, int a, int b, int total, int et, int eb, int thr) {
-    if (d >= 0) return d;
-    if (total == 0) return -1;
-    if (total == 1) return a >= 0 ? a : b;
-    if (a >= 0 && b >= 0) return peek_estimate(a, b, thr);
-    return a < 0 ? et : eb;
+// Branch-free (selects only): the cases of reconstruct.cpp:57-106 for one
+// pixel given its nearest known above (a) and below (b), -1 = none.  The
+// column's total is folded into et / eb by the caller: total == 0 -> both -1,
+// total == 1 -> a or b is the single known, so "a < 0 ? b : a" covers it.
+__device__ __forceinline__ int peek_resolve(int d, int a, int b, int single, int et, int eb, int thr) {
+    const int r = a >= b ? a - b : b - a;
+    const int est = r > thr ? min(a, b) : (a + b) >> 1;
+    const int edge = a < 0 ? et : eb;
+    const int two = (a >= 0 && b >= 0) ? est : edge;
+    const int one = a >= 0 ? a : b;
+    const int u = single ? one : two;
+    return d >= 0 ? d : u;
 }
 
 __global__ void __launch_bounds__(P5C * P5S, 2) k_peek_cols5(Frame f, const int16_t* __restrict__ in,
@@ -470,10 +476,10 @@ __global__ void __launch_bounds__(P5C * P5S, 2) k_peek_cols5(Frame f, const int1
     int n0 = 0, n1 = 0, b0 = -1, b1 = -1;
     int f10 = -1, f20 = -1, l10 = -1, l20 = -1, f11 = -1, f21 = -1, l11 = -1, l21 = -1;
     if (col) {
-        const uint32_t* ip = in2 + x / 2;
-        uint32_t* op = out2 + x / 2;
-        auto row = [&](uint32_t v, size_t o) {
-            op[o] = pack2(b0, b1);
+        const uint32_t* ip = in2 + x / 2 + (size_t)(yb - 1) * W2;
+        uint32_t* op = out2 + x / 2 + (size_t)(yb - 1) * W2;
+        auto row = [&](uint32_t v, uint32_t* dst) {
+            *dst = pack2(b0, b1);
             const int d0 = lo16(v), d1 = hi16s(v);
             if (d0 >= 0) {
                 l20 = n0 == 1 ? d0 : l20;
@@ -493,14 +499,14 @@ __global__ void __launch_bounds__(P5C * P5S, 2) k_peek_cols5(Frame f, const int1
             }
         };
         int y = yb - 1;
-        for (; y - P4B + 1 >= ya; y -= P4B) {
+        for (; y - P4B + 1 >= ya; y -= P4B, ip -= P4B * W2, op -= P4B * W2) {
             uint32_t v[P4B];
 #pragma unroll
-            for (int k = 0; k < P4B; ++k) v[k] = __ldg(ip + (size_t)(y - k) * W2);
+            for (int k = 0; k < P4B; ++k) v[k] = __ldg(ip - k * W2);
 #pragma unroll
-            for (int k = 0; k < P4B; ++k) row(v[k], (size_t)(y - k) * W2);
+            for (int k = 0; k < P4B; ++k) row(v[k], op - k * W2);
         }
-        for (; y >= ya; --y) row(__ldg(ip + (size_t)y * W2), (size_t)y * W2);
+        for (; y >= ya; --y, ip -= W2, op -= W2) row(__ldg(ip), op);
     }
     s_cnt[s][2 * cp] = n0;
     s_cnt[s][2 * cp + 1] = n1;
@@ -583,36 +589,38 @@ __global__ void __launch_bounds__(P5C * P5S, 2) k_peek_cols5(Frame f, const int1
     unsigned long long known = 0;
     if (col) {
         const int t0 = col_total[2 * cp], t1 = col_total[2 * cp + 1];
-        const int et0 = col_top[2 * cp], et1 = col_top[2 * cp + 1];
-        const int eb0 = col_bot[2 * cp], eb1 = col_bot[2 * cp + 1];
+        // total 0: every estimate is -1; total 1: the single known is a or b
+        const int sg0 = t0 == 1, sg1 = t1 == 1;
+        const int et0 = t0 ? col_top[2 * cp] : -1, et1 = t1 ? col_top[2 * cp + 1] : -1;
+        const int eb0 = t0 ? col_bot[2 * cp] : -1, eb1 = t1 ? col_bot[2 * cp + 1] : -1;
         int a0 = ctx_ab[s][2 * cp], a1 = ctx_ab[s][2 * cp + 1];
         const int bl0 = ctx_bl[s][2 * cp], bl1 = ctx_bl[s][2 * cp + 1];
-        const uint32_t* ip = in2 + x / 2;
-        uint32_t* op = out2 + x / 2;
-        auto row = [&](uint32_t v, uint32_t bw, size_t o) {
+        const uint32_t* ip = in2 + x / 2 + (size_t)ya * W2;
+        uint32_t* op = out2 + x / 2 + (size_t)ya * W2;
+        auto row = [&](uint32_t v, uint32_t bw, uint32_t* dst) {
             const int d0 = lo16(v), d1 = hi16s(v);
             const int s0 = lo16(bw), s1 = hi16s(bw);
-            const int r0 = peek_resolve(d0, a0, s0 >= 0 ? s0 : bl0, t0, et0, eb0, thr);
-            const int r1 = peek_resolve(d1, a1, s1 >= 0 ? s1 : bl1, t1, et1, eb1, thr);
+            const int r0 = peek_resolve(d0, a0, s0 >= 0 ? s0 : bl0, sg0, et0, eb0, thr);
+            const int r1 = peek_resolve(d1, a1, s1 >= 0 ? s1 : bl1, sg1, et1, eb1, thr);
             a0 = d0 >= 0 ? d0 : a0;
             a1 = d1 >= 0 ? d1 : a1;
-            op[o] = pack2(r0, r1);
+            *dst = pack2(r0, r1);
             known += (r0 >= 0) + (r1 >= 0);
         };
         // batches: all loads of P4B rows (input and scratch) issue before the
         // stores (the scratch loads would otherwise wait behind them)
         int y = ya;
-        for (; y + P4B <= yb; y += P4B) {
+        for (; y + P4B <= yb; y += P4B, ip += P4B * W2, op += P4B * W2) {
             uint32_t v[P4B], bw[P4B];
 #pragma unroll
             for (int k = 0; k < P4B; ++k) {
-                v[k] = __ldg(ip + (size_t)(y + k) * W2);
-                bw[k] = op[(size_t)(y + k) * W2];
+                v[k] = __ldg(ip + k * W2);
+                bw[k] = op[k * W2];
             }
 #pragma unroll
-            for (int k = 0; k < P4B; ++k) row(v[k], bw[k], (size_t)(y + k) * W2);
+            for (int k = 0; k < P4B; ++k) row(v[k], bw[k], op + k * W2);
         }
-        for (; y < yb; ++y) row(__ldg(ip + (size_t)y * W2), op[(size_t)y * W2], (size_t)y * W2);
+        for (; y < yb; ++y, ip += W2, op += W2) row(__ldg(ip), *op, op);
     }
     for (int o = 16; o > 0; o >>= 1) known += __shfl_xor_sync(0xffffffffu, known, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = known;
