@@ -637,58 +637,67 @@ __global__ void __launch_bounds__(V3Geom<K>::NT) k_blur_v3(Frame f, BlurParams b
 #pragma unroll
     for (int k = 0; k <= K; ++k) wp[k] = wpair[k];
     __syncthreads();
-    // ---- horizontal: item = (row, 4 outputs q4..q4+3); output pairs (0,1),
-    // (2,3) with the input value broadcast, taps in the reference's order
-    for (int it = tid; it < BY * (BX / 4); it += NT) {
-        const int oy = it / (BX / 4), q4 = (it % (BX / 4)) * 4;
-        if (oy >= ny || q4 >= nx) continue;
-        uint32_t z[12];  // byte 3*o + c: output o, channel c
+    // ---- horizontal: item = (row, 8 outputs q8..q8+7); output pairs (0,1),
+    // (2,3), (4,5), (6,7) with the input value broadcast (one row window of
+    // K + 7 floats serves all eight), taps in the reference's order
+    constexpr int IW = 8, NV = K + IW - 1;
+    for (int it = tid; it < BY * (BX / IW); it += NT) {
+        const int oy = it / (BX / IW), q8 = (it % (BX / IW)) * IW;
+        if (oy >= ny || q8 >= nx) continue;
+        uint32_t z[3 * IW];  // byte 3*o + c: output o, channel c
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const float* row = vp + ((size_t)c * BY + oy) * NCP + q4;
-            float v[K + 3 + 1];
+            const float* row = vp + ((size_t)c * BY + oy) * NCP + q8;
+            float v[(NV + 3) / 4 * 4];
 #pragma unroll
-            for (int i = 0; i < (K + 3 + 3) / 4; ++i) {
+            for (int i = 0; i < (NV + 3) / 4; ++i) {
                 const float4 t4 = reinterpret_cast<const float4*>(row)[i];
                 v[4 * i] = t4.x;
-                if (4 * i + 1 < K + 4) v[4 * i + 1] = t4.y;
-                if (4 * i + 2 < K + 4) v[4 * i + 2] = t4.z;
-                if (4 * i + 3 < K + 4) v[4 * i + 3] = t4.w;
+                v[4 * i + 1] = t4.y;
+                v[4 * i + 2] = t4.z;
+                v[4 * i + 3] = t4.w;
             }
-            unsigned long long a01 = 0ull, a23 = 0ull;
+            unsigned long long a[IW / 2] = {};
 #pragma unroll
-            for (int p = 0; p < K + 3; ++p) {
-                const unsigned long long vv = f2pack(v[p], v[p]);
-                if (p <= K) a01 = ffma2(vv, wp[p], a01);
-                if (p >= 2) a23 = ffma2(vv, wp[p - 2], a23);
+            for (int q = 0; q < NV; ++q) {
+                const unsigned long long vv = f2pack(v[q], v[q]);
+#pragma unroll
+                for (int j = 0; j < IW / 2; ++j)
+                    if (q >= 2 * j && q <= 2 * j + K) a[j] = ffma2(vv, wp[q - 2 * j], a[j]);
             }
             // floor(x + 0.5) in the low mantissa byte: (x + 0.5) + 2^23 rounded down
             // (x in [0, 255 (1 + eps)]: non-negative normalised weights, 8-bit inputs)
-            const unsigned long long q01 = fadd2_rm(fadd2(a01, kHalf2), kMagic2);
-            const unsigned long long q23 = fadd2_rm(fadd2(a23, kHalf2), kMagic2);
-            z[c] = (uint32_t)q01;
-            z[3 + c] = (uint32_t)(q01 >> 32);
-            z[6 + c] = (uint32_t)q23;
-            z[9 + c] = (uint32_t)(q23 >> 32);
+#pragma unroll
+            for (int j = 0; j < IW / 2; ++j) {
+                const unsigned long long qq = fadd2_rm(fadd2(a[j], kHalf2), kMagic2);
+                z[6 * j + c] = (uint32_t)qq;
+                z[6 * j + 3 + c] = (uint32_t)(qq >> 32);
+            }
         }
-        uint32_t ob[3];
 #pragma unroll
-        for (int k = 0; k < 3; ++k)
-            ob[k] = __byte_perm(__byte_perm(z[4 * k], z[4 * k + 1], 0x0040), __byte_perm(z[4 * k + 2], z[4 * k + 3], 0x0040),
-                                0x5410);
-        // sharp pixels keep their input bytes
-        const uint32_t m = *reinterpret_cast<const uint32_t*>(shf + oy * BX + q4) * 0xffu;
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(stage + (size_t)(oy + h) * ROWB + G::LB + 3 * q4);
-        const uint32_t mw[3] = {__byte_perm(m, 0, 0x1000), __byte_perm(m, 0, 0x2211), __byte_perm(m, 0, 0x3332)};
+        for (int hh = 0; hh < 2; ++hh) {  // two groups of 4 outputs = 12 bytes each
+            const int q4 = q8 + 4 * hh;
+            if (q4 >= nx) break;
+            const uint32_t* zz = z + 12 * hh;
+            uint32_t ob[3];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) ob[k] = (ob[k] & ~mw[k]) | (src[k] & mw[k]);
-        uint8_t* dst = out + ((size_t)(y0 + oy) * W + x0 + q4) * 3;
-        if (q4 + 4 <= nx && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
-            reinterpret_cast<uint32_t*>(dst)[0] = ob[0];
-            reinterpret_cast<uint32_t*>(dst)[1] = ob[1];
-            reinterpret_cast<uint32_t*>(dst)[2] = ob[2];
-        } else {
-            for (int bi = 0; bi < 3 * min(4, nx - q4); ++bi) dst[bi] = (uint8_t)(ob[bi >> 2] >> (8 * (bi & 3)));
+            for (int k = 0; k < 3; ++k)
+                ob[k] = __byte_perm(__byte_perm(zz[4 * k], zz[4 * k + 1], 0x0040),
+                                    __byte_perm(zz[4 * k + 2], zz[4 * k + 3], 0x0040), 0x5410);
+            // sharp pixels keep their input bytes
+            const uint32_t m = *reinterpret_cast<const uint32_t*>(shf + oy * BX + q4) * 0xffu;
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(stage + (size_t)(oy + h) * ROWB + G::LB + 3 * q4);
+            const uint32_t mw[3] = {__byte_perm(m, 0, 0x1000), __byte_perm(m, 0, 0x2211), __byte_perm(m, 0, 0x3332)};
+#pragma unroll
+            for (int k = 0; k < 3; ++k) ob[k] = (ob[k] & ~mw[k]) | (src[k] & mw[k]);
+            uint8_t* dst = out + ((size_t)(y0 + oy) * W + x0 + q4) * 3;
+            if (q4 + 4 <= nx && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
+                reinterpret_cast<uint32_t*>(dst)[0] = ob[0];
+                reinterpret_cast<uint32_t*>(dst)[1] = ob[1];
+                reinterpret_cast<uint32_t*>(dst)[2] = ob[2];
+            } else {
+                for (int bi = 0; bi < 3 * min(4, nx - q4); ++bi) dst[bi] = (uint8_t)(ob[bi >> 2] >> (8 * (bi & 3)));
+            }
         }
     }
 }
