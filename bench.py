@@ -199,6 +199,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    all_cpus = os.sched_getaffinity(0)
+    affinity = _pin_near_gpu(torch, local)  # host thread near the GPU's PCIe root
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -436,9 +438,11 @@ def main():
         "roofline_frame": roofline_frame,
         "roofline_stages": stages,
         "sad_ops_per_frame": int(sad_ops),
+        "host_affinity": affinity,
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        os.sched_setaffinity(0, all_cpus)  # the CPU baseline gets every host core
         fps, cores, kind, sample, _ = cpu_reference(args.config, args.cpu_sample_s, warmup=0,
                                                     pool=args.pool)
         line["cpu_baseline"] = {"value": fps, "unit": "frames/s", "cores": cores, "kind": kind,
@@ -456,6 +460,29 @@ def main():
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def _pin_near_gpu(torch, local):
+    """Best effort: bind this rank to the CPUs of the NUMA node the GPU hangs
+    off (its PCIe root), before any pinned host buffer is touched, so staging
+    memory is node-local.  Returns a description for the JSON line."""
+    try:
+        p = torch.cuda.get_device_properties(local)
+        bus = "%04x:%02x:%02x.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+        base = "/sys/bus/pci/devices/" + bus
+        node = int(open(base + "/numa_node").read().strip())
+        cpus_txt = open(base + "/local_cpulist").read().strip()
+        cpus = set()
+        for part in cpus_txt.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if cpus and len(cpus) < os.cpu_count():
+            os.sched_setaffinity(0, cpus)
+            return {"gpu_pci": bus, "numa_node": node, "cpus": cpus_txt}
+        return {"gpu_pci": bus, "numa_node": node, "cpus": "all (single node)"}
+    except (OSError, ValueError, AttributeError):
+        return None
 
 
 def _cpu_model():
