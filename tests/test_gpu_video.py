@@ -97,3 +97,23 @@ def test_video_cli(stk, frames_dir, tmp_path):
     cfg, focus = _cfg(stk)
     l, rr = pairs[5]
     assert np.array_equal(stk.load_image(out / "f005.ppm"), stk.run_refocus_pipeline(l, rr, cfg, focus))
+
+
+def test_video_cli_png_and_disparity(stk, frames_dir, tmp_path, port):
+    """`stereotk video --png 1 --disparity-scale 2`: PNG outputs equal the
+    pipeline, the disparity files decode to its dense maps."""
+    d, pairs = frames_dir
+    cli = os.path.join(ROOT, "paper_2001_07809_b200", "stereotk")
+    out = tmp_path / "cli_png"
+    r = subprocess.run([cli, "video", str(d), "--out-dir", str(out), "--focus", "8:16", "--k", "4",
+                        "--window", "9", "--max-disparity", str(D), "--png", "1", "--disparity-scale", "2",
+                        "--decode-threads", "3", "--write-threads", "3"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    cfg, focus = _cfg(stk)
+    for f in (0, 6):
+        l, rr = pairs[f]
+        depth = []
+        want = stk.run_refocus_pipeline(l, rr, cfg, focus, depth_out=depth)
+        assert np.array_equal(stk.load_image(out / f"f{f:03d}.png"), want)
+        assert np.array_equal(stk.load_disparity(out / f"f{f:03d}_disp.pgm"), depth[0].dense)

@@ -440,3 +440,29 @@ def test_cpp_dropin_file_io(tmp_path):
                     f"-Wl,-rpath,{lib}", "-o", exe], check=True)
     r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_png_rgb16_trns_and_palette_alpha(stk, tmp_path):
+    """16-bit RGB with an sRGB chunk scales exactly; an RGB tRNS key colour
+    and palette alpha 0 composite to black; opaque palette entries stay exact."""
+    rng = np.random.default_rng(23)
+    rgb16 = rng.integers(0, 65536, (4, 6, 3))
+    p = tmp_path / "rgb16.png"
+    p.write_bytes(_encode_png(rgb16, 2, 16, False, _png_chunk(b"sRGB", b"\x00")))
+    assert np.array_equal(stk.load_image(p), ((rgb16 * 255 + 32895) >> 16).astype(np.uint8))
+    rgb8 = rng.integers(0, 256, (5, 5, 3))
+    rgb8[2, 3] = (10, 20, 30)
+    trns = _png_chunk(b"tRNS", struct.pack(">HHH", 10, 20, 30))
+    p = tmp_path / "rgb_trns.png"
+    p.write_bytes(_encode_png(rgb8, 2, 8, True, trns))
+    want = rgb8.astype(np.uint8).copy()
+    want[(rgb8 == (10, 20, 30)).all(-1)] = 0
+    assert np.array_equal(stk.load_image(p), want)
+    pal = np.array([[1, 2, 3], [200, 100, 50], [9, 9, 9]], np.uint8)
+    idx = rng.integers(0, 3, (4, 7, 1))
+    extra = _png_chunk(b"PLTE", pal.tobytes()) + _png_chunk(b"tRNS", bytes([255, 0]))
+    p = tmp_path / "pal_alpha.png"
+    p.write_bytes(_encode_png(idx, 3, 8, False, extra))
+    want = pal[idx[..., 0]].copy()
+    want[idx[..., 0] == 1] = 0
+    assert np.array_equal(stk.load_image(p), want)
