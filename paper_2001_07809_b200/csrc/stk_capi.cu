@@ -501,8 +501,7 @@ int enqueue_kernels(stk_ctx* ctx, Slot& s, const Frame& f, const BlurParams* bp,
     cudaMemsetAsync(f.sc, 0, sizeof(DevScalars), st);
     cudaMemsetAsync(f.lb, 0, sizeof(unsigned long long) * LB_COUNT * f.lb_stride, st);
     rec(0);
-    launch_lightness(f, ctx->d_tab, true, true, true, st, ctx->d_lut);  // left (+histogram), right
-    n += 2;
+    n += launch_lightness(f, ctx->d_tab, true, true, true, st, ctx->d_lut);  // left (+histogram), right
     rec(1);
     launch_kmeans(f, 0, 100, 0.5, st);
     ++n;

@@ -119,8 +119,9 @@ constexpr int kLstarBuckets = 4096;
 // ---------------------------------------------------------------- launchers --
 // Every launcher enqueues on `st` and never synchronises.  Implementations in
 // k_*.cu.
-void launch_lightness(const Frame& f, const LstarTables* dtab, bool left, bool right,
-                      bool hist, cudaStream_t st, const uint8_t* lut = nullptr);
+// returns the number of kernels launched
+int launch_lightness(const Frame& f, const LstarTables* dtab, bool left, bool right,
+                     bool hist, cudaStream_t st, const uint8_t* lut = nullptr);
 // the exact 2^24-entry L* table (lut[r << 16 | g << 8 | b]) used by the frame path
 void build_lstar_lut(const LstarTables* dtab, uint8_t* lut, cudaStream_t st);
 void launch_histogram(const Frame& f, const uint8_t* gray, cudaStream_t st);
