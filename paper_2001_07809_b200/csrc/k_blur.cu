@@ -254,186 +254,6 @@ __global__ void __launch_bounds__(kThreads) k_blur_sep_k(Frame f, BlurParams bp,
     }
 }
 
-// v2 (default separable path): 128 x 32 output tile, 256 threads.
-//  stage   interior tiles: aligned 16-byte loads of each input row's byte run
-//          (replicate-clamped copy for edge tiles); the tile's blur decisions
-//          from the dense disparity and the per-disparity focus LUT;
-//  horiz   thread = (staged row, 4 outputs): 3 float planes in shared memory;
-//  vert    thread = (column, 16 output rows), taps slide in registers;
-//  output  sharp pixels keep their input bytes; the tile leaves through
-//          shared memory as coalesced 16-byte stores.
-constexpr int V2X = 128, V2Y = 32;
-
-template <int K>
-struct V2Geom {
-    static constexpr int h = K / 2;
-    static constexpr int IH = V2Y + 2 * h;
-    static constexpr int LB = (3 * h + 15) / 16 * 16;  // interior rows load from byte 3*x0 - LB
-    static constexpr int ROWB = ((3 * (V2X + 2 * h) + LB + 15) & ~15) + 16;  // staged row bytes
-    static constexpr int XOFF = LB - 3 * h;  // smem byte of input column x0 - h
-    static constexpr size_t SM_STAGE = (size_t)IH * ROWB;
-    static constexpr size_t SM_H = (size_t)3 * IH * V2X * sizeof(float);
-    static constexpr size_t SM_OUT = (size_t)V2Y * 3 * V2X;
-    static constexpr size_t SM = SM_STAGE + SM_H + SM_OUT + (size_t)V2X * V2Y + 16;
-};
-
-template <int K>
-__global__ void __launch_bounds__(kThreads) k_blur_v2(Frame f, BlurParams bp,
-                                                      const uint8_t* __restrict__ in,
-                                                      uint8_t* __restrict__ out,
-                                                      const int16_t* __restrict__ depth) {
-    using G = V2Geom<K>;
-    constexpr int h = G::h, IH = G::IH, ROWB = G::ROWB, XOFF = G::XOFF;
-    extern __shared__ __align__(16) unsigned char smem[];
-    uint8_t* stage = smem;
-    float* hs = reinterpret_cast<float*>(smem + G::SM_STAGE);      // [3][IH][V2X]
-    uint8_t* otile = smem + G::SM_STAGE + G::SM_H;                  // [V2Y][3*V2X]
-    uint8_t* shf = otile + G::SM_OUT;                               // [V2Y][V2X] sharp flags
-    __shared__ uint8_t lut[1024];
-    const int W = f.W, H = f.H, tid = threadIdx.x;
-    const int x0 = blockIdx.x * V2X, y0 = blockIdx.y * V2Y;
-    const int nx = min(V2X, W - x0), ny = min(V2Y, H - y0);
-    for (int i = tid; i < bp.lut_len && i < 1024; i += kThreads) lut[i] = bp.sharp_lut[i];
-    __syncthreads();
-    {
-        int any = 0;
-        for (int i = tid; i < V2X * V2Y; i += kThreads) {
-            const int ox = i % V2X, oy = i / V2X;
-            uint8_t sh = 1;
-            if (ox < nx && oy < ny) {
-                const int d = depth[(size_t)(y0 + oy) * W + x0 + ox];
-                sh = d >= 0 && d < bp.lut_len && lut[d];
-                any |= !sh;
-            }
-            shf[i] = sh;
-        }
-        if (__syncthreads_or(any) == 0) {
-            // every pixel sharp: copy the tile
-            for (int r = tid / 32; r < ny; r += kThreads / 32) {
-                const uint8_t* src = in + ((size_t)(y0 + r) * W + x0) * 3;
-                uint8_t* dst = out + ((size_t)(y0 + r) * W + x0) * 3;
-                for (int b = tid % 32; b < 3 * nx; b += 32) dst[b] = src[b];
-            }
-            return;
-        }
-    }
-    // ---- stage rows y0-h .. y0+V2Y+h-1 (clamped), columns x0-h .. x0+V2X+h-1;
-    // input column x0 - h sits at smem byte XOFF of every staged row
-    // interior: the 16-byte run [3(x0) - LB, ...) lies inside the row and the image
-    const bool interior = 3 * x0 - G::LB >= 0 && x0 + V2X + h <= W && y0 - h >= 0 &&
-                          y0 + V2Y + h <= H && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
-                          (W * 3) % 16 == 0 &&
-                          3 * (x0 + V2X + h) + 16 <= 3 * W;  // last uint4 stays in the row
-    if (interior) {
-        constexpr int NV = (3 * (V2X + 2 * h) + G::LB + 15) / 16;  // uint4 per row
-        for (int i = tid; i < IH * NV; i += kThreads) {
-            const int r = i / NV, v = i % NV;
-            const uint4* src = reinterpret_cast<const uint4*>(in + ((size_t)(y0 - h + r) * W + x0) * 3 - G::LB);
-            *reinterpret_cast<uint4*>(stage + (size_t)r * ROWB + 16 * v) = __ldg(src + v);
-        }
-    } else {
-        for (int i = tid; i < IH * (V2X + 2 * h); i += kThreads) {
-            const int r = i / (V2X + 2 * h), c = i % (V2X + 2 * h);
-            const int sy = min(max(y0 - h + r, 0), H - 1), sx = min(max(x0 - h + c, 0), W - 1);
-            const uint8_t* p = in + ((size_t)sy * W + sx) * 3;
-            uint8_t* q = stage + (size_t)r * ROWB + XOFF + 3 * c;
-            q[0] = p[0];
-            q[1] = p[1];
-            q[2] = p[2];
-        }
-    }
-    __syncthreads();
-    float wk[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) wk[i] = __ldg(bp.g1 + i);
-    // ---- horizontal: item = (staged row, 4 outputs); bytes from aligned words
-    constexpr int SH = XOFF & 3;           // byte misalignment (3 * q4 % 4 == 0)
-    constexpr int NB = 3 * (K + 3);        // bytes of the 4 outputs' taps
-    constexpr int NWD = (SH + NB + 3) / 4;
-    for (int it = tid; it < IH * (V2X / 4); it += kThreads) {
-        const int r = it / (V2X / 4), q4 = (it % (V2X / 4)) * 4;
-        const uint32_t* wr = reinterpret_cast<const uint32_t*>(stage + (size_t)r * ROWB + ((XOFF + 3 * q4) & ~3));
-        uint32_t wv[NWD];
-#pragma unroll
-        for (int i = 0; i < NWD; ++i) wv[i] = wr[i];
-        float a[4][3];
-#pragma unroll
-        for (int o = 0; o < 4; ++o) a[o][0] = a[o][1] = a[o][2] = 0.f;
-#pragma unroll
-        for (int p = 0; p < K + 3; ++p) {
-            float v[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const int bi = SH + 3 * p + c;
-                v[c] = byte_f(wv[bi >> 2], bi & 3);
-            }
-#pragma unroll
-            for (int o = 0; o < 4; ++o) {
-                if (p - o >= 0 && p - o < K) {
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) a[o][c] = fmaf(wk[p - o], v[c], a[o][c]);
-                }
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-            *reinterpret_cast<float4*>(hs + ((size_t)c * IH + r) * V2X + q4) =
-                make_float4(a[0][c], a[1][c], a[2][c], a[3][c]);
-    }
-    __syncthreads();
-    // ---- vertical: thread = (column, 16 rows)
-    {
-        const int ox = tid % V2X, oy0 = (tid / V2X) * 16;
-        float a[16][3];
-#pragma unroll
-        for (int o = 0; o < 16; ++o) a[o][0] = a[o][1] = a[o][2] = 0.f;
-#pragma unroll
-        for (int r = 0; r < 16 + K - 1; ++r) {
-            const float v0 = hs[((size_t)0 * IH + oy0 + r) * V2X + ox];
-            const float v1 = hs[((size_t)1 * IH + oy0 + r) * V2X + ox];
-            const float v2 = hs[((size_t)2 * IH + oy0 + r) * V2X + ox];
-#pragma unroll
-            for (int o = 0; o < 16; ++o) {
-                if (r - o >= 0 && r - o < K) {
-                    a[o][0] = fmaf(wk[r - o], v0, a[o][0]);
-                    a[o][1] = fmaf(wk[r - o], v1, a[o][1]);
-                    a[o][2] = fmaf(wk[r - o], v2, a[o][2]);
-                }
-            }
-        }
-#pragma unroll
-        for (int o = 0; o < 16; ++o) {
-            const int oy = oy0 + o;
-            uint8_t* dst = otile + (size_t)oy * 3 * V2X + 3 * ox;
-            if (shf[oy * V2X + ox]) {
-                const uint8_t* t = stage + (size_t)(oy + h) * ROWB + XOFF + 3 * (ox + h);
-                dst[0] = t[0];
-                dst[1] = t[1];
-                dst[2] = t[2];
-            } else {
-                dst[0] = (uint8_t)min(max((int)floorf(a[o][0] + 0.5f), 0), 255);
-                dst[1] = (uint8_t)min(max((int)floorf(a[o][1] + 0.5f), 0), 255);
-                dst[2] = (uint8_t)min(max((int)floorf(a[o][2] + 0.5f), 0), 255);
-            }
-        }
-    }
-    __syncthreads();
-    // ---- output rows
-    if (nx == V2X && (W * 3) % 16 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
-        constexpr int NV = 3 * V2X / 16;  // 24 uint4 per row
-        for (int i = tid; i < ny * NV; i += kThreads) {
-            const int r = i / NV, v = i % NV;
-            reinterpret_cast<uint4*>(out + ((size_t)(y0 + r) * W + x0) * 3)[v] =
-                reinterpret_cast<const uint4*>(otile + (size_t)r * 3 * V2X)[v];
-        }
-    } else {
-        for (int i = tid; i < ny * 3 * V2X; i += kThreads) {
-            const int r = i / (3 * V2X), b = i % (3 * V2X);
-            if (b < 3 * nx) out[((size_t)(y0 + r) * W + x0) * 3 + b] = otile[(size_t)r * 3 * V2X + b];
-        }
-    }
-}
-
 // v3 (default separable path): vertical pass first, in registers.
 // Tile = 128 x 16 outputs; thread t < NC = 128 + 2h owns input column
 // x0 - h + t and walks the tile's 16 + 2h staged rows once: every converted

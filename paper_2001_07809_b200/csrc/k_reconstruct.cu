@@ -185,114 +185,6 @@ struct SegSum {
     int16_t l1, l2;  // last known, second last, -1 if absent
 };
 
-__global__ void __launch_bounds__(PC * PS) k_peek_cols(Frame f, const int16_t* __restrict__ in,
-                                                       int16_t* __restrict__ out) {
-    __shared__ SegSum seg[PS][PC];
-    __shared__ unsigned long long red[PS];
-    const int W = f.W, H = f.H, thr = f.thr;
-    const int cx = threadIdx.x % PC, s = threadIdx.x / PC;
-    const int x = blockIdx.x * PC + cx;
-    const int sr = (H + PS - 1) / PS;
-    const int ya = min(H, s * sr), yb = min(H, ya + sr);
-    const bool col = x < W;
-    // phase 1
-    SegSum m{0, -1, -1, -1, -1};
-    if (col)
-        for (int yy = ya; yy < yb; yy += PB) {
-            int16_t v[PB];
-#pragma unroll
-            for (int k = 0; k < PB; ++k) v[k] = yy + k < yb ? __ldg(in + (size_t)(yy + k) * W + x) : -1;
-#pragma unroll
-            for (int k = 0; k < PB; ++k) {
-                const int16_t d = v[k];
-                if (d >= 0) {
-                    if (m.count == 0) m.f1 = d;
-                    else if (m.count == 1) m.f2 = d;
-                    m.l2 = m.l1;
-                    m.l1 = d;
-                    ++m.count;
-                }
-            }
-        }
-    seg[s][cx] = m;
-    __syncthreads();
-    // phase 2
-    int total = 0;
-    for (int i = 0; i < PS; ++i) total += seg[i][cx].count;
-    int above = -1, below = -1;
-    for (int i = s - 1; i >= 0 && above < 0; --i)
-        if (seg[i][cx].count) above = seg[i][cx].l1;
-    for (int i = s + 1; i < PS && below < 0; ++i)
-        if (seg[i][cx].count) below = seg[i][cx].f1;
-    int cf1 = -1, cf2 = -1, cl1 = -1, cl2 = -1;  // column first two / last two
-    for (int i = 0; i < PS && cf2 < 0; ++i) {
-        const SegSum& g = seg[i][cx];
-        if (!g.count) continue;
-        if (cf1 < 0) {
-            cf1 = g.f1;
-            if (g.count > 1) cf2 = g.f2;
-        } else {
-            cf2 = g.f1;
-        }
-    }
-    for (int i = PS - 1; i >= 0 && cl2 < 0; --i) {
-        const SegSum& g = seg[i][cx];
-        if (!g.count) continue;
-        if (cl1 < 0) {
-            cl1 = g.l1;
-            if (g.count > 1) cl2 = g.l2;
-        } else {
-            cl2 = g.l1;
-        }
-    }
-    // phase 3
-    unsigned long long known = 0;
-    if (col) {
-        int cur = above;  // nearest known above the current run
-        int rs = -1;      // first row of the pending run of unknowns
-        auto resolve = [&](int nb, int y_end) {  // nb: nearest known below the run
-            int16_t v;
-            if (total == 0) v = -1;
-            else if (total == 1) v = (int16_t)(cur >= 0 ? cur : nb);
-            else if (cur >= 0 && nb >= 0) v = peek_estimate(cur, nb, thr);
-            else if (cur < 0) v = peek_estimate(cf1, cf2, thr);
-            else v = peek_estimate(cl2, cl1, thr);
-            for (int q = rs; q < y_end; ++q) out[(size_t)q * W + x] = v;
-            if (v >= 0) known += (unsigned long long)(y_end - rs);
-            rs = -1;
-        };
-        for (int yy = ya; yy < yb; yy += PB) {
-            int16_t v[PB];
-#pragma unroll
-            for (int k = 0; k < PB; ++k) v[k] = yy + k < yb ? __ldg(in + (size_t)(yy + k) * W + x) : -1;
-#pragma unroll
-            for (int k = 0; k < PB; ++k) {
-                const int y = yy + k;
-                if (y >= yb) break;
-                const int16_t d = v[k];
-                if (d < 0) {
-                    if (rs < 0) rs = y;
-                    continue;
-                }
-                if (rs >= 0) resolve(d, y);
-                out[(size_t)y * W + x] = d;
-                ++known;
-                cur = d;
-            }
-        }
-        if (rs >= 0) resolve(below, yb);
-    }
-    // known count for DepthStats::known_fraction
-    for (int o = 16; o > 0; o >>= 1) known += __shfl_xor_sync(0xffffffffu, known, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = known;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long t = 0;
-        for (int i = 0; i < PC * PS / 32; ++i) t += red[i];
-        if (t) atomicAdd(&f.sc->known, t);
-    }
-}
-
 // K7 v2: the same segments, branch-free.  Pass 1 (top-down) builds the
 // segment summary and stores, per pixel, the nearest known above it inside the
 // segment (or -1) into `out` as scratch; after the cross-segment context
