@@ -1,19 +1,19 @@
 // K8 blur_sep -- depth-range-masked Gaussian blur of the left view
 // (reference: refocus.cpp:45-113, pipeline.cpp:141-146).
 //
-// A CTA owns a 64x32 output tile.  The RGB tile plus a kernel-half-width halo
-// is staged in shared memory with the reference's replicate-border rule coded
+// A CTA owns an output tile; the RGB tile plus a kernel-half-width halo is
+// staged in shared memory with the reference's replicate-border rule coded
 // explicitly (clamped source coordinates, refocus.cpp:97-99).  The blur
 // decision is fused: a pixel stays sharp iff its dense disparity is known and
 // inside a focus range (refocus.cpp:45-73, as a per-disparity LUT), so the
 // blur map never exists in HBM.  Tiles with no blurred pixel just copy.
 //
-//   default : separable FP32, register-blocked: a thread computes 4
-//             horizontally adjacent outputs of one staged row (16+2h bytes
-//             per channel converted once with the 2^23 magic-number trick),
-//             then 4 vertically adjacent outputs of one column from float4
-//             shared rows -- within 1 LSB of the reference's 2-D FP64 sum
-//             (tests bound it);
+//   k_blur_v3 (default, kernel sizes 3..25): separable FP32, 128 x 16 tiles,
+//             vertical pass first in registers (FFMA2 over column pairs),
+//             horizontal pass over 8-output items (FFMA2 over output pairs)
+//             -- within 1 LSB of the reference's 2-D FP64 sum (tests bound
+//             it); k_blur_sep_k / k_blur_sep: the same separable rule for
+//             other sizes and for an explicit blur map;
 //   exact   : 2-D FP64 in the reference's i-outer / j-inner order with
 //             __dmul_rn/__dadd_rn and lround -- bit-identical.
 #include "stk_device.cuh"

@@ -2,16 +2,16 @@
 // (reference: reconstruct.cpp:11-109, the paper's Algorithms 1 and 2).
 //
 // K6: one CTA per row; every thread owns a contiguous chunk (16 pixels in
-//     registers when W % 16 == 0, else a shared-memory row), and two block
-//     scans give each chunk the nearest known (x, d) on either side.  A run of
-//     unknowns between consecutive knowns of equal disparity is filled; knowns
-//     never change (reconstruct.cpp:11-33).
-// K7: one CTA per 16 columns x 64 row segments (a warp = 16 columns x 2
-//     segments: 32-byte row accesses).  Phase 1 summarises each
-//     segment (known count, first/last known); phase 2 derives, per segment,
-//     the nearest known above/below and, per column, the first two / last two
-//     knowns; phase 3 walks the segment again and resolves each run of
-//     unknowns with peek_estimate (reconstruct.cpp:40-46) on the snapshot:
+//     registers when W % 16 == 0, else a shared-memory row), and block scans
+//     give each chunk the nearest known on either side.  A run of unknowns
+//     between consecutive knowns of equal disparity is filled; knowns never
+//     change (reconstruct.cpp:11-33).
+// K7: one CTA per 16 columns x 64 row segments.  One pass summarises each
+//     segment (known count, first two / last two knowns); warp-level scans
+//     derive, per segment, the nearest known above/below and, per column,
+//     the first two / last two knowns; a second pass walks the segment again
+//     and resolves each unknown with peek_estimate (reconstruct.cpp:40-46)
+//     on the snapshot:
 //       0 knowns -> stays unknown, 1 known -> copy,
 //       above & below -> est(above, below),
 //       nothing above -> est(first two), nothing below -> est(last two).
