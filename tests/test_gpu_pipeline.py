@@ -243,10 +243,12 @@ def test_frame_lightness_all_2pow24_triples(dev, stk, port):
     eq(res.right_lightness, want[::-1], "right_lightness")
 
 
-def test_pipeline_8k_config_e(dev, stk, synth):
+def test_pipeline_8k_config_e(dev, stk, synth, port):
     """Config E (7680x4320, D=256, w=31, K=8, sigma=8 -> 49-tap blur): the
     warp-specialised SAD (G=5 lanes per column group for w=31) equals the
-    list kernel on every pixel; reconstruction and blur invariants hold."""
+    list kernel on every pixel; every O(N) stage equals the oracle exactly on
+    the GPU's own inputs (L*, fused histogram -> K-Means, detect, refine,
+    anchors, fill, peek); reconstruction and blur invariants hold."""
     W, H, D, win, K = 7680, 4320, 256, 31, 8
     l, r = synth.dead_leaves(W, H, D, frame=0)
     dev.set_sad_kernel("ws")
@@ -256,6 +258,15 @@ def test_pipeline_8k_config_e(dev, stk, synth):
     dev.set_sad_kernel("auto")
     eq(a.sparse, b.sparse, "ws vs list")
     assert 0.1 < a.stats.matched_fraction < 0.3
+    eq(a.left_lightness, port.lightness(l), "L* (8K)")
+    c, _, it = port.kmeans(port.histogram(a.left_lightness), K)
+    assert (a.clustering.centers == c).all() and a.clustering.iterations_run == it
+    eq(a.boundary_raw, port.detect(a.labels), "detect (8K)")
+    refined = port.prune(port.remove(port.fill(a.boundary_raw)), 0.04)
+    eq(a.boundary_refined, refined, "refine (8K)")
+    eq(a.boundary_anchored, port.anchors(refined, win // 2), "anchors (8K)")
+    eq(a.row_filled, port.fill_scanlines(a.sparse), "fill (8K)")
+    eq(a.dense, port.peek_columns(a.row_filled, 1), "peek (8K)")
     k = a.sparse >= 0
     assert (a.row_filled[k] == a.sparse[k]).all()
     k = a.row_filled >= 0
