@@ -615,6 +615,7 @@ void launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, ui
                 STK_BLUR_V3(13)
                 STK_BLUR_V3(17)
                 STK_BLUR_V3(25)
+                STK_BLUR_V3(49)
                 default: break;
             }
 #undef STK_BLUR_V3
