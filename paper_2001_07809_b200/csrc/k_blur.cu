@@ -8,7 +8,8 @@
 // inside a focus range (refocus.cpp:45-73, as a per-disparity LUT), so the
 // blur map never exists in HBM.  Tiles with no blurred pixel just copy.
 //
-//   k_blur_v3 (default, kernel sizes 3..25): separable FP32, 128 x 16 tiles,
+//   k_blur_v3 (default; kernel sizes 3-13, 17, 19, 23, 25, 31, 37, 43, 49 --
+//             every integer sigma up to 8): separable FP32, 128 x 16 tiles,
 //             vertical pass first in registers (FFMA2 over column pairs),
 //             horizontal pass over 8-output items (FFMA2 over output pairs)
 //             -- within 1 LSB of the reference's 2-D FP64 sum (tests bound
@@ -615,6 +616,11 @@ void launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, ui
                 STK_BLUR_V3(13)
                 STK_BLUR_V3(17)
                 STK_BLUR_V3(25)
+                STK_BLUR_V3(19)
+                STK_BLUR_V3(23)
+                STK_BLUR_V3(31)
+                STK_BLUR_V3(37)
+                STK_BLUR_V3(43)
                 STK_BLUR_V3(49)
                 default: break;
             }

@@ -304,11 +304,13 @@ np.save({str(tmp_path / 'r.npy')!r}, res.right_lightness)
     eq(np.load(tmp_path / "r.npy"), want[::-1], "lut right_lightness")
 
 
-def test_pipeline_wide_blur_vs_oracle(dev, stk, port, synth):
-    """sigma = 8 (49-tap kernel, config E's blur) through the frame path's
-    separable blur, against the oracle's FP64 2-D blur: <= 1 LSB."""
+@pytest.mark.parametrize("sigma", [3.0, 5.0, 8.0])
+def test_pipeline_wide_blur_vs_oracle(dev, stk, port, synth, sigma):
+    """Wide kernels (sigma 3 / 5 / 8 -> 19 / 31 / 49 taps; 8 is config E's
+    blur) through the frame path's separable blur, against the oracle's FP64
+    2-D blur: <= 1 LSB."""
     l, r = synth.dead_leaves(320, 240, 16, frame=4)
-    res, img = run(stk, dev, l, r, k=4, window=9, D=16, focus=[(8, 16)], sigma=8.0)
-    want = port.run_frame(l, r, k=4, window=9, max_disparity=16, focus=[(8, 16)], sigma=8.0)
+    res, img = run(stk, dev, l, r, k=4, window=9, D=16, focus=[(8, 16)], sigma=sigma)
+    want = port.run_frame(l, r, k=4, window=9, max_disparity=16, focus=[(8, 16)], sigma=sigma)
     eq(res.dense, want["dense"], "dense")
     assert np.abs(img.astype(int) - want["refocused"].astype(int)).max() <= BLUR_TOL_LSB
