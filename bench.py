@@ -14,9 +14,10 @@ leaves" synthetic frame (~18-19 % boundary pixels).
           compiled from /root/reference sources; else the C port) on the host
           cores, rank 0 only.
 
-Multi-GPU (torchrun): frames are sharded by index, frame f -> rank f % N, no
-collective on the data path ("scaling": "weak"); NCCL only carries the
-barrier and the max-over-ranks of the device time.
+Multi-GPU (torchrun): frames are sharded by index, frame f -> rank f % N
+(shard.shard_frames), no collective on the data path ("scaling": "weak");
+gloo (CPU) carries only the barrier and the max-over-ranks of the device
+time -- NCCL is never initialised.
 """
 from __future__ import annotations
 
@@ -43,6 +44,77 @@ CONFIGS = {
 METRIC = "4096x2304 stereo frames/sec end-to-end (per-stage HBM GB/s in roofline_stages)"
 
 
+def workload(cfgname):
+    """The workload string both arms print (identical config => same_config)."""
+    W, H, D, win, K, focus, sigma = CONFIGS[cfgname]
+    return (f"{W}x{H} G2 dead-leaves stereo video, D={D}, w={win}, K={K}, "
+            f"focus={focus}, sigma={sigma}, threshold=1, prune=0.04")
+
+
+class Control:
+    """Control plane of the multi-GPU job: barrier and max-over-ranks over
+    gloo (CPU).  No frame data crosses ranks and NCCL is never initialised:
+    the path has no collective."""
+
+    def __init__(self, world, rank):
+        self.world, self.rank = world, rank
+        self.dist = None
+        if world > 1:
+            import torch.distributed as dist
+
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def max(self, value):
+        from paper_2001_07809_b200 import shard
+
+        return shard.max_over_ranks(value, self.dist)
+
+    def close(self):
+        if self.dist is not None:
+            self.dist.destroy_process_group()
+
+
+class Job:
+    """This rank's share of a weak-scaled run: `steps` frames per rank, global
+    frame f -> rank f % world (shard.shard_frames); the frame pool holds this
+    rank's first P frame indices (synthetic seed 2001 + f)."""
+
+    def __init__(self, world, rank, steps, pool):
+        from paper_2001_07809_b200 import shard
+
+        self.world, self.rank, self.steps = world, rank, steps
+        self.frames = shard.shard_frames(steps * world, rank, world)
+        self.pool_ids = shard.shard_frames(max(1, pool) * world, rank, world)
+
+    def pool_slot(self, i):
+        """Pool entry used by this rank's i-th frame."""
+        return i % len(self.pool_ids)
+
+
+def timed_region(ctrl, sync, start, stop, submit, steps, drain):
+    """W untimed warm-up frames happen before this.  Barrier + device sync on
+    both sides; the device time of `steps` submits (start/stop return the
+    event bracket, stop returns ms); the max over ranks is the job's time."""
+    drain()
+    sync()
+    ctrl.barrier()
+    start()
+    for i in range(steps):
+        submit(i)
+    ms = stop()
+    drain()
+    sync()
+    ms = ctrl.max(ms)
+    ctrl.barrier()
+    return ms
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -56,9 +128,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-s", type=float, default=20.0)
     p.add_argument("--cpu-serial", type=int, default=1, help="also time one reference frame at workers = 1")
-    p.add_argument("--e2e-dense", action="store_true",
-                   help="also read the dense disparity back in the e2e leg (run_refocus_pipeline "
-                        "returns only the refocused image; DepthResult is optional)")
+    p.add_argument("--e2e-rgb-only", action="store_true",
+                   help="e2e leg reads back only the refocused RGB (default: refocused RGB + dense "
+                        "disparity, SURVEY.md 8(d))")
     return p.parse_args()
 
 
@@ -176,8 +248,7 @@ def impl_reference(args):
         "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
         "ms_per_step": 1e3 / fps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8/i16/f64", "data": "synthetic",
-        "config": {"workload": f"{W}x{H} G2 dead-leaves stereo video, D={D}, w={win}, K={K}, "
-                               f"focus={focus}, sigma={sigma}", "frames_pool": args.pool},
+        "config": {"workload": workload(args.config), "frames_pool": args.pool},
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -201,11 +272,7 @@ def main():
     torch.cuda.set_device(local)
     all_cpus = os.sched_getaffinity(0)
     affinity = _pin_near_gpu(torch, local)  # host thread near the GPU's PCIe root
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctrl = Control(world, rank)  # gloo: barrier + max over ranks; no NCCL, no data collective
 
     from paper_2001_07809_b200 import _lib, synth
     from paper_2001_07809_b200 import stereotk as stk
@@ -221,9 +288,10 @@ def main():
     fspec = stk.FocusSpec(ranges=focus, sigma=sigma)
     c_focus, _keep = stk._focus_c(fspec, 0)
 
-    # frame pool: frame index f = rank + i * world (frame sharding)
-    P = max(1, args.pool)
-    frames = [synth.dead_leaves(W, H, D, frame=(rank + i * world)) for i in range(P)]
+    # frame pool: this rank's first P global frame indices (f = rank + i * world)
+    job = Job(world, rank, args.steps, args.pool)
+    P = len(job.pool_ids)
+    frames = [synth.dead_leaves(W, H, D, frame=f) for f in job.pool_ids]
     d_in = [(torch.from_numpy(l).cuda(), torch.from_numpy(r).cuda()) for l, r in frames]
     d_out = [(torch.empty((H, W, 3), dtype=torch.uint8, device="cuda"),
               torch.empty((H, W), dtype=torch.int16, device="cuda")) for _ in range(S)]
@@ -240,10 +308,14 @@ def main():
             check(L.stk_frame_wait(dev.h, slot, None, None, C.byref(info) if want_info else None))
             inflight[slot] = False
 
+    def drain():
+        for s in range(S):
+            wait(s)
+
     def submit_device(i):
         slot = i % S
         wait(slot)
-        l, r = d_in[i % P]
+        l, r = d_in[job.pool_slot(i)]
         o, dd = d_out[slot]
         check(L.stk_frame_submit_device(dev.h, slot, C.c_void_p(l.data_ptr()),
                                         C.c_void_p(r.data_ptr()), W, H, C.byref(c_cfg),
@@ -251,38 +323,27 @@ def main():
                                         C.c_void_p(dd.data_ptr()), 0))
         inflight[slot] = True
 
-    def barrier():
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
+    # CUDA events: start on slot 0's stream (every slot stream waits on it),
+    # end on slot 0's stream after joining every slot stream
+    ev = {}
 
-    def timed_region(submit, steps):
-        """CUDA events: start on slot 0's stream, end after every slot stream."""
-        for s in range(S):
-            wait(s)
-        barrier()
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record(streams[0])
+    def start():
+        ev["0"] = torch.cuda.Event(enable_timing=True)
+        ev["1"] = torch.cuda.Event(enable_timing=True)
+        ev["0"].record(streams[0])
         for s in range(1, S):
-            streams[s].wait_event(ev0)
-        for i in range(steps):
-            submit(i)
+            streams[s].wait_event(ev["0"])
+
+    def stop():
         for s in range(1, S):
             e = torch.cuda.Event()
             e.record(streams[s])
             streams[0].wait_event(e)
-        ev1.record(streams[0])
-        for s in range(S):
-            wait(s)
-        torch.cuda.synchronize()
-        ms = ev0.elapsed_time(ev1)
-        if dist is not None:
-            t = torch.tensor([ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        barrier()
-        return ms
+        ev["1"].record(streams[0])
+        ev["1"].synchronize()
+        return ev["0"].elapsed_time(ev["1"])
+
+    sync = torch.cuda.synchronize
 
     # ---- warm-up (also builds the per-slot CUDA graphs: at least one untimed
     # frame per slot so no graph is captured inside the timed region)
@@ -296,11 +357,13 @@ def main():
     # ---- device-resident timed region
     clocks = ClockSampler(local)
     clocks.start()
-    ms_dev = timed_region(submit_device, args.steps)
+    ms_dev = timed_region(ctrl, sync, start, stop, submit_device, args.steps, drain)
     clk = clocks.stop()
     fps_dev = world * args.steps / (ms_dev / 1e3)
 
-    # ---- end-to-end through the host-pointer C-ABI entry (pinned buffers)
+    # ---- end-to-end through the host-pointer C-ABI entry (pinned buffers):
+    # H2D of the RGB pair, D2H of the refocused RGB + dense disparity
+    dense_back = not args.e2e_rgb_only
     hp = []
     for i in range(P):
         l, r = frames[i]
@@ -317,12 +380,12 @@ def main():
     outs = [_lib.StkFrameOut() for _ in range(S)]
     for s in range(S):
         outs[s].refocused = ho[s][0].ctypes.data
-        outs[s].dense = ho[s][1].ctypes.data if args.e2e_dense else None
+        outs[s].dense = ho[s][1].ctypes.data if dense_back else None
 
     def submit_host(i):
         slot = i % S
         wait(slot)
-        bl, br = hp[i % P]
+        bl, br = hp[job.pool_slot(i)]
         check(L.stk_frame_submit(dev.h, slot, C.c_void_p(bl.ctypes.data),
                                  C.c_void_p(br.ctypes.data), W, H, C.byref(c_cfg),
                                  C.byref(c_focus), C.byref(outs[slot]), 0))
@@ -330,8 +393,10 @@ def main():
 
     for i in range(n_warm):
         submit_host(i)
-    ms_e2e = timed_region(submit_host, args.steps)
+    ms_e2e = timed_region(ctrl, sync, start, stop, submit_host, args.steps, drain)
     fps_e2e = world * args.steps / (ms_e2e / 1e3)
+    h2d_bytes = 2 * 3 * N
+    d2h_bytes = 3 * N + (2 * N if dense_back else 0)
     for s in range(S):
         wait(s)
     pcie = _pcie_probe(local)
@@ -420,17 +485,16 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_dev / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u8/i16 (int stages), f64 (L*, K-Means), f32 (blur)", "data": "synthetic",
-        "config": {"workload": f"{W}x{H} G2 dead-leaves stereo video, D={D}, w={win}, K={K}, "
-                               f"focus={focus}, sigma={sigma}, threshold=1, prune=0.04",
+        "config": {"workload": workload(args.config),
                    "frames_pool": P, "frames_in_flight": S, "warmup_frames": n_warm,
                    "l2": "inputs larger than L2 (pool of distinct frames, ~56.6 MB each)",
                    "parallelism": f"frame-sharded x{world} (frame f -> rank f % {world}, no NCCL)",
                    "sad_kernel": args.sad, "matched_fraction": round(matched_frac, 4)},
         "e2e": {"value": round(fps_e2e, 3), "unit": "frames/s",
-                "h2d_bytes_per_step": 2 * 3 * N,
-                "d2h_bytes_per_step": 3 * N + (2 * N if args.e2e_dense else 0),
+                "h2d_bytes_per_step": h2d_bytes,
+                "d2h_bytes_per_step": d2h_bytes,
                 "path": "stk_frame_submit (C-ABI, pinned host buffers)",
-                "pcie": _pcie_model(pcie, 2 * 3 * N, 3 * N + (2 * N if args.e2e_dense else 0),
+                "pcie": _pcie_model(pcie, h2d_bytes, d2h_bytes,
                                     fps_e2e / world, frame_ms_dev)},
         "gpu_launches": int(kernels_per_frame * args.steps * 2),
         "kernels_per_frame": int(kernels_per_frame),
@@ -457,8 +521,7 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     dev.close()
-    if dist is not None:
-        dist.destroy_process_group()
+    ctrl.close()
     return 0
 
 

@@ -327,12 +327,15 @@ __global__ void __launch_bounds__(V3Geom<K>::NT) k_blur_v3(Frame f, BlurParams b
     __syncthreads();
     // ---- one latency exposure: the staged rows (rows y0-h .. y0+BY+h-1,
     // columns x0-h .. x0+BX+h-1, replicate-clamped) and the tile's disparities
-    const bool interior = 3 * x0 - G::LB >= 0 && 3 * (x0 + BX + h) + 16 <= 3 * W && y0 - h >= 0 &&
+    // the interior loads cover row bytes [3*x0 - LB, 3*x0 - LB + 16*NV): the
+    // guard is exactly that range (no read past the row / the buffer end)
+    constexpr int NVL = (3 * NC + G::LB + 15) / 16;
+    const bool interior = 3 * x0 - G::LB >= 0 && 3 * x0 - G::LB + 16 * NVL <= 3 * W && y0 - h >= 0 &&
                           y0 + BY + h <= H && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
                           (reinterpret_cast<uintptr_t>(depth) & 15) == 0 && (W * 3) % 16 == 0;
     int any = 0;
     if (interior) {
-        constexpr int NV = (3 * NC + G::LB + 15) / 16;
+        constexpr int NV = NVL;
         constexpr int PER = (IH * NV + NT - 1) / NT;
         uint4 buf[PER];
 #pragma unroll
@@ -655,7 +658,7 @@ void launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, ui
 void launch_blur_map(const Frame& f, const int16_t* depth, const uint8_t* sharp_lut, int lut_len,
                      uint8_t* out, cudaStream_t st) {
     if (f.N == 0) return;
-    const long long blocks = std::min<long long>((f.N + 255) / 256, 148 * 16);
+    const long long blocks = std::min<long long>((f.N + 255) / 256, f.sms * 16);
     k_blur_map<<<(int)blocks, 256, 0, st>>>(f, depth, sharp_lut, lut_len, out);
 }
 

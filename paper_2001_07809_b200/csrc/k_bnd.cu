@@ -1006,14 +1006,14 @@ void launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, in
     k_ccl_borders<<<nreg, RW + RH, 0, st>>>(f, bord);
     cudaMemsetAsync(sbits, 0, (size_t)sbits_words * 4, st);
     {   // B4-B7 in one cooperative launch (co-resident blocks, grid barriers)
-        static int g_blocks = 0;
-        if (!g_blocks) {
-            int per_sm = 0, sms = 148, dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_prune_fused, 256, 0);
-            g_blocks = std::min(512, std::max(1, std::min(per_sm, 2)) * sms);  // <= gsum/gcnt slots
-        }
+        // co-resident blocks per SM depend only on the kernel (thread-safe
+        // static init); the grid follows the context's device SM count
+        static const int per_sm = [] {
+            int n = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_prune_fused, 256, 0);
+            return n;
+        }();
+        const int g_blocks = std::min(512, std::max(1, std::min(per_sm, 2)) * f.sms);  // <= gsum/gcnt slots
         int nw = sbits_words;
         void* args[] = {(void*)&f, (void*)&sbits, (void*)&nw};
         cudaLaunchCooperativeKernel((const void*)k_prune_fused, dim3(g_blocks), dim3(256), args, 0, st);
@@ -1025,7 +1025,7 @@ void launch_prune_mask_bits(const Frame& f, const uint8_t* mask, uint32_t* rbits
                             int32_t* bord, uint32_t* sbits, int sbits_words, cudaStream_t st) {
     if (f.N == 0) return;
     const long long nw = (long long)((f.W + 31) / 32) * f.H;
-    k_mask_to_bits<<<(int)std::min<long long>((nw + 255) / 256, 148 * 8), 256, 0, st>>>(f, mask, rbits);
+    k_mask_to_bits<<<(int)std::min<long long>((nw + 255) / 256, f.sms * 8), 256, 0, st>>>(f, mask, rbits);
     launch_ccl_prune_bits(f, rbits, runroot, bord, sbits, sbits_words, false, st);
 }
 

@@ -573,14 +573,14 @@ void launch_apply(const Frame& f, bool use_prune, bool anchors, cudaStream_t st)
 
 void launch_count_mask(const Frame& f, const uint8_t* mask, cudaStream_t st) {
     if (f.N == 0) return;
-    const long long blocks = std::min<long long>((f.N + 255) / 256, 148 * 8);
+    const long long blocks = std::min<long long>((f.N + 255) / 256, f.sms * 8);
     k_count_mask<<<(int)blocks, 256, 0, st>>>(f, mask);
 }
 
 void launch_anchor_only(const Frame& f, const uint8_t* in, uint8_t* out, int margin,
                         cudaStream_t st) {
     if (f.N == 0) return;
-    const long long blocks = std::min<long long>((f.N + 255) / 256, 148 * 16);
+    const long long blocks = std::min<long long>((f.N + 255) / 256, f.sms * 16);
     k_anchor_only<<<(int)blocks, 256, 0, st>>>(f, in, out, margin);
 }
 
@@ -590,13 +590,13 @@ void launch_ccl(const Frame& f, cudaStream_t st) {
     const int ntiles = tiles.x * tiles.y;
     k_ccl_local<<<(ntiles + kLocalWarps - 1) / kLocalWarps, 32 * kLocalWarps, 0, st>>>(f);
     k_ccl_merge<<<tiles, 128, 0, st>>>(f);
-    k_ccl_compress<<<148 * 8, 256, 0, st>>>(f);
+    k_ccl_compress<<<f.sms * 8, 256, 0, st>>>(f);
     k_ccl_roots<<<f.n_chunks, 256, 0, st>>>(f, f.full);
 }
 
 void launch_ccl_compress(const Frame& f, cudaStream_t st) {
     if (f.N == 0) return;
-    k_ccl_compress<<<148 * 8, 256, 0, st>>>(f);
+    k_ccl_compress<<<f.sms * 8, 256, 0, st>>>(f);
 }
 
 void launch_prune_select(const Frame& f, cudaStream_t st) {
@@ -607,15 +607,15 @@ void launch_prune_select(const Frame& f, cudaStream_t st) {
 void launch_prune(const Frame& f, bool anchors, cudaStream_t st) {
     if (f.N == 0) return;
     k_prune_select<<<1, 1024, 0, st>>>(f);
-    k_prune_mark<<<148 * 4, 256, 0, st>>>(f);
+    k_prune_mark<<<f.sms * 4, 256, 0, st>>>(f);
     k_apply<<<f.n_chunks, 256, 0, st>>>(f, 1, anchors ? 1 : 0);
 }
 
 void launch_component_table(const Frame& f, int32_t* d_labels, uint32_t* d_sizes, int32_t* d_ids,
                             cudaStream_t st) {
     if (f.N == 0) return;
-    k_sizes_by_label<<<148 * 2, 256, 0, st>>>(f, d_sizes, d_ids);
-    const long long blocks = std::min<long long>((f.N + 255) / 256, 148 * 16);
+    k_sizes_by_label<<<f.sms * 2, 256, 0, st>>>(f, d_sizes, d_ids);
+    const long long blocks = std::min<long long>((f.N + 255) / 256, f.sms * 16);
     k_labels_out<<<(int)blocks, 256, 0, st>>>(f, d_labels);
 }
 

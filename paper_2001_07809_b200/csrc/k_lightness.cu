@@ -391,7 +391,7 @@ int launch_lightness(const Frame& f, const LstarTables* dtab, bool left, bool ri
         // frame path: both views in one launch, then the histogram pass
         const long long nch = (long long)(f.W / 16) * f.H;
         if (lut) {
-            const int bx = (int)std::min<long long>((nch + 255) / 256, 148 * 4);
+            const int bx = (int)std::min<long long>((nch + 255) / 256, f.sms * 4);
             k_lstar_lut<<<dim3(bx, 2), 256, 0, st>>>(f, lut);
         } else {
             const int bx = (int)std::min<long long>((nch + kL2Threads - 1) / kL2Threads, 74);
@@ -404,7 +404,7 @@ int launch_lightness(const Frame& f, const LstarTables* dtab, bool left, bool ri
             k_lstar2<false><<<dim3(bx, 2), kL2Threads, kL2Smem, st>>>(f, dtab);
         }
         if (hist) {
-            const int hb = (int)std::min<long long>((nch + kThreads - 1) / kThreads, 148 * 4);
+            const int hb = (int)std::min<long long>((nch + kThreads - 1) / kThreads, f.sms * 4);
             k_hist_warp<<<hb, kThreads, 0, st>>>(f, f.grayL);
             return 2;
         }
@@ -440,12 +440,12 @@ int launch_lightness(const Frame& f, const LstarTables* dtab, bool left, bool ri
 
 void launch_histogram(const Frame& f, const uint8_t* gray, cudaStream_t st) {
     if (f.N == 0) return;
-    k_hist<<<std::min(f.H, 148 * 4), kThreads, 0, st>>>(f, gray);
+    k_hist<<<std::min(f.H, f.sms * 4), kThreads, 0, st>>>(f, gray);
 }
 
 void launch_assign(const Frame& f, const uint8_t* gray, uint16_t* out, cudaStream_t st) {
     if (f.N == 0) return;
-    const long long blocks = std::min<long long>((f.N + 255) / 256, 148 * 16);
+    const long long blocks = std::min<long long>((f.N + 255) / 256, f.sms * 16);
     k_assign<<<(int)blocks, 256, 0, st>>>(f, gray, out);
 }
 

@@ -140,7 +140,7 @@ void run_list(const Frame& f, const CUtensorMap* tmL, const CUtensorMap* tmR, cu
     cudaFuncSetAttribute(k_sad_list<MAXJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sad_list<MAXJ>, kThreads, sm);
-    k_sad_list<MAXJ><<<148 * std::max(per_sm, 1), kThreads, sm, st>>>(*tmL, *tmR, f);
+    k_sad_list<MAXJ><<<f.sms * std::max(per_sm, 1), kThreads, sm, st>>>(*tmL, *tmR, f);
 }
 
 // sad_cost for one (x, y, d) (stereo.cpp:12-28): one warp, lanes stride the

@@ -522,7 +522,7 @@ bool launch_sad_ws(const Frame& f, cudaStream_t st, bool dry) {
     const int NQB = (p.QMAIN + per_block - 1) / per_block;
     if (NQB > 2) return false;
     // strip width: as wide as shared memory allows (fewer halo columns)
-    const int sms = 148;
+    const int sms = f.sms > 0 ? f.sms : 148;
     size_t sm = 0;
     for (int SW : {256, 192, 128, 96, 64}) {
         p.SW = SW;

@@ -44,10 +44,15 @@ struct TMap {
     int W = -1, H = -1, pitch = -1, bw = -1, bh = -1, esz = -1;
 };
 
+// Everything a captured frame graph bakes in: geometry, configuration and
+// every device pointer its nodes read or write (the caller's buffers and the
+// slot's focus tables, which upload_focus may reallocate).  Zeroed as a
+// whole (padding included) so memcmp is a field-by-field comparison.
 struct GraphKey {
-    int W = -1, H = -1, kcfg, window, D, thr, full, focus, hw, exact, lut_len, sad, want_raw;
+    int W, H, kcfg, window, D, thr, full, focus, hw, exact, lut_len, sad, want_raw, pad_;
     double frac;
-    const void *rgbL, *rgbR, *out_rgb, *dense;
+    const void *rgbL, *rgbR, *out_rgb, *dense, *lut, *g1, *g2;
+    GraphKey() { std::memset(this, 0, sizeof(*this)); W = H = -1; }
     bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
 
@@ -59,6 +64,7 @@ struct Slot {
     size_t bytes = 0;
     // layout for the current frame geometry
     int W = 0, H = 0, P = 0;
+    int sms = 148;  // copied from the context at creation
     uint8_t *rgbL, *rgbR, *grayL, *grayR, *mraw, *mref, *mprn, *manc, *out_rgb;
     uint16_t *labels16, *scratch16;
     uint32_t* mbits;
@@ -81,6 +87,11 @@ struct Slot {
     std::vector<uint8_t> h_lut;
     std::vector<float> h_g1;
     std::vector<double> h_g2;
+    // pinned staging of the focus tables: uploads are stream-ordered async
+    // copies (no host synchronisation when the focus changes between frames)
+    uint8_t* p_lut = nullptr;
+    float* p_g1 = nullptr;
+    double* p_g2 = nullptr;
     // label_components scratch
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
@@ -109,6 +120,7 @@ struct stk_ctx {
     std::vector<Slot> slots;
     int sad_kernel = SAD_AUTO;
     int use_graphs = 1;
+    int sms = 148;  // cudaDevAttrMultiProcessorCount of `device` (grid sizing)
     EncodeTiledFn encode = nullptr;
 };
 
@@ -306,6 +318,7 @@ Frame make_frame(const Slot& s, int W, int H, const stk_config* cfg) {
     f.n_tiles = H * f.TX;
     f.n_chunks = (f.n_tiles + kTilesPerChunk - 1) / kTilesPerChunk;
     f.bits_words = f.TX * 4;
+    f.sms = s.sms;
     if (cfg) {
         f.kcfg = cfg->k;
         f.window = cfg->window;
@@ -442,30 +455,56 @@ stk_status upload_focus(stk_ctx* ctx, Slot& s, const int* lo, const int* hi, int
         for (int i = 0; i < size; ++i) g1[i] = (float)(t[i] / sum);
         stk_gaussian_kernel(sigma, size, g2.data());
     }
+    if (lut_len > s.lut_cap || (int)g2.size() > s.g_cap) {
+        // the slot's stream may still read the old tables (a stage entry or a
+        // frame); every captured graph holds their addresses -> drop it
+        CK(cudaStreamSynchronize(s.st));
+        if (s.gexec) {
+            cudaGraphExecDestroy(s.gexec);
+            s.gexec = nullptr;
+            s.gkey = GraphKey{};
+        }
+    }
     if (lut_len > s.lut_cap) {
         if (s.d_lut) CK(cudaFree(s.d_lut));
+        if (s.p_lut) CK(cudaFreeHost(s.p_lut));
+        s.d_lut = nullptr;
+        s.p_lut = nullptr;
         s.lut_cap = std::max(lut_len, 1024);
         CK(cudaMalloc(&s.d_lut, s.lut_cap));
+        CK(cudaMallocHost(&s.p_lut, s.lut_cap));
         s.h_lut.clear();
     }
     if ((int)g2.size() > s.g_cap) {
         if (s.d_g1) CK(cudaFree(s.d_g1));
         if (s.d_g2) CK(cudaFree(s.d_g2));
+        if (s.p_g1) CK(cudaFreeHost(s.p_g1));
+        if (s.p_g2) CK(cudaFreeHost(s.p_g2));
+        s.d_g1 = nullptr;
+        s.d_g2 = nullptr;
+        s.p_g1 = nullptr;
+        s.p_g2 = nullptr;
         s.g_cap = std::max((int)g2.size(), 4096);
         CK(cudaMalloc(&s.d_g1, s.g_cap * sizeof(float)));
         CK(cudaMalloc(&s.d_g2, s.g_cap * sizeof(double)));
+        CK(cudaMallocHost(&s.p_g1, s.g_cap * sizeof(float)));
+        CK(cudaMallocHost(&s.p_g2, s.g_cap * sizeof(double)));
         s.h_g1.clear();
         s.h_g2.clear();
     }
+    // A slot has at most one frame in flight and stage entries are
+    // synchronous, so the previous copy out of the staging buffers has
+    // completed by now; the new copies are ordered before this frame's kernels.
     if (s.h_lut != lut) {
-        CK(cudaStreamSynchronize(s.st));  // a previous frame may still read it
-        CK(cudaMemcpy(s.d_lut, lut.data(), lut_len, cudaMemcpyHostToDevice));
+        std::memcpy(s.p_lut, lut.data(), lut_len);
+        CK(cudaMemcpyAsync(s.d_lut, s.p_lut, lut_len, cudaMemcpyHostToDevice, s.st));
         s.h_lut = lut;
     }
     if (s.h_g1 != g1 || s.h_g2 != g2) {
-        CK(cudaStreamSynchronize(s.st));
-        CK(cudaMemcpy(s.d_g1, g1.data(), g1.size() * sizeof(float), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(s.d_g2, g2.data(), g2.size() * sizeof(double), cudaMemcpyHostToDevice));
+        std::memcpy(s.p_g1, g1.data(), g1.size() * sizeof(float));
+        std::memcpy(s.p_g2, g2.data(), g2.size() * sizeof(double));
+        CK(cudaMemcpyAsync(s.d_g1, s.p_g1, g1.size() * sizeof(float), cudaMemcpyHostToDevice, s.st));
+        CK(cudaMemcpyAsync(s.d_g2, s.p_g2, g2.size() * sizeof(double), cudaMemcpyHostToDevice, s.st));
         s.h_g1 = g1;
         s.h_g2 = g2;
     }
@@ -594,7 +633,6 @@ stk_status submit(stk_ctx* ctx, int slot, const uint8_t* rgbL, const uint8_t* rg
     if (focus)
         TRY(upload_focus(ctx, s, focus->lo, focus->hi, focus->n_ranges, cfg->max_disparity,
                          focus->sigma, ksize, focus->exact_blur != 0, &bp));
-    TRY(encode(ctx, s.tm_morph, s.grayL, 1, w, h, s.P, 160, 38));
     TRY(encode(ctx, s.tm_sadL, s.grayL, 1, w, h, s.P, 128, cfg->window));
     TRY(encode(ctx, s.tm_sadR, s.grayR, 1, w, h, s.P, 128, cfg->window));
     cudaStream_t st = s.st;
@@ -606,7 +644,7 @@ stk_status submit(stk_ctx* ctx, int slot, const uint8_t* rgbL, const uint8_t* rg
     int nk = 0;
     bool graphed = false;
     if (!timed && ctx->use_graphs) {
-        GraphKey key{};
+        GraphKey key;
         key.W = w;
         key.H = h;
         key.kcfg = cfg->k;
@@ -625,6 +663,9 @@ stk_status submit(stk_ctx* ctx, int slot, const uint8_t* rgbL, const uint8_t* rg
         key.rgbR = f.rgbR;
         key.out_rgb = f.out_rgb;
         key.dense = f.dense;
+        key.lut = bp.sharp_lut;
+        key.g1 = bp.g1;
+        key.g2 = bp.g2;
         if (!(s.gexec && s.gkey == key)) {
             if (s.gexec) {
                 cudaGraphExecDestroy(s.gexec);
@@ -762,8 +803,10 @@ stk_status stk_create(int device, int max_width, int max_height, int slots, stk_
             if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
             cudaGetLastError();
         }
+        cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
         ctx->slots.resize(std::max(slots, 1));
         for (Slot& s : ctx->slots) {
+            s.sms = ctx->sms;
             if (cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking) != cudaSuccess ||
                 cudaEventCreate(&s.done) != cudaSuccess ||
                 cudaMallocHost(&s.h_sc, sizeof(DevScalars)) != cudaSuccess) {
@@ -806,6 +849,9 @@ void stk_destroy(stk_ctx* ctx) {
         if (s.d_lut) cudaFree(s.d_lut);
         if (s.d_g1) cudaFree(s.d_g1);
         if (s.d_g2) cudaFree(s.d_g2);
+        if (s.p_lut) cudaFreeHost(s.p_lut);
+        if (s.p_g1) cudaFreeHost(s.p_g1);
+        if (s.p_g2) cudaFreeHost(s.p_g2);
         if (s.cub_tmp) cudaFree(s.cub_tmp);
         if (s.h_sc) cudaFreeHost(s.h_sc);
         for (auto& e : s.ev)

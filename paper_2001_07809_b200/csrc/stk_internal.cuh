@@ -64,6 +64,7 @@ struct Frame {
     int n_tiles;        // H * TX
     int n_chunks;       // ceil(n_tiles / kTilesPerChunk)
     int bits_words;     // u32 words per row of the matchable bit-mask
+    int sms;            // SM count of the context's device (grid sizing)
     // configuration (PipelineConfig, pipeline.hpp:18-25)
     int kcfg, window, hw, D, thr;
     double frac;

@@ -314,3 +314,36 @@ def test_pipeline_wide_blur_vs_oracle(dev, stk, port, synth, sigma):
     want = port.run_frame(l, r, k=4, window=9, max_disparity=16, focus=[(8, 16)], sigma=sigma)
     eq(res.dense, want["dense"], "dense")
     assert np.abs(img.astype(int) - want["refocused"].astype(int)).max() <= BLUR_TOL_LSB
+
+
+def test_graph_survives_focus_table_reallocation(dev, stk, port, synth):
+    """A stage entry that grows the slot's focus tables (a 67x67 blur kernel:
+    > 4096 weights; max_disparity >= 1024: > 1024 LUT entries) between two
+    graph-replayed frames of the same geometry must not leave the frame graph
+    reading freed tables (stk_capi.cu upload_focus)."""
+    W, H = 320, 240
+    l, r = synth.dead_leaves(W, H, 16, frame=2)
+    want = port.run_frame(l, r, k=4, window=9, max_disparity=16, focus=[(8, 16)], sigma=2.0)
+    res, img = run(stk, dev, l, r, k=4, window=9, D=16, focus=[(8, 16)])
+    assert np.abs(img.astype(int) - want["refocused"].astype(int)).max() <= BLUR_TOL_LSB
+    # grow the weights (67 x 67 taps) and the LUT (D = 1100) on the same slot
+    bmap = np.ones((H, W), np.uint8)
+    stk.selective_blur(l, bmap, stk.gaussian_kernel(11.0, 67), device=dev)
+    stk.build_blur_map(np.zeros((H, W), np.int16), [(0, 5)], 1100, device=dev)
+    res2, img2 = run(stk, dev, l, r, k=4, window=9, D=16, focus=[(8, 16)])
+    eq(res2.dense, want["dense"], "dense after realloc")
+    eq(img2, img, "refocused after realloc")
+
+
+def test_wide_blur_tile_edge_shape(dev, stk, ref, synth):
+    """K = 49 (sigma 8) at W = 32 (mod 128), H = h (mod 16): the v3 interior
+    fast path's last staged row ends exactly at the buffer end (ADVICE r1:
+    k_blur.cu interior guard)."""
+    W, H = 1440, 1080
+    l, r = synth.dead_leaves(W, H, 32, frame=6)
+    res, img = run(stk, dev, l, r, k=5, window=11, D=32, focus=[(16, 32)], sigma=8.0)
+    want = ref.run_frame(l, r, k=5, window=11, max_disparity=32, focus=[(16, 32)], sigma=8.0,
+                         workers=os.cpu_count() or 1)
+    for k in INTERMEDIATES:
+        eq(getattr(res, k), want[k], k)
+    assert np.abs(img.astype(int) - want["refocused"].astype(int)).max() <= BLUR_TOL_LSB
