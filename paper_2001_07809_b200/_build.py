@@ -31,8 +31,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = [
     "k_lightness.cu",
     "k_kmeans.cu",
-    "k_boundary.cu",
-    "k_ccl.cu",
+    "k_apply.cu",
     "k_bnd.cu",
     "k_sad.cu",
     "k_sad_strip.cu",

@@ -34,6 +34,8 @@
 //                   the frame counts (bytes in full mode).
 //   B9 list_bits    (only for the per-pixel SAD list kernel) ordered
 //                   compaction of the matchable bits.
+#include <cub/device/device_scan.cuh>
+
 #include "stk_device.cuh"
 
 namespace stk {
@@ -156,23 +158,51 @@ __device__ __forceinline__ void gunite_n(int* p, int a, const int (&b)[3], int n
 // NPL label bit-planes.  lutp[v] holds bit p of lut[v] at bit 8p (p < 4), so
 // 8 pixels combine with shift-adds into one word whose byte p is plane p's
 // 8 bits; planes 4..7 use lutq the same way.
-template <int NPL>
-__global__ void __launch_bounds__(128) k_morph_bits(Frame f, uint32_t* __restrict__ rbits) {
+//
+// MODE selects where the streamed rows enter the detect -> fill -> remove
+// pipeline (same word ops, same edge rules, same row schedule):
+//   MB_FRAME   gray (pitched u8) -> K-Means LUT planes -> detect -> fill ->
+//              remove -> refined bits (+ raw bytes in full mode); the frame path
+//   MB_DET16   u16 labels (pitch 2P) -> planes poff..poff+NPL-1 -> detect ->
+//              raw bits (OR-ed in when poff > 0); detect_boundaries entry
+//   MB_FILL    byte mask -> (as raw bits) fill -> filled bits; morph_fill entry
+//   MB_REMOVE  byte mask -> (as filled bits) remove -> bits; morph_remove entry
+enum { MB_FRAME = 0, MB_DET16 = 1, MB_FILL = 2, MB_REMOVE = 3 };
+
+__device__ __forceinline__ uint32_t bytes_nz_bits(const uint4 (&g)[2]) {  // 32 bytes -> 32 bits (!= 0)
+    const uint32_t w8[8] = {g[0].x, g[0].y, g[0].z, g[0].w, g[1].x, g[1].y, g[1].z, g[1].w};
+    uint32_t m = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t t = __vcmpne4(w8[i], 0u) & 0x01010101u;  // flag of byte b at bit 8b
+        m |= ((t | (t >> 7) | (t >> 14) | (t >> 21)) & 0xfu) << (4 * i);
+    }
+    return m;
+}
+
+template <int NPL, int MODE>
+__global__ void __launch_bounds__(128) k_morph_bits(Frame f, uint32_t* __restrict__ rbits,
+                                                    const uint8_t* __restrict__ src, int poff) {
+    constexpr int NQ = MODE == MB_DET16 ? 4 : 2;  // uint4 per 32-pixel word column
     __shared__ uint32_t lutp[256], lutq[256];
     __shared__ unsigned long long red[2][4];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    for (int v = tid; v < 256; v += blockDim.x) {
-        const uint32_t l = f.sc->lut[v];
-        uint32_t a = 0, b = 0;
+    if constexpr (MODE == MB_FRAME) {
+        for (int v = tid; v < 256; v += blockDim.x) {
+            const uint32_t l = f.sc->lut[v];
+            uint32_t a = 0, b = 0;
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            a |= ((l >> p) & 1u) << (8 * p);
-            b |= ((l >> (p + 4)) & 1u) << (8 * p);
+            for (int p = 0; p < 4; ++p) {
+                a |= ((l >> p) & 1u) << (8 * p);
+                b |= ((l >> (p + 4)) & 1u) << (8 * p);
+            }
+            lutp[v] = a;
+            lutq[v] = b;
         }
-        lutp[v] = a;
-        lutq[v] = b;
+        __syncthreads();
+        src = f.grayL;
     }
-    __syncthreads();
+    const size_t pitch = MODE == MB_DET16 ? 2 * (size_t)f.P : (size_t)f.P;
     const int W = f.W, H = f.H, BW = (W + 31) >> 5;
     const int strips = (BW + MB_WPW - 1) / MB_WPW;
     const int gw = blockIdx.x * 4 + wid;
@@ -202,30 +232,45 @@ __global__ void __launch_bounds__(128) k_morph_bits(Frame f, uint32_t* __restric
             return (v >> 1) | ((last ? (v >> 31) : (r & 1u)) << 31);
         };
         // rows are fetched two iterations ahead of their use (load latency)
-        auto load_row = [&](int ri, uint4 (&g)[2]) {
+        auto load_row = [&](int ri, uint4 (&g)[NQ]) {
             ri = min(max(ri, 0), H - 1);
-            const uint4* src = reinterpret_cast<const uint4*>(f.grayL + (size_t)ri * f.P + 32 * wcl);
-            g[0] = __ldg(src);
-            g[1] = __ldg(src + 1);
+            const uint4* p = reinterpret_cast<const uint4*>(src + (size_t)ri * pitch + 16 * NQ * wcl);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) g[q] = __ldg(p + q);
         };
-        auto planes_of = [&](const uint4 (&gq)[2], uint32_t (&pl)[NPL]) {
-            const uint4 g0 = gq[0], g1 = gq[1];
-            const uint32_t gw8[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        auto planes_of = [&](const uint4 (&gq)[NQ], uint32_t (&pl)[NPL]) {
 #pragma unroll
             for (int p = 0; p < NPL; ++p) pl[p] = 0;
+            if constexpr (MODE == MB_FRAME) {
+                const uint4 g0 = gq[0], g1 = gq[1];
+                const uint32_t gw8[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
-            for (int oct = 0; oct < 4; ++oct) {
-                uint32_t a = 0, b = 0;
+                for (int oct = 0; oct < 4; ++oct) {
+                    uint32_t a = 0, b = 0;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const uint32_t v = (gw8[2 * oct + (i >> 2)] >> (8 * (i & 3))) & 0xffu;
-                    a += lutp[v] << i;
-                    if (NPL > 4) b += lutq[v] << i;
+                    for (int i = 0; i < 8; ++i) {
+                        const uint32_t v = (gw8[2 * oct + (i >> 2)] >> (8 * (i & 3))) & 0xffu;
+                        a += lutp[v] << i;
+                        if (NPL > 4) b += lutq[v] << i;
+                    }
+#pragma unroll
+                    for (int p = 0; p < NPL; ++p) {
+                        const uint32_t byte = p < 4 ? (a >> (8 * p)) & 0xffu : (b >> (8 * (p - 4))) & 0xffu;
+                        pl[p] |= byte << (8 * oct);
+                    }
+                }
+            } else if constexpr (MODE == MB_DET16) {
+                uint32_t w16[16];
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    w16[4 * q] = gq[q].x, w16[4 * q + 1] = gq[q].y;
+                    w16[4 * q + 2] = gq[q].z, w16[4 * q + 3] = gq[q].w;
                 }
 #pragma unroll
-                for (int p = 0; p < NPL; ++p) {
-                    const uint32_t byte = p < 4 ? (a >> (8 * p)) & 0xffu : (b >> (8 * (p - 4))) & 0xffu;
-                    pl[p] |= byte << (8 * oct);
+                for (int i = 0; i < 32; ++i) {
+                    const uint32_t lab = ((w16[i >> 1] >> (16 * (i & 1))) & 0xffffu) >> poff;
+#pragma unroll
+                    for (int p = 0; p < NPL; ++p) pl[p] |= ((lab >> p) & 1u) << i;
                 }
             }
             if (last && nvalid < 32) {  // pixels beyond W replicate pixel W-1
@@ -236,49 +281,78 @@ __global__ void __launch_bounds__(128) k_morph_bits(Frame f, uint32_t* __restric
         // sliding windows: label planes (3 rows + shifted), raw (3 rows), fill (3 rows)
         uint32_t P0[NPL], P1[NPL], P2[NPL], L1[NPL], R1[NPL], L0[NPL], R0[NPL], L2[NPL], R2[NPL];
         uint32_t raw0 = 0, raw1 = 0, raw2 = 0, fil0 = 0, fil1 = 0, fil2 = 0;
-        uint4 qa[2], qb[2], qc[2];
+        uint32_t m0 = 0, m1 = 0, m2 = 0;  // mask modes: bits of rows ri, ri-1, ri-2
+        uint4 qa[NQ], qb[NQ], qc[NQ];
         load_row(yb - 3, qa);
         load_row(yb - 2, qb);
         for (int i = 0; i < MB_ROWS + 6; ++i) {
             const int ri = yb - 3 + i;
-            // shift the plane window: (P0, P1, P2) = rows ri-2, ri-1, ri
+            if constexpr (MODE == MB_FILL || MODE == MB_REMOVE) {
+                m2 = m1;
+                m1 = m0;
+                m0 = bytes_nz_bits(qa) & valid;  // row ri (qa holds row ri)
+                load_row(ri + 2, qc);
 #pragma unroll
-            for (int p = 0; p < NPL; ++p) {
-                P0[p] = P1[p], L0[p] = L1[p], R0[p] = R1[p];
-                P1[p] = P2[p], L1[p] = L2[p], R1[p] = R2[p];
-            }
-            load_row(ri + 2, qc);
-            planes_of(qa, P2);
-            qa[0] = qb[0], qa[1] = qb[1], qb[0] = qc[0], qb[1] = qc[1];
+                for (int q = 0; q < NQ; ++q) qa[q] = qb[q], qb[q] = qc[q];
+            } else {
+                // shift the plane window: (P0, P1, P2) = rows ri-2, ri-1, ri
 #pragma unroll
-            for (int p = 0; p < NPL; ++p) {
-                L2[p] = shl(P2[p]);
-                R2[p] = shr(P2[p]);
+                for (int p = 0; p < NPL; ++p) {
+                    P0[p] = P1[p], L0[p] = L1[p], R0[p] = R1[p];
+                    P1[p] = P2[p], L1[p] = L2[p], R1[p] = R2[p];
+                }
+                load_row(ri + 2, qc);
+                planes_of(qa, P2);
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) qa[q] = qb[q], qb[q] = qc[q];
+#pragma unroll
+                for (int p = 0; p < NPL; ++p) {
+                    L2[p] = shl(P2[p]);
+                    R2[p] = shr(P2[p]);
+                }
             }
             if (i < 2) continue;
             // detect row rd = ri - 1 (planes rows ri-2, ri-1, ri)
             const int rd = ri - 1;
-            uint32_t diff = 0;
+            uint32_t rawn;
+            if constexpr (MODE == MB_FILL || MODE == MB_REMOVE) {
+                rawn = rd >= 0 && rd < H ? m1 : 0u;  // the input mask enters as the raw rows
+            } else {
+                uint32_t diff = 0;
 #pragma unroll
-            for (int p = 0; p < NPL; ++p) {
-                const uint32_t c = P1[p];
-                diff |= (c ^ P0[p]) | (c ^ L0[p]) | (c ^ R0[p]) | (c ^ L1[p]) | (c ^ R1[p]) |
-                        (c ^ P2[p]) | (c ^ L2[p]) | (c ^ R2[p]);
+                for (int p = 0; p < NPL; ++p) {
+                    const uint32_t c = P1[p];
+                    diff |= (c ^ P0[p]) | (c ^ L0[p]) | (c ^ R0[p]) | (c ^ L1[p]) | (c ^ R1[p]) |
+                            (c ^ P2[p]) | (c ^ L2[p]) | (c ^ R2[p]);
+                }
+                rawn = rd >= 0 && rd < H ? diff & valid : 0u;
             }
-            const uint32_t rawn = rd >= 0 && rd < H ? diff & valid : 0u;
             if (out_lane && rd >= yb && rd < yb + MB_ROWS && rd < H) {
                 n_raw += __popc(rawn);
-                if (f.full) store_bits_as_bytes(f.mraw + (size_t)rd * f.P + 32 * wc, rawn);
+                if constexpr (MODE == MB_FRAME) {
+                    if (f.full) store_bits_as_bytes(f.mraw + (size_t)rd * f.P + 32 * wc, rawn);
+                } else if constexpr (MODE == MB_DET16) {
+                    uint32_t* o = rbits + (size_t)rd * f.bits_words + wc;
+                    *o = poff ? (*o | rawn) : rawn;
+                }
             }
+            if constexpr (MODE == MB_DET16) continue;
             raw0 = raw1, raw1 = raw2, raw2 = rawn;  // rows rd-2, rd-1, rd
             if (i < 4) continue;
             // fill row rf = rd - 1 (raw rows rd-2, rd-1, rd)
             const int rf = rd - 1;
             uint32_t filn = raw1;
-            if (rf >= 1 && rf <= H - 2) {
+            if constexpr (MODE == MB_REMOVE) {
+                filn = rf >= 0 && rf < H ? m2 : 0u;  // the input mask enters as the filled rows
+            } else if (rf >= 1 && rf <= H - 2) {
                 const uint32_t all8 = raw0 & shl(raw0) & shr(raw0) & shl(raw1) & shr(raw1) & raw2 &
                                       shl(raw2) & shr(raw2);
                 filn |= all8 & icol;
+            }
+            if constexpr (MODE == MB_FILL) {
+                if (out_lane && rf >= yb && rf < yb + MB_ROWS && rf < H)
+                    rbits[(size_t)rf * f.bits_words + wc] = filn;
+                continue;
             }
             fil0 = fil1, fil1 = fil2, fil2 = filn;  // rows rf-2, rf-1, rf
             if (i < 6) continue;
@@ -293,6 +367,7 @@ __global__ void __launch_bounds__(128) k_morph_bits(Frame f, uint32_t* __restric
             }
         }
     }
+    if constexpr (MODE != MB_FRAME) return;
     for (int o = 16; o > 0; o >>= 1) {
         n_raw += __shfl_xor_sync(0xffffffffu, n_raw, o);
         n_ref += __shfl_xor_sync(0xffffffffu, n_ref, o);
@@ -307,6 +382,38 @@ __global__ void __launch_bounds__(128) k_morph_bits(Frame f, uint32_t* __restric
         const unsigned long long b = red[1][0] + red[1][1] + red[1][2] + red[1][3];
         if (a) atomicAdd(&f.sc->raw_count, a);
         if (b) atomicAdd(&f.sc->refined_count, b);
+    }
+}
+
+// Stage entries: B1's result bits -> the reference's bytes.  detect: 0/1;
+// fill: out = mask copy with filled zeros set to 1 (boundary.cpp:42, :58);
+// remove: out = mask copy with removed pixels cleared (boundary.cpp:66, :81).
+template <int MODE>
+__global__ void __launch_bounds__(256) k_bits_to_bytes(Frame f, const uint32_t* __restrict__ rbits,
+                                                       const uint8_t* __restrict__ in,
+                                                       uint8_t* __restrict__ out) {
+    const int BW = (f.W + 31) / 32;
+    const long long nw = (long long)BW * f.H;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nw;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(i / BW), wc = (int)(i - (long long)y * BW);
+        const uint32_t b = rbits[(size_t)y * f.bits_words + wc];
+        uint8_t* o = out + (size_t)y * f.P + 32 * wc;
+        if constexpr (MODE == MB_DET16) {
+            store_bits_as_bytes(o, b);
+        } else {
+            const uint4* ip = reinterpret_cast<const uint4*>(in + (size_t)y * f.P + 32 * wc);
+            uint4 v[2] = {ip[0], ip[1]};
+            uint32_t* vw = reinterpret_cast<uint32_t*>(v);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t flag = bits_to_bytes4((b >> (4 * k)) & 15u);  // 0/1 bytes
+                if constexpr (MODE == MB_FILL) vw[k] = vw[k] | (flag & ~__vcmpne4(vw[k], 0u));
+                else vw[k] &= flag * 0xffu;
+            }
+            reinterpret_cast<uint4*>(o)[0] = v[0];
+            reinterpret_cast<uint4*>(o)[1] = v[1];
+        }
     }
 }
 
@@ -1041,14 +1148,163 @@ void launch_boundary_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int
     while ((1 << npl) < f.kcfg && npl < 8) ++npl;
     const int gb = (warps + 3) / 4;
     switch (npl) {
-        case 1: k_morph_bits<1><<<gb, 128, 0, st>>>(f, rbits); break;
-        case 2: k_morph_bits<2><<<gb, 128, 0, st>>>(f, rbits); break;
-        case 3: k_morph_bits<3><<<gb, 128, 0, st>>>(f, rbits); break;
-        case 4: k_morph_bits<4><<<gb, 128, 0, st>>>(f, rbits); break;
-        default: k_morph_bits<8><<<gb, 128, 0, st>>>(f, rbits); break;
+        case 1: k_morph_bits<1, MB_FRAME><<<gb, 128, 0, st>>>(f, rbits, nullptr, 0); break;
+        case 2: k_morph_bits<2, MB_FRAME><<<gb, 128, 0, st>>>(f, rbits, nullptr, 0); break;
+        case 3: k_morph_bits<3, MB_FRAME><<<gb, 128, 0, st>>>(f, rbits, nullptr, 0); break;
+        case 4: k_morph_bits<4, MB_FRAME><<<gb, 128, 0, st>>>(f, rbits, nullptr, 0); break;
+        default: k_morph_bits<8, MB_FRAME><<<gb, 128, 0, st>>>(f, rbits, nullptr, 0); break;
     }
     launch_ccl_prune_bits(f, rbits, runroot, bord, sbits, sbits_words, anchors, st);
     if (want_list) k_list_bits<<<f.n_chunks, 128, 0, st>>>(f);
+}
+
+// Stage entries detect_boundaries / morph_fill / morph_remove on B1 (the frame
+// path's word-parallel morphology), then bits -> the reference's bytes.
+// mode: 1 detect (src = u16 labels, pitch 2P), 2 fill, 3 remove (src = byte
+// mask, pitch P); out = pitched bytes.
+void launch_morph_stage_bits(const Frame& f, int mode, const uint8_t* src, uint32_t* rbits,
+                             uint8_t* out, cudaStream_t st) {
+    if (f.N == 0) return;
+    const int BW = (f.W + 31) / 32;
+    const int strips = (BW + MB_WPW - 1) / MB_WPW, bands = (f.H + MB_ROWS - 1) / MB_ROWS;
+    const int gb = (strips * bands + 3) / 4;
+    const long long nw = (long long)BW * f.H;
+    const int cb = (int)std::min<long long>((nw + 255) / 256, f.sms * 8);
+    if (mode == MB_DET16) {
+        k_morph_bits<8, MB_DET16><<<gb, 128, 0, st>>>(f, rbits, src, 0);  // label bits 0..7
+        k_morph_bits<8, MB_DET16><<<gb, 128, 0, st>>>(f, rbits, src, 8);  // label bits 8..15
+        k_bits_to_bytes<MB_DET16><<<cb, 256, 0, st>>>(f, rbits, nullptr, out);
+    } else if (mode == MB_FILL) {
+        k_morph_bits<1, MB_FILL><<<gb, 128, 0, st>>>(f, rbits, src, 0);
+        k_bits_to_bytes<MB_FILL><<<cb, 256, 0, st>>>(f, rbits, src, out);
+    } else {
+        k_morph_bits<1, MB_REMOVE><<<gb, 128, 0, st>>>(f, rbits, src, 0);
+        k_bits_to_bytes<MB_REMOVE><<<cb, 256, 0, st>>>(f, rbits, src, out);
+    }
+}
+
+// ------------------------------------------------ label_components ------
+// The stage entry label_components (boundary.cpp:87-148) on the frame path's
+// run CCL (B2/B3): the reference's label of a component is the rank, in raster
+// order, of its first pixel (its minimum raster index g, which B2/B4 keep at
+// every root).  L1 compresses the region-root forest (as B4); L2 marks g of
+// every root in a raster bitmap and counts roots; the bitmap's word popcounts
+// are scanned (cub, in place); L3 gives each root label = rank(g) = word
+// offset + popcount below g, sizes[label], ids[label] = label; L4 writes the
+// per-pixel labels from the runs (-1 on unset pixels).
+namespace {
+
+__global__ void __launch_bounds__(256) k_cc_compress(Frame f) {
+    const int n = (int)f.sc->n_lroots;
+    for (int id = blockIdx.x * blockDim.x + threadIdx.x; id < n; id += gridDim.x * blockDim.x) {
+        const int r = gfind(f.par, id);
+        if (r != id) {
+            f.par[id] = r;
+            atomicAdd(f.cnt + r, __ldcg(f.cnt + id));
+            atomicMin(f.roots + r, __ldcg(f.roots + id));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_cc_mark(Frame f, uint32_t* __restrict__ gbits) {
+    const int n = (int)f.sc->n_lroots;
+    unsigned nr = 0;
+    for (int id = blockIdx.x * blockDim.x + threadIdx.x; id < n; id += gridDim.x * blockDim.x) {
+        if (__ldcg(f.par + id) == id) {
+            const int g = __ldcg(f.roots + id);
+            atomicOr(gbits + (g >> 5), 1u << (g & 31));
+            ++nr;
+        }
+    }
+    nr = __reduce_add_sync(0xffffffffu, nr);
+    if ((threadIdx.x & 31) == 0 && nr) atomicAdd(&f.sc->n_roots, nr);
+}
+
+__global__ void __launch_bounds__(256) k_cc_popc(const uint32_t* __restrict__ gbits, uint32_t* __restrict__ wcnt,
+                                                 int nw) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x)
+        wcnt[i] = __popc(gbits[i]);
+}
+
+__global__ void __launch_bounds__(256) k_cc_root_labels(Frame f, const uint32_t* __restrict__ gbits,
+                                                        const uint32_t* __restrict__ woff,
+                                                        uint32_t* __restrict__ sizes, int32_t* __restrict__ ids) {
+    const int n = (int)f.sc->n_lroots;
+    for (int id = blockIdx.x * blockDim.x + threadIdx.x; id < n; id += gridDim.x * blockDim.x) {
+        if (__ldcg(f.par + id) != id) continue;
+        const int g = __ldcg(f.roots + id);
+        const int label = (int)(woff[g >> 5] + __popc(gbits[g >> 5] & ((1u << (g & 31)) - 1u)));
+        f.rank[id] = label;
+        sizes[label] = __ldcg(f.cnt + id);
+        ids[label] = label;
+    }
+}
+
+__global__ void __launch_bounds__(128) k_cc_write_labels(Frame f, const uint32_t* __restrict__ rbits,
+                                                         const int32_t* __restrict__ runroot,
+                                                         int32_t* __restrict__ labels) {
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int TXc = (f.W + CT - 1) / CT, TYc = (f.H + CT - 1) / CT;
+    const int tile = blockIdx.x * 4 + wid;
+    if (tile >= TXc * TYc) return;
+    const int tx = tile % TXc, x0 = tx * CT, y = (tile / TXc) * CT + lane;
+    const uint32_t m = y < f.H ? __ldg(rbits + (size_t)y * f.bits_words + tx) : 0u;
+    const uint32_t s = m & ~(m << 1);
+    const int nr = __popc(s);
+    int rinc = nr;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, rinc, o);
+        if (lane >= o) rinc += v;
+    }
+    if (y >= f.H) return;
+    const int32_t* rr = runroot + (size_t)tile * kRunCap + (rinc - nr);
+    int32_t* out = labels + (size_t)y * f.W + x0;
+    const int nx = min(CT, f.W - x0);
+    int k = 0, x = 0;
+    for (uint32_t t = s; t; t &= t - 1, ++k) {
+        const int a = __ffs(t) - 1, len = run_len(m, a);
+        const int lab = __ldcg(f.rank + __ldcg(f.par + __ldg(rr + k)));
+        for (; x < a; ++x) out[x] = -1;
+        for (; x < a + len; ++x) out[x] = lab;
+    }
+    for (; x < nx; ++x) out[x] = -1;
+}
+
+}  // namespace
+
+// mask (pitched bytes) -> labels (dense i32, -1 unset), sizes[C], ids[C] =
+// 0..C-1 (the caller sorts them into by_size); C in f.sc->n_roots.  gbits:
+// N/32-word raster bitmap, wscan: >= N/32 + 1 words, tmp/tmp_bytes: cub.
+void launch_label_components_bits(const Frame& f, const uint8_t* mask, uint32_t* rbits, int32_t* runroot,
+                                  int32_t* bord, uint32_t* gbits, int gbits_words, uint32_t* wscan,
+                                  void* tmp, size_t tmp_bytes, int32_t* labels, uint32_t* sizes,
+                                  int32_t* ids, cudaStream_t st) {
+    if (f.N == 0) return;
+    const long long nw = (long long)((f.W + 31) / 32) * f.H;
+    const int gb = (int)std::min<long long>((nw + 255) / 256, f.sms * 8);
+    k_mask_to_bits<<<gb, 256, 0, st>>>(f, mask, rbits);
+    const int nreg = ((f.W + RW - 1) / RW) * ((f.H + RH - 1) / RH);
+    const size_t rsm = sizeof(RunSmem) * NRW;
+    cudaFuncSetAttribute(k_ccl_region, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
+    k_ccl_region<<<nreg, 32 * NRW, rsm, st>>>(f, rbits, runroot, bord);  // B2
+    k_ccl_borders<<<nreg, RW + RH, 0, st>>>(f, bord);                    // B3
+    const int ib = f.sms * 4;
+    k_cc_compress<<<ib, 256, 0, st>>>(f);
+    cudaMemsetAsync(gbits, 0, (size_t)gbits_words * 4, st);
+    k_cc_mark<<<ib, 256, 0, st>>>(f, gbits);
+    k_cc_popc<<<(gbits_words + 255) / 256, 256, 0, st>>>(gbits, wscan, gbits_words);
+    size_t need = tmp_bytes;
+    cub::DeviceScan::ExclusiveSum(tmp, need, wscan, wscan, gbits_words, st);  // in place
+    k_cc_root_labels<<<ib, 256, 0, st>>>(f, gbits, wscan, sizes, ids);
+    const int ntiles = ((f.W + CT - 1) / CT) * ((f.H + CT - 1) / CT);
+    k_cc_write_labels<<<(ntiles + 3) / 4, 128, 0, st>>>(f, rbits, runroot, labels);
+}
+
+size_t label_components_tmp_bytes(int gbits_words) {
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, (uint32_t*)nullptr, (uint32_t*)nullptr, gbits_words);
+    return need;
 }
 
 }  // namespace stk

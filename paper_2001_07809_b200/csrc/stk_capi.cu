@@ -96,7 +96,7 @@ struct Slot {
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
     // tensor maps
-    TMap tm_morph, tm_sadL, tm_sadR, tm_stage;
+    TMap tm_sadL, tm_sadR;
     // graph
     cudaGraphExec_t gexec = nullptr;
     GraphKey gkey;
@@ -1074,17 +1074,20 @@ stk_status stk_assign_pixels(stk_ctx* ctx, const uint8_t* gray, int w, int h,
     FINISH();
 }
 
+// detect / fill / remove on the frame path's B1 kernel (k_morph_bits in stage
+// mode: the same word-parallel morphology and edge rules the frame runs).
 static stk_status morph_stage(stk_ctx* ctx, int mode, const void* in, int w, int h, uint8_t* out) {
     STAGE_BEGIN(w, h);
     if (N == 0) return STK_OK;
+    const uint8_t* src;
     if (mode == MORPH_DETECT16) {
         H2D_PLANE(s.scratch16, in, 2);
-        TRY(encode(ctx, s.tm_stage, s.scratch16, 2, w, h, s.P * 2, 160, 38));
+        src = reinterpret_cast<const uint8_t*>(s.scratch16);
     } else {
         H2D_PLANE(s.mref, in, 1);
-        TRY(encode(ctx, s.tm_stage, s.mref, 1, w, h, s.P, 160, 38));
+        src = s.mref;
     }
-    launch_morph(f, mode, &s.tm_stage.map, s.mraw, nullptr, st);
+    launch_morph_stage_bits(f, mode, src, s.rbits, s.mraw, st);
     D2H_PLANE(out, s.mraw, 1);
     FINISH();
 }
@@ -1110,33 +1113,41 @@ stk_status stk_label_components(stk_ctx* ctx, const uint8_t* mask, int w, int h,
     if (N == 0) return STK_OK;
     H2D_PLANE(s.mref, mask, 1);
     CK(cudaMemsetAsync(s.sc, 0, sizeof(DevScalars), st));
-    CK(cudaMemsetAsync(s.lb, 0, sizeof(unsigned long long) * LB_COUNT * s.lb_stride, st));
-    f.full = 1;
     f.frac = 0.0;
-    launch_ccl(f, st);
+    // ComponentTable (boundary.hpp:39-45) from the frame path's run CCL
+    // (k_bnd.cu B2/B3 + label kernels): canonical labels = rank of the
+    // component's first pixel in raster order; sizes by label; by_size =
+    // STABLE radix sort of the label ids by size, i.e. (size asc, label asc)
+    // as boundary.cpp:136-146.  8-connected components are >= 2 px apart, so
+    // C <= ceil(W/2) * ceil(H/2) ids fit the 2*P*H-byte scratch plane.
+    uint32_t* d_sizes = s.szhist;                              // C
+    int32_t* d_ids = reinterpret_cast<int32_t*>(s.scratch16);  // C
+    int32_t* d_labels = reinterpret_cast<int32_t*>(s.list);    // N
+    const size_t scan_need = label_components_tmp_bytes(s.sbits_words);
+    if (scan_need > s.cub_bytes) {
+        if (s.cub_tmp) CK(cudaFree(s.cub_tmp));
+        s.cub_tmp = nullptr;
+        CK(cudaMalloc(&s.cub_tmp, scan_need));
+        s.cub_bytes = scan_need;
+    }
+    launch_label_components_bits(f, s.mref, s.rbits, s.runroot, s.bord, s.sbits, s.sbits_words,
+                                 s.mbits, s.cub_tmp, s.cub_bytes, d_labels, d_sizes, d_ids, st);
     CK(cudaMemcpyAsync(s.h_sc, s.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     const int C = (int)s.h_sc->n_roots;
     if ((size_t)C > cap) return fail(ctx, STK_EPARAM, "label_components: capacity too small");
-    // ComponentTable (boundary.hpp:39-45): canonical labels = rank of the root
-    // in raster order; sizes by label; by_size = STABLE radix sort of the
-    // label ids by size, i.e. (size asc, label asc) as boundary.cpp:136-146.
-    // 8-connected components are >= 2 px apart, so C <= N/4 + W + H fits the
-    // 2*P*H-byte scratch plane used for the ids.
-    uint32_t* d_sizes = s.szhist;                       // C
-    int32_t* d_ids = reinterpret_cast<int32_t*>(s.scratch16);  // C
-    int32_t* d_labels = reinterpret_cast<int32_t*>(s.list);    // N
-    launch_component_table(f, d_labels, d_sizes, d_ids, st);   // reads mref, par, rank, cnt, roots
     CK(cudaMemcpyAsync(labels, d_labels, 4 * N, cudaMemcpyDeviceToHost, st));
-    if (C > 0) CK(cudaMemcpyAsync(sizes, d_sizes, 4 * (size_t)C, cudaMemcpyDeviceToHost, st));
     if (C > 0) {
+        CK(cudaMemcpyAsync(sizes, d_sizes, 4 * (size_t)C, cudaMemcpyDeviceToHost, st));
         size_t need = 0;
-        uint32_t* k_out = reinterpret_cast<uint32_t*>(s.roots);  // read above, free now
-        int32_t* v_out = reinterpret_cast<int32_t*>(s.cnt);      // read above, free now
+        uint32_t* k_out = reinterpret_cast<uint32_t*>(s.roots);  // dense-id arrays: free now
+        int32_t* v_out = reinterpret_cast<int32_t*>(s.cnt);
         CK(cub::DeviceRadixSort::SortPairs(nullptr, need, d_sizes, k_out, d_ids, v_out, C, 0, 32, st));
         if (need > s.cub_bytes) {
+            CK(cudaStreamSynchronize(st));
             if (s.cub_tmp) CK(cudaFree(s.cub_tmp));
+            s.cub_tmp = nullptr;
             CK(cudaMalloc(&s.cub_tmp, need));
             s.cub_bytes = need;
         }
@@ -1216,7 +1227,7 @@ stk_status stk_match_boundary_pixels(stk_ctx* ctx, const uint8_t* left, const ui
     f.D = max_disparity;
     TRY(encode(ctx, s.tm_sadL, s.grayL, 1, w, h, s.P, 128, window));
     TRY(encode(ctx, s.tm_sadR, s.grayR, 1, w, h, s.P, 128, window));
-    launch_apply(f, false, false, st);
+    launch_apply(f, false, st);
     if (w >= window && h >= window) launch_sad(f, ctx->sad_kernel, &s.tm_sadL.map, &s.tm_sadR.map, st);
     CK(cudaMemcpyAsync(out, s.sparse, 2 * N, cudaMemcpyDeviceToHost, st));
     FINISH();
@@ -1245,7 +1256,7 @@ stk_status stk_dense_sad_baseline(stk_ctx* ctx, const uint8_t* left, const uint8
     f.D = max_disparity;
     TRY(encode(ctx, s.tm_sadL, s.grayL, 1, w, h, s.P, 128, window));
     TRY(encode(ctx, s.tm_sadR, s.grayR, 1, w, h, s.P, 128, window));
-    launch_apply(f, false, false, st);
+    launch_apply(f, false, st);
     if (w >= window && h >= window) launch_sad(f, ctx->sad_kernel, &s.tm_sadL.map, &s.tm_sadR.map, st);
     CK(cudaMemcpyAsync(out, s.sparse, 2 * N, cudaMemcpyDeviceToHost, st));
     FINISH();

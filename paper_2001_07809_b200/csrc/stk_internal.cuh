@@ -129,13 +129,9 @@ void launch_histogram(const Frame& f, const uint8_t* gray, cudaStream_t st);
 void launch_kmeans(const Frame& f, int k_fixed, int max_iter, double tol, cudaStream_t st);
 void launch_assign(const Frame& f, const uint8_t* gray, uint16_t* out, cudaStream_t st);
 
-enum MorphMode { MORPH_FUSED = 0, MORPH_DETECT16 = 1, MORPH_FILL = 2, MORPH_REMOVE = 3 };
-void launch_morph(const Frame& f, int mode, const CUtensorMap* tmap, uint8_t* out_a,
-                  uint8_t* out_b, cudaStream_t st);
+// stage modes of the frame path's B1 kernel (k_bnd.cu MB_*)
+enum MorphMode { MORPH_DETECT16 = 1, MORPH_FILL = 2, MORPH_REMOVE = 3 };
 
-void launch_ccl(const Frame& f, cudaStream_t st);                 // K4a-c (+ roots, hist)
-void launch_ccl_compress(const Frame& f, cudaStream_t st);        // K4c alone
-void launch_prune_select(const Frame& f, cudaStream_t st);        // K4e alone
 // Bit-packed boundary stage of the frame path (k_bnd.cu): morphology from
 // gray, run-based CCL, prune, anchors, matchable bits and frame counts
 // (+ raw / pruned / anchored bytes in full mode; + the SAD list if asked).
@@ -145,6 +141,14 @@ void launch_boundary_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int
 // B2-B8 alone on refined bits already in rbits (refined_count set)
 void launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
                            uint32_t* sbits, int sbits_words, bool anchors, cudaStream_t st);
+// stage entries detect_boundaries / morph_fill / morph_remove on B1
+void launch_morph_stage_bits(const Frame& f, int mode, const uint8_t* src, uint32_t* rbits,
+                             uint8_t* out, cudaStream_t st);  // B1 in stage mode (k_bnd.cu)
+void launch_label_components_bits(const Frame& f, const uint8_t* mask, uint32_t* rbits, int32_t* runroot,
+                                  int32_t* bord, uint32_t* gbits, int gbits_words, uint32_t* wscan,
+                                  void* tmp, size_t tmp_bytes, int32_t* labels, uint32_t* sizes,
+                                  int32_t* ids, cudaStream_t st);  // run CCL labels (k_bnd.cu)
+size_t label_components_tmp_bytes(int gbits_words);
 // stage entry prune_components on a pitched byte mask (writes f.mprn / f.manc)
 void launch_prune_mask_bits(const Frame& f, const uint8_t* mask, uint32_t* rbits, int32_t* runroot,
                             int32_t* bord, uint32_t* sbits, int sbits_words, cudaStream_t st);
@@ -155,12 +159,9 @@ void launch_bad_pixel(const int16_t* comp, const int16_t* truth, long long n, do
                       unsigned long long* out, cudaStream_t st);
 // true when launch_sad will run the per-pixel list kernel (it needs f.list)
 bool sad_uses_list(const Frame& f, int kernel);
-void launch_prune(const Frame& f, bool anchors, cudaStream_t st); // K4e-g
-void launch_apply(const Frame& f, bool use_prune, bool anchors, cudaStream_t st);
-void launch_count_mask(const Frame& f, const uint8_t* mask, cudaStream_t st);
+// stage entries: byte mask (f.mref) -> matchable bits + list (k_apply.cu)
+void launch_apply(const Frame& f, bool anchors, cudaStream_t st);
 void launch_anchor_only(const Frame& f, const uint8_t* in, uint8_t* out, int margin, cudaStream_t st);
-void launch_component_table(const Frame& f, int32_t* d_labels, uint32_t* d_sizes, int32_t* d_ids,
-                            cudaStream_t st);
 size_t sad_list_smem_bytes(int window, int D);
 size_t blur_smem_bytes(int hw, bool exact);
 void launch_sad_cost(const Frame& f, int x, int y, int d, uint32_t* out, cudaStream_t st);

@@ -328,7 +328,7 @@ def test_graph_survives_focus_table_reallocation(dev, stk, port, synth):
     assert np.abs(img.astype(int) - want["refocused"].astype(int)).max() <= BLUR_TOL_LSB
     # grow the weights (67 x 67 taps) and the LUT (D = 1100) on the same slot
     bmap = np.ones((H, W), np.uint8)
-    stk.selective_blur(l, bmap, stk.gaussian_kernel(11.0, 67), device=dev)
+    stk.selective_blur(l, bmap, stk.gaussian_kernel(11.0, 67), sigma=11.0, device=dev)
     stk.build_blur_map(np.zeros((H, W), np.int16), [(0, 5)], 1100, device=dev)
     res2, img2 = run(stk, dev, l, r, k=4, window=9, D=16, focus=[(8, 16)])
     eq(res2.dense, want["dense"], "dense after realloc")

@@ -106,6 +106,27 @@ def test_detect_fill_remove_edge_cases(dev, stk, port, synth):
         eq(stk.detect_boundaries(lab, device=dev), port.detect(lab))
 
 
+def test_detect_fill_remove_hot_path_kernel_cases(dev, stk, port, synth):
+    """The stage entries run the frame path's B1 kernel (k_morph_bits in stage
+    mode).  Cases beyond the frame's own inputs: 16-bit labels above 255 (the
+    second bit-plane pass), label pairs differing only in high bits, mask
+    bytes other than 0/1 (the reference copies them through, boundary.cpp:42,
+    :66), widths around the 32-pixel word and the 30-word warp strip, and
+    heights around the 8-row band."""
+    rng = np.random.default_rng(7)
+    for w, h in ((31, 9), (32, 8), (33, 17), (959, 7), (960, 16), (961, 3), (1000, 41)):
+        lab = rng.integers(0, 65536, size=(h, w), dtype=np.uint16)
+        lab[: h // 2] = lab[: h // 2] & 0xFF00  # blocks equal in the low byte
+        lab[:, ::7] = 0x8000
+        eq(stk.detect_boundaries(lab, device=dev), port.detect(lab))
+        lab2 = (synth.random_gray(w, h, w * h) % 2).astype(np.uint16) * 0x0100  # only bit 8 differs
+        eq(stk.detect_boundaries(lab2, device=dev), port.detect(lab2))
+        m = synth.random_mask(w, h, w + 3 * h, 70)
+        m = m * rng.choice(np.array([1, 2, 255], np.uint8), size=m.shape)
+        eq(stk.morph_fill(m, device=dev), port.fill(m))
+        eq(stk.morph_remove(m, device=dev), port.remove(m))
+
+
 def test_morph_golden(dev, stk, golden, synth):
     for s in range(20):
         m = synth.random_mask(40, 30, 400 + s, 35)
@@ -134,6 +155,31 @@ def test_components_and_prune_random(dev, stk, port, synth, w, h, pct):
     eq(t.by_size, bys)
     for frac in (0.0, 0.04, 0.1, 0.5, 0.999):
         eq(stk.prune_components(m, frac, device=dev), port.prune(m, frac))
+
+
+@pytest.mark.parametrize("case", ["random_1080p", "comb", "frame_mask"])
+def test_components_run_ccl_large(dev, stk, port, synth, case):
+    """label_components on the frame path's run CCL (B2 region merge, B3
+    global union, label kernels): large masks crossing many 128x64 regions,
+    one giant component, and a real frame's refined boundary mask."""
+    if case == "random_1080p":
+        m = synth.random_mask(1920, 1080, 99, 45)
+    elif case == "comb":
+        m = np.zeros((300, 700), np.uint8)
+        m[5, :] = 1
+        m[5:290, ::31] = 1
+        m[63:65, :600] = 1
+        m[100:300:4, 3:700:5] = 1
+        m[31:33, 127:129] = 1
+    else:
+        l, r = synth.dead_leaves(1024, 576, 32, frame=3)
+        res = port.run_frame(l, r, k=6, window=9, max_disparity=32)
+        m = res["boundary_refined"]
+    t = stk.label_components(m, device=dev)
+    lab, sz, bys = port.label_components(m)
+    eq(t.labels, lab)
+    eq(t.sizes, sz)
+    eq(t.by_size, bys)
 
 
 def test_prune_golden_and_spec(dev, stk, golden, synth):
