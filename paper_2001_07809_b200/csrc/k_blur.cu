@@ -579,6 +579,94 @@ __global__ void k_blur_map(Frame f, const int16_t* __restrict__ depth, const uin
     }
 }
 
+// Global-memory fallback for kernels too wide for a shared-memory tile (any
+// odd size; refocus.cpp:16-43 puts no upper bound on it).  Separable: pass 1
+// sums each pixel's column window (FP32, taps in order) into a float plane,
+// pass 2 sums the row window of those and rounds (the v3 order: vertical
+// first); exact: FP64 2-D per pixel in the reference's order.
+__global__ void __launch_bounds__(256) k_blur_vert_global(Frame f, BlurParams bp,
+                                                          const uint8_t* __restrict__ in) {
+    const int K = 2 * bp.hw + 1, h = bp.hw, W = f.W, H = f.H;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < f.N;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(i / W), x = (int)(i - (long long)y * W);
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+        for (int k = 0; k < K; ++k) {
+            const int sy = min(max(y + k - h, 0), H - 1);
+            const uint8_t* p = in + ((size_t)sy * W + x) * 3;
+            const float wt = __ldg(bp.g1 + k);
+            a0 = fmaf(wt, (float)p[0], a0);
+            a1 = fmaf(wt, (float)p[1], a1);
+            a2 = fmaf(wt, (float)p[2], a2);
+        }
+        bp.scratch[3 * i] = a0;
+        bp.scratch[3 * i + 1] = a1;
+        bp.scratch[3 * i + 2] = a2;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_blur_horz_global(Frame f, BlurParams bp,
+                                                          const uint8_t* __restrict__ in,
+                                                          uint8_t* __restrict__ out,
+                                                          const int16_t* __restrict__ depth) {
+    const int K = 2 * bp.hw + 1, h = bp.hw, W = f.W;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < f.N;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(i / W), x = (int)(i - (long long)y * W);
+        if (sharp_px(bp, f, depth, x, y)) {
+            out[3 * i] = in[3 * i];
+            out[3 * i + 1] = in[3 * i + 1];
+            out[3 * i + 2] = in[3 * i + 2];
+            continue;
+        }
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+        const float* row = bp.scratch + (size_t)y * W * 3;
+        for (int k = 0; k < K; ++k) {
+            const int sx = min(max(x + k - h, 0), W - 1);
+            const float wt = __ldg(bp.g1 + k);
+            a0 = fmaf(wt, row[3 * sx], a0);
+            a1 = fmaf(wt, row[3 * sx + 1], a1);
+            a2 = fmaf(wt, row[3 * sx + 2], a2);
+        }
+        out[3 * i] = (uint8_t)min(max((int)floorf(a0 + 0.5f), 0), 255);
+        out[3 * i + 1] = (uint8_t)min(max((int)floorf(a1 + 0.5f), 0), 255);
+        out[3 * i + 2] = (uint8_t)min(max((int)floorf(a2 + 0.5f), 0), 255);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_blur_exact_global(Frame f, BlurParams bp,
+                                                           const uint8_t* __restrict__ in,
+                                                           uint8_t* __restrict__ out,
+                                                           const int16_t* __restrict__ depth) {
+    const int K = 2 * bp.hw + 1, h = bp.hw, W = f.W, H = f.H;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < f.N;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(i / W), x = (int)(i - (long long)y * W);
+        if (sharp_px(bp, f, depth, x, y)) {
+            out[3 * i] = in[3 * i];
+            out[3 * i + 1] = in[3 * i + 1];
+            out[3 * i + 2] = in[3 * i + 2];
+            continue;
+        }
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        for (int r = 0; r < K; ++r) {  // i outer, j inner (refocus.cpp:95-105)
+            const int sy = min(max(y + r - h, 0), H - 1);
+            const uint8_t* row = in + (size_t)sy * W * 3;
+            const double* wr = bp.g2 + (size_t)r * K;
+            for (int c = 0; c < K; ++c) {
+                const int sx = min(max(x + c - h, 0), W - 1);
+                const double wt = __ldg(wr + c);
+                a0 = __dadd_rn(a0, __dmul_rn(wt, (double)row[3 * sx]));
+                a1 = __dadd_rn(a1, __dmul_rn(wt, (double)row[3 * sx + 1]));
+                a2 = __dadd_rn(a2, __dmul_rn(wt, (double)row[3 * sx + 2]));
+            }
+        }
+        out[3 * i] = (uint8_t)min(max(lround(a0), 0L), 255L);
+        out[3 * i + 1] = (uint8_t)min(max(lround(a1), 0L), 255L);
+        out[3 * i + 2] = (uint8_t)min(max(lround(a2), 0L), 255L);
+    }
+}
+
 size_t tile_bytes(int hw) {
     const int IW = BX + 2 * hw, IH = BY + 2 * hw;
     return (size_t)IH * ((((size_t)IW * 3 + 15) & ~(size_t)15) + 16);
@@ -586,17 +674,41 @@ size_t tile_bytes(int hw) {
 
 }  // namespace
 
+constexpr size_t kBlurSmemMax = 220 * 1024;
+
+bool v3_sizes(int K) {
+    switch (K) {
+        case 3: case 5: case 7: case 9: case 11: case 13: case 17: case 19: case 23: case 25:
+        case 31: case 37: case 43: case 49: return true;
+        default: return false;
+    }
+}
+
 size_t blur_smem_bytes(int hw, bool exact) {
     const int K = 2 * hw + 1, IH = BY + 2 * hw;
     if (exact) return (size_t)K * K * sizeof(double) + tile_bytes(hw);
     return (((size_t)K * 4 + 15) & ~(size_t)15) + (size_t)IH * BX * sizeof(float4) + tile_bytes(hw);
 }
 
-void launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, uint8_t* out_rgb,
-                 const int16_t* depth, cudaStream_t st) {
-    if (f.N == 0) return;
+bool blur_needs_scratch(int hw, bool exact) {
+    return !exact && !v3_sizes(2 * hw + 1) && blur_smem_bytes(hw, false) > kBlurSmemMax;
+}
+
+int launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, uint8_t* out_rgb,
+                const int16_t* depth, cudaStream_t st) {
+    if (f.N == 0) return 0;
     const dim3 grid((f.W + BX - 1) / BX, (f.H + BY - 1) / BY);
     const size_t sm = blur_smem_bytes(bp.hw, bp.exact != 0);
+    const int gblocks = (int)std::min<long long>((f.N + 255) / 256, f.sms * 16);
+    if (bp.exact && sm > kBlurSmemMax) {
+        k_blur_exact_global<<<gblocks, 256, 0, st>>>(f, bp, in_rgb, out_rgb, depth);
+        return 1;
+    }
+    if (!bp.exact && blur_needs_scratch(bp.hw, false)) {
+        k_blur_vert_global<<<gblocks, 256, 0, st>>>(f, bp, in_rgb);
+        k_blur_horz_global<<<gblocks, 256, 0, st>>>(f, bp, in_rgb, out_rgb, depth);
+        return 2;
+    }
     if (bp.exact) {
         cudaFuncSetAttribute(k_blur_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         k_blur_exact<<<grid, kThreads, sm, st>>>(f, bp, in_rgb, out_rgb, depth);
@@ -609,7 +721,7 @@ void launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, ui
         cudaFuncSetAttribute(k_blur_v3<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                              (int)V3Geom<KK>::SM);                                              \
         k_blur_v3<KK><<<g3, V3Geom<KK>::NT, V3Geom<KK>::SM, st>>>(f, bp, in_rgb, out_rgb, depth); \
-        return;
+        return 1;
             switch (K) {
                 STK_BLUR_V3(3)
                 STK_BLUR_V3(5)
@@ -636,7 +748,7 @@ void launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, ui
         cudaFuncSetAttribute(k_blur_sep_k<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
                              (int)smk);                                                         \
         k_blur_sep_k<KK><<<grid, kThreads, smk, st>>>(f, bp, in_rgb, out_rgb, depth);           \
-        return;
+        return 1;
         switch (K) {
             STK_BLUR_K(3)
             STK_BLUR_K(5)
@@ -653,6 +765,7 @@ void launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, ui
         cudaFuncSetAttribute(k_blur_sep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         k_blur_sep<<<grid, kThreads, sm, st>>>(f, bp, in_rgb, out_rgb, depth);
     }
+    return 1;
 }
 
 void launch_blur_map(const Frame& f, const int16_t* depth, const uint8_t* sharp_lut, int lut_len,

@@ -143,6 +143,47 @@ void run_list(const Frame& f, const CUtensorMap* tmL, const CUtensorMap* tmR, cu
     k_sad_list<MAXJ><<<f.sms * std::max(per_sm, 1), kThreads, sm, st>>>(*tmL, *tmR, f);
 }
 
+// K5w sad_wide: any window and disparity range (the reference accepts any odd
+// window >= 1 and any max_disparity >= 0, stereo.cpp:49-57).  One warp per
+// list entry, lanes = disparities d = lane + 32 j (ascending per lane, strict
+// <), exact u32 sums (wrapping like the reference's uint32_t) of byte SADs four
+// at a time from the pitched gray planes (L2-resident); the winner is the warp
+// minimum of the 64-bit key (cost << 32 | d): ties to the smallest d.
+__global__ void __launch_bounds__(kThreads) k_sad_wide(Frame f) {
+    const int w = f.window, h = f.hw, D = f.D;
+    const int nw = (w + 3) >> 2;
+    const uint32_t tail = (w & 3) ? (0xffffffffu >> (32 - 8 * (w & 3))) : 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const long long n = f.sc->n_list;
+    for (long long e = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; e < n;
+         e += ((long long)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t code = f.list[e];
+        const int x = (int)(code & 0xffffu), y = (int)(code >> 16);
+        const int dl = min(D, x - h);
+        unsigned long long best = ~0ull;
+        for (int d = lane; d <= dl; d += 32) {
+            uint32_t cost = 0;
+            for (int r = 0; r < w; ++r) {
+                const uint8_t* lrow = f.grayL + (size_t)(y - h + r) * f.P;
+                const uint8_t* rrow = f.grayR + (size_t)(y - h + r) * f.P;
+                for (int k = 0; k < nw; ++k) {
+                    const uint32_t m = k == nw - 1 ? tail : 0xffffffffu;
+                    cost = vsad4_acc(ld_unaligned(lrow, x - h + 4 * k) & m,
+                                     ld_unaligned(rrow, x - d - h + 4 * k) & m, cost);
+                }
+            }
+            const unsigned long long key = ((unsigned long long)cost << 32) | (uint32_t)d;
+            best = key < best ? key : best;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long v = __shfl_xor_sync(0xffffffffu, best, o);
+            best = v < best ? v : best;
+        }
+        if (lane == 0) f.sparse[(size_t)y * f.W + x] = (int16_t)(uint32_t)best;
+    }
+}
+
 // sad_cost for one (x, y, d) (stereo.cpp:12-28): one warp, lanes stride the
 // window rows, exact u32 sum.
 __global__ void k_sad_cost(Frame f, int x, int y, int d, uint32_t* out) {
@@ -171,6 +212,12 @@ size_t sad_list_smem_bytes(int window, int D) {
            (size_t)window * (nbR * kBox + 16);
 }
 
+// the TMA list kernel's reach: 16 words per window row, d in 10 key bits,
+// its staged rows in shared memory
+static bool list_fits(const Frame& f) {
+    return f.window <= 63 && f.D <= 1023 && sad_list_smem_bytes(f.window, f.D) <= 227 * 1024;
+}
+
 bool sad_uses_list(const Frame& f, int kernel) {
     if (f.N == 0 || f.W < f.window || f.H < f.window) return false;
     if ((kernel == SAD_AUTO || kernel == SAD_WS) && launch_sad_ws(f, nullptr, true)) return false;
@@ -183,6 +230,10 @@ void launch_sad(const Frame& f, int kernel, const CUtensorMap* tmL, const CUtens
     if (f.N == 0 || f.W < f.window || f.H < f.window) return;
     if ((kernel == SAD_AUTO || kernel == SAD_WS) && launch_sad_ws(f, st)) return;
     if (kernel != SAD_LIST && launch_sad_strip(f, st)) return;
+    if (!list_fits(f)) {
+        k_sad_wide<<<f.sms * 8, kThreads, 0, st>>>(f);
+        return;
+    }
     const int J = (f.D + 1 + 31) / 32;
     if (J <= 1) run_list<1>(f, tmL, tmR, st);
     else if (J <= 2) run_list<2>(f, tmL, tmR, st);

@@ -304,7 +304,7 @@ bool launch_sad_strip(const Frame& f, cudaStream_t st, bool dry) {
     g.h = f.hw;
     g.w = f.window;
     g.D = f.D;
-    if (g.w > 31 || f.W > 65535) return false;
+    if (g.w > 31 || g.D > 1023 || f.W > 65535) return false;  // key packs d in 10 bits
     g.Q = (g.D + 1 + 3) / 4;
     g.CW = SW + 2 * g.h;
     static const int kMaxc[] = {4, 8, 12, 16, 24};

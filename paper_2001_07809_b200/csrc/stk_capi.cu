@@ -28,8 +28,9 @@ namespace {
 
 thread_local std::string t_err;
 
-constexpr int kMaxWindow = 63;     // nw <= 16 words per window row (k_sad_list)
-constexpr int kMaxDisparity = 1023;  // argmin key packs d in 10 bits
+// Disparities are int16 (DisparityMap, stereo.hpp:13-40), so no map holds a
+// value above 32767: the focus LUT never needs more entries than this.
+constexpr int kMaxLut = 32768;
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -51,7 +52,7 @@ struct TMap {
 struct GraphKey {
     int W, H, kcfg, window, D, thr, full, focus, hw, exact, lut_len, sad, want_raw, pad_;
     double frac;
-    const void *rgbL, *rgbR, *out_rgb, *dense, *lut, *g1, *g2;
+    const void *rgbL, *rgbR, *out_rgb, *dense, *lut, *g1, *g2, *blur_tmp;
     GraphKey() { std::memset(this, 0, sizeof(*this)); W = H = -1; }
     bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
@@ -92,6 +93,9 @@ struct Slot {
     uint8_t* p_lut = nullptr;
     float* p_g1 = nullptr;
     double* p_g2 = nullptr;
+    // vertical-sum plane of the global-memory blur fallback (very wide kernels)
+    float* blur_tmp = nullptr;
+    size_t blur_tmp_bytes = 0;
     // label_components scratch
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
@@ -404,16 +408,6 @@ stk_status check_config(stk_ctx* ctx, const stk_config* c) {
     return STK_OK;
 }
 
-stk_status check_gpu_limits(stk_ctx* ctx, int window, int D) {
-    if (window > kMaxWindow)
-        return fail(ctx, STK_EPARAM, "stk_b200: window " + std::to_string(window) +
-                                         " exceeds the GPU kernel limit " + std::to_string(kMaxWindow));
-    if (D > kMaxDisparity)
-        return fail(ctx, STK_EPARAM, "stk_b200: max_disparity " + std::to_string(D) +
-                                         " exceeds the GPU kernel limit " + std::to_string(kMaxDisparity));
-    return STK_OK;
-}
-
 stk_status check_focus(stk_ctx* ctx, const stk_focus* fo, int D, int* size_out) {
     if (fo->n_ranges <= 0 || !fo->lo || !fo->hi)
         return fail(ctx, STK_EPARAM, "build_blur_map: no focus ranges given");
@@ -427,9 +421,6 @@ stk_status check_focus(stk_ctx* ctx, const stk_focus* fo, int D, int* size_out) 
         return fail(ctx, STK_EPARAM, "gaussian_kernel: sigma must be positive, got " + std::to_string(fo->sigma));
     if (size < 1 || size % 2 == 0)
         return fail(ctx, STK_EPARAM, "gaussian_kernel: size must be odd and positive, got " + std::to_string(size));
-    if (blur_smem_bytes(size / 2, fo->exact_blur != 0) > 220 * 1024)
-        return fail(ctx, STK_EPARAM, "stk_b200: blur kernel size " + std::to_string(size) +
-                                         " exceeds the GPU tile limit");
     *size_out = size;
     return STK_OK;
 }
@@ -437,7 +428,7 @@ stk_status check_focus(stk_ctx* ctx, const stk_focus* fo, int D, int* size_out) 
 // Upload the focus LUT and blur weights for slot s (host-cached).
 stk_status upload_focus(stk_ctx* ctx, Slot& s, const int* lo, const int* hi, int n, int D,
                         double sigma, int size, bool exact, BlurParams* bp) {
-    const int lut_len = D + 1;
+    const int lut_len = std::min(D, kMaxLut - 1) + 1;
     std::vector<uint8_t> lut(lut_len, 0);
     for (int d = 0; d < lut_len; ++d)
         for (int r = 0; r < n; ++r)
@@ -518,6 +509,28 @@ stk_status upload_focus(stk_ctx* ctx, Slot& s, const int* lo, const int* hi, int
     return STK_OK;
 }
 
+// The global-memory blur fallback's float plane (12 bytes per pixel), only
+// for separable kernels too wide for a shared-memory tile.
+stk_status ensure_blur_scratch(stk_ctx* ctx, Slot& s, size_t N, BlurParams* bp) {
+    bp->scratch = nullptr;
+    if (!blur_needs_scratch(bp->hw, bp->exact != 0)) return STK_OK;
+    const size_t need = 12 * std::max<size_t>(N, 1);
+    if (need > s.blur_tmp_bytes) {
+        CK(cudaStreamSynchronize(s.st));
+        if (s.gexec) {  // a captured frame graph holds the old plane's address
+            cudaGraphExecDestroy(s.gexec);
+            s.gexec = nullptr;
+            s.gkey = GraphKey{};
+        }
+        if (s.blur_tmp) CK(cudaFree(s.blur_tmp));
+        s.blur_tmp = nullptr;
+        CK(cudaMalloc(&s.blur_tmp, need));
+        s.blur_tmp_bytes = need;
+    }
+    bp->scratch = s.blur_tmp;
+    return STK_OK;
+}
+
 // --------------------------------------------------------- frame enqueue ---
 // NVTX range for the host-side enqueue of one stage (SURVEY.md §5 tracing;
 // free when no tool is attached)
@@ -566,10 +579,7 @@ int enqueue_kernels(stk_ctx* ctx, Slot& s, const Frame& f, const BlurParams* bp,
     launch_peek_cols(f, f.rowf, f.dense, nullptr, st);
     ++n;
     rec(6);
-    if (bp) {
-        launch_blur(f, *bp, f.rgbL, f.out_rgb, f.dense, st);
-        ++n;
-    }
+    if (bp) n += launch_blur(f, *bp, f.rgbL, f.out_rgb, f.dense, st);
     rec(7);
     cudaMemcpyAsync(s.h_sc, f.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
     return n;
@@ -593,7 +603,6 @@ stk_status check_frame_args(stk_ctx* ctx, int slot, int w, int h, const stk_conf
     if (2 * margin >= w)
         return fail(ctx, STK_EPARAM, "add_border_anchors: margin " + std::to_string(margin) +
                                          " does not fit in width " + std::to_string(w));
-    TRY(check_gpu_limits(ctx, cfg->window, cfg->max_disparity));
     if (w > 65535 || h > 65535)
         return fail(ctx, STK_EPARAM, "stk_b200: frame " + dims(w, h) + " exceeds 65535 per side");
     if (focus) TRY(check_focus(ctx, focus, cfg->max_disparity, ksize));
@@ -630,9 +639,11 @@ stk_status submit(stk_ctx* ctx, int slot, const uint8_t* rgbL, const uint8_t* rg
         if (d_dense) f.dense = d_dense;
     }
     BlurParams bp{};
-    if (focus)
+    if (focus) {
         TRY(upload_focus(ctx, s, focus->lo, focus->hi, focus->n_ranges, cfg->max_disparity,
                          focus->sigma, ksize, focus->exact_blur != 0, &bp));
+        TRY(ensure_blur_scratch(ctx, s, N, &bp));
+    }
     TRY(encode(ctx, s.tm_sadL, s.grayL, 1, w, h, s.P, 128, cfg->window));
     TRY(encode(ctx, s.tm_sadR, s.grayR, 1, w, h, s.P, 128, cfg->window));
     cudaStream_t st = s.st;
@@ -666,6 +677,7 @@ stk_status submit(stk_ctx* ctx, int slot, const uint8_t* rgbL, const uint8_t* rg
         key.lut = bp.sharp_lut;
         key.g1 = bp.g1;
         key.g2 = bp.g2;
+        key.blur_tmp = bp.scratch;
         if (!(s.gexec && s.gkey == key)) {
             if (s.gexec) {
                 cudaGraphExecDestroy(s.gexec);
@@ -852,6 +864,7 @@ void stk_destroy(stk_ctx* ctx) {
         if (s.p_lut) cudaFreeHost(s.p_lut);
         if (s.p_g1) cudaFreeHost(s.p_g1);
         if (s.p_g2) cudaFreeHost(s.p_g2);
+        if (s.blur_tmp) cudaFree(s.blur_tmp);
         if (s.cub_tmp) cudaFree(s.cub_tmp);
         if (s.h_sc) cudaFreeHost(s.h_sc);
         for (auto& e : s.ev)
@@ -1214,7 +1227,6 @@ stk_status stk_match_boundary_pixels(stk_ctx* ctx, const uint8_t* left, const ui
         return fail(ctx, STK_EPARAM, "stereo: window must be odd and positive, got " + std::to_string(window));
     if (max_disparity < 0)
         return fail(ctx, STK_EPARAM, "stereo: max_disparity must be >= 0, got " + std::to_string(max_disparity));
-    TRY(check_gpu_limits(ctx, window, max_disparity));
     STAGE_BEGIN(w, h);
     if (N == 0) return STK_OK;
     H2D_PLANE(s.grayL, left, 1);
@@ -1243,7 +1255,6 @@ stk_status stk_dense_sad_baseline(stk_ctx* ctx, const uint8_t* left, const uint8
     if (max_disparity < 0)
         return fail(ctx, STK_EPARAM, "dense_sad_baseline: max_disparity must be >= 0, got " +
                                          std::to_string(max_disparity));
-    TRY(check_gpu_limits(ctx, window, max_disparity));
     STAGE_BEGIN(w, h);
     if (N == 0) return STK_OK;
     H2D_PLANE(s.grayL, left, 1);
@@ -1345,13 +1356,12 @@ stk_status stk_selective_blur(stk_ctx* ctx, const uint8_t* rgb, const uint8_t* m
         return fail(ctx, STK_EPARAM, "gaussian_kernel: sigma must be positive, got " + std::to_string(sigma));
     if (size < 1 || size % 2 == 0)
         return fail(ctx, STK_EPARAM, "gaussian_kernel: size must be odd and positive, got " + std::to_string(size));
-    if (blur_smem_bytes(size / 2, exact != 0) > 220 * 1024)
-        return fail(ctx, STK_EPARAM, "stk_b200: blur kernel size exceeds the GPU tile limit");
     STAGE_BEGIN(w, h);
     if (N == 0) return STK_OK;
     const int lo0 = 0, hi0 = 0;
     BlurParams bp{};
     TRY(upload_focus(ctx, s, &lo0, &hi0, 1, 0, sigma, size, exact != 0, &bp));
+    TRY(ensure_blur_scratch(ctx, s, N, &bp));
     bp.blur_map = s.mraw;
     CK(cudaMemcpyAsync(s.rgbL, rgb, 3 * N, cudaMemcpyHostToDevice, st));
     H2D_PLANE(s.mraw, map, 1);
@@ -1365,8 +1375,6 @@ stk_status stk_selective_blur_weights(stk_ctx* ctx, const uint8_t* rgb, const ui
     if (size < 1 || size % 2 == 0)
         return fail(ctx, STK_EPARAM, "selective_blur: kernel size must be odd and positive, got " +
                                          std::to_string(size));
-    if (blur_smem_bytes(size / 2, true) > 220 * 1024)
-        return fail(ctx, STK_EPARAM, "stk_b200: blur kernel size exceeds the GPU tile limit");
     STAGE_BEGIN(w, h);
     if (N == 0) return STK_OK;
     const int lo0 = 0, hi0 = 0;

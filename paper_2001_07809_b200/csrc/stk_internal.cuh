@@ -188,9 +188,13 @@ struct BlurParams {
     const uint8_t* sharp_lut;  // sharp_lut[d] for d in [0, lut_len)
     int lut_len;
     const uint8_t* blur_map;   // if non-null: explicit map (stage entry), pitched P
+    float* scratch;            // 3 floats per pixel: vertical sums of the global-memory
+                               // fallback for kernels too wide for a shared-memory tile
 };
-void launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, uint8_t* out_rgb,
-                 const int16_t* depth, cudaStream_t st);
+// true when launch_blur needs bp.scratch (separable kernel beyond the tiles)
+bool blur_needs_scratch(int hw, bool exact);
+int launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, uint8_t* out_rgb,
+                const int16_t* depth, cudaStream_t st);  // returns the launches
 void launch_blur_map(const Frame& f, const int16_t* depth, const uint8_t* sharp_lut,
                      int lut_len, uint8_t* out, cudaStream_t st);
 
