@@ -286,6 +286,46 @@ std::vector<BenchReport> run_benchmark(const std::vector<StereoPair>& frames,
                                        const PipelineConfig& config);
 std::string benchmark_csv(const std::vector<BenchReport>& reports);
 
+// B200 extension of bench.hpp: the same batch timed
+// once per GPU COUNT instead of per worker count.  Frame f goes to GPU
+// f mod G; each GPU is one context (two frame slots, H2D / kernels / D2H of
+// consecutive frames overlapped) driven by its own host thread; GPU g runs on
+// device g mod (visible devices), so G may exceed the device count (contexts
+// then share a device).  Every frame is the whole refocus path (blur
+// included when `focus` is given) from host buffers to host buffers.
+//   times / blur : per-stage device ms (CUDA events) summed over a GPU's
+//                  frames, max over GPUs (the stage's critical path)
+//   wall_ms      : host wall clock of the batch (first submit to last result)
+//   alg_bytes    : the stage's algorithmic HBM bytes over the batch
+//                  (8N, N, 12N+4M, 4N+4M, 4N, 4N, 8N per frame)
+//   digests      : FNV-1a of each frame's dense disparity and refocused image,
+//                  in frame order (identical for every G)
+// ParamError when `frames` or `gpu_counts` is empty, a count is < 1, or 1
+// (the single-GPU baseline) is missing.
+struct GpuBenchReport {
+    int gpus = 0;
+    int frames = 0;
+    StageTimes times;
+    double blur = 0.0;
+    StageTimes serial;
+    double serial_blur = 0.0;
+    double wall_ms = 0.0;
+    double serial_wall_ms = 0.0;
+    double frames_per_s = 0.0;
+    double speedup = 0.0;  // serial_wall_ms / wall_ms
+    std::array<double, 7> alg_bytes{};  // convert, segment, boundary, match, fill, peek, blur
+    std::vector<std::uint64_t> digests;
+};
+std::vector<GpuBenchReport> run_benchmark_gpus(const std::vector<StereoPair>& frames,
+                                               const std::vector<int>& gpu_counts,
+                                               const PipelineConfig& config,
+                                               const FocusSpec* focus = nullptr,
+                                               int kernel_size = 0);
+// CSV: the reference's columns (frames, gpus in place of workers, stage,
+// serial_ms, parallel_ms, speedup) plus alg_bytes and gb_per_s; rows convert
+// .. peek, blur, total (total = wall clock).
+std::string benchmark_csv(const std::vector<GpuBenchReport>& reports);
+
 // Frame-pair discovery of the reference CLI (tools/main.cpp:247-284): every
 // <stem>_L.<ext> with a sibling <stem>_R.<ext> (.png/.ppm/.pgm), by stem.
 // IoError if `dir` is not a directory, ParamError if no pair is found.

@@ -120,6 +120,8 @@ void stk_destroy(stk_ctx* ctx);
 const char* stk_last_error(const stk_ctx* ctx); /* ctx may be NULL (thread-local) */
 const char* stk_status_string(stk_status s);
 int stk_abi_version(void);
+/* CUDA devices visible to this process (0 without a GPU; never fails). */
+int stk_device_count(void);
 /* 0 = auto (3, else 2, else 1), 1 = per-pixel list kernel, 2 = column-sum strip
  * kernel, 3 = warp-specialised column-sum kernel (windows 9/15/21/31) */
 stk_status stk_set_sad_kernel(stk_ctx* ctx, int kernel);

@@ -640,12 +640,59 @@ int run_eval(const EvalOpts& o) {  // main.cpp:388-405
 }
 
 struct BenchOpts {
-    std::string frames_dir, workers_text = "1,4", csv_path;
+    std::string frames_dir, workers_text = "1,4", csv_path, gpus_text, focus_text;
+    double sigma = 2.0;
+    int kernel_size = 0;
     PipelineFlags pipeline;
 };
 
+// --gpus (B200 extension): the batch per GPU count,
+// frame f -> GPU f mod G; CSV with a blur row and GB/s columns; the summary
+// adds frames/s per count.
+int run_bench_gpus(BenchOpts& o) {
+    std::vector<int> gpus;
+    try {
+        gpus = parse_worker_list(o.gpus_text);
+    } catch (const ParamError&) {
+        throw ParamError("GPU list '" + o.gpus_text + "' is not a comma-separated list of integers");
+    }
+    const std::vector<StereoPair> frames = load_frames(o.frames_dir);
+    FocusSpec focus;
+    focus.sigma = o.sigma;
+    if (!o.focus_text.empty()) {
+        focus.ranges = parse_focus(o.focus_text);
+        for (auto& [lo, hi] : focus.ranges) {
+            lo = std::min(lo, o.pipeline.config.max_disparity);
+            hi = std::min(hi, o.pipeline.config.max_disparity);
+        }
+    }
+    const std::vector<GpuBenchReport> reports = run_benchmark_gpus(
+        frames, gpus, o.pipeline.config, o.focus_text.empty() ? nullptr : &focus, o.kernel_size);
+    const std::string csv = benchmark_csv(reports);
+    if (o.csv_path.empty()) {
+        std::cout << csv;
+        return 0;
+    }
+    std::ofstream out(o.csv_path, std::ios::trunc);
+    if (!out) throw IoError("cannot open " + o.csv_path + " for writing");
+    out << csv;
+    if (!out) throw IoError("write failed: " + o.csv_path);
+    JsonOut summary, speedup, fps;
+    summary.str("csv", o.csv_path);
+    summary.integer("frames", reports.front().frames);
+    for (const GpuBenchReport& r : reports) {
+        speedup.num(std::to_string(r.gpus), r.speedup);
+        fps.num(std::to_string(r.gpus), r.frames_per_s);
+    }
+    summary.obj("frames_per_s", fps);
+    summary.obj("speedup", speedup);
+    std::cout << summary.dump() << "\n";
+    return 0;
+}
+
 int run_bench(BenchOpts& o) {  // main.cpp:412-440
     if (!o.pipeline.config_path.empty()) apply_config_file(o.pipeline.config_path, o.pipeline.bindings());
+    if (!o.gpus_text.empty()) return run_bench_gpus(o);
     const std::vector<int> workers = parse_worker_list(o.workers_text);
     const std::vector<StereoPair> frames = load_frames(o.frames_dir);
     const std::vector<BenchReport> reports = run_benchmark(frames, workers, o.pipeline.config);
@@ -779,6 +826,11 @@ int main(int argc, char** argv) {
     bench.text("frames", bench_opts.frames_dir, "Directory of <stem>_L/<stem>_R frame pairs");
     bench.text("--workers", bench_opts.workers_text, "Comma-separated worker counts (must include 1)");
     bench.text("--csv", bench_opts.csv_path, "Write the CSV here instead of stdout");
+    bench.text("--gpus", bench_opts.gpus_text,
+               "B200: comma-separated GPU counts (must include 1); frame f -> GPU f mod G");
+    bench.text("--focus", bench_opts.focus_text, "B200 --gpus: in-focus ranges lo:hi[,...] (adds the blur)");
+    bench.num("--sigma", bench_opts.sigma, "B200 --gpus: Gaussian blur strength");
+    bench.num("--kernel-size", bench_opts.kernel_size, "B200 --gpus: odd kernel side (default from sigma)");
     bench_opts.pipeline.add(bench, /*with_workers=*/false);
 
     VideoOpts video_opts;

@@ -4,7 +4,12 @@
 // STK_EPARAM becomes stereotk::ParamError with the C-ABI's message (which
 // mirrors the reference's text); any other failure becomes std::runtime_error.
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <sstream>
+#include <thread>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -294,6 +299,232 @@ std::string benchmark_csv(const std::vector<BenchReport>& reports) {
         row(r.frames, r.workers, "fill", s.fill, t.fill);
         row(r.frames, r.workers, "peek", s.peek, t.peek);
         row(r.frames, r.workers, "total", s.total(), t.total());
+    }
+    return out.str();
+}
+
+// --------------------------------------------- GPU-count benchmark axis --
+namespace {
+
+uint64_t fnv1a(const void* p, size_t n, uint64_t h = 1469598103934665603ull) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+    return h;
+}
+
+struct GpuShare {  // one GPU's part of a batch
+    StageTimes t;
+    double blur = 0.0;
+    std::array<double, 7> bytes{};
+    std::vector<std::pair<int, uint64_t>> digests;
+    std::string err;
+    int err_code = 0;
+};
+
+struct StartGate {  // every GPU warmed up before the clock starts
+    std::mutex m;
+    std::condition_variable cv;
+    int ready = 0;
+    bool go = false;
+};
+
+// GPU g of G: frames g, g + G, ... on two slots of its own context.
+void gpu_share(int g, int G, int device, const std::vector<StereoPair>& frames, const stk_config& cfg,
+               const stk_focus* fo, StartGate& gate, GpuShare& out) {
+    stk_ctx* c = nullptr;
+    auto fail = [&](stk_status st) {
+        out.err_code = st;
+        out.err = stk_last_error(c);
+    };
+    const int w = frames.front().left.width, h = frames.front().left.height;
+    stk_status st = stk_create(device, w, h, 2, &c);
+    struct Buf {
+        std::vector<int16_t> dense;
+        std::vector<uint8_t> rgb;
+        int frame = -1;
+    } buf[2];
+    if (st == STK_OK) {  // warm-up (bench.cpp:15-20): one untimed frame
+        for (Buf& b : buf) {
+            b.dense.resize((size_t)w * h);
+            b.rgb.resize(fo ? (size_t)w * h * 3 : 0);
+        }
+        stk_frame_out o{};
+        o.dense = buf[0].dense.data();
+        o.refocused = fo ? buf[0].rgb.data() : nullptr;
+        const StereoPair& p = frames[g % frames.size()];
+        st = stk_frame_submit(c, 0, p.left.data.data(), p.right.data.data(), w, h, &cfg, fo, &o, 1);
+        if (st == STK_OK) st = stk_frame_wait(c, 0, nullptr, nullptr, nullptr);
+    }
+    if (st != STK_OK) fail(st);
+    {
+        std::unique_lock<std::mutex> lk(gate.m);
+        ++gate.ready;
+        gate.cv.notify_all();
+        gate.cv.wait(lk, [&] { return gate.go; });
+    }
+    const double N = (double)w * h;
+    auto collect = [&](int slot) -> stk_status {
+        stk_stats sst{};
+        stk_times tm{};
+        const stk_status r = stk_frame_wait(c, slot, &sst, &tm, nullptr);
+        if (r != STK_OK) return r;
+        out.t.convert += tm.convert;
+        out.t.segment += tm.segment;
+        out.t.boundary += tm.boundary;
+        out.t.match += tm.match;
+        out.t.fill += tm.fill;
+        out.t.peek += tm.peek;
+        out.blur += tm.blur;
+        const double M = (double)sst.matched;
+        const double b[7] = {8 * N, N, 12 * N + 4 * M, 4 * N + 4 * M, 4 * N, 4 * N, fo ? 8 * N : 0.0};
+        for (int i = 0; i < 7; ++i) out.bytes[i] += b[i];
+        Buf& bb = buf[slot];
+        uint64_t dg = fnv1a(bb.dense.data(), bb.dense.size() * 2);
+        if (fo) dg = fnv1a(bb.rgb.data(), bb.rgb.size(), dg);
+        out.digests.emplace_back(bb.frame, dg);
+        bb.frame = -1;
+        return STK_OK;
+    };
+    if (st == STK_OK) {
+        int k = 0;
+        for (size_t f = g; f < frames.size() && st == STK_OK; f += G, ++k) {
+            const int slot = k & 1;
+            if (buf[slot].frame >= 0 && (st = collect(slot)) != STK_OK) break;
+            stk_frame_out o{};
+            o.dense = buf[slot].dense.data();
+            o.refocused = fo ? buf[slot].rgb.data() : nullptr;
+            const StereoPair& p = frames[f];
+            st = stk_frame_submit(c, slot, p.left.data.data(), p.right.data.data(), w, h, &cfg, fo, &o, 1);
+            if (st == STK_OK) buf[slot].frame = (int)f;
+        }
+        for (int slot = 0; slot < 2 && st == STK_OK; ++slot)
+            if (buf[slot].frame >= 0) st = collect(slot);
+        if (st != STK_OK) fail(st);
+    }
+    if (c) stk_destroy(c);
+}
+
+struct BatchResult {
+    StageTimes t;       // max over GPUs of the per-GPU stage sums
+    double blur = 0.0;
+    double wall_ms = 0.0;
+    std::array<double, 7> bytes{};
+    std::vector<uint64_t> digests;
+};
+
+BatchResult gpu_batch(const std::vector<StereoPair>& frames, int G, const stk_config& cfg,
+                      const stk_focus* fo) {
+    const int ndev = std::max(1, stk_device_count());
+    std::vector<GpuShare> shares(G);
+    StartGate gate;
+    std::vector<std::thread> th;
+    for (int g = 0; g < G; ++g)
+        th.emplace_back(gpu_share, g, G, g % ndev, std::cref(frames), std::cref(cfg), fo, std::ref(gate),
+                        std::ref(shares[g]));
+    std::chrono::steady_clock::time_point t0;
+    {
+        std::unique_lock<std::mutex> lk(gate.m);
+        gate.cv.wait(lk, [&] { return gate.ready == G; });
+        t0 = std::chrono::steady_clock::now();
+        gate.go = true;
+        gate.cv.notify_all();
+    }
+    for (auto& t : th) t.join();
+    const auto t1 = std::chrono::steady_clock::now();
+    BatchResult r;
+    r.wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    r.digests.assign(frames.size(), 0);
+    for (const GpuShare& s : shares) {
+        if (s.err_code) {
+            if (s.err_code == STK_EPARAM) throw ParamError(s.err);
+            throw std::runtime_error(s.err);
+        }
+        r.t.convert = std::max(r.t.convert, s.t.convert);
+        r.t.segment = std::max(r.t.segment, s.t.segment);
+        r.t.boundary = std::max(r.t.boundary, s.t.boundary);
+        r.t.match = std::max(r.t.match, s.t.match);
+        r.t.fill = std::max(r.t.fill, s.t.fill);
+        r.t.peek = std::max(r.t.peek, s.t.peek);
+        r.blur = std::max(r.blur, s.blur);
+        for (int i = 0; i < 7; ++i) r.bytes[i] += s.bytes[i];
+        for (const auto& d : s.digests) r.digests[d.first] = d.second;
+    }
+    return r;
+}
+
+}  // namespace
+
+std::vector<GpuBenchReport> run_benchmark_gpus(const std::vector<StereoPair>& frames,
+                                               const std::vector<int>& gpu_counts,
+                                               const PipelineConfig& config, const FocusSpec* focus,
+                                               int kernel_size) {
+    if (frames.empty()) throw ParamError("benchmark: no frames given");
+    if (gpu_counts.empty()) throw ParamError("benchmark: no GPU counts given");
+    if (std::find(gpu_counts.begin(), gpu_counts.end(), 1) == gpu_counts.end())
+        throw ParamError("benchmark: GPU counts must include 1, the single-GPU baseline");
+    for (int g : gpu_counts)
+        if (g < 1) throw ParamError("benchmark: GPU count must be >= 1, got " + std::to_string(g));
+    validate_config(config);
+    for (const StereoPair& p : frames)
+        if (!p.left.same_size(p.right) || !p.left.same_size(frames.front().left))
+            throw ParamError("benchmark: frames differ in size, " + dims(p.left.width, p.left.height) +
+                             " vs " + dims(frames.front().left.width, frames.front().left.height));
+    const stk_config cfg{config.k, config.window, config.max_disparity, config.threshold,
+                         config.prune_fraction, config.workers};
+    std::vector<int> lo, hi;
+    stk_focus fo{};
+    if (focus) {
+        for (const auto& r : focus->ranges) {
+            lo.push_back(r.first);
+            hi.push_back(r.second);
+        }
+        fo = stk_focus{lo.data(), hi.data(), static_cast<int>(lo.size()), focus->sigma, kernel_size,
+                       t_fast_blur ? 0 : 1};
+    }
+    const BatchResult serial = gpu_batch(frames, 1, cfg, focus ? &fo : nullptr);
+    std::vector<GpuBenchReport> reports;
+    for (int G : gpu_counts) {
+        const BatchResult b = G == 1 ? serial : gpu_batch(frames, G, cfg, focus ? &fo : nullptr);
+        GpuBenchReport r;
+        r.gpus = G;
+        r.frames = static_cast<int>(frames.size());
+        r.times = b.t;
+        r.blur = b.blur;
+        r.serial = serial.t;
+        r.serial_blur = serial.blur;
+        r.wall_ms = b.wall_ms;
+        r.serial_wall_ms = serial.wall_ms;
+        r.frames_per_s = b.wall_ms > 0.0 ? 1e3 * r.frames / b.wall_ms : 0.0;
+        r.speedup = b.wall_ms > 0.0 ? serial.wall_ms / b.wall_ms : 0.0;
+        r.alg_bytes = b.bytes;
+        r.digests = b.digests;
+        reports.push_back(std::move(r));
+    }
+    return reports;
+}
+
+std::string benchmark_csv(const std::vector<GpuBenchReport>& reports) {
+    std::ostringstream out;
+    out << "frames,gpus,stage,serial_ms,parallel_ms,speedup,alg_bytes,gb_per_s\n";
+    auto row = [&](const GpuBenchReport& r, const char* stage, double s, double p, double bytes) {
+        out << r.frames << ',' << r.gpus << ',' << stage << ',' << s << ',' << p << ','
+            << (p > 0.0 ? s / p : 0.0) << ',' << bytes << ',' << (p > 0.0 ? bytes / (p * 1e-3) / 1e9 : 0.0)
+            << '\n';
+    };
+    for (const GpuBenchReport& r : reports) {
+        const StageTimes& s = r.serial;
+        const StageTimes& t = r.times;
+        const auto& b = r.alg_bytes;
+        row(r, "convert", s.convert, t.convert, b[0]);
+        row(r, "segment", s.segment, t.segment, b[1]);
+        row(r, "boundary", s.boundary, t.boundary, b[2]);
+        row(r, "match", s.match, t.match, b[3]);
+        row(r, "fill", s.fill, t.fill, b[4]);
+        row(r, "peek", s.peek, t.peek, b[5]);
+        row(r, "blur", r.serial_blur, r.blur, b[6]);
+        double tot = 0.0;
+        for (double v : b) tot += v;
+        row(r, "total", r.serial_wall_ms, r.wall_ms, tot);
     }
     return out.str();
 }

@@ -736,6 +736,15 @@ extern "C" {
 
 int stk_abi_version(void) { return STK_ABI_VERSION; }
 
+int stk_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
 const char* stk_status_string(stk_status s) {
     switch (s) {
         case STK_OK: return "ok";

@@ -302,3 +302,28 @@ def test_bench_csv(stk, synth, tmp_path):
     s = json.loads(so)
     assert csv.exists() and s["frames"] == 2 and len(s["speedup"]) == 2 and s["speedup"]["1"] == 1.0
     assert run_cli("bench", d, "--workers", "2,4")[0] == 2
+
+
+@pytest.mark.gpu
+def test_bench_gpus_csv(stk, synth, tmp_path):
+    """stereotk bench --gpus (B200 extension): the GPU-count axis with a blur
+    row and GB/s columns; G = 2 runs as two contexts (device g mod count)."""
+    d = tmp_path / "frames"
+    d.mkdir()
+    for i in range(3):
+        l, r = synth.dead_leaves(192, 128, 16, frame=i)
+        stk.save_rgb(l, d / f"frame{i}_L.ppm")
+        stk.save_rgb(r, d / f"frame{i}_R.ppm")
+    csv = tmp_path / "gpus.csv"
+    rc, so, err = run_cli("bench", d, "--gpus", "1,2", "--max-disparity", "16", "--k", "4",
+                          "--focus", "8:16", "--csv", csv)
+    assert rc == 0, err
+    s = json.loads(so)
+    assert s["frames"] == 3 and set(s["speedup"]) == {"1", "2"} and s["speedup"]["1"] == 1.0
+    assert set(s["frames_per_s"]) == {"1", "2"} and s["frames_per_s"]["2"] > 0
+    text = csv.read_text()
+    assert text.startswith("frames,gpus,stage,serial_ms,parallel_ms,speedup,alg_bytes,gb_per_s\n")
+    rows = [l.split(",") for l in text.strip().split("\n")[1:]]
+    assert len(rows) == 16 and rows[6][2] == "blur" and float(rows[6][4]) > 0
+    assert run_cli("bench", d, "--gpus", "2")[0] == 2  # the single-GPU baseline is required
+    assert run_cli("bench", d, "--gpus", "1,x")[0] == 2

@@ -35,3 +35,19 @@ def test_cpp_dropin(tmp_path, golden, port, synth):
     want = np.empty_like(l)
     port.lib.orc_selective_blur(l.reshape(-1), np.ones(n, np.uint8), 96, 72, w, 3, want.reshape(-1))
     assert (boxed == want).all()
+
+
+def test_cpp_run_benchmark_gpus(tmp_path):
+    """run_benchmark_gpus: G = 1, 2, 3 contexts (sharing device 0 on a one-GPU
+    box), frame f -> GPU f mod G, byte-identical outputs, the CSV layout."""
+    exe = str(tmp_path / "bench_gpus_test")
+    lib = os.path.join(ROOT, "paper_2001_07809_b200")
+    subprocess.run(["/usr/bin/g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "bench_gpus_test.cpp"), "-L", lib, "-lstk_b200",
+                    f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    rows = [l.split(",") for l in r.stdout.strip().split("\n")[1:]]
+    assert [x[2] for x in rows[:8]] == ["convert", "segment", "boundary", "match", "fill", "peek",
+                                        "blur", "total"]
+    assert {x[1] for x in rows} == {"1", "2", "3"}
