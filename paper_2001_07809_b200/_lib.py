@@ -68,6 +68,7 @@ class StkVideoReport(C.Structure):
 VP, I, D, SZ = C.c_void_p, C.c_int, C.c_double, C.c_size_t
 SIGNATURES = {
     "stk_abi_version": (I, []),
+    "stk_device_count": (I, []),
     "stk_status_string": (C.c_char_p, [I]),
     "stk_last_error": (C.c_char_p, [VP]),
     "stk_create": (I, [I, I, I, I, C.POINTER(VP)]),
