@@ -347,3 +347,4 @@ def test_wide_blur_tile_edge_shape(dev, stk, ref, synth):
     for k in INTERMEDIATES:
         eq(getattr(res, k), want[k], k)
     assert np.abs(img.astype(int) - want["refocused"].astype(int)).max() <= BLUR_TOL_LSB
+
