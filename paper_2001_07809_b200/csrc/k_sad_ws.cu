@@ -356,6 +356,21 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
         }
         named_sync(BAR_H, 32 * p.NHW);
     }
+    // per-lane quad-row bases of both colsum buffers, hoisted out of the row
+    // loop (keeps WP fields out of the pixel loop: no constant reloads there)
+    const char* qrow0[NQB];
+    const char* qrow1[NQB];
+    bool qokv[NQB];
+#pragma unroll
+    for (int qb = 0; qb < NQB; ++qb) {
+        const int q = qb * QPB + qlane;
+        qokv[qb] = q < p.QMAIN;
+        qrow0[qb] = reinterpret_cast<const char*>(cs + (size_t)(qokv[qb] ? q : 0) * p.CSW);
+        qrow1[qb] = qrow0[qb] + bufstride * sizeof(uint2);
+    }
+    uint32_t* const best0 = best;
+    uint32_t* const best1 = best + p.SW;
+    const int Dm = p.D;
     uint32_t m = load_mask(yb0);
     uint32_t mprev = 0;
     for (int t = 0; t < T; ++t) {
@@ -365,23 +380,23 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
         // results of row t-1 are complete: write and reset them
         if ((mprev >> lane) & 1u) {
             const int x = pos_of(lane);
-            uint32_t* bp = best + (b ^ 1) * p.SW;
+            const uint32_t* bp = b ? best0 : best1;
             f.sparse[(size_t)(y - 1) * f.W + x0 + x] = (int16_t)(bp[hwb + lane] & 1023u);
         }
         if (m) {
             const uint2* cb = cs + b * bufstride;
-            uint32_t* bp = best + b * p.SW;
+            uint32_t* bp = b ? best1 : best0;
             auto pixels = [&](auto fast_tag) {
                 constexpr bool FAST = decltype(fast_tag)::value;
                 // in-lane min key of the main quads at mask bit r
                 auto keyof = [&](int r) {
-                    const int lim = FAST ? p.D : min(p.D, x0 + pos_of(r) - h);
+                    const int lim = FAST ? Dm : min(Dm, x0 + pos_of(r) - h);
                     uint32_t key = 0xffffffffu;
 #pragma unroll
                     for (int qb = 0; qb < NQB; ++qb) {
                         const int q = qb * QPB + qlane;
-                        const bool qok = q < p.QMAIN;
-                        const char* cq = reinterpret_cast<const char*>(cb + (size_t)(qok ? q : 0) * p.CSW);
+                        const bool qok = qokv[qb];
+                        const char* cq = b ? qrow1[qb] : qrow0[qb];
                         const uint32_t dbase = 4 * q + 2 * region;
                         uint32_t lo[HQ], hi[HQ];
                         window_sum<WIN, K, HQ>(cq, tab + (hwb + r) * NE, region != 0, lo, hi);
