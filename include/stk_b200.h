@@ -89,7 +89,8 @@ typedef struct stk_frame_info {
     int k;                 /* effective clusters = min(cfg.k, occupied bins) */
     int iterations_run;
     int kernels;           /* kernel launches enqueued for this frame */
-    int graph;             /* 1 if the frame ran as a CUDA graph replay */
+    int graph;             /* 1 if the frame ran as a CUDA graph */
+    int captured;          /* 1 if this submit captured (re-instantiated) that graph */
 } stk_frame_info;
 
 /* Outputs of one frame (host pointers, or device pointers for the *_device

@@ -40,7 +40,8 @@ class StkTimes(C.Structure):
 
 class StkFrameInfo(C.Structure):
     _fields_ = [("sad_ops", C.c_uint64), ("components", C.c_uint64), ("k", C.c_int),
-                ("iterations_run", C.c_int), ("kernels", C.c_int), ("graph", C.c_int)]
+                ("iterations_run", C.c_int), ("kernels", C.c_int), ("graph", C.c_int),
+                ("captured", C.c_int)]
 
 
 class StkFrameOut(C.Structure):

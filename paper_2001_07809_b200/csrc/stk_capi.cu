@@ -108,6 +108,7 @@ struct Slot {
     bool pending = false;
     bool timed = false;
     bool graph = false;
+    bool captured = false;
     int kernels = 0;
     int k_for_out = 0;
     Frame f{};
@@ -653,7 +654,7 @@ stk_status submit(stk_ctx* ctx, int slot, const uint8_t* rgbL, const uint8_t* rg
     }
     const bool want_labels = full && out->labels;
     int nk = 0;
-    bool graphed = false;
+    bool graphed = false, captured = false;
     if (!timed && ctx->use_graphs) {
         GraphKey key;
         key.W = w;
@@ -691,6 +692,7 @@ stk_status submit(stk_ctx* ctx, int slot, const uint8_t* rgbL, const uint8_t* rg
             cudaGraphDestroy(g);
             CK(ie);
             s.gkey = key;
+            captured = true;
         }
         CK(cudaGraphLaunch(s.gexec, st));
         nk = s.kernels;
@@ -719,6 +721,7 @@ stk_status submit(stk_ctx* ctx, int slot, const uint8_t* rgbL, const uint8_t* rg
     s.pending = true;
     s.timed = timed;
     s.graph = graphed;
+    s.captured = captured;
     s.kernels = nk;
     s.f = f;
     s.out = (host_out && out) ? *out : stk_frame_out{};
@@ -998,6 +1001,7 @@ stk_status stk_frame_wait(stk_ctx* ctx, int slot, stk_stats* stats, stk_times* t
         info->iterations_run = h.iters;
         info->kernels = s.kernels;
         info->graph = s.graph ? 1 : 0;
+        info->captured = s.captured ? 1 : 0;
     }
     return STK_OK;
 }

@@ -348,3 +348,46 @@ def test_wide_blur_tile_edge_shape(dev, stk, ref, synth):
         eq(getattr(res, k), want[k], k)
     assert np.abs(img.astype(int) - want["refocused"].astype(int)).max() <= BLUR_TOL_LSB
 
+
+
+def test_async_slots_focus_changes_per_frame(dev, stk, synth):
+    """A video whose focus ranges and sigma change every frame: frames in
+    flight on three slots (focus tables uploaded stream-ordered, no host
+    synchronisation) give the same bytes as synchronous frames, and every
+    frame after the first per slot replays the slot's CUDA graph (same kernel
+    size: no re-capture)."""
+    from paper_2001_07809_b200 import _lib
+
+    L = _lib.lib()
+    W, H = 512, 256
+    cfg = stk.PipelineConfig(k=5, window=9, max_disparity=24)
+    frames = [synth.dead_leaves(W, H, 24, frame=i) for i in range(9)]
+    focuses = [stk.FocusSpec([(i % 5, 10 + i)], 1.5 + 0.05 * (i % 3)) for i in range(9)]  # 11 taps
+    want = [stk.run_refocus_pipeline(l, r, cfg, fo, device=dev) for (l, r), fo in zip(frames, focuses)]
+    c_cfg = cfg.c()
+    keep = []
+    outs = [np.empty((H, W, 3), np.uint8) for _ in frames]
+    fo_c = [_lib.StkFrameOut() for _ in frames]
+    info = _lib.StkFrameInfo()
+    graphs = []
+    pending = [None] * 3
+    for i, (l, r) in enumerate(frames):
+        s = i % 3
+        if pending[s] is not None:
+            stk._raise(L.stk_frame_wait(dev.h, s, None, None, C.byref(info)), dev.h)
+            graphs.append((pending[s], info.graph, info.captured))
+        fo_c[i].refocused = outs[i].ctypes.data
+        c_focus, k = stk._focus_c(focuses[i], 0)
+        keep.append((c_focus, k))
+        stk._raise(L.stk_frame_submit(dev.h, s, l.ctypes.data, r.ctypes.data, W, H, C.byref(c_cfg),
+                                      C.byref(c_focus), C.byref(fo_c[i]), 0), dev.h)
+        pending[s] = i
+    for s in range(3):
+        stk._raise(L.stk_frame_wait(dev.h, s, None, None, C.byref(info)), dev.h)
+        graphs.append((pending[s], info.graph, info.captured))
+    for a, b in zip(outs, want):
+        eq(a, b, "async focus change")
+    assert all(g == 1 for _, g, _ in graphs)
+    # slots 1 and 2 capture on their first frame; every later frame replays
+    # (slot 0 already holds the synchronous frames' graph of this geometry)
+    assert [i for i, _, cap in graphs if cap] == [1, 2], graphs
