@@ -82,6 +82,19 @@ __device__ __forceinline__ int gfind(int* p, int x) {  // path halving
     return x;
 }
 
+// Read-only find for the compress passes after the union phase: a thread
+// then writes only final roots (par[id] = root), so no concurrent path-
+// halving store can overwrite an already-compressed entry with an
+// intermediate node (a race gfind would have there).
+__device__ __forceinline__ int gfind_ro(const int* p, int x) {
+    int q = __ldcg(p + x);
+    while (q != x) {
+        x = q;
+        q = __ldcg(p + x);
+    }
+    return x;
+}
+
 // Global union-find over region roots: link by a hash priority of the node
 // (random-permutation order keeps the trees O(log n) deep even for one giant
 // component); the component's minimum raster index is tracked separately
@@ -944,7 +957,7 @@ __global__ void __launch_bounds__(256) k_prune_fused(Frame f, uint32_t* __restri
     const int n = (int)sc->n_lroots;
     // B4 compress
     for (int id = gt; id < n; id += gs) {
-        const int r = gfind(f.par, id);
+        const int r = gfind_ro(f.par, id);
         if (r != id) {
             f.par[id] = r;
             atomicAdd(f.cnt + r, __ldcg(f.cnt + id));
@@ -1205,7 +1218,7 @@ namespace {
 __global__ void __launch_bounds__(256) k_cc_compress(Frame f) {
     const int n = (int)f.sc->n_lroots;
     for (int id = blockIdx.x * blockDim.x + threadIdx.x; id < n; id += gridDim.x * blockDim.x) {
-        const int r = gfind(f.par, id);
+        const int r = gfind_ro(f.par, id);
         if (r != id) {
             f.par[id] = r;
             atomicAdd(f.cnt + r, __ldcg(f.cnt + id));

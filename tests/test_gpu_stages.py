@@ -182,6 +182,20 @@ def test_components_run_ccl_large(dev, stk, port, synth, case):
     eq(t.by_size, bys)
 
 
+def test_components_and_prune_repeated_large(dev, stk, port, synth):
+    """Repeated large masks (the compress passes run concurrently with no
+    ordering between threads): labels, sizes, by_size and the pruned mask equal
+    the oracle on every run."""
+    for seed in range(6):
+        m = synth.random_mask(1920, 1080, 1000 + seed, 40 + seed)
+        t = stk.label_components(m, device=dev)
+        lab, sz, bys = port.label_components(m)
+        eq(t.labels, lab)
+        eq(t.sizes, sz)
+        eq(t.by_size, bys)
+        eq(stk.prune_components(m, 0.04, device=dev), port.prune(m, 0.04))
+
+
 def test_prune_golden_and_spec(dev, stk, golden, synth):
     for s in range(20):
         m = synth.random_mask(40, 30, 800 + s, 20)
