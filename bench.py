@@ -460,7 +460,7 @@ def main():
         "byte_sad_per_s": sad_ops / t_match,
         "alu_pipe_pct_active": sad_prof.get("alu_pipe_pct_active"),
         "shared_wavefronts_pct": sad_prof.get("lsu_shared_wavefronts_pct"),
-        "traffic_source": "profiles/r01_ncu_kernels.json (ncu --set full, one 4K launch)" if traffic else None,
+        "traffic_source": "profiles/r02_ncu_kernels.json (ncu --set full, one 4K launch)" if traffic else None,
     }
     # the brute-force SAD ceiling (VABSDIFF4 issue rate,
     # microbenchmarked here) and the frame roofline 1 / (bytes/BW + SAD/peak)
@@ -640,7 +640,7 @@ def _pcie_model(pcie, h2d_bytes, d2h_bytes, fps_e2e, frame_ms_dev):
 def _ncu_profile():
     """Per-kernel ncu summary committed under profiles/ (scripts/ncu_to_json.py)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_kernels.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_kernels.json")) as f:
             return json.load(f)
     except Exception:
         return {}
