@@ -269,6 +269,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # STK_BENCH_ONE_DEVICE=1: every rank on device 0 -- a functional check of
+    # the multi-process path on a one-GPU box (ranks never wait on each
+    # other's kernels, only on the gloo barrier); its throughput is not a
+    # scaling number
+    if os.environ.get("STK_BENCH_ONE_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     all_cpus = os.sched_getaffinity(0)
     affinity = _pin_near_gpu(torch, local)  # host thread near the GPU's PCIe root
