@@ -391,3 +391,36 @@ def test_async_slots_focus_changes_per_frame(dev, stk, synth):
     # slots 1 and 2 capture on their first frame; every later frame replays
     # (slot 0 already holds the synchronous frames' graph of this geometry)
     assert [i for i, _, cap in graphs if cap] == [1, 2], graphs
+
+
+def test_4k_frames_deterministic_across_slots(dev, stk, synth):
+    """Twelve 4K frames (two distinct pairs) through three async slots with
+    graphs: every repeat of a pair gives byte-identical dense disparity and
+    refocused image (the union-find phases run lock-free, in any order)."""
+    from paper_2001_07809_b200 import _lib
+
+    L = _lib.lib()
+    W, H, D = 4096, 2304, 128
+    cfg = stk.PipelineConfig(k=8, window=21, max_disparity=D)
+    c_cfg = cfg.c()
+    c_focus, _keep = stk._focus_c(stk.FocusSpec([(64, 128)], 2.0), 0)
+    pairs = [synth.dead_leaves(W, H, D, frame=i) for i in (3, 4)]
+    n = 12
+    outs = [(np.empty((H, W, 3), np.uint8), np.empty((H, W), np.int16)) for _ in range(n)]
+    fo = [_lib.StkFrameOut() for _ in range(n)]
+    pending = [None] * 3
+    for i in range(n):
+        s = i % 3
+        if pending[s] is not None:
+            stk._raise(L.stk_frame_wait(dev.h, s, None, None, None), dev.h)
+        fo[i].refocused = outs[i][0].ctypes.data
+        fo[i].dense = outs[i][1].ctypes.data
+        l, r = pairs[i % 2]
+        stk._raise(L.stk_frame_submit(dev.h, s, l.ctypes.data, r.ctypes.data, W, H, C.byref(c_cfg),
+                                      C.byref(c_focus), C.byref(fo[i]), 0), dev.h)
+        pending[s] = i
+    for s in range(3):
+        stk._raise(L.stk_frame_wait(dev.h, s, None, None, None), dev.h)
+    for i in range(2, n):
+        eq(outs[i][1], outs[i % 2][1], f"dense repeat {i}")
+        eq(outs[i][0], outs[i % 2][0], f"refocused repeat {i}")
