@@ -44,7 +44,8 @@ namespace stk {
 namespace {
 
 constexpr int CT = 32;         // CCL tile side
-constexpr int kRunCap = 512;   // max runs in a 32x32 tile (16 per row)
+constexpr int kRunCap = 512;   // max runs in a 32x32 tile (16 per row): runroot stride
+constexpr int kRunCapFast = 256;  // B2's shared-memory run table (overflow tiles: second pass)
 constexpr int MB_ROWS = 8;     // B1 output rows per warp (8: twice the warps of 16 -- the kernel is latency-bound)
 constexpr int MB_WPW = 30;     // B1 output words per warp (+1 halo word each side)
 
@@ -444,7 +445,7 @@ __device__ __forceinline__ unsigned long long budget_of(const Frame& f) {
 //     converged; 8-connected unions with the overlapping runs of the row
 //     above; min-linking makes a component's root its first run, i.e. its
 //     minimum raster index.
-//  2. region merge in shared memory: node = warp * kRunCap + ridx; the tiles'
+//  2. region merge in shared memory: node = warp * CAP + ridx; the tiles'
 //     inner borders are united, and every region component gets the minimum
 //     raster index g of its tile components (its key) and their size sum.
 //  3. region components -> root list (g, size), par[g] = g; every run records
@@ -454,13 +455,14 @@ constexpr int RGX = 4, RGY = 2, NRW = RGX * RGY;  // 128 x 64-pixel regions
 constexpr int RW = RGX * CT, RH = RGY * CT;
 constexpr int RBORD = 2 * RW + 2 * RH;             // [top RW][bottom RW][left RH][right RH]
 
-struct RunSmem {
+template <int CAP>
+struct RunSmemT {
     uint32_t rowm[CT], rows[CT];   // row masks, run starts
     int rs[CT + 1];                // first ridx of each row
-    uint8_t rstart[kRunCap], rlen[kRunCap], rrow[kRunCap];
-    int par[kRunCap];              // region node ids after step 1
-    int sz[kRunCap];
-    int key[kRunCap];              // g of tile-local roots, INT_MAX otherwise
+    uint8_t rstart[CAP], rlen[CAP], rrow[CAP];
+    int par[CAP];                  // region node ids after step 1
+    int sz[CAP];
+    int key[CAP];                  // g of tile-local roots, INT_MAX otherwise
 };
 
 __device__ __forceinline__ int rfind(int* p, int x) {  // with path halving
@@ -490,10 +492,12 @@ __device__ __forceinline__ void runite(int* p, int a, int b) {
     }
 }
 
-// region-wide union-find over nodes w * kRunCap + ridx
-__device__ __forceinline__ int* cpar(RunSmem* R, int node) { return &R[node / kRunCap].par[node % kRunCap]; }
+// region-wide union-find over nodes w * CAP + ridx
+template <int CAP>
+__device__ __forceinline__ int* cpar(RunSmemT<CAP>* R, int node) { return &R[node / CAP].par[node % CAP]; }
 
-__device__ __forceinline__ int cfind(RunSmem* R, int x) {
+template <int CAP>
+__device__ __forceinline__ int cfind(RunSmemT<CAP>* R, int x) {
     int q = *cpar(R, x);
     while (q != x) {
         const int g = *cpar(R, q);
@@ -504,7 +508,8 @@ __device__ __forceinline__ int cfind(RunSmem* R, int x) {
     return x;
 }
 
-__device__ __forceinline__ void cunite(RunSmem* R, int a, int b) {
+template <int CAP>
+__device__ __forceinline__ void cunite(RunSmemT<CAP>* R, int a, int b) {
     while (true) {
         a = cfind(R, a);
         b = cfind(R, b);
@@ -521,28 +526,27 @@ __device__ __forceinline__ void cunite(RunSmem* R, int a, int b) {
 }
 
 // region node of pixel (row, col) of warp w's tile, -1 when unset
-__device__ __forceinline__ int node_at(const RunSmem* R, int w, int row, int col) {
-    const RunSmem& S = R[w];
+template <int CAP>
+__device__ __forceinline__ int node_at(const RunSmemT<CAP>* R, int w, int row, int col) {
+    const RunSmemT<CAP>& S = R[w];
     if (!((S.rowm[row] >> col) & 1u)) return -1;
-    return w * kRunCap + S.rs[row] + __popc(S.rows[row] & upto_mask(col)) - 1;
+    return w * CAP + S.rs[row] + __popc(S.rows[row] & upto_mask(col)) - 1;
 }
 
-__global__ void __launch_bounds__(32 * NRW) k_ccl_region(Frame f, const uint32_t* __restrict__ rbits,
-                                                         int32_t* __restrict__ runroot,
-                                                         int32_t* __restrict__ bord) {
-    extern __shared__ __align__(16) uint8_t smraw[];
-    RunSmem* R = reinterpret_cast<RunSmem*>(smraw);
+// Region body: CAP = the run table's per-tile capacity.  FIRST (CAP = 256):
+// a region with a tile of more runs appends itself to the overflow list
+// (f.list, count in sc->n_ovf) and writes nothing; the overflow pass (CAP =
+// 512, the most a 32x32 tile can hold) then runs those regions.
+template <int CAP, bool FIRST>
+__device__ __forceinline__ void ccl_region_body(const Frame& f, const uint32_t* __restrict__ rbits,
+                                                int32_t* __restrict__ runroot, int32_t* __restrict__ bord,
+                                                int reg, RunSmemT<CAP>* R) {
+    using RunSmem = RunSmemT<CAP>;
+    __shared__ int s_ovf;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    {   // zero the size-histogram bins the prune will use (0..B+1)
-        const unsigned long long B = budget_of(f);
-        const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-        const long long stride = (long long)gridDim.x * blockDim.x;
-        for (long long s = gt; s <= (long long)B + 1; s += stride) f.szhist[s] = 0;
-        if (gt == 0) f.sc->budget = B;
-    }
     const int TXc = (f.W + CT - 1) / CT, TYc = (f.H + CT - 1) / CT;
     const int RXc = (f.W + RW - 1) / RW;
-    const int rx = blockIdx.x % RXc, ry = blockIdx.x / RXc;
+    const int rx = reg % RXc, ry = reg / RXc;
     const int tc = wid % RGX, tr = wid / RGX;
     const int tx = rx * RGX + tc, ty = ry * RGY + tr;
     const bool tile_ok = tx < TXc && ty < TYc;
@@ -559,6 +563,16 @@ __global__ void __launch_bounds__(32 * NRW) k_ccl_region(Frame f, const uint32_t
         if (lane >= o) rinc += v;
     }
     const int nruns = __shfl_sync(0xffffffffu, rinc, 31);
+    if constexpr (FIRST) {
+        if (threadIdx.x == 0) s_ovf = 0;
+        __syncthreads();
+        if (lane == 0 && nruns > CAP) s_ovf = 1;
+        __syncthreads();
+        if (s_ovf) {  // uniform: the whole region goes to the overflow pass
+            if (threadIdx.x == 0) f.list[atomicAdd(&f.sc->n_ovf, 1u)] = (uint32_t)reg;
+            return;
+        }
+    }
     S.rowm[lane] = m;
     S.rows[lane] = s;
     S.rs[lane] = rinc - nr;
@@ -606,7 +620,7 @@ __global__ void __launch_bounds__(32 * NRW) k_ccl_region(Frame f, const uint32_t
     for (int i = lane; i < nruns; i += 32) {
         const int rt = S.par[i];
         S.key[i] = rt == i ? gof(S, i, x0, y0) : 0x7fffffff;
-        S.par[i] = wid * kRunCap + rt;
+        S.par[i] = wid * CAP + rt;
     }
     __syncthreads();
     // 2. inner borders of the region (the tile above / left, and the two
@@ -640,19 +654,19 @@ __global__ void __launch_bounds__(32 * NRW) k_ccl_region(Frame f, const uint32_t
     __syncthreads();
     // region roots: key = min g, size = sum over their tile components
     for (int i = lane; i < nruns; i += 32) {
-        const int self = wid * kRunCap + i;
+        const int self = wid * CAP + i;
         const int rt = cfind(R, self);
         if (S.key[i] != 0x7fffffff && rt != self) {  // a tile root merged into another
-            RunSmem& Q = R[rt / kRunCap];
-            atomicAdd(&Q.sz[rt % kRunCap], S.sz[i]);
-            atomicMin(&Q.key[rt % kRunCap], S.key[i]);
+            RunSmem& Q = R[rt / CAP];
+            atomicAdd(&Q.sz[rt % CAP], S.sz[i]);
+            atomicMin(&Q.key[rt % CAP], S.key[i]);
         }
     }
     __syncthreads();
     // 3. region roots -> list; runs -> g; outer borders
     int nroots = 0;
     for (int i = lane; i < nruns; i += 32) {
-        const int self = wid * kRunCap + i;
+        const int self = wid * CAP + i;
         nroots += cfind(R, self) == self;
     }
     int incl = nroots;
@@ -669,7 +683,7 @@ __global__ void __launch_bounds__(32 * NRW) k_ccl_region(Frame f, const uint32_t
     // cmin = minimum raster index live in the first n_lroots entries of
     // f.par / f.cnt / f.roots, small enough to stay in L2)
     for (int i = lane; i < nruns; i += 32) {
-        const int self = wid * kRunCap + i;
+        const int self = wid * CAP + i;
         if (cfind(R, self) == self) {
             const int id = (int)pos++;
             f.par[id] = id;
@@ -681,13 +695,13 @@ __global__ void __launch_bounds__(32 * NRW) k_ccl_region(Frame f, const uint32_t
     __syncthreads();
     auto gnode = [&](int node) {
         const int rt = cfind(R, node);
-        return R[rt / kRunCap].key[rt % kRunCap];
+        return R[rt / CAP].key[rt % CAP];
     };
     if (tile_ok) {
         int32_t* rr = runroot + (size_t)tile * kRunCap;
-        for (int i = lane; i < nruns; i += 32) rr[i] = gnode(wid * kRunCap + i);
+        for (int i = lane; i < nruns; i += 32) rr[i] = gnode(wid * CAP + i);
     }
-    int32_t* bd = bord + (size_t)blockIdx.x * RBORD;
+    int32_t* bd = bord + (size_t)reg * RBORD;
     if (tr == 0) {
         const int a = node_at(R, wid, 0, lane);
         bd[tc * CT + lane] = a >= 0 ? gnode(a) : -1;
@@ -704,6 +718,45 @@ __global__ void __launch_bounds__(32 * NRW) k_ccl_region(Frame f, const uint32_t
         const int a = node_at(R, wid, lane, 31);
         bd[2 * RW + RH + tr * CT + lane] = a >= 0 ? gnode(a) : -1;
     }
+}
+
+// B2 first pass: one CTA per region, 256-run tables (32 KB of shared memory
+// per CTA: twice the resident CTAs of the 512-run layout)
+__global__ void __launch_bounds__(32 * NRW) k_ccl_region(Frame f, const uint32_t* __restrict__ rbits,
+                                                         int32_t* __restrict__ runroot,
+                                                         int32_t* __restrict__ bord) {
+    extern __shared__ __align__(16) uint8_t smraw[];
+    {   // zero the size-histogram bins the prune will use (0..B+1)
+        const unsigned long long B = budget_of(f);
+        const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+        const long long stride = (long long)gridDim.x * blockDim.x;
+        for (long long s = gt; s <= (long long)B + 1; s += stride) f.szhist[s] = 0;
+        if (gt == 0) f.sc->budget = B;
+    }
+    ccl_region_body<kRunCapFast, true>(f, rbits, runroot, bord, blockIdx.x,
+                                       reinterpret_cast<RunSmemT<kRunCapFast>*>(smraw));
+}
+
+// B2 overflow pass: the regions the first pass listed (none on typical
+// boundary masks), with the full 512-run tables
+__global__ void __launch_bounds__(32 * NRW) k_ccl_region_ovf(Frame f, const uint32_t* __restrict__ rbits,
+                                                             int32_t* __restrict__ runroot,
+                                                             int32_t* __restrict__ bord) {
+    extern __shared__ __align__(16) uint8_t smraw[];
+    const unsigned n = *(volatile unsigned*)&f.sc->n_ovf;
+    for (unsigned i = blockIdx.x; i < n; i += gridDim.x)
+        ccl_region_body<kRunCap, false>(f, rbits, runroot, bord, (int)f.list[i],
+                                        reinterpret_cast<RunSmemT<kRunCap>*>(smraw));
+}
+
+void launch_ccl_region(const Frame& f, const uint32_t* rbits, int32_t* runroot, int32_t* bord,
+                       cudaStream_t st) {
+    const int nreg = ((f.W + RW - 1) / RW) * ((f.H + RH - 1) / RH);
+    const size_t s1 = sizeof(RunSmemT<kRunCapFast>) * NRW, s2 = sizeof(RunSmemT<kRunCap>) * NRW;
+    cudaFuncSetAttribute(k_ccl_region, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
+    cudaFuncSetAttribute(k_ccl_region_ovf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
+    k_ccl_region<<<nreg, 32 * NRW, s1, st>>>(f, rbits, runroot, bord);
+    k_ccl_region_ovf<<<std::min(nreg, f.sms), 32 * NRW, s2, st>>>(f, rbits, runroot, bord);
 }
 
 // ------------------------------------------------------------------ B3 ----
@@ -1121,9 +1174,7 @@ void launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, in
     const int ntiles = ((f.W + CT - 1) / CT) * ((f.H + CT - 1) / CT);
     const int tb = (ntiles + 3) / 4;
     const int nreg = ((f.W + RW - 1) / RW) * ((f.H + RH - 1) / RH);
-    const size_t rsm = sizeof(RunSmem) * NRW;
-    cudaFuncSetAttribute(k_ccl_region, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
-    k_ccl_region<<<nreg, 32 * NRW, rsm, st>>>(f, rbits, runroot, bord);
+    launch_ccl_region(f, rbits, runroot, bord, st);
     k_ccl_borders<<<nreg, RW + RH, 0, st>>>(f, bord);
     cudaMemsetAsync(sbits, 0, (size_t)sbits_words * 4, st);
     {   // B4-B7 in one cooperative launch (co-resident blocks, grid barriers)
@@ -1306,9 +1357,7 @@ void launch_label_components_bits(const Frame& f, const uint8_t* mask, uint32_t*
     const int gb = (int)std::min<long long>((nw + 255) / 256, f.sms * 8);
     k_mask_to_bits<<<gb, 256, 0, st>>>(f, mask, rbits);
     const int nreg = ((f.W + RW - 1) / RW) * ((f.H + RH - 1) / RH);
-    const size_t rsm = sizeof(RunSmem) * NRW;
-    cudaFuncSetAttribute(k_ccl_region, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
-    k_ccl_region<<<nreg, 32 * NRW, rsm, st>>>(f, rbits, runroot, bord);  // B2
+    launch_ccl_region(f, rbits, runroot, bord, st);  // B2
     k_ccl_borders<<<nreg, RW + RH, 0, st>>>(f, bord);                    // B3
     const int ib = f.sms * 4;
     k_cc_compress<<<ib, 256, 0, st>>>(f);

@@ -45,7 +45,7 @@ struct DevScalars {
     unsigned int n_roots;              // component count C
     unsigned int n_list;               // == matched
     unsigned int n_lroots;             // tile-local roots (K4a -> K4c)
-    unsigned int pad1;
+    unsigned int n_ovf;                // B2 regions with a tile of > 256 runs (second pass)
     unsigned int ctr[LB_COUNT];        // dynamic chunk counters
     unsigned int psel_done;            // prune select: finished blocks
     unsigned int gbar_count;           // grid barrier (cooperative prune kernel)

@@ -196,6 +196,28 @@ def test_components_and_prune_repeated_large(dev, stk, port, synth):
         eq(stk.prune_components(m, 0.04, device=dev), port.prune(m, 0.04))
 
 
+def test_components_overflow_tiles(dev, stk, port, synth):
+    """B2 keeps 256 runs per 32x32 tile in shared memory; regions with a
+    denser tile go through the 512-run overflow pass.  Checkerboard rows (16
+    runs per row: every tile overflows), a mask where only some regions
+    overflow, and a dense random mask: labels, sizes, by_size and the pruned
+    mask equal the oracle."""
+    W, H = 700, 300
+    yy, xx = np.mgrid[0:H, 0:W]
+    checker = (((xx + (yy // 3)) % 2) == 0).astype(np.uint8)          # all tiles > 256 runs
+    mixed = synth.random_mask(W, H, 5, 20)
+    mixed[64:192, 128:384] = checker[64:192, 128:384]                 # a block of overflow regions
+    dense = synth.random_mask(W, H, 6, 50)
+    for m in (checker, mixed, dense):
+        t = stk.label_components(m, device=dev)
+        lab, sz, bys = port.label_components(m)
+        eq(t.labels, lab)
+        eq(t.sizes, sz)
+        eq(t.by_size, bys)
+        for frac in (0.0, 0.04, 0.3):
+            eq(stk.prune_components(m, frac, device=dev), port.prune(m, frac))
+
+
 def test_prune_golden_and_spec(dev, stk, golden, synth):
     for s in range(20):
         m = synth.random_mask(40, 30, 800 + s, 20)
