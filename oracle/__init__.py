@@ -493,14 +493,35 @@ def _ref_io_call(L, rc):
         raise RefIOError(_IO_KINDS.get(rc, "other"), L.ref_last_error().decode(errors="replace"))
 
 
-def ref_io(name: str, *args):
+_png_lib: list = []
+
+
+def ref_png_lib():
+    """oracle/_ref/libstk_ref_png.so: the reference library with image_io.cpp
+    linked to a real libpng 1.6 (pillow's), or None where it was not built."""
+    if not _png_lib:
+        so = HERE / "_ref" / "libstk_ref_png.so"
+        try:
+            _png_lib.append(C.CDLL(str(so)) if so.exists() else None)
+        except OSError:
+            _png_lib.append(None)
+    return _png_lib[0]
+
+
+def ref_io(name: str, *args, png: bool = False):
     """The reference's own image_io.cpp / evaluate.cpp file entry points
-    (compiled against oracle/pngstub/png.h: PGM/PPM only).  Raises RefIOError
-    with the reference's exception class and message; None without oracle/_ref."""
-    r = reference()
-    if r is None:
-        return None
-    L = r.lib
+    (compiled against oracle/pngstub/png.h: PGM/PPM only; png=True: the build
+    linked to a real libpng, for PNG files).  Raises RefIOError with the
+    reference's exception class and message; None without that library."""
+    if png:
+        L = ref_png_lib()
+        if L is None:
+            return None
+    else:
+        r = reference()
+        if r is None:
+            return None
+        L = r.lib
     L.ref_last_error.restype = C.c_char_p
     w, h = C.c_int(), C.c_int()
     if name in ("load_image", "load_gray", "load_disparity", "load_ground_truth"):

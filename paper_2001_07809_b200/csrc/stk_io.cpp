@@ -314,9 +314,19 @@ RgbImage decode_png(const Bytes& b, const std::string& path) {
         const double e = double(v) / maxv;
         return srgb_like ? srgb_to_lin(e) : std::pow(e, 100000.0 / gamma);
     };
+    // 8-bit (and expanded 1/2/4-bit) samples under a non-sRGB gAMA: libpng's
+    // simplified reader corrects them to its sRGB output gamma (a 2.2 power)
+    // with an 8-bit table, out = floor(255 (v/255)^(1/(2.2 g)) + 0.5) --
+    // checked against libpng 1.6 (tests/golden/png_golden.npz); palette
+    // entries go through the same table
+    std::uint8_t gtab[256];
+    for (int v = 0; v < 256; ++v)
+        gtab[v] = srgb_like ? static_cast<std::uint8_t>(v)
+                            : static_cast<std::uint8_t>(std::floor(
+                                  255.0 * std::pow(v / 255.0, 100000.0 / (2.2 * gamma)) + 0.5));
     auto to8 = [&](std::uint32_t v) -> std::uint8_t {
-        if (in.depth == 8 && srgb_like) return static_cast<std::uint8_t>(v);
-        if (in.depth < 8 && srgb_like) return static_cast<std::uint8_t>(v * 255 / maxv);
+        if (in.depth == 8) return gtab[v];
+        if (in.depth < 8) return gtab[v * 255 / maxv];
         if (srgb_like) return static_cast<std::uint8_t>((v * 255 + 32895) >> 16);  // 16-bit sRGB
         return q8(lin_to_srgb(to_lin(v)));
     };
@@ -340,7 +350,7 @@ RgbImage decode_png(const Bytes& b, const std::string& path) {
                     if (3 * i + 2 >= in.plte.size()) throw FormatError(path + ": PNG palette index out of range");
                     const std::uint8_t* c = &in.plte[3 * i];
                     const int a = i < in.trns.size() ? in.trns[i] : 255;
-                    for (int k = 0; k < 3; ++k) o[k] = a == 255 ? c[k] : q8(lin_to_srgb(srgb_to_lin(c[k] / 255.0) * a / 255.0));
+                    for (int k = 0; k < 3; ++k) o[k] = a == 255 ? gtab[c[k]] : q8(lin_to_srgb(srgb_to_lin(c[k] / 255.0) * a / 255.0));
                     continue;
                 }
                 std::uint32_t s[4] = {0, 0, 0, amax};
