@@ -123,7 +123,7 @@ def parse():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--config", default="C", choices=sorted(CONFIGS))
     p.add_argument("--pool", type=int, default=8, help="distinct synthetic frames cycled")
-    p.add_argument("--slots", type=int, default=8, help="frames in flight per GPU")
+    p.add_argument("--slots", type=int, default=16, help="frames in flight per GPU")
     p.add_argument("--sad", default="auto", choices=["auto", "list", "strip"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-s", type=float, default=20.0)
