@@ -424,3 +424,38 @@ def test_4k_frames_deterministic_across_slots(dev, stk, synth):
     for i in range(2, n):
         eq(outs[i][1], outs[i % 2][1], f"dense repeat {i}")
         eq(outs[i][0], outs[i % 2][0], f"refocused repeat {i}")
+
+
+@pytest.mark.parametrize("case", ["uniform", "two_levels", "thin_row", "thin_col", "tiny", "window1"])
+def test_pipeline_degenerate_frames_vs_oracle(dev, stk, port, synth, case):
+    """Frames at the edges of the algorithm: a uniform frame (one occupied
+    bin, no boundary, everything unknown -> everything blurred), two grey
+    levels with K = 8 (k = min(K, occupied) = 2), single-row / single-column
+    frames, a 3x3 frame and window 1: every intermediate and the refocused
+    image against the oracle."""
+    rng = np.random.default_rng(11)
+    k, win, D, focus = 8, 9, 16, [(4, 12)]
+    if case == "uniform":
+        l = np.full((240, 320, 3), 97, np.uint8)
+        r = l.copy()
+    elif case == "two_levels":
+        l = np.where(rng.random((200, 300, 1)) < 0.5, 40, 200).astype(np.uint8).repeat(3, axis=2)
+        r = np.roll(l, -3, axis=1)
+    elif case == "thin_row":
+        l, r = synth.dead_leaves(4096, 1, 16, frame=1)
+        win = 1
+    elif case == "thin_col":
+        l, r = synth.dead_leaves(1, 2048, 16, frame=2)
+        win = 1
+    elif case == "tiny":
+        l, r = synth.dead_leaves(3, 3, 2, frame=3)
+        win, D, focus = 3, 2, [(0, 1)]
+    else:
+        l, r = synth.dead_leaves(257, 129, 16, frame=4)
+        win = 1
+    res, img = run(stk, dev, l, r, k=k, window=win, D=D, focus=focus)
+    want = port.run_frame(l, r, k=k, window=win, max_disparity=D, focus=focus, sigma=2.0)
+    for name in INTERMEDIATES:
+        eq(getattr(res, name), want[name], f"{case} {name}")
+    assert np.abs(img.astype(int) - want["refocused"].astype(int)).max() <= BLUR_TOL_LSB
+    assert res.stats.matched == want["stats"]["matched"]
