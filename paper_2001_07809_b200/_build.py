@@ -10,6 +10,7 @@ newer than its output.
 """
 from __future__ import annotations
 
+import concurrent.futures
 import os
 import subprocess
 import sys
@@ -66,23 +67,27 @@ def build(verbose: bool = False, force: bool = False) -> None:
     objdir.mkdir(exist_ok=True)
     deps = [CSRC / h for h in HEADERS] + [INCLUDE / "stk_b200.h"]
     deps += list((INCLUDE / "stereotk").glob("*.hpp"))
-    objs = []
+    objs, jobs = [], []
     for src in CU_SOURCES:
         s = CSRC / src
         o = objdir / (src + ".o")
         objs.append(o)
         if force or _newer([s] + deps, o):
-            _run([NVCC, *ARCH, *os.environ.get("STK_NVCC_EXTRA", "").split(), "-O3", "-lineinfo",
-                  "-std=c++17", "-Xcompiler", "-fPIC",
-                  "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr",
-                  "-I", INCLUDE, "-I", CSRC, "-rdc=false", "-c", s, "-o", o], verbose)
+            jobs.append([NVCC, *ARCH, *os.environ.get("STK_NVCC_EXTRA", "").split(), "-O3", "-lineinfo",
+                         "-std=c++17", "-Xcompiler", "-fPIC",
+                         "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr",
+                         "-I", INCLUDE, "-I", CSRC, "-rdc=false", "-c", s, "-o", o])
     for src in CXX_SOURCES:
         s = CSRC / src
         o = objdir / (src + ".o")
         objs.append(o)
         if force or _newer([s] + deps, o):
-            _run(["/usr/bin/g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-pthread", "-I", INCLUDE,
-                  "-c", s, "-o", o], verbose)
+            jobs.append(["/usr/bin/g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-pthread", "-I", INCLUDE,
+                         "-c", s, "-o", o])
+    # independent translation units: compile them concurrently
+    with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(_run, j, verbose) for j in jobs]:
+            f.result()
     if force or _newer(objs, LIB):
         _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lz", "-lrt",
               "-ldl", "-lpthread"], verbose)
