@@ -17,6 +17,9 @@
 //             other sizes and for an explicit blur map;
 //   exact   : 2-D FP64 in the reference's i-outer / j-inner order with
 //             __dmul_rn/__dadd_rn and lround -- bit-identical.
+#include <cstdlib>
+#include <cuda_fp16.h>
+
 #include "stk_device.cuh"
 
 namespace stk {
@@ -285,6 +288,7 @@ __device__ __forceinline__ unsigned long long fadd2_rm(unsigned long long a, uns
 }
 constexpr unsigned long long kMagicNeg2 = 0xcb000000cb000000ull;  // (-2^23, -2^23)
 constexpr unsigned long long kMagic2 = 0x4b0000004b000000ull;     // (2^23, 2^23)
+constexpr unsigned long long kInv4096x2 = 0x3980000039800000ull;  // (2^-12, 2^-12)
 constexpr unsigned long long kHalf2 = 0x3f0000003f000000ull;      // (0.5, 0.5)
 __device__ __forceinline__ float f2lo(unsigned long long v) { return __uint_as_float((uint32_t)v); }
 __device__ __forceinline__ float f2hi(unsigned long long v) { return __uint_as_float((uint32_t)(v >> 32)); }
@@ -526,6 +530,329 @@ __global__ void __launch_bounds__(V3Geom<K>::NT) k_blur_v3(Frame f, BlurParams b
     }
 }
 
+// ------------------------------------------------------------------ K8t --
+// Tensor-core separable blur (mma.sync m16n8k16, f16 in, f32 accumulate).
+// Both passes are banded matrix products: per channel, V = Wv X (16 output
+// rows x 32 staged rows, band of K taps) and out = V Wh (16 staged px x 8
+// output px per 16-px k-block).  Precision: X is exact in f16 (bytes); the
+// weights and V are split into f16 hi + lo parts (hi*hi + hi*lo + lo*hi,
+// f32 accumulation), so each product carries ~22 significant bits -- the
+// result is the FP32 separable sum to ~1e-4 LSB, within 1 LSB of the
+// reference's FP64 2-D sum like v3.  The vertical result fragments are the
+// horizontal A fragments register for register (m16n8 D of n-tiles 2s, 2s+1
+// == m16k16 A of k-block s), so V never goes through shared memory; the
+// horizontal pass streams left to right with two k-blocks live.
+// CTA = 32 output rows x 128 output px; warp = (16-row slab, channel).
+// Staging: channel-planar f16 rows (16-B-aligned, conflict-free ldmatrix
+// .trans for the vertical B operand), filled from 12-byte (4 px) loads.
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t h2pack(float lo, float hi) {  // (lo, hi) -> f16x2, round to nearest
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+__device__ __forceinline__ void h2split(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+    hi = h2pack(x0, x1);
+    const __half2 h = *reinterpret_cast<const __half2*>(&hi);
+    lo = h2pack(x0 - __low2float(h), x1 - __high2float(h));
+}
+// bytes (b0, b1) of w (selector nibbles s0, s1) -> f16x2 exact: 0x64xx - 1024
+__device__ __forceinline__ uint32_t bytes_h2(uint32_t w, uint32_t sel) {
+    const uint32_t x = __byte_perm(w, 0x64u, sel);
+    const __half2 v = __hsub2(*reinterpret_cast<const __half2*>(&x), __float2half2_rn(1024.f));
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+template <int K>
+struct TcGeom {
+    static constexpr int h = K / 2, BX = 128, BY = 32, NT = 192;
+    static constexpr int IR = BY + 16;   // staged rows (two 16-row k-steps per slab)
+    static constexpr int IPX = 144;      // staged px: image x0 - 8 + p (18 vertical n-tiles)
+    static constexpr int XS = IPX + 8;   // f16 per staged row (304 B: conflict-free ldmatrix)
+    static constexpr size_t SM_X = (size_t)3 * IR * XS * 2;
+    static constexpr size_t SM = SM_X + (size_t)BX * BY + 2 * 64 * 4;  // + weight pair table
+    static_assert(K <= 17, "two 16-px k-blocks cover 8 outputs + 2h taps");
+    static_assert(BY == 32 && BX <= 2 * XS, "output rows 0-15 / 32-47 of each plane");
+};
+
+#ifndef STK_TC_MINB
+#define STK_TC_MINB 4
+#endif
+#ifndef STK_TC_EARLY
+#define STK_TC_EARLY 0
+#endif
+template <int K>
+__global__ void __launch_bounds__(TcGeom<K>::NT, STK_TC_MINB) k_blur_tc(Frame f, BlurParams bp,
+                                                              const uint8_t* __restrict__ in,
+                                                              uint8_t* __restrict__ out,
+                                                              const int16_t* __restrict__ depth) {
+    using G = TcGeom<K>;
+    constexpr int h = G::h, BX = G::BX, BY = G::BY, NT = G::NT, IR = G::IR, XS = G::XS;
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint16_t* xin = reinterpret_cast<uint16_t*>(smem);  // [3][IR][XS] f16 bits
+    uint8_t* shf = smem + G::SM_X;                      // [BY][BX] sharp flags
+    __shared__ uint8_t lut[1024];
+    const int W = f.W, H = f.H, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
+    const int nx = min(BX, W - x0), ny = min(BY, H - y0);
+    const bool a4 = (W & 3) == 0 && (reinterpret_cast<uintptr_t>(in) & 3) == 0;
+    // staged (row r, px p) = image (y0 - h + r, x0 - 8 + p), replicate-clamped;
+    // staging item = (row, 4 px): one 12-byte load, three 8-byte f16 stores
+    // (one per channel plane)
+    constexpr int NG = G::IPX / 4, NI = IR * NG, PER = NI / NT, DV = BX * BY / 8, DPER = (DV + NT - 1) / NT;
+    static_assert(NI % NT == 0, "whole staging items per thread");
+    // fast CTAs (full tile, aligned rows, staged columns inside the image)
+    // issue every global load -- image rows, disparities, sharp table --
+    // before the first use: one latency exposure
+    const bool fast = a4 && x0 - 8 >= 0 && x0 + G::IPX - 8 <= W && nx == BX && ny == BY && (W & 7) == 0 &&
+                      (reinterpret_cast<uintptr_t>(depth) & 15) == 0;
+    uint32_t w[PER][3];
+    uint4 dv[DPER];
+    const int lut_n = min(bp.lut_len, 1024);
+    auto load_rows = [&]() {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = tid + k * NT, sy = min(max(y0 - h + i / NG, 0), H - 1);
+            const uint32_t* p = reinterpret_cast<const uint32_t*>(in) + (sy * W + x0 - 8) * 3 / 4 + 3 * (i % NG);
+            w[k][0] = __ldg(p);
+            w[k][1] = __ldg(p + 1);
+            w[k][2] = __ldg(p + 2);
+        }
+    };
+    if (fast) {
+        if (STK_TC_EARLY) load_rows();
+#pragma unroll
+        for (int k = 0; k < DPER; ++k) {
+            const int i = tid + k * NT;
+            if (i < DV)
+                dv[k] = __ldg(reinterpret_cast<const uint4*>(depth + (size_t)(y0 + i / (BX / 8)) * W + x0) +
+                              i % (BX / 8));
+        }
+    }
+    if ((reinterpret_cast<uintptr_t>(bp.sharp_lut) & 3) == 0) {
+        for (int i = tid; 4 * i + 3 < lut_n; i += NT)
+            reinterpret_cast<uint32_t*>(lut)[i] = __ldg(reinterpret_cast<const uint32_t*>(bp.sharp_lut) + i);
+        if (tid < (lut_n & 3)) lut[(lut_n & ~3) + tid] = bp.sharp_lut[(lut_n & ~3) + tid];
+    } else {
+        for (int i = tid; i < lut_n; i += NT) lut[i] = bp.sharp_lut[i];
+    }
+    __syncthreads();
+    // ---- sharp flags of the output tile
+    int any = 0;
+    if (fast) {
+#pragma unroll
+        for (int k = 0; k < DPER; ++k) {
+            const int i = tid + k * NT;
+            if (i < DV) {
+                const uint32_t dw[4] = {dv[k].x, dv[k].y, dv[k].z, dv[k].w};
+                uint32_t sh[2] = {0, 0};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int d = (int16_t)(dw[e >> 1] >> (16 * (e & 1)));
+                    const uint32_t b = (uint32_t)d < (uint32_t)lut_n && lut[d];
+                    sh[e >> 2] |= b << (8 * (e & 3));
+                }
+                *reinterpret_cast<uint2*>(shf + 8 * i) = make_uint2(sh[0], sh[1]);
+                any |= (sh[0] & sh[1]) != 0x01010101u;
+            }
+        }
+    } else {
+        for (int i = tid; i < BX * BY; i += NT) {
+            const int ox = i % BX, oy = i / BX;
+            uint8_t sh = 1;
+            if (ox < nx && oy < ny) {
+                const int d = depth[(size_t)(y0 + oy) * W + x0 + ox];
+                sh = d >= 0 && d < lut_n && lut[d];
+                any |= !sh;
+            }
+            shf[i] = sh;
+        }
+    }
+    if (__syncthreads_or(any) == 0) {  // every pixel sharp: copy
+        for (int i = tid; i < ny * 3 * nx; i += NT) {
+            const int r = i / (3 * nx), b = i % (3 * nx);
+            const size_t o = ((size_t)(y0 + r) * W + x0) * 3 + b;
+            out[o] = in[o];
+        }
+        return;
+    }
+    // ---- stage
+    auto put = [&](int i, uint32_t w0, uint32_t w1, uint32_t w2) {
+        // w0 = R0 G0 B0 R1, w1 = G1 B1 R2 G2, w2 = B2 R3 G3 B3
+        const uint32_t R = __byte_perm(__byte_perm(w0, w1, 0x0630), w2, 0x5210);   // R0 R1 R2 R3
+        const uint32_t Gc = __byte_perm(__byte_perm(w0, w1, 0x0741), w2, 0x6210);  // G0 G1 G2 G3
+        const uint32_t Bc = __byte_perm(__byte_perm(w0, w1, 0x0052), w2, 0x7410);  // B0 B1 B2 B3
+        uint16_t* d = xin + (size_t)(i / NG) * XS + 4 * (i % NG);
+        *reinterpret_cast<uint2*>(d) = make_uint2(bytes_h2(R, 0x4140), bytes_h2(R, 0x4342));
+        *reinterpret_cast<uint2*>(d + IR * XS) = make_uint2(bytes_h2(Gc, 0x4140), bytes_h2(Gc, 0x4342));
+        *reinterpret_cast<uint2*>(d + 2 * IR * XS) = make_uint2(bytes_h2(Bc, 0x4140), bytes_h2(Bc, 0x4342));
+    };
+    if (fast) {
+        if (!STK_TC_EARLY) load_rows();
+#pragma unroll
+        for (int k = 0; k < PER; ++k) put(tid + k * NT, w[k][0], w[k][1], w[k][2]);
+    } else {
+        for (int i = tid; i < NI; i += NT) {
+            const int sy = min(max(y0 - h + i / NG, 0), H - 1), sx = x0 - 8 + 4 * (i % NG);
+            uint32_t b[12];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint8_t* q = in + ((size_t)sy * W + min(max(sx + k, 0), W - 1)) * 3;
+                b[3 * k] = q[0];
+                b[3 * k + 1] = q[1];
+                b[3 * k + 2] = q[2];
+            }
+            put(i, b[0] | b[1] << 8 | b[2] << 16 | b[3] << 24, b[4] | b[5] << 8 | b[6] << 16 | b[7] << 24,
+                b[8] | b[9] << 8 | b[10] << 16 | b[11] << 24);
+        }
+    }
+    // weight pair table: wtab[j] = (w1(j - OFF), w1(j - OFF + 1)) as f16x2 hi, and lo at
+    // wtab[NTAB + j]; weights scaled by 2^6 per pass (exact) so the lo parts stay normal
+    constexpr int OFF = 24, NTAB = 64;
+    uint32_t* wtab = reinterpret_cast<uint32_t*>(shf + BX * BY);
+    if (tid < NTAB) {
+        auto w1 = [&](int k) { return (k >= 0 && k < K) ? 64.f * __ldg(bp.g1 + k) : 0.f; };
+        uint32_t hi, lo;
+        h2split(w1(tid - OFF), w1(tid - OFF + 1), hi, lo);
+        wtab[tid] = hi;
+        wtab[NTAB + tid] = lo;
+    }
+    __syncthreads();
+    const int g = lane >> 2, t = lane & 3;
+    const int c = wid % 3, slab = wid / 3;
+    // wt[tap] = pair (tap + 2t - g, +1).  Every fragment register gets its own
+    // load: the Toeplitz structure repeats values, and a merged load would
+    // cost a move into each mma operand quad instead.
+    const uint32_t wt_s = (uint32_t)__cvta_generic_to_shared(wtab + OFF + 2 * t - g);
+    auto wt = [&](int tap) {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(wt_s + 4 * tap));
+        return v;
+    };
+    // vertical A_q[o][k] = w1(16q + k - o): regs (g,2t) (g+8,2t) (g,2t+8) (g+8,2t+8) (+1 in the high half)
+    uint32_t av_hi[2][4], av_lo[2][4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int rg = 0; rg < 4; ++rg) {
+            const int tap = 16 * q + (rg >> 1) * 8 - (rg & 1) * 8;
+            av_hi[q][rg] = wt(tap);
+            av_lo[q][rg] = wt(NTAB + tap);
+        }
+    // horizontal: output px x = 16 s0 + 8 pp + nn reads staged px x + 8 - h .. x + 8 + h,
+    // B_{pp,q}[kk][nn] = w1(16q + kk - nn - 8pp - 8 + h); regs (kk 2t, 2t+1; nn g), (kk 2t+8, 2t+9; nn g)
+    uint32_t bh_hi[2][2][2], bh_lo[2][2][2];
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int rg = 0; rg < 2; ++rg) {
+                const int tap = 16 * q + 8 * rg - 8 * pp - 8 + h;
+                bh_hi[pp][q][rg] = wt(tap);
+                bh_lo[pp][q][rg] = wt(NTAB + tap);
+            }
+    // ---- vertical n-tile i (staged px 8i..8i+7): one ldmatrix.x4.trans = both k-steps
+    const uint32_t xaddr =
+        (uint32_t)__cvta_generic_to_shared(xin + ((size_t)c * IR + 16 * slab + lane) * XS);
+    auto vert = [&](int i, float (&d)[4]) {
+        uint32_t b0, b1, b2, b3;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                     : "r"(xaddr + 16 * i));
+        d[0] = d[1] = d[2] = d[3] = 0.f;
+        mma16816(d, av_hi[0], b0, b1);
+        mma16816(d, av_lo[0], b0, b1);
+        mma16816(d, av_hi[1], b2, b3);
+        mma16816(d, av_lo[1], b2, b3);
+    };
+    // k-block s as A fragments: n-tiles 2s (regs 0, 1) and 2s+1 (regs 2, 3)
+    auto to_a = [&](const float (&d0)[4], const float (&d1)[4], uint32_t (&ahi)[4], uint32_t (&alo)[4]) {
+        h2split(d0[0], d0[1], ahi[0], alo[0]);
+        h2split(d0[2], d0[3], ahi[1], alo[1]);
+        h2split(d1[0], d1[1], ahi[2], alo[2]);
+        h2split(d1[2], d1[3], ahi[3], alo[3]);
+    };
+    // Output bytes go straight back into the warp's own channel plane, in
+    // staged rows no other warp reads (slab 0: rows 0-15, slab 1: rows 32-47)
+    // and in bytes [0, 128) of the row, which this warp's ldmatrix reads have
+    // passed by then (tile j is written after staged px 16 (j / 2) + 31 are
+    // read: bytes >= 32 (j / 2) + 64 stay ahead of the output bytes < 8 j + 8).
+    uint8_t* const orow = reinterpret_cast<uint8_t*>(xin + ((size_t)c * IR + (slab ? 32 : 0) + g) * XS) + 2 * t;
+    auto horz = [&](int j, const uint32_t (&a0h)[4], const uint32_t (&a0l)[4], const uint32_t (&a1h)[4],
+                    const uint32_t (&a1l)[4]) {
+        const int pp = j & 1;
+        float d[4] = {0.f, 0.f, 0.f, 0.f};
+        mma16816(d, a0h, bh_hi[pp][0][0], bh_hi[pp][0][1]);
+        mma16816(d, a0h, bh_lo[pp][0][0], bh_lo[pp][0][1]);
+        mma16816(d, a0l, bh_hi[pp][0][0], bh_hi[pp][0][1]);
+        mma16816(d, a1h, bh_hi[pp][1][0], bh_hi[pp][1][1]);
+        mma16816(d, a1h, bh_lo[pp][1][0], bh_lo[pp][1][1]);
+        mma16816(d, a1l, bh_hi[pp][1][0], bh_hi[pp][1][1]);
+        // floor(x + 1/2) = low byte of round_down(RN(d / 4096 + 1/2) + 2^23), as v3
+        // (x in [0, 255 (1 + eps)]: non-negative normalised weights, 8-bit inputs)
+        const unsigned long long lo2 = fadd2_rm(ffma2(f2pack(d[0], d[1]), kInv4096x2, kHalf2), kMagic2);
+        const unsigned long long hi2 = fadd2_rm(ffma2(f2pack(d[2], d[3]), kInv4096x2, kHalf2), kMagic2);
+        *reinterpret_cast<uint16_t*>(orow + 8 * j) = (uint16_t)__byte_perm((uint32_t)lo2, (uint32_t)(lo2 >> 32), 0x0040);
+        *reinterpret_cast<uint16_t*>(orow + 8 * XS * 2 + 8 * j) =
+            (uint16_t)__byte_perm((uint32_t)hi2, (uint32_t)(hi2 >> 32), 0x0040);
+    };
+    float dA[4], dB[4];
+    uint32_t k0h[4], k0l[4], k1h[4], k1l[4];
+    vert(0, dA);
+    vert(1, dB);
+    to_a(dA, dB, k0h, k0l);
+#pragma unroll
+    for (int s0 = 0; s0 < 8; ++s0) {
+        vert(2 * s0 + 2, dA);
+        vert(2 * s0 + 3, dB);
+        to_a(dA, dB, k1h, k1l);
+        horz(2 * s0, k0h, k0l, k1h, k1l);
+        horz(2 * s0 + 1, k0h, k0l, k1h, k1l);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) k0h[r] = k1h[r], k0l[r] = k1l[r];
+    }
+    __syncthreads();
+    // ---- interleave the planes, keep sharp pixels' input bytes, 12-byte stores
+    const bool a4o = a4 && (reinterpret_cast<uintptr_t>(out) & 3) == 0;
+    for (int i = tid; i < BY * (BX / 4); i += NT) {
+        const int oy = i / (BX / 4), q4 = 4 * (i % (BX / 4));
+        if (oy >= ny || q4 >= nx) continue;
+        const uint8_t* op = reinterpret_cast<const uint8_t*>(xin + (size_t)(oy < 16 ? oy : oy + 16) * XS) + q4;
+        const uint32_t R = *reinterpret_cast<const uint32_t*>(op);
+        const uint32_t Gc = *reinterpret_cast<const uint32_t*>(op + IR * XS * 2);
+        const uint32_t Bc = *reinterpret_cast<const uint32_t*>(op + 2 * IR * XS * 2);
+        uint32_t ow[3] = {__byte_perm(__byte_perm(R, Gc, 0x1040), Bc, 0x3410),
+                          __byte_perm(__byte_perm(Gc, Bc, 0x2051), R, 0x3610),
+                          __byte_perm(__byte_perm(Bc, Gc, 0x3702), R, 0x3270)};
+        const uint32_t m = *reinterpret_cast<const uint32_t*>(shf + oy * BX + q4) * 0xffu;
+        const size_t o = ((size_t)(y0 + oy) * W + x0 + q4) * 3;
+        if (a4o && q4 + 4 <= nx) {
+            if (m) {
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(in + o);
+                const uint32_t mw[3] = {__byte_perm(m, 0, 0x1000), __byte_perm(m, 0, 0x2211),
+                                        __byte_perm(m, 0, 0x3332)};
+#pragma unroll
+                for (int k = 0; k < 3; ++k) ow[k] = (ow[k] & ~mw[k]) | (__ldg(src + k) & mw[k]);
+            }
+            uint32_t* dst = reinterpret_cast<uint32_t*>(out + o);
+            dst[0] = ow[0];
+            dst[1] = ow[1];
+            dst[2] = ow[2];
+        } else {
+            for (int bi = 0; bi < 3 * min(4, nx - q4); ++bi)
+                out[o + bi] = ((m >> (8 * (bi / 3))) & 1)
+                                  ? in[o + bi]
+                                  : (uint8_t)((bi < 4 ? ow[0] : bi < 8 ? ow[1] : ow[2]) >> (8 * (bi & 3)));
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) k_blur_exact(Frame f, BlurParams bp,
                                                          const uint8_t* __restrict__ in,
                                                          uint8_t* __restrict__ out,
@@ -714,6 +1041,32 @@ int launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, uin
         k_blur_exact<<<grid, kThreads, sm, st>>>(f, bp, in_rgb, out_rgb, depth);
     } else {
         const int K = 2 * bp.hw + 1;
+        // K8t (tensor cores) for K <= 17; STK_BLUR_TC=0 selects v3 instead (A/B)
+        static const bool tc_on = [] {
+            const char* e = getenv("STK_BLUR_TC");
+            return e ? atoi(e) != 0 : true;
+        }();
+        if (tc_on && !bp.blur_map && bp.lut_len <= 1024 && K <= 17 && f.N * 3 < (1ll << 31)) {
+            const dim3 gt((f.W + TcGeom<3>::BX - 1) / TcGeom<3>::BX, (f.H + TcGeom<3>::BY - 1) / TcGeom<3>::BY);
+#define STK_BLUR_TC(KK)                                                                          \
+    case KK:                                                                                     \
+        cudaFuncSetAttribute(k_blur_tc<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                             (int)TcGeom<KK>::SM);                                               \
+        k_blur_tc<KK><<<gt, TcGeom<KK>::NT, TcGeom<KK>::SM, st>>>(f, bp, in_rgb, out_rgb, depth); \
+        return 1;
+            switch (K) {
+                STK_BLUR_TC(3)
+                STK_BLUR_TC(5)
+                STK_BLUR_TC(7)
+                STK_BLUR_TC(9)
+                STK_BLUR_TC(11)
+                STK_BLUR_TC(13)
+                STK_BLUR_TC(15)
+                STK_BLUR_TC(17)
+                default: break;
+            }
+#undef STK_BLUR_TC
+        }
         if (!bp.blur_map && bp.lut_len <= 1024) {
             const dim3 g3((f.W + V3Geom<3>::BX - 1) / V3Geom<3>::BX, (f.H + V3Geom<3>::BY - 1) / V3Geom<3>::BY);
 #define STK_BLUR_V3(KK)                                                                         \

@@ -316,6 +316,36 @@ def test_pipeline_wide_blur_vs_oracle(dev, stk, port, synth, sigma):
     assert np.abs(img.astype(int) - want["refocused"].astype(int)).max() <= BLUR_TOL_LSB
 
 
+# sigma -> kernel size 2 ceil(3 sigma) + 1: 3, 5, 7, 9, 11, (13: default), 15, 17
+@pytest.mark.parametrize("sigma", [0.3, 0.6, 1.0, 1.3, 1.6, 2.3, 2.6])
+def test_pipeline_tc_blur_sizes_vs_oracle(dev, stk, port, synth, sigma):
+    """Every kernel size of the tensor-core blur (K8t, K <= 17) through the
+    frame path against the oracle's FP64 2-D blur: <= 1 LSB everywhere and
+    almost everywhere exact (hi/lo f16 splits carry ~22 bits, so only sums
+    within ~1e-4 of a rounding boundary may differ)."""
+    l, r = synth.dead_leaves(320, 240, 16, frame=5)
+    res, img = run(stk, dev, l, r, k=4, window=9, D=16, focus=[(8, 16)], sigma=sigma)
+    want = port.run_frame(l, r, k=4, window=9, max_disparity=16, focus=[(8, 16)], sigma=sigma)
+    eq(res.dense, want["dense"], "dense")
+    d = np.abs(img.astype(int) - want["refocused"].astype(int))
+    assert d.max() <= BLUR_TOL_LSB
+    assert (d != 0).mean() < 1e-3, (d != 0).mean()
+
+
+@pytest.mark.parametrize("W,H,sigma", [(333, 201, 2.0), (100, 50, 2.6), (7, 5, 1.0), (136, 33, 2.0),
+                                       (264, 64, 0.6), (130, 31, 2.3)])
+def test_pipeline_tc_blur_edge_shapes(dev, stk, port, synth, W, H, sigma):
+    """K8t at shapes that exercise its slow paths: W not a multiple of 4
+    (unaligned rows), W < 136 (no CTA has its staged columns inside the
+    image), partial tiles in x and y, a frame smaller than one tile."""
+    D = 8
+    l, r = synth.dead_leaves(W, H, D, frame=3)
+    res, img = run(stk, dev, l, r, k=3, window=3, D=D, focus=[(2, 6)], sigma=sigma)
+    want = port.run_frame(l, r, k=3, window=3, max_disparity=D, focus=[(2, 6)], sigma=sigma)
+    eq(res.dense, want["dense"], "dense")
+    assert np.abs(img.astype(int) - want["refocused"].astype(int)).max() <= BLUR_TOL_LSB
+
+
 def test_graph_survives_focus_table_reallocation(dev, stk, port, synth):
     """A stage entry that grows the slot's focus tables (a 67x67 blur kernel:
     > 4096 weights; max_disparity >= 1024: > 1024 LUT entries) between two
