@@ -524,6 +524,206 @@ __global__ void __launch_bounds__(P5C * P5S, 2) k_peek_cols5(Frame f, const int1
     }
 }
 
+// int16x2 lane helpers for K7 v6: sign masks, per-lane add / min / max
+// (__byte_perm drops bit 3 of the selector nibbles: the sign-replicating
+// selector 0xbb99 needs prmt itself)
+__device__ __forceinline__ uint32_t sgn2(uint32_t v) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, 0, 0xbb99;" : "=r"(r) : "r"(v));
+    return r;
+}
+__device__ __forceinline__ uint32_t vadd2(uint32_t a, uint32_t b) { return __vadd2(a, b); }
+__device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) { return __vmins2(a, b); }
+__device__ __forceinline__ uint32_t vmax2(uint32_t a, uint32_t b) { return __vmaxs2(a, b); }
+
+// K7 v6: K7 v5 with both columns of a thread in int16x2 lanes (PRMT sign
+// masks, LOP3 selects, VIADD/VIMNMX.16x2): half the instructions per row.
+__global__ void __launch_bounds__(P5C * P5S, 2) k_peek_cols6(Frame f, const int16_t* __restrict__ in,
+                                                          int16_t* __restrict__ out) {
+    __shared__ int s_cnt[P5S][2 * P5C];
+    __shared__ uint32_t s_first[P5S][2 * P5C];  // f1 | f2 << 16 (int16 each, -1 = none)
+    __shared__ uint32_t s_last[P5S][2 * P5C];   // l1 | l2 << 16 (last, second last)
+    __shared__ int16_t ctx_ab[P5S][2 * P5C], ctx_bl[P5S][2 * P5C];
+    __shared__ int col_total[2 * P5C], col_top[2 * P5C], col_bot[2 * P5C];
+    __shared__ unsigned long long red[P5C * P5S / 32];
+    const int W = f.W, H = f.H, thr = f.thr;
+    const int cp = threadIdx.x % P5C, s = threadIdx.x / P5C;
+    const int x = 2 * (blockIdx.x * P5C + cp);  // W even
+    const int sr = (H + P5S - 1) / P5S;
+    const int ya = min(H, s * sr), yb = min(H, ya + sr);
+    const bool col = x < W;
+    const uint32_t* __restrict__ in2 = reinterpret_cast<const uint32_t*>(in);
+    uint32_t* __restrict__ out2 = reinterpret_cast<uint32_t*>(out);
+    const size_t W2 = (size_t)W / 2;
+    // ---- pass 1 (bottom-up), both columns in int16x2 lanes: lane masks by
+    // sign replication (PRMT 0xbb99: 0xffff where negative), selects by LOP3.
+    //   f1 / f2: nearest / second nearest known going up (the segment's first
+    //   two from the top once the walk ends; f1 is also "nearest known
+    //   below" for the rows above), l1 / l2: the first two met (the
+    //   segment's last two), n2: known counts.
+    uint32_t f1 = 0xffffffffu, f2 = 0xffffffffu, l1 = 0xffffffffu, l2 = 0xffffffffu, n2 = 0;
+    if (col) {
+        const uint32_t* ip = in2 + x / 2 + (size_t)(yb - 1) * W2;
+        uint32_t* op = out2 + x / 2 + (size_t)(yb - 1) * W2;
+        auto row = [&](uint32_t v, uint32_t* dst) {
+            *dst = f1;
+            const uint32_t md = sgn2(v);  // unknown lanes
+            const uint32_t m2 = ~md & ~sgn2(l1) & sgn2(l2);
+            l2 = (v & m2) | (l2 & ~m2);
+            const uint32_t m1 = ~md & sgn2(l1);
+            l1 = (v & m1) | (l1 & ~m1);
+            f2 = (f2 & md) | (f1 & ~md);
+            f1 = (f1 & md) | (v & ~md);
+            n2 += ~md & 0x00010001u;
+        };
+        int y = yb - 1;
+        for (; y - P4B + 1 >= ya; y -= P4B, ip -= P4B * W2, op -= P4B * W2) {
+            uint32_t v[P4B];
+#pragma unroll
+            for (int k = 0; k < P4B; ++k) v[k] = __ldg(ip - k * W2);
+#pragma unroll
+            for (int k = 0; k < P4B; ++k) row(v[k], op - k * W2);
+        }
+        for (; y >= ya; --y, ip -= W2, op -= W2) row(__ldg(ip), op);
+    }
+    s_cnt[s][2 * cp] = (int)(n2 & 0xffffu);
+    s_cnt[s][2 * cp + 1] = (int)(n2 >> 16);
+    s_first[s][2 * cp] = pack2(lo16(f1), lo16(f2));
+    s_first[s][2 * cp + 1] = pack2(hi16s(f1), hi16s(f2));
+    s_last[s][2 * cp] = pack2(lo16(l1), lo16(l2));
+    s_last[s][2 * cp + 1] = pack2(hi16s(l1), hi16s(l2));
+    __syncthreads();
+    // ---- phase 2: warp = column, lane = segments (2 lane, 2 lane + 1)
+    {
+        const unsigned full = 0xffffffffu;
+        const int cx = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int i0 = 2 * lane, i1 = i0 + 1;
+        const int c0 = s_cnt[i0][cx], c1 = s_cnt[i1][cx];
+        const uint32_t F0 = s_first[i0][cx], F1 = s_first[i1][cx];
+        const uint32_t L0 = s_last[i0][cx], L1 = s_last[i1][cx];
+        // nearest known above each segment: "latest known" exclusive scan
+        int inc = c1 ? lo16(L1) : (c0 ? lo16(L0) : -1);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(full, inc, o);
+            if (lane >= o && inc < 0) inc = t;
+        }
+        int ex = __shfl_up_sync(full, inc, 1);
+        if (lane == 0) ex = -1;
+        ctx_ab[i0][cx] = (int16_t)ex;
+        ctx_ab[i1][cx] = (int16_t)(c0 ? lo16(L0) : ex);
+        // nearest known below each segment: "earliest known" suffix scan
+        int sinc = c0 ? lo16(F0) : (c1 ? lo16(F1) : -1);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_down_sync(full, sinc, o);
+            if (lane + o < 32 && sinc < 0) sinc = t;
+        }
+        int sx = __shfl_down_sync(full, sinc, 1);
+        if (lane == 31) sx = -1;
+        ctx_bl[i1][cx] = (int16_t)sx;
+        ctx_bl[i0][cx] = (int16_t)(c1 ? lo16(F1) : sx);
+        const int total = __reduce_add_sync(full, c0 + c1);
+        // first two knowns of the column: ordered combine of (k1, k2)
+        auto comb_first = [](int a1, int a2, int b1, int& r1, int& r2) {
+            if (a2 >= 0) { r1 = a1; r2 = a2; }
+            else if (a1 >= 0) { r1 = a1; r2 = b1; }
+            else { r1 = b1; r2 = -2; }  // -2: take b's second below
+        };
+        int k1, k2;
+        {
+            int r1, r2;
+            comb_first(lo16(F0), hi16s(F0), lo16(F1), r1, r2);
+            k1 = r1;
+            k2 = r2 == -2 ? hi16s(F1) : r2;
+        }
+        // last two: (m1 = last, m2 = second last), ordered combine, later wins
+        int m1, m2;
+        if (hi16s(L1) >= 0) { m1 = lo16(L1); m2 = hi16s(L1); }
+        else if (lo16(L1) >= 0) { m1 = lo16(L1); m2 = lo16(L0); }
+        else { m1 = lo16(L0); m2 = hi16s(L0); }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int ok1 = __shfl_down_sync(full, k1, o), ok2 = __shfl_down_sync(full, k2, o);
+            const int om1 = __shfl_down_sync(full, m1, o), om2 = __shfl_down_sync(full, m2, o);
+            if ((lane & (2 * o - 1)) == 0 && lane + o < 32) {
+                // this lane's range precedes the other's
+                if (k2 < 0) {
+                    if (k1 >= 0) k2 = ok1;
+                    else { k1 = ok1; k2 = ok2; }
+                }
+                if (om2 >= 0) { m1 = om1; m2 = om2; }
+                else if (om1 >= 0) { m2 = m1; m1 = om1; }
+            }
+        }
+        if (lane == 0) {
+            col_total[cx] = total;
+            col_top[cx] = total >= 2 ? peek_estimate(k1, k2, thr) : -1;
+            col_bot[cx] = total >= 2 ? peek_estimate(m2, m1, thr) : -1;
+        }
+    }
+    __syncthreads();
+    // ---- pass 2 (top-down), int16x2 lanes as pass 1 (peek_resolve per lane)
+    unsigned long long known = 0;
+    if (col) {
+        const int t0 = col_total[2 * cp], t1 = col_total[2 * cp + 1];
+        // total 0: every estimate is -1; total 1: the single known is a or b
+        const uint32_t sg = (t0 == 1 ? 0x0000ffffu : 0u) | (t1 == 1 ? 0xffff0000u : 0u);
+        const uint32_t et = pack2(t0 ? col_top[2 * cp] : -1, t1 ? col_top[2 * cp + 1] : -1);
+        const uint32_t eb = pack2(t0 ? col_bot[2 * cp] : -1, t1 ? col_bot[2 * cp + 1] : -1);
+        uint32_t a = pack2(ctx_ab[s][2 * cp], ctx_ab[s][2 * cp + 1]);
+        const uint32_t bl = pack2(ctx_bl[s][2 * cp], ctx_bl[s][2 * cp + 1]);
+        // r <= thr as the sign of r - thr - 1 (thr clamped to [-1, 32767]: r is in [0, 32767])
+        const int tc = min(max(thr, -1), 32767);
+        const uint32_t nthr = pack2(-(tc + 1), -(tc + 1));
+        uint32_t kacc = 0;  // known counts per lane
+        const uint32_t* ip = in2 + x / 2 + (size_t)ya * W2;
+        uint32_t* op = out2 + x / 2 + (size_t)ya * W2;
+        auto row = [&](uint32_t v, uint32_t bw, uint32_t* dst) {
+            const uint32_t mbw = sgn2(bw);
+            const uint32_t b = (bl & mbw) | (bw & ~mbw);
+            const uint32_t ma = sgn2(a), mab = ma | sgn2(b);
+            const uint32_t mx = vmax2(a, b), mn = vmin2(a, b);
+            const uint32_t r = vadd2(mx, vadd2(~mn, 0x00010001u));  // |a - b| (lanes with a, b >= 0)
+            const uint32_t le = sgn2(vadd2(r, nthr));                // r <= thr
+            const uint32_t avg = vadd2(a & b, ((a ^ b) >> 1) & 0x7fff7fffu);  // (a + b) >> 1, no overflow
+            const uint32_t est = (avg & le) | (mn & ~le);
+            const uint32_t edge = (et & ma) | (eb & ~ma);
+            const uint32_t two = (edge & mab) | (est & ~mab);
+            const uint32_t one = (b & ma) | (a & ~ma);
+            const uint32_t u = (one & sg) | (two & ~sg);
+            const uint32_t md = sgn2(v);
+            const uint32_t res = (u & md) | (v & ~md);
+            a = (a & md) | (v & ~md);
+            *dst = res;
+            kacc += (~res >> 15) & 0x00010001u;
+        };
+        // batches: all loads of P4B rows (input and scratch) issue before the
+        // stores (the scratch loads would otherwise wait behind them)
+        int y = ya;
+        for (; y + P4B <= yb; y += P4B, ip += P4B * W2, op += P4B * W2) {
+            uint32_t v[P4B], bw[P4B];
+#pragma unroll
+            for (int k = 0; k < P4B; ++k) {
+                v[k] = __ldg(ip + k * W2);
+                bw[k] = op[k * W2];
+            }
+#pragma unroll
+            for (int k = 0; k < P4B; ++k) row(v[k], bw[k], op + k * W2);
+        }
+        for (; y < yb; ++y, ip += W2, op += W2) row(__ldg(ip), *op, op);
+        known = (kacc & 0xffffu) + (kacc >> 16);
+    }
+    for (int o = 16; o > 0; o >>= 1) known += __shfl_xor_sync(0xffffffffu, known, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = known;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int i = 0; i < P5C * P5S / 32; ++i) t += red[i];
+        if (t) atomicAdd(&f.sc->known, t);
+    }
+}
+
 }  // namespace
 
 void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStream_t st) {
@@ -542,7 +742,7 @@ void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStrea
 void launch_peek_cols(const Frame& f, const int16_t* in, int16_t* out, int16_t*, cudaStream_t st) {
     if (f.N == 0) return;
     if (f.W % 2 == 0 && (reinterpret_cast<uintptr_t>(in) & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 3) == 0) {
-        k_peek_cols5<<<(f.W + 2 * P5C - 1) / (2 * P5C), P5C * P5S, 0, st>>>(f, in, out);
+        k_peek_cols6<<<(f.W + 2 * P5C - 1) / (2 * P5C), P5C * P5S, 0, st>>>(f, in, out);
         return;
     }
     k_peek_cols2<<<(f.W + PC - 1) / PC, PC * PS, 0, st>>>(f, in, out);

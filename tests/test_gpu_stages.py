@@ -430,6 +430,19 @@ def test_reconstruct_random_vs_oracle(dev, stk, port, synth, w, h, pct):
         eq(stk.peek_columns(f, thr, device=dev), port.peek_columns(f, thr))
 
 
+@pytest.mark.parametrize("w,h,p,vmax", [(320, 240, 0.3, 257), (64, 2304, 0.3, 257), (64, 4320, 0.02, 257),
+                                        (66, 700, 0.05, 1024), (48, 300, 0.2, 32767), (2, 4321, 0.01, 32767)])
+def test_peek_wide_values_vs_oracle(dev, stk, port, w, h, p, vmax):
+    """K7 keeps both columns of a thread in int16x2 lanes (sign masks by PRMT,
+    selects by LOP3): disparities with a high byte (>= 256, up to 32767), tall
+    columns (many segments, load batches), thresholds up to beyond the int16
+    range -- against the oracle's scalar int arithmetic."""
+    rng = np.random.default_rng(w * 7919 + h)
+    m = np.where(rng.random((h, w)) < p, rng.integers(0, vmax + 1, (h, w)), -1).astype(np.int16)
+    for thr in (0, 1, 300, 40000):
+        eq(stk.peek_columns(m, thr, device=dev), port.peek_columns(m, thr))
+
+
 # ----------------------------------------------------------------- K8 -------
 def test_blur_map(dev, stk, golden, port, synth):
     eq(stk.build_blur_map(np.array([[2, 4, 11, 7]], np.int16), [(3, 5), (10, 12)], 16, device=dev),
