@@ -7,7 +7,7 @@ K-Means) gives meaningless periods.  Usage: python scripts/loo_apply.py ROOT"""
 import sys
 root = sys.argv[1] + "/paper_2001_07809_b200/csrc/"
 edits = {
-    "stk_internal.cuh": [("namespace stk {\n", "namespace stk {\n\ninline int skipk(int bit) {\n"
+    "stk_internal.cuh": [("namespace stk {\n", "#include <cstdlib>\nnamespace stk {\n\ninline int skipk(int bit) {\n"
                           "    static const int v = [] { const char* e = getenv(\"STK_SKIP\"); return e ? atoi(e) : 0; }();\n"
                           "    return v & bit;\n}\n")],
     "k_bnd.cu": [("    launch_ccl_region(f, rbits, runroot, bord, st);\n    k_ccl_borders",
