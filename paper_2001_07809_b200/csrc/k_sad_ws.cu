@@ -50,7 +50,7 @@ constexpr int kSegW = 32;  // output columns per horizontal segment
 #define STK_SAD_HB 6
 #endif
 constexpr int HB = STK_SAD_HB;  // matchable pixels per horizontal batch
-enum { BAR_FULL0 = 1, BAR_FULL1 = 2, BAR_EMPTY0 = 3, BAR_EMPTY1 = 4, BAR_H = 5 };
+enum { BAR_FULL0 = 1, BAR_FULL1 = 2, BAR_EMPTY0 = 3, BAR_EMPTY1 = 4, BAR_H = 5, BAR_V = 6 };
 
 struct WP {
     int h, D, Q, QP, NG, NCH, CW, SW, CSW, TH;
@@ -62,44 +62,56 @@ struct WP {
 __device__ __forceinline__ uint32_t lo16(uint32_t v) { return v & 0xffffu; }
 __device__ __forceinline__ uint32_t hi16(uint32_t v) { return v >> 16; }
 
-// (byte p, 0, byte p-1, 0) of a run of words (p compile-time after unrolling).
-template <int N>
-__device__ __forceinline__ uint32_t r_pair(const uint32_t (&w)[N], int p) {
-    const int i = p >> 2, s = p & 3;
-    if (s) return __byte_perm(w[i], 0u, (uint32_t)s | 0x40u | (uint32_t)(s - 1) << 8 | 0x4000u);
-    // byte p = byte 0 of w[i], byte p-1 = byte 3 of w[i-1]
-    return __byte_perm(w[i - 1], w[i], 0x0304u) & 0x00ff00ffu;
+// Vertical update of the G x K colsum units of one thread for one row pair.
+// INIT: add the new row only.  Lw: L words of the row(s); Un/Uo: the rows'
+// pair-ring words, pointer at word c - 1 of the thread (see pair_at).
+template <int WIN, int G, int K>
+struct VGeom {
+    static constexpr int h = WIN / 2;
+    static constexpr int rL = ((-h) % 4 + 4) % 4;     // byte residue of the L column base
+    static constexpr int rR = ((1 - h) % 4 + 4) % 4;  // byte residue of the R window base
+    static constexpr int NWL = (rL + K - 1) / 4 + 1;
+    static constexpr int PMIN = rR + 1, PMAX = rR + K + 4 * G - 2;  // pair positions p used
+    static constexpr int JMIN = (PMIN - 1) / 2, JMAX = PMAX / 2;    // pair-ring words w[j] = U[c - j]
+    static constexpr int NJ = JMAX - JMIN + 1;
+};
+
+// (R(P), 0, R(P-1), 0) for the thread's run position p (P = 4 rw0 + p): the
+// pair ring stores R reversed as u16 (U[k] = R(Pmax - k)), so the pair is the
+// u32 at U[k], k = Pmax - P = kb - p with kb odd: k even (one word) for odd p,
+// a funnel of two words for even p.  w[j - JMIN] = U32[c - j], c = (kb - 1) / 2.
+template <int JMIN, int NJ>
+__device__ __forceinline__ uint32_t pair_at(const uint32_t (&w)[NJ], int p) {
+    if (p & 1) return w[(p - 1) / 2 - JMIN];
+    // U32[c - p/2] holds (U[k - 1], U[k]), U32[c - p/2 + 1] holds (U[k + 1], U[k + 2])
+    return __byte_perm(w[p / 2 - JMIN], w[p / 2 - 1 - JMIN], 0x5432);
 }
 
-// Vertical update of the G x K colsum units of one thread for one row pair.
-// INIT: add the new row only.  Rw/Lw: R and L words of the row(s).
 template <int WIN, int G, int K, bool INIT>
-__device__ __forceinline__ void v_rows(const uint32_t* __restrict__ Ln, const uint32_t* __restrict__ Rn,
-                                       const uint32_t* __restrict__ Lo, const uint32_t* __restrict__ Ro,
+__device__ __forceinline__ void v_rows(const uint32_t* __restrict__ Ln, const uint32_t* __restrict__ Un,
+                                       const uint32_t* __restrict__ Lo, const uint32_t* __restrict__ Uo,
                                        uint32_t (&A)[G][K], uint32_t (&B)[G][K]) {
-    constexpr int h = WIN / 2;
-    constexpr int rL = ((-h) % 4 + 4) % 4;        // byte residue of the L column base
-    constexpr int rR = ((1 - h) % 4 + 4) % 4;     // byte residue of the R window base
-    constexpr int NWL = (rL + K - 1) / 4 + 1;
-    constexpr int NWR = (G - 1) + (rR + K - 1) / 4 + 2;
-    uint32_t ln[NWL], rn[NWR], lo[NWL], ro[NWR];
+    using V = VGeom<WIN, G, K>;
+    constexpr int rL = V::rL, rR = V::rR, NWL = V::NWL, JMIN = V::JMIN, NJ = V::NJ;
+    uint32_t ln[NWL], lo[NWL], un[NJ], uo[NJ];
 #pragma unroll
     for (int i = 0; i < NWL; ++i) ln[i] = Ln[i];
+    // Un points at U32[c - 1]: w[j - JMIN] = U32[c - j] = Un[1 - j]
 #pragma unroll
-    for (int i = 0; i < NWR; ++i) rn[i] = Rn[i];
+    for (int j = 0; j < NJ; ++j) un[j] = Un[1 - (j + JMIN)];
     if (!INIT) {
 #pragma unroll
         for (int i = 0; i < NWL; ++i) lo[i] = Lo[i];
 #pragma unroll
-        for (int i = 0; i < NWR; ++i) ro[i] = Ro[i];
+        for (int j = 0; j < NJ; ++j) uo[j] = Uo[1 - (j + JMIN)];
     }
     // Spread words: the L byte as (L, 0, L, 0) and R byte pairs as
     // (R(x), 0, R(x-1), 0), so one VABSDIFF4 yields two disparities already
     // in u16x2 lanes (no per-result unpacking).  R(c - 4q - m) sits at byte
     // o + 3 - m of the run, o = rR + k - 4j + 4(G-1); word A (d = 4q, 4q+1)
     // takes the pair at p = o + 3, word B (d = 4q+2, 4q+3) the pair at
-    // p = o + 1.  Pairs are pure functions of compile-time p, so each is
-    // built once per row and shared by every (k, j) that uses it.
+    // p = o + 1.  The pairs come ready-made from the pair ring (built once per
+    // row for the whole CTA instead of once per thread).
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const int lb = rL + k;
@@ -110,14 +122,14 @@ __device__ __forceinline__ void v_rows(const uint32_t* __restrict__ Ln, const ui
 #pragma unroll
         for (int j = 0; j < G; ++j) {
             const int o = rR + k - 4 * j + 4 * (G - 1);
-            const uint32_t an = __vabsdiffu4(spn, r_pair<NWR>(rn, o + 3));
-            const uint32_t bn = __vabsdiffu4(spn, r_pair<NWR>(rn, o + 1));
+            const uint32_t an = __vabsdiffu4(spn, pair_at<JMIN, NJ>(un, o + 3));
+            const uint32_t bn = __vabsdiffu4(spn, pair_at<JMIN, NJ>(un, o + 1));
             if (INIT) {
                 A[j][k] += an;
                 B[j][k] += bn;
             } else {
-                const uint32_t ao = __vabsdiffu4(spo, r_pair<NWR>(ro, o + 3));
-                const uint32_t bo = __vabsdiffu4(spo, r_pair<NWR>(ro, o + 1));
+                const uint32_t ao = __vabsdiffu4(spo, pair_at<JMIN, NJ>(uo, o + 3));
+                const uint32_t bo = __vabsdiffu4(spo, pair_at<JMIN, NJ>(uo, o + 1));
                 A[j][k] = A[j][k] + an - ao;
                 B[j][k] = B[j][k] + bn - bo;
             }
@@ -184,6 +196,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
     uint32_t* best = reinterpret_cast<uint32_t*>(fullb + p.RS);
     constexpr int NE = WinTab<WIN, K>::NE;
     uint32_t* tab = best + 2 * p.SW;  // [SW][NE] byte offsets (16-byte aligned)
+    // pair ring: PR rows of R reversed as u16 (see pair_at), RP / 2 words each
+    constexpr int PR = WIN + 4;
+    uint32_t* pring = tab + (size_t)p.SW * NE;
 
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
     const int x0 = blockIdx.x * p.SW;
@@ -248,6 +263,35 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
             for (int k = 0; k < K; ++k) A[j][k] = B[j][k] = 0u;
         uint2* csq = cs + (size_t)(g * G) * p.CSW + ch * (K + 1);
         const size_t bufstride = (size_t)p.QP * p.CSW;
+        // Pair ring: row i's R bytes reversed into u16 lanes, U[k] = R(RP - 1 - k),
+        // so every (R(x), 0, R(x-1), 0) pair the vertical pass needs is one
+        // u32 (or a funnel of two): built once per row for the CTA, not once
+        // per thread.  Item m = 8 u16 from two aligned raw words.
+        const int RPW = p.RP / 2;  // u32 words per pair-ring row
+        // spread(raw slot, its phase, pair slot)
+        auto spread = [&](int rsl, uint32_t ph, int psl) {
+            mbar_wait(&fullb[rsl], ph);
+            const uint8_t* R = ring + (size_t)rsl * (p.LP + p.RP) + p.LP;
+            uint32_t* U = pring + (size_t)psl * RPW;
+            for (int m = tv; m < p.RP / 8; m += 32 * p.NVW) {
+                const int k0 = 8 * m;
+                const uint32_t wb = *reinterpret_cast<const uint32_t*>(R + p.RP - 4 - k0);
+                const uint32_t wa = *reinterpret_cast<const uint32_t*>(R + p.RP - 8 - k0);
+                *reinterpret_cast<uint4*>(U + k0 / 2) =
+                    make_uint4(__byte_perm(wb, 0u, 0x4243), __byte_perm(wb, 0u, 0x4041),
+                               __byte_perm(wa, 0u, 0x4243), __byte_perm(wa, 0u, 0x4041));
+            }
+        };
+        // the thread's pair-ring word c - 1, c = (RP - 2) / 2 - 2 rw0 (see pair_at)
+        const uint32_t* const ubase = pring + (RPW - 2 - 2 * rw0);
+        // prologue: pair rows 0 .. PR-1 (rows are then built three steps ahead)
+        for (int i = 0; i < min(PR, NRR); ++i) spread(i % p.RS, (uint32_t)((i / p.RS) & 1), i);
+        named_sync(BAR_V, 32 * p.NVW);
+        // pair slots of the entering / leaving rows and of the row built next
+        // (PR + 2 = WIN + 6 > RS: its raw slot and phase tracked separately)
+        int pn = WIN - 1, po = PR - 1, psp = (WIN + 4) % PR;
+        int rsp = (WIN + 4) % p.RS;
+        uint32_t php = (uint32_t)(((WIN + 4) / p.RS) & 1);
         int rs_n = WIN % p.RS, ph_n = (WIN / p.RS) & 1, rs_o = 0;
         for (int t = 0; t < T; ++t) {
             if (t == 0) {
@@ -255,8 +299,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                     const int s = i % p.RS;
                     mbar_wait(&fullb[s], (uint32_t)((i / p.RS) & 1));
                     const uint32_t* Ls = reinterpret_cast<const uint32_t*>(ring + (size_t)s * (p.LP + p.RP));
-                    const uint32_t* Rs = reinterpret_cast<const uint32_t*>(ring + (size_t)s * (p.LP + p.RP) + p.LP);
-                    if (act) v_rows<WIN, G, K, true>(Ls + lw0, Rs + rw0, nullptr, nullptr, A, B);
+                    if (act) v_rows<WIN, G, K, true>(Ls + lw0, ubase + (size_t)i * RPW, nullptr, nullptr, A, B);
                 }
             } else {
                 // slot / phase of the entering row t+WIN-1 and the leaving row t-1
@@ -266,11 +309,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                 if (++rs_o == p.RS) rs_o = 0;
                 const uint8_t* bn = ring + (size_t)sn * (p.LP + p.RP);
                 const uint8_t* bo = ring + (size_t)so * (p.LP + p.RP);
+                if (++pn == PR) pn = 0;
+                if (++po == PR) po = 0;
                 if (act)
-                    v_rows<WIN, G, K, false>(reinterpret_cast<const uint32_t*>(bn) + lw0,
-                                             reinterpret_cast<const uint32_t*>(bn + p.LP) + rw0,
-                                             reinterpret_cast<const uint32_t*>(bo) + lw0,
-                                             reinterpret_cast<const uint32_t*>(bo + p.LP) + rw0, A, B);
+                    v_rows<WIN, G, K, false>(reinterpret_cast<const uint32_t*>(bn) + lw0, ubase + (size_t)pn * RPW,
+                                             reinterpret_cast<const uint32_t*>(bo) + lw0, ubase + (size_t)po * RPW,
+                                             A, B);
             }
             const int b = t & 1;
             if (t >= 2) {
@@ -281,6 +325,11 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                     fence_proxy_async();
                     for (; issued < min(t - 1 + p.RS + 1, NRR); ++issued) issue_row(issued);
                 }
+                // pair row t+WIN+2 (used from step t+3, after two more EMPTY
+                // barriers) into the slot of row t-2, last read at step t-1
+                if (t + WIN + 2 < NRR) spread(rsp, php, psp);
+                if (++psp == PR) psp = 0;
+                if (++rsp == p.RS) rsp = 0, php ^= 1u;
             }
             if (act) {
                 uint2* dst = csq + b * bufstride;
@@ -591,7 +640,7 @@ bool launch_sad_ws(const Frame& f, cudaStream_t st, bool dry) {
         p.RP = (p.NCH * K + 4 * p.QP + oR + 16 + 15) & ~15;
         const int NE = w <= 21 ? (w == 21 ? WinTab<21, 12>::NE : WinTab<15, 12>::NE) : WinTab<31, 8>::NE;
         sm = (size_t)2 * p.QP * p.CSW * 8 + (size_t)p.RS * (p.LP + p.RP) + p.RS * 8 +
-             2 * SW * 4 + (size_t)SW * NE * 4;
+             2 * SW * 4 + (size_t)SW * NE * 4 + (size_t)(w + 4) * p.RP * 2;  // + pair ring
         if (sm <= 226 * 1024 && p.nthreads <= kMaxThreads) break;
         sm = 0;
     }
