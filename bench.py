@@ -490,7 +490,7 @@ def main():
         "metric": METRIC, "value": round(fps_dev, 3), "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_dev / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u8/i16 (int stages), f64 (L*, K-Means), f32 (blur)", "data": "synthetic",
+        "dtype": "u8/i16 (int stages), f64 (L*, K-Means), f32-accumulated blur (f16 hi/lo tensor-core products)", "data": "synthetic",
         "config": {"workload": workload(args.config),
                    "frames_pool": P, "frames_in_flight": S, "warmup_frames": n_warm,
                    "l2": "inputs larger than L2 (pool of distinct frames, ~56.6 MB each)",

@@ -149,7 +149,7 @@ struct WinTab {
     static constexpr int NE = (2 + NT + 3) / 4 * 4;   // entry words (uint4 multiple)
 };
 
-template <int WIN, int K, int NW>
+template <int WIN, int K, int NW, bool MIXED = false>
 __device__ __forceinline__ void window_sum(const char* __restrict__ cq, const uint32_t* __restrict__ ent,
                                            bool sel_y, uint32_t (&lo)[NW], uint32_t (&hi)[NW]) {
     constexpr int NT = WinTab<WIN, K>::NT, NE = WinTab<WIN, K>::NE;
@@ -179,7 +179,7 @@ __device__ __forceinline__ void window_sum(const char* __restrict__ cq, const ui
         const uint32_t xs = y ? t[1].y : t[1].x;
         X -= xs;
         Y -= hi16(xs);
-        lo[w] = X - (Y << 16);
+        lo[w] = MIXED ? X : X - (Y << 16);  // MIXED: the caller folds Y << 16 into its key
         hi[w] = Y;
     }
 }
@@ -459,12 +459,16 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                         }
                         const uint32_t dbase = 4 * q + 2 * region;
                         uint32_t lo[HQ], hi[HQ];
-                        window_sum<WIN, K, HQ>(cq, tab + (hwb + r) * NE, region != 0, lo, hi);
+                        window_sum<WIN, K, HQ, true>(cq, tab + (hwb + r) * NE, region != 0, lo, hi);
 #pragma unroll
                         for (int w = 0; w < HQ; ++w) {
-                            // word w: d = dbase + 2w (lo lane), dbase + 2w + 1 (hi lane)
+                            // word w: d = dbase + 2w (lo lane), dbase + 2w + 1 (hi lane);
+                            // lo[w] = X = low sum + (hi sum << 16) mod 2^32, so the low
+                            // lane's key (X - (Y << 16)) * 1024 + d0 is X * 1024 + d0 -
+                            // Y * 2^26 (mod 2^32): two multiply-adds
                             const uint32_t d0 = dbase + 2 * w;
-                            uint32_t k0 = lo[w] * 1024u + d0, k1 = hi[w] * 1024u + d0 + 1;
+                            uint32_t k0 = hi[w] * (uint32_t)(-(1 << 26)) + (lo[w] * 1024u + d0),
+                                     k1 = hi[w] * 1024u + d0 + 1;
                             if (!FAST) {
                                 if ((int)d0 > lim) k0 = 0xffffffffu;
                                 if ((int)d0 + 1 > lim) k1 = 0xffffffffu;
