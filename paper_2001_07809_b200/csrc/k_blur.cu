@@ -571,28 +571,31 @@ __device__ __forceinline__ uint32_t bytes_h2(uint32_t w, uint32_t sel) {
 template <int K>
 struct TcGeom {
     static constexpr int h = K / 2, BX = 128, BY = 32, NT = 192;
-    static constexpr int IR = BY + 16;   // staged rows (two 16-row k-steps per slab)
-    static constexpr int IPX = 144;      // staged px: image x0 - 8 + p (18 vertical n-tiles)
-    static constexpr int XS = IPX + 8;   // f16 per staged row (304 B: conflict-free ldmatrix)
+    static constexpr int XO = 8 * ((h + 7) / 8);        // staged px p = image x0 - XO + p (XO - h < 8)
+    static constexpr int NKV = (16 + 2 * h + 15) / 16;  // vertical 16-row k-steps per 16-row slab
+    static constexpr int NKH = (15 + XO + h) / 16 + 1;  // horizontal 16-px k-blocks per 8-px output tile
+    static constexpr int IR = 16 + 16 * NKV;            // staged rows: slab 0 [0, 16 NKV), slab 1 [16, IR)
+    static constexpr int IPX = 16 * (7 + NKH);          // staged px (IPX / 8 vertical n-tiles)
+    static constexpr int XS = IPX + 8;                  // f16 per staged row (stride = 4 mod 8 words:
+                                                        // conflict-free ldmatrix)
+    static constexpr int OFF = 24, NTAB = OFF + 16 * (NKV > NKH ? NKV : NKH) + 16;  // weight-pair table
+    static constexpr bool WIDE = NKV > 2 || NKH > 2;
+    static constexpr int MINB = WIDE ? 2 : 4;           // CTAs per SM (80 / 168 registers)
     static constexpr size_t SM_X = (size_t)3 * IR * XS * 2;
-    static constexpr size_t SM = SM_X + (size_t)BX * BY + 2 * 64 * 4;  // + weight pair table
-    static_assert(K <= 17, "two 16-px k-blocks cover 8 outputs + 2h taps");
-    static_assert(BY == 32 && BX <= 2 * XS, "output rows 0-15 / 32-47 of each plane");
+    static constexpr size_t SM = SM_X + (size_t)BX * BY + 2 * NTAB * 4;
+    static_assert(K >= 3 && h <= 24, "3..49 taps");
+    static_assert(BY == 32 && BX <= 2 * XS, "output rows: 0-15 and IR-16..IR-1 of each plane");
+    static_assert(NTAB <= NT, "one table entry per thread");
 };
 
-#ifndef STK_TC_MINB
-#define STK_TC_MINB 4
-#endif
-#ifndef STK_TC_EARLY
-#define STK_TC_EARLY 0
-#endif
 template <int K>
-__global__ void __launch_bounds__(TcGeom<K>::NT, STK_TC_MINB) k_blur_tc(Frame f, BlurParams bp,
+__global__ void __launch_bounds__(TcGeom<K>::NT, TcGeom<K>::MINB) k_blur_tc(Frame f, BlurParams bp,
                                                               const uint8_t* __restrict__ in,
                                                               uint8_t* __restrict__ out,
                                                               const int16_t* __restrict__ depth) {
     using G = TcGeom<K>;
-    constexpr int h = G::h, BX = G::BX, BY = G::BY, NT = G::NT, IR = G::IR, XS = G::XS;
+    constexpr int h = G::h, BX = G::BX, BY = G::BY, NT = G::NT, IR = G::IR, XS = G::XS, XO = G::XO;
+    constexpr int NKV = G::NKV, NKH = G::NKH;
     extern __shared__ __align__(16) unsigned char smem[];
     uint16_t* xin = reinterpret_cast<uint16_t*>(smem);  // [3][IR][XS] f16 bits
     uint8_t* shf = smem + G::SM_X;                      // [BY][BX] sharp flags
@@ -601,15 +604,15 @@ __global__ void __launch_bounds__(TcGeom<K>::NT, STK_TC_MINB) k_blur_tc(Frame f,
     const int x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
     const int nx = min(BX, W - x0), ny = min(BY, H - y0);
     const bool a4 = (W & 3) == 0 && (reinterpret_cast<uintptr_t>(in) & 3) == 0;
-    // staged (row r, px p) = image (y0 - h + r, x0 - 8 + p), replicate-clamped;
+    // staged (row r, px p) = image (y0 - h + r, x0 - XO + p), replicate-clamped;
     // staging item = (row, 4 px): one 12-byte load, three 8-byte f16 stores
     // (one per channel plane)
-    constexpr int NG = G::IPX / 4, NI = IR * NG, PER = NI / NT, DV = BX * BY / 8, DPER = (DV + NT - 1) / NT;
-    static_assert(NI % NT == 0, "whole staging items per thread");
+    constexpr int NG = G::IPX / 4, NI = IR * NG, PER = (NI + NT - 1) / NT, DV = BX * BY / 8,
+                  DPER = (DV + NT - 1) / NT;
     // fast CTAs (full tile, aligned rows, staged columns inside the image)
     // issue every global load -- image rows, disparities, sharp table --
     // before the first use: one latency exposure
-    const bool fast = a4 && x0 - 8 >= 0 && x0 + G::IPX - 8 <= W && nx == BX && ny == BY && (W & 7) == 0 &&
+    const bool fast = a4 && x0 - XO >= 0 && x0 + G::IPX - XO <= W && nx == BX && ny == BY && (W & 7) == 0 &&
                       (reinterpret_cast<uintptr_t>(depth) & 15) == 0;
     uint32_t w[PER][3];
     uint4 dv[DPER];
@@ -618,14 +621,15 @@ __global__ void __launch_bounds__(TcGeom<K>::NT, STK_TC_MINB) k_blur_tc(Frame f,
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const int i = tid + k * NT, sy = min(max(y0 - h + i / NG, 0), H - 1);
-            const uint32_t* p = reinterpret_cast<const uint32_t*>(in) + (sy * W + x0 - 8) * 3 / 4 + 3 * (i % NG);
-            w[k][0] = __ldg(p);
-            w[k][1] = __ldg(p + 1);
-            w[k][2] = __ldg(p + 2);
+            if (NI % NT == 0 || i < NI) {
+                const uint32_t* p = reinterpret_cast<const uint32_t*>(in) + (sy * W + x0 - XO) * 3 / 4 + 3 * (i % NG);
+                w[k][0] = __ldg(p);
+                w[k][1] = __ldg(p + 1);
+                w[k][2] = __ldg(p + 2);
+            }
         }
     };
     if (fast) {
-        if (STK_TC_EARLY) load_rows();
 #pragma unroll
         for (int k = 0; k < DPER; ++k) {
             const int i = tid + k * NT;
@@ -693,12 +697,13 @@ __global__ void __launch_bounds__(TcGeom<K>::NT, STK_TC_MINB) k_blur_tc(Frame f,
         *reinterpret_cast<uint2*>(d + 2 * IR * XS) = make_uint2(bytes_h2(Bc, 0x4140), bytes_h2(Bc, 0x4342));
     };
     if (fast) {
-        if (!STK_TC_EARLY) load_rows();
+        load_rows();
 #pragma unroll
-        for (int k = 0; k < PER; ++k) put(tid + k * NT, w[k][0], w[k][1], w[k][2]);
+        for (int k = 0; k < PER; ++k)
+            if (NI % NT == 0 || tid + k * NT < NI) put(tid + k * NT, w[k][0], w[k][1], w[k][2]);
     } else {
         for (int i = tid; i < NI; i += NT) {
-            const int sy = min(max(y0 - h + i / NG, 0), H - 1), sx = x0 - 8 + 4 * (i % NG);
+            const int sy = min(max(y0 - h + i / NG, 0), H - 1), sx = x0 - XO + 4 * (i % NG);
             uint32_t b[12];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -713,7 +718,7 @@ __global__ void __launch_bounds__(TcGeom<K>::NT, STK_TC_MINB) k_blur_tc(Frame f,
     }
     // weight pair table: wtab[j] = (w1(j - OFF), w1(j - OFF + 1)) as f16x2 hi, and lo at
     // wtab[NTAB + j]; weights scaled by 2^6 per pass (exact) so the lo parts stay normal
-    constexpr int OFF = 24, NTAB = 64;
+    constexpr int OFF = G::OFF, NTAB = G::NTAB;
     uint32_t* wtab = reinterpret_cast<uint32_t*>(shf + BX * BY);
     if (tid < NTAB) {
         auto w1 = [&](int k) { return (k >= 0 && k < K) ? 64.f * __ldg(bp.g1 + k) : 0.f; };
@@ -735,41 +740,55 @@ __global__ void __launch_bounds__(TcGeom<K>::NT, STK_TC_MINB) k_blur_tc(Frame f,
         return v;
     };
     // vertical A_q[o][k] = w1(16q + k - o): regs (g,2t) (g+8,2t) (g,2t+8) (g+8,2t+8) (+1 in the high half)
-    uint32_t av_hi[2][4], av_lo[2][4];
+    uint32_t av_hi[NKV][4], av_lo[NKV][4];
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
+    for (int q = 0; q < NKV; ++q)
 #pragma unroll
         for (int rg = 0; rg < 4; ++rg) {
             const int tap = 16 * q + (rg >> 1) * 8 - (rg & 1) * 8;
             av_hi[q][rg] = wt(tap);
             av_lo[q][rg] = wt(NTAB + tap);
         }
-    // horizontal: output px x = 16 s0 + 8 pp + nn reads staged px x + 8 - h .. x + 8 + h,
-    // B_{pp,q}[kk][nn] = w1(16q + kk - nn - 8pp - 8 + h); regs (kk 2t, 2t+1; nn g), (kk 2t+8, 2t+9; nn g)
-    uint32_t bh_hi[2][2][2], bh_lo[2][2][2];
+    // horizontal: output px x = 16 s0 + 8 pp + nn reads staged px x + XO - h .. x + XO + h
+    // (k-blocks s0 .. s0 + NKH - 1), B_{pp,q}[kk][nn] = w1(16q + kk - nn - 8pp - XO + h);
+    // regs (kk 2t, 2t+1; nn g), (kk 2t+8, 2t+9; nn g)
+    uint32_t bh_hi[2][NKH][2], bh_lo[2][NKH][2];
 #pragma unroll
     for (int pp = 0; pp < 2; ++pp)
 #pragma unroll
-        for (int q = 0; q < 2; ++q)
+        for (int q = 0; q < NKH; ++q)
 #pragma unroll
             for (int rg = 0; rg < 2; ++rg) {
-                const int tap = 16 * q + 8 * rg - 8 * pp - 8 + h;
+                const int tap = 16 * q + 8 * rg - 8 * pp - XO + h;
                 bh_hi[pp][q][rg] = wt(tap);
                 bh_lo[pp][q][rg] = wt(NTAB + tap);
             }
-    // ---- vertical n-tile i (staged px 8i..8i+7): one ldmatrix.x4.trans = both k-steps
+    // ---- vertical n-tile i (staged px 8i..8i+7): one ldmatrix.x4.trans per two k-steps
     const uint32_t xaddr =
         (uint32_t)__cvta_generic_to_shared(xin + ((size_t)c * IR + 16 * slab + lane) * XS);
+    const uint32_t xaddr2 =  // .x2 (odd last k-step): lanes 0-15 address rows 32 (NKV / 2) + lane
+        (uint32_t)__cvta_generic_to_shared(xin + ((size_t)c * IR + 16 * slab + 32 * (NKV / 2) + (lane & 15)) * XS);
     auto vert = [&](int i, float (&d)[4]) {
-        uint32_t b0, b1, b2, b3;
-        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
-                     : "r"(xaddr + 16 * i));
         d[0] = d[1] = d[2] = d[3] = 0.f;
-        mma16816(d, av_hi[0], b0, b1);
-        mma16816(d, av_lo[0], b0, b1);
-        mma16816(d, av_hi[1], b2, b3);
-        mma16816(d, av_lo[1], b2, b3);
+#pragma unroll
+        for (int qq = 0; qq < NKV / 2; ++qq) {
+            uint32_t b0, b1, b2, b3;
+            asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                         : "r"(xaddr + 16 * i + qq * 32 * XS * 2));
+            mma16816(d, av_hi[2 * qq], b0, b1);
+            mma16816(d, av_lo[2 * qq], b0, b1);
+            mma16816(d, av_hi[2 * qq + 1], b2, b3);
+            mma16816(d, av_lo[2 * qq + 1], b2, b3);
+        }
+        if constexpr (NKV % 2) {
+            uint32_t b0, b1;
+            asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
+                         : "=r"(b0), "=r"(b1)
+                         : "r"(xaddr2 + 16 * i));
+            mma16816(d, av_hi[NKV - 1], b0, b1);
+            mma16816(d, av_lo[NKV - 1], b0, b1);
+        }
     };
     // k-block s as A fragments: n-tiles 2s (regs 0, 1) and 2s+1 (regs 2, 3)
     auto to_a = [&](const float (&d0)[4], const float (&d1)[4], uint32_t (&ahi)[4], uint32_t (&alo)[4]) {
@@ -779,21 +798,24 @@ __global__ void __launch_bounds__(TcGeom<K>::NT, STK_TC_MINB) k_blur_tc(Frame f,
         h2split(d1[2], d1[3], ahi[3], alo[3]);
     };
     // Output bytes go straight back into the warp's own channel plane, in
-    // staged rows no other warp reads (slab 0: rows 0-15, slab 1: rows 32-47)
-    // and in bytes [0, 128) of the row, which this warp's ldmatrix reads have
-    // passed by then (tile j is written after staged px 16 (j / 2) + 31 are
-    // read: bytes >= 32 (j / 2) + 64 stay ahead of the output bytes < 8 j + 8).
-    uint8_t* const orow = reinterpret_cast<uint8_t*>(xin + ((size_t)c * IR + (slab ? 32 : 0) + g) * XS) + 2 * t;
-    auto horz = [&](int j, const uint32_t (&a0h)[4], const uint32_t (&a0l)[4], const uint32_t (&a1h)[4],
-                    const uint32_t (&a1l)[4]) {
+    // staged rows no other warp reads (slab 0: rows 0-15, slab 1: rows
+    // IR-16..IR-1) and in bytes [0, 128) of the row, which this warp's
+    // ldmatrix reads have passed by then (tile j = 2 s0 + pp is written after
+    // n-tiles < 2 (s0 + NKH) are read: later reads start at byte 32 (s0 + NKH),
+    // ahead of the output bytes < 16 s0 + 16).
+    uint8_t* const orow =
+        reinterpret_cast<uint8_t*>(xin + ((size_t)c * IR + (slab ? IR - 16 : 0) + g) * XS) + 2 * t;
+    uint32_t kh[NKH][4], kl[NKH][4];  // sliding window of k-blocks (index s % NKH)
+    auto horz = [&](int j, int s0) {
         const int pp = j & 1;
         float d[4] = {0.f, 0.f, 0.f, 0.f};
-        mma16816(d, a0h, bh_hi[pp][0][0], bh_hi[pp][0][1]);
-        mma16816(d, a0h, bh_lo[pp][0][0], bh_lo[pp][0][1]);
-        mma16816(d, a0l, bh_hi[pp][0][0], bh_hi[pp][0][1]);
-        mma16816(d, a1h, bh_hi[pp][1][0], bh_hi[pp][1][1]);
-        mma16816(d, a1h, bh_lo[pp][1][0], bh_lo[pp][1][1]);
-        mma16816(d, a1l, bh_hi[pp][1][0], bh_hi[pp][1][1]);
+#pragma unroll
+        for (int q = 0; q < NKH; ++q) {
+            const int sb = (s0 + q) % NKH;
+            mma16816(d, kh[sb], bh_hi[pp][q][0], bh_hi[pp][q][1]);
+            mma16816(d, kh[sb], bh_lo[pp][q][0], bh_lo[pp][q][1]);
+            mma16816(d, kl[sb], bh_hi[pp][q][0], bh_hi[pp][q][1]);
+        }
         // floor(x + 1/2) = low byte of round_down(RN(d / 4096 + 1/2) + 2^23), as v3
         // (x in [0, 255 (1 + eps)]: non-negative normalised weights, 8-bit inputs)
         const unsigned long long lo2 = fadd2_rm(ffma2(f2pack(d[0], d[1]), kInv4096x2, kHalf2), kMagic2);
@@ -803,19 +825,20 @@ __global__ void __launch_bounds__(TcGeom<K>::NT, STK_TC_MINB) k_blur_tc(Frame f,
             (uint16_t)__byte_perm((uint32_t)hi2, (uint32_t)(hi2 >> 32), 0x0040);
     };
     float dA[4], dB[4];
-    uint32_t k0h[4], k0l[4], k1h[4], k1l[4];
-    vert(0, dA);
-    vert(1, dB);
-    to_a(dA, dB, k0h, k0l);
+#pragma unroll
+    for (int sb = 0; sb < NKH - 1; ++sb) {
+        vert(2 * sb, dA);
+        vert(2 * sb + 1, dB);
+        to_a(dA, dB, kh[sb], kl[sb]);
+    }
 #pragma unroll
     for (int s0 = 0; s0 < 8; ++s0) {
-        vert(2 * s0 + 2, dA);
-        vert(2 * s0 + 3, dB);
-        to_a(dA, dB, k1h, k1l);
-        horz(2 * s0, k0h, k0l, k1h, k1l);
-        horz(2 * s0 + 1, k0h, k0l, k1h, k1l);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) k0h[r] = k1h[r], k0l[r] = k1l[r];
+        const int sn = s0 + NKH - 1;  // the block this step adds
+        vert(2 * sn, dA);
+        vert(2 * sn + 1, dB);
+        to_a(dA, dB, kh[sn % NKH], kl[sn % NKH]);
+        horz(2 * s0, s0);
+        horz(2 * s0 + 1, s0);
     }
     __syncthreads();
     // ---- interleave the planes, keep sharp pixels' input bytes, 12-byte stores
@@ -823,7 +846,7 @@ __global__ void __launch_bounds__(TcGeom<K>::NT, STK_TC_MINB) k_blur_tc(Frame f,
     for (int i = tid; i < BY * (BX / 4); i += NT) {
         const int oy = i / (BX / 4), q4 = 4 * (i % (BX / 4));
         if (oy >= ny || q4 >= nx) continue;
-        const uint8_t* op = reinterpret_cast<const uint8_t*>(xin + (size_t)(oy < 16 ? oy : oy + 16) * XS) + q4;
+        const uint8_t* op = reinterpret_cast<const uint8_t*>(xin + (size_t)(oy < 16 ? oy : IR - 32 + oy) * XS) + q4;
         const uint32_t R = *reinterpret_cast<const uint32_t*>(op);
         const uint32_t Gc = *reinterpret_cast<const uint32_t*>(op + IR * XS * 2);
         const uint32_t Bc = *reinterpret_cast<const uint32_t*>(op + 2 * IR * XS * 2);
@@ -1041,12 +1064,13 @@ int launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, uin
         k_blur_exact<<<grid, kThreads, sm, st>>>(f, bp, in_rgb, out_rgb, depth);
     } else {
         const int K = 2 * bp.hw + 1;
-        // K8t (tensor cores) for K <= 17; STK_BLUR_TC=0 selects v3 instead (A/B)
+        // K8t (tensor cores) for K <= 17 and the integer-sigma sizes to 49; STK_BLUR_TC=0
+        // selects v3 instead (A/B)
         static const bool tc_on = [] {
             const char* e = getenv("STK_BLUR_TC");
             return e ? atoi(e) != 0 : true;
         }();
-        if (tc_on && !bp.blur_map && bp.lut_len <= 1024 && K <= 17 && f.N * 3 < (1ll << 31)) {
+        if (tc_on && !bp.blur_map && bp.lut_len <= 1024 && f.N * 3 < (1ll << 31)) {
             const dim3 gt((f.W + TcGeom<3>::BX - 1) / TcGeom<3>::BX, (f.H + TcGeom<3>::BY - 1) / TcGeom<3>::BY);
 #define STK_BLUR_TC(KK)                                                                          \
     case KK:                                                                                     \
@@ -1054,7 +1078,7 @@ int launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, uin
                              (int)TcGeom<KK>::SM);                                               \
         k_blur_tc<KK><<<gt, TcGeom<KK>::NT, TcGeom<KK>::SM, st>>>(f, bp, in_rgb, out_rgb, depth); \
         return 1;
-            switch (K) {
+            switch (K) {  // every K <= 17, and the integer-sigma sizes up to 49 (sigma 3 .. 8)
                 STK_BLUR_TC(3)
                 STK_BLUR_TC(5)
                 STK_BLUR_TC(7)
@@ -1063,6 +1087,13 @@ int launch_blur(const Frame& f, const BlurParams& bp, const uint8_t* in_rgb, uin
                 STK_BLUR_TC(13)
                 STK_BLUR_TC(15)
                 STK_BLUR_TC(17)
+                STK_BLUR_TC(19)
+                STK_BLUR_TC(23)
+                STK_BLUR_TC(25)
+                STK_BLUR_TC(31)
+                STK_BLUR_TC(37)
+                STK_BLUR_TC(43)
+                STK_BLUR_TC(49)
                 default: break;
             }
 #undef STK_BLUR_TC

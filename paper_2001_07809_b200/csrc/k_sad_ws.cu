@@ -45,6 +45,7 @@ namespace stk {
 namespace {
 
 constexpr int kMaxThreads = 512;  // 4 warps per SMSP: 128 registers
+constexpr size_t kSmemMax = 226 * 1024;  // dynamic shared memory per CTA
 constexpr int kSegW = 32;  // output columns per horizontal segment
 #ifndef STK_SAD_HB
 #define STK_SAD_HB 6
@@ -62,6 +63,15 @@ struct WP {
 __device__ __forceinline__ uint32_t lo16(uint32_t v) { return v & 0xffffu; }
 __device__ __forceinline__ uint32_t hi16(uint32_t v) { return v >> 16; }
 
+// (byte p, 0, byte p-1, 0) of a run of words (p compile-time after unrolling).
+template <int N>
+__device__ __forceinline__ uint32_t r_pair(const uint32_t (&w)[N], int p) {
+    const int i = p >> 2, s = p & 3;
+    if (s) return __byte_perm(w[i], 0u, (uint32_t)s | 0x40u | (uint32_t)(s - 1) << 8 | 0x4000u);
+    // byte p = byte 0 of w[i], byte p-1 = byte 3 of w[i-1]
+    return __byte_perm(w[i - 1], w[i], 0x0304u) & 0x00ff00ffu;
+}
+
 // Vertical update of the G x K colsum units of one thread for one row pair.
 // INIT: add the new row only.  Lw: L words of the row(s); Un/Uo: the rows'
 // pair-ring words, pointer at word c - 1 of the thread (see pair_at).
@@ -71,6 +81,7 @@ struct VGeom {
     static constexpr int rL = ((-h) % 4 + 4) % 4;     // byte residue of the L column base
     static constexpr int rR = ((1 - h) % 4 + 4) % 4;  // byte residue of the R window base
     static constexpr int NWL = (rL + K - 1) / 4 + 1;
+    static constexpr int NWR = (G - 1) + (rR + K - 1) / 4 + 2;      // raw R words (no pair ring)
     static constexpr int PMIN = rR + 1, PMAX = rR + K + 4 * G - 2;  // pair positions p used
     static constexpr int JMIN = (PMIN - 1) / 2, JMAX = PMAX / 2;    // pair-ring words w[j] = U[c - j]
     static constexpr int NJ = JMAX - JMIN + 1;
@@ -87,24 +98,31 @@ __device__ __forceinline__ uint32_t pair_at(const uint32_t (&w)[NJ], int p) {
     return __byte_perm(w[p / 2 - JMIN], w[p / 2 - 1 - JMIN], 0x5432);
 }
 
-template <int WIN, int G, int K, bool INIT>
+// PAIRS: Un / Uo point at the pair-ring words (word c - 1 of the thread, see
+// pair_at); otherwise at the rows' raw R words (pairs built here, r_pair).
+template <int WIN, int G, int K, bool INIT, bool PAIRS>
 __device__ __forceinline__ void v_rows(const uint32_t* __restrict__ Ln, const uint32_t* __restrict__ Un,
                                        const uint32_t* __restrict__ Lo, const uint32_t* __restrict__ Uo,
                                        uint32_t (&A)[G][K], uint32_t (&B)[G][K]) {
     using V = VGeom<WIN, G, K>;
-    constexpr int rL = V::rL, rR = V::rR, NWL = V::NWL, JMIN = V::JMIN, NJ = V::NJ;
-    uint32_t ln[NWL], lo[NWL], un[NJ], uo[NJ];
+    constexpr int rL = V::rL, rR = V::rR, NWL = V::NWL, JMIN = V::JMIN;
+    constexpr int NU = PAIRS ? V::NJ : V::NWR;
+    uint32_t ln[NWL], lo[NWL], un[NU], uo[NU];
 #pragma unroll
     for (int i = 0; i < NWL; ++i) ln[i] = Ln[i];
-    // Un points at U32[c - 1]: w[j - JMIN] = U32[c - j] = Un[1 - j]
+    // pair ring: Un points at U32[c - 1], w[j - JMIN] = U32[c - j] = Un[1 - j]
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) un[j] = Un[1 - (j + JMIN)];
+    for (int j = 0; j < NU; ++j) un[j] = PAIRS ? Un[1 - (j + JMIN)] : Un[j];
     if (!INIT) {
 #pragma unroll
         for (int i = 0; i < NWL; ++i) lo[i] = Lo[i];
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) uo[j] = Uo[1 - (j + JMIN)];
+        for (int j = 0; j < NU; ++j) uo[j] = PAIRS ? Uo[1 - (j + JMIN)] : Uo[j];
     }
+    auto pair = [&](const uint32_t (&w)[NU], int p) {
+        if constexpr (PAIRS) return pair_at<JMIN, NU>(w, p);
+        else return r_pair<NU>(w, p);
+    };
     // Spread words: the L byte as (L, 0, L, 0) and R byte pairs as
     // (R(x), 0, R(x-1), 0), so one VABSDIFF4 yields two disparities already
     // in u16x2 lanes (no per-result unpacking).  R(c - 4q - m) sits at byte
@@ -122,14 +140,14 @@ __device__ __forceinline__ void v_rows(const uint32_t* __restrict__ Ln, const ui
 #pragma unroll
         for (int j = 0; j < G; ++j) {
             const int o = rR + k - 4 * j + 4 * (G - 1);
-            const uint32_t an = __vabsdiffu4(spn, pair_at<JMIN, NJ>(un, o + 3));
-            const uint32_t bn = __vabsdiffu4(spn, pair_at<JMIN, NJ>(un, o + 1));
+            const uint32_t an = __vabsdiffu4(spn, pair(un, o + 3));
+            const uint32_t bn = __vabsdiffu4(spn, pair(un, o + 1));
             if (INIT) {
                 A[j][k] += an;
                 B[j][k] += bn;
             } else {
-                const uint32_t ao = __vabsdiffu4(spo, pair_at<JMIN, NJ>(uo, o + 3));
-                const uint32_t bo = __vabsdiffu4(spo, pair_at<JMIN, NJ>(uo, o + 1));
+                const uint32_t ao = __vabsdiffu4(spo, pair(uo, o + 3));
+                const uint32_t bo = __vabsdiffu4(spo, pair(uo, o + 1));
                 A[j][k] = A[j][k] + an - ao;
                 B[j][k] = B[j][k] + bn - bo;
             }
@@ -184,7 +202,7 @@ __device__ __forceinline__ void window_sum(const char* __restrict__ cq, const ui
     }
 }
 
-template <int WIN, int G, int K, int HQ, int NQB>
+template <int WIN, int G, int K, int HQ, int NQB, bool PAIRS>
 __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
     constexpr int h = WIN / 2;
     static_assert(K * WIN * 255 <= 65535, "chunk prefix must fit a u16 lane");
@@ -285,8 +303,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
         // the thread's pair-ring word c - 1, c = (RP - 2) / 2 - 2 rw0 (see pair_at)
         const uint32_t* const ubase = pring + (RPW - 2 - 2 * rw0);
         // prologue: pair rows 0 .. PR-1 (rows are then built three steps ahead)
-        for (int i = 0; i < min(PR, NRR); ++i) spread(i % p.RS, (uint32_t)((i / p.RS) & 1), i);
-        named_sync(BAR_V, 32 * p.NVW);
+        if constexpr (PAIRS) {
+            for (int i = 0; i < min(PR, NRR); ++i) spread(i % p.RS, (uint32_t)((i / p.RS) & 1), i);
+            named_sync(BAR_V, 32 * p.NVW);
+        }
         // pair slots of the entering / leaving rows and of the row built next
         // (PR + 2 = WIN + 6 > RS: its raw slot and phase tracked separately)
         int pn = WIN - 1, po = PR - 1, psp = (WIN + 4) % PR;
@@ -299,7 +319,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                     const int s = i % p.RS;
                     mbar_wait(&fullb[s], (uint32_t)((i / p.RS) & 1));
                     const uint32_t* Ls = reinterpret_cast<const uint32_t*>(ring + (size_t)s * (p.LP + p.RP));
-                    if (act) v_rows<WIN, G, K, true>(Ls + lw0, ubase + (size_t)i * RPW, nullptr, nullptr, A, B);
+                    const uint32_t* Rs = PAIRS ? ubase + (size_t)i * RPW
+                                               : reinterpret_cast<const uint32_t*>(ring + (size_t)s * (p.LP + p.RP) + p.LP) + rw0;
+                    if (act) v_rows<WIN, G, K, true, PAIRS>(Ls + lw0, Rs, nullptr, nullptr, A, B);
                 }
             } else {
                 // slot / phase of the entering row t+WIN-1 and the leaving row t-1
@@ -311,10 +333,11 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                 const uint8_t* bo = ring + (size_t)so * (p.LP + p.RP);
                 if (++pn == PR) pn = 0;
                 if (++po == PR) po = 0;
+                const uint32_t* Rn = PAIRS ? ubase + (size_t)pn * RPW : reinterpret_cast<const uint32_t*>(bn + p.LP) + rw0;
+                const uint32_t* Ro = PAIRS ? ubase + (size_t)po * RPW : reinterpret_cast<const uint32_t*>(bo + p.LP) + rw0;
                 if (act)
-                    v_rows<WIN, G, K, false>(reinterpret_cast<const uint32_t*>(bn) + lw0, ubase + (size_t)pn * RPW,
-                                             reinterpret_cast<const uint32_t*>(bo) + lw0, ubase + (size_t)po * RPW,
-                                             A, B);
+                    v_rows<WIN, G, K, false, PAIRS>(reinterpret_cast<const uint32_t*>(bn) + lw0, Rn,
+                                                    reinterpret_cast<const uint32_t*>(bo) + lw0, Ro, A, B);
             }
             const int b = t & 1;
             if (t >= 2) {
@@ -327,7 +350,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
                 }
                 // pair row t+WIN+2 (used from step t+3, after two more EMPTY
                 // barriers) into the slot of row t-2, last read at step t-1
-                if (t + WIN + 2 < NRR) spread(rsp, php, psp);
+                if (PAIRS && t + WIN + 2 < NRR) spread(rsp, php, psp);
                 if (++psp == PR) psp = 0;
                 if (++rsp == p.RS) rsp = 0, php ^= 1u;
             }
@@ -551,9 +574,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sad_ws(Frame f, WP p) {
     }
 }
 
-template <int WIN, int G, int K, int HQ, int NQB>
+template <int WIN, int G, int K, int HQ, int NQB, bool PAIRS>
 void run_ws(const Frame& f, const WP& p, size_t sm, int bands, cudaStream_t st) {
-    auto kern = k_sad_ws<WIN, G, K, HQ, NQB>;
+    auto kern = k_sad_ws<WIN, G, K, HQ, NQB, PAIRS>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     const dim3 grid((f.W + p.SW - 1) / p.SW, bands);
     kern<<<grid, p.nthreads, sm, st>>>(f, p);
@@ -567,16 +590,22 @@ struct Shape {
     static constexpr int G = WIN <= 21 ? 3 : 5;  // 33 / 65 quads at D = 128 / 256
 };
 
-template <int WIN>
-void run_win(const Frame& f, const WP& p, int HQ, int NQB, size_t sm, int bands, cudaStream_t st) {
+template <int WIN, bool PAIRS>
+void run_win_p(const Frame& f, const WP& p, int HQ, int NQB, size_t sm, int bands, cudaStream_t st) {
     constexpr int G = Shape<WIN>::G, K = Shape<WIN>::K;
     if (HQ == 2) {
-        if (NQB == 1) run_ws<WIN, G, K, 2, 1>(f, p, sm, bands, st);
-        else run_ws<WIN, G, K, 2, 2>(f, p, sm, bands, st);
+        if (NQB == 1) run_ws<WIN, G, K, 2, 1, PAIRS>(f, p, sm, bands, st);
+        else run_ws<WIN, G, K, 2, 2, PAIRS>(f, p, sm, bands, st);
     } else {
-        if (NQB == 1) run_ws<WIN, G, K, 1, 1>(f, p, sm, bands, st);
-        else run_ws<WIN, G, K, 1, 2>(f, p, sm, bands, st);
+        if (NQB == 1) run_ws<WIN, G, K, 1, 1, PAIRS>(f, p, sm, bands, st);
+        else run_ws<WIN, G, K, 1, 2, PAIRS>(f, p, sm, bands, st);
     }
+}
+
+template <int WIN>
+void run_win(const Frame& f, const WP& p, int HQ, int NQB, bool pairs, size_t sm, int bands, cudaStream_t st) {
+    if (pairs) run_win_p<WIN, true>(f, p, HQ, NQB, sm, bands, st);
+    else run_win_p<WIN, false>(f, p, HQ, NQB, sm, bands, st);
 }
 
 }  // namespace
@@ -644,11 +673,19 @@ bool launch_sad_ws(const Frame& f, cudaStream_t st, bool dry) {
         p.RP = (p.NCH * K + 4 * p.QP + oR + 16 + 15) & ~15;
         const int NE = w <= 21 ? (w == 21 ? WinTab<21, 12>::NE : WinTab<15, 12>::NE) : WinTab<31, 8>::NE;
         sm = (size_t)2 * p.QP * p.CSW * 8 + (size_t)p.RS * (p.LP + p.RP) + p.RS * 8 +
-             2 * SW * 4 + (size_t)SW * NE * 4 + (size_t)(w + 4) * p.RP * 2;  // + pair ring
-        if (sm <= 226 * 1024 && p.nthreads <= kMaxThreads) break;
+             2 * SW * 4 + (size_t)SW * NE * 4;
+        if (sm <= kSmemMax && p.nthreads <= kMaxThreads) break;
         sm = 0;
     }
     if (!sm) return false;
+    // the pair ring only where it fits beside the strip width chosen without it
+    // (a narrower strip costs more halo columns than the ring saves: config E
+    // 5.9 -> 9.2 ms) and where the vertical role is the long one -- many
+    // disparity quads per row (4K, 33 quads: 0.481 -> 0.477 ms; 1080p, 18
+    // quads: 0.117 -> 0.122 ms, the per-row build is not amortised)
+    const size_t ring_bytes = (size_t)(w + 4) * p.RP * 2;
+    const bool pairs = sm + ring_bytes <= kSmemMax && p.QP >= 24;
+    if (pairs) sm += ring_bytes;
     const int strips = (f.W + p.SW - 1) / p.SW;
     const int rows = f.H - 2 * h;
     // one wave of one CTA per SM when possible; bands of >= 32 rows.
@@ -664,10 +701,10 @@ bool launch_sad_ws(const Frame& f, cudaStream_t st, bool dry) {
     bands = (rows + p.TH - 1) / p.TH;
     if (dry) return true;
     switch (w) {
-        case 9: run_win<9>(f, p, HQ, NQB, sm, bands, st); break;
-        case 15: run_win<15>(f, p, HQ, NQB, sm, bands, st); break;
-        case 21: run_win<21>(f, p, HQ, NQB, sm, bands, st); break;
-        default: run_win<31>(f, p, HQ, NQB, sm, bands, st); break;
+        case 9: run_win<9>(f, p, HQ, NQB, pairs, sm, bands, st); break;
+        case 15: run_win<15>(f, p, HQ, NQB, pairs, sm, bands, st); break;
+        case 21: run_win<21>(f, p, HQ, NQB, pairs, sm, bands, st); break;
+        default: run_win<31>(f, p, HQ, NQB, pairs, sm, bands, st); break;
     }
     return true;
 }

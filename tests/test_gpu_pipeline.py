@@ -316,10 +316,11 @@ def test_pipeline_wide_blur_vs_oracle(dev, stk, port, synth, sigma):
     assert np.abs(img.astype(int) - want["refocused"].astype(int)).max() <= BLUR_TOL_LSB
 
 
-# sigma -> kernel size 2 ceil(3 sigma) + 1: 3, 5, 7, 9, 11, (13: default), 15, 17
-@pytest.mark.parametrize("sigma", [0.3, 0.6, 1.0, 1.3, 1.6, 2.3, 2.6])
+# sigma -> kernel size 2 ceil(3 sigma) + 1: 3, 5, 7, 9, 11, (13: default), 15, 17, and the
+# wide tensor-core tiles 19 (3.0), 25, 31, 37, 43, 49 (8.0: config E)
+@pytest.mark.parametrize("sigma", [0.3, 0.6, 1.0, 1.3, 1.6, 2.3, 2.6, 3.0, 4.0, 5.0, 6.0, 7.0, 8.0])
 def test_pipeline_tc_blur_sizes_vs_oracle(dev, stk, port, synth, sigma):
-    """Every kernel size of the tensor-core blur (K8t, K <= 17) through the
+    """Every kernel size of the tensor-core blur (K8t, K <= 17 and 19..49) through the
     frame path against the oracle's FP64 2-D blur: <= 1 LSB everywhere and
     almost everywhere exact (hi/lo f16 splits carry ~22 bits, so only sums
     within ~1e-4 of a rounding boundary may differ)."""
@@ -333,7 +334,8 @@ def test_pipeline_tc_blur_sizes_vs_oracle(dev, stk, port, synth, sigma):
 
 
 @pytest.mark.parametrize("W,H,sigma", [(333, 201, 2.0), (100, 50, 2.6), (7, 5, 1.0), (136, 33, 2.0),
-                                       (264, 64, 0.6), (130, 31, 2.3)])
+                                       (264, 64, 0.6), (130, 31, 2.3), (333, 201, 8.0), (150, 90, 3.0),
+                                       (7, 5, 5.0), (176, 40, 6.0)])
 def test_pipeline_tc_blur_edge_shapes(dev, stk, port, synth, W, H, sigma):
     """K8t at shapes that exercise its slow paths: W not a multiple of 4
     (unaligned rows), W < 136 (no CTA has its staged columns inside the
