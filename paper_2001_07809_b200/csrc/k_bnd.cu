@@ -1194,10 +1194,16 @@ void launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, in
             return e ? atoi(e) : 1;
         }();
         // the phases are short loops between grid barriers and the blocks mostly
-        // wait: few blocks (one per 2^19 pixels, >= 8) leave the other SMs to
-        // other frames' kernels (4K: 1605 -> 1620 frames/s vs one per SM)
+        // wait: fewer blocks than SMs leave the others to other frames' kernels.
+        // One block per 2^17 pixels (>= 8; 72 at 4K): 1605 -> 1642 frames/s vs
+        // one per SM with the stage's own time unchanged (0.155 ms; 2^19: 18
+        // blocks, same frames/s, 0.163-0.181 ms).  STK_PRUNE_SHIFT: experiment knob.
+        static const int pshift = [] {
+            const char* e = getenv("STK_PRUNE_SHIFT");
+            return e ? atoi(e) : 17;
+        }();
         int g_blocks = std::min(512, std::max(1, std::min(per_sm, bps)) * f.sms);  // <= gsum/gcnt slots
-        g_blocks = std::min<long long>(g_blocks, std::max<long long>(8, (f.N + (1 << 19) - 1) >> 19));
+        g_blocks = std::min<long long>(g_blocks, std::max<long long>(8, (f.N + (1ll << pshift) - 1) >> pshift));
         int nw = sbits_words;
         void* args[] = {(void*)&f, (void*)&sbits, (void*)&nw};
         cudaLaunchCooperativeKernel((const void*)k_prune_fused, dim3(g_blocks), dim3(256), args, 0, st);
