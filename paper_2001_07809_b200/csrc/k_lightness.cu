@@ -120,16 +120,18 @@ __device__ __forceinline__ void split36(double y, uint32_t& bk, uint32_t& yq) {
 // warp access is two half-warp wavefronts).  The 512 output bytes go back
 // through shared memory as one 16-byte store per chunk.
 constexpr int kL2Threads = 1024, kL2Copies = 16;
-constexpr size_t kL2TabBytes = 3 * 256 * kL2Copies * sizeof(double);          // 96 KB
-constexpr size_t kL2Smem = kL2TabBytes + (kLstarBuckets + 4) * sizeof(uint32_t) +  // + 16 KB
+constexpr size_t kL2TabBytes = 3 * 256 * kL2Copies * sizeof(float);           // 48 KB
+constexpr size_t kL2Smem = 3 * 256 * sizeof(double) +                               // FP64 products (6 KB)
+                           kL2TabBytes + (kLstarBuckets + 4) * sizeof(uint32_t) +  // + 16 KB
                            (size_t)(kL2Threads / 32) * (97 + 32) * sizeof(uint4) +   // + 64.5 KB
                            (size_t)(kL2Threads / 32) * 256 * sizeof(uint32_t);       // + 32 KB histograms
 
 template <bool HIST>
 __global__ void __launch_bounds__(kL2Threads, 1) k_lstar2(Frame f, const LstarTables* __restrict__ tab) {
     extern __shared__ __align__(16) unsigned char l2s[];
-    double* tabs = reinterpret_cast<double*>(l2s);  // [3][256][16]
-    uint32_t* bw = reinterpret_cast<uint32_t*>(l2s + kL2TabBytes);
+    double* prod = reinterpret_cast<double*>(l2s);                        // [3][256] FP64 (redo path)
+    float* tabs = reinterpret_cast<float*>(l2s + 3 * 256 * sizeof(double));  // [3][256][16]
+    uint32_t* bw = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(tabs) + kL2TabBytes);
     uint4* xin_all = reinterpret_cast<uint4*>(bw + kLstarBuckets + 4);  // [32 warps][97]
     uint4* xout_all = xin_all + (kL2Threads / 32) * 97;                 // [32 warps][32]
     // left view: warp-private 256-bin histograms of the converted bytes
@@ -140,11 +142,11 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_lstar2(Frame f, const LstarTa
         for (int i = threadIdx.x; i < (kL2Threads / 32) * 256; i += kL2Threads) hist_all[i] = 0u;
     {  // all loads in flight before the stores
         constexpr int NT = 3 * 256 * kL2Copies / kL2Threads;  // 12 table entries per thread
-        double t[NT];
+        float t[NT];
 #pragma unroll
         for (int k = 0; k < NT; ++k) {
             const int i = threadIdx.x + k * kL2Threads;  // = (table * 256 + e) * 16 + c
-            t[k] = __ldg(&tab->prod[0][0] + (i >> 4));
+            t[k] = __ldg(&tab->fprod[0][0] + (i >> 4));
         }
         constexpr int NV = kLstarBuckets / 4 / kL2Threads;
         uint4 v[NV];
@@ -155,19 +157,36 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_lstar2(Frame f, const LstarTa
 #pragma unroll
         for (int k = 0; k < NV; ++k) reinterpret_cast<uint4*>(bw)[threadIdx.x + k * kL2Threads] = v[k];
         if (threadIdx.x == 0) bw[kLstarBuckets] = tab->bw[kLstarBuckets];
+        for (int i = threadIdx.x; i < 3 * 256; i += kL2Threads) prod[i] = __ldg(&tab->prod[0][0] + i);
     }
     __syncthreads();
-    // Y = (0.2126 lin[R] + 0.7152 lin[G]) + 0.0722 lin[B], products tabulated
-    // (byte v of channel c at copy-base + 128 v); floor(2^36 Y) = bucket << 24
-    // | position in the bucket in 2^-24 steps (exact, see split36).
-    // Y <= 1 (coefficients sum to 1, linear[] <= 1), so the bucket is <= 4096.
-    const char* prb = reinterpret_cast<const char*>(tabs) + (threadIdx.x & (kL2Copies - 1)) * 8;
-    const char* pgb = prb + 256 * kL2Copies * 8;
-    const char* pbb = pgb + 256 * kL2Copies * 8;
-    auto y_of = [&](uint32_t v) {  // v = R | G << 8 | B << 16
-        return __dadd_rn(__dadd_rn(*reinterpret_cast<const double*>(prb + ((v << 7) & 0x7f80u)),
-                                   *reinterpret_cast<const double*>(pgb + ((v >> 1) & 0x7f80u))),
-                         *reinterpret_cast<const double*>(pbb + ((v >> 9) & 0x7f80u)));
+    // FP32 screen: Y32 = (f[R] + f[G]) + f[B] from the products rounded to
+    // float (f[c][v] = RN32(prod[c][v]), byte v of channel c at copy-base +
+    // 64 v) is within 3 * 2^-24 of the reference's FP64 Y (three product
+    // roundings <= 2^-24 * coefficient, two sums <= 2^-24 each; Y <= 1), and
+    // RZ(Y32 + 1) in [1, 2) adds <= 2^-23: |Y' - Y| <= 5 * 2^-24 < 2^-21.6,
+    // i.e. < 2^14.4 steps of 2^-36.  Y' = 1 + mantissa 2^-23: bucket = its top
+    // 12 bits, position in the bucket (2^-36 steps, as split36) = the low 11
+    // bits << 13.  With a margin of 2^16 steps the FP32 bucket and the side of
+    // the bucket's threshold are exact; pixels inside the margin (threshold or
+    // bucket edge: ~1 % of random RGB) are redone in FP64 below.
+    constexpr uint32_t kMargin = 1u << 16;
+    const char* frb = reinterpret_cast<const char*>(tabs) + (threadIdx.x & (kL2Copies - 1)) * 4;
+    const char* fgb = frb + 256 * kL2Copies * 4;
+    const char* fbb = fgb + 256 * kL2Copies * 4;
+    auto gray32 = [&](uint32_t v, bool& unsure) {  // v = R | G << 8 | B << 16
+        const float y = __fadd_rn(__fadd_rn(*reinterpret_cast<const float*>(frb + ((v << 6) & 0x3fc0u)),
+                                            *reinterpret_cast<const float*>(fgb + ((v >> 2) & 0x3fc0u))),
+                                  *reinterpret_cast<const float*>(fbb + ((v >> 10) & 0x3fc0u)));
+        const uint32_t m = __float_as_uint(__fadd_rz(y, 1.0f));
+        const uint32_t bk = (m >> 11) & 0xfffu, pos = (m & 0x7ffu) << 13;
+        const uint32_t w = bw[bk], q = w & 0xffffffu;
+        unsure = m >= 0x40000000u || pos - kMargin > (1u << 24) - 2 * kMargin || pos - q + kMargin < 2 * kMargin;
+        return (w >> 24) + (pos > q ? 1u : 0u);
+    };
+    // the reference's FP64 Y (host-tabulated products, __dadd_rn in its order)
+    auto y64_of = [&](uint32_t v) {
+        return __dadd_rn(__dadd_rn(prod[v & 0xffu], prod[256 + ((v >> 8) & 0xffu)]), prod[512 + ((v >> 16) & 0xffu)]);
     };
     const int view = blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint8_t* __restrict__ rgb = view == 0 ? f.rgbL : f.rgbR;
@@ -202,7 +221,7 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_lstar2(Frame f, const LstarTa
             if (lane + 32 * k < 3 * nc) xin[lane + 32 * k] = t[k];
         __syncwarp();
         if (cw + stride < nch) load_group(cw + stride, t);
-        uint32_t ties = 0;
+        uint32_t redo = 0;
         auto pair_of = [&](int p) {
             return ((unsigned long long)xw[48 * p + wb + 1] << 32 | xw[48 * p + wb]) >> sh;
         };
@@ -212,24 +231,23 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_lstar2(Frame f, const LstarTa
             uint32_t g2 = 0;
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                uint32_t bk, yq;
-                split36(y_of((uint32_t)(x >> (24 * e))), bk, yq);
-                const uint32_t w = bw[bk], q = w & 0xffffffu;
-                g2 |= ((w >> 24) + (yq > q ? 1u : 0u)) << (8 * e);
-                ties |= (yq == q ? 1u : 0u) << (2 * p + e);
+                bool u;
+                g2 |= gray32((uint32_t)(x >> (24 * e)), u) << (8 * e);
+                redo |= (u ? 1u : 0u) << (2 * p + e);
             }
             xo2[lane + 32 * p] = (uint16_t)g2;
         }
-        if (ties) {  // rare: Y's position equals the threshold's 2^-24 step, read tb[b]
-#pragma unroll 1
-            for (int i = 0; i < 16; ++i) {
-                if ((ties >> i) & 1u) {
-                    const double y = y_of((uint32_t)(pair_of(i >> 1) >> (24 * (i & 1))));
-                    uint32_t bk, yq;
-                    split36(y, bk, yq);
-                    if (y >= __ldg(&tab->tb[bk])) xo[2 * (lane + 32 * (i >> 1)) + (i & 1)] += 1;
-                }
-            }
+        // rare (~1 % of pixels, a lane has 0-2): the exact FP64 path (split36,
+        // the bucket word, a tie decided by the FP64 threshold)
+        while (redo) {
+            const int i = __ffs(redo) - 1;
+            redo &= redo - 1;
+            const double y = y64_of((uint32_t)(pair_of(i >> 1) >> (24 * (i & 1))));
+            uint32_t bk, yq;
+            split36(y, bk, yq);
+            const uint32_t w = bw[bk], q = w & 0xffffffu;
+            const uint32_t gv = (w >> 24) + (yq > q || (yq == q && y >= __ldg(&tab->tb[bk])) ? 1u : 0u);
+            xo[2 * (lane + 32 * (i >> 1)) + (i & 1)] = (uint8_t)gv;
         }
         __syncwarp();
         if (lane < nc) {

@@ -169,6 +169,7 @@ void make_lstar_tables(LstarTables* t) {
         t->prod[0][v] = 0.2126 * l;
         t->prod[1][v] = 0.7152 * l;
         t->prod[2][v] = 0.0722 * l;
+        for (int c = 0; c < 3; ++c) t->fprod[c][v] = (float)t->prod[c][v];
     }
     t->thr[0] = -1.0;
     uint64_t hi_bits;

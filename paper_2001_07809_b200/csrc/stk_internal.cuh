@@ -114,6 +114,8 @@ struct LstarTables {
     // a Y in bucket b with floor(2^24 * (4096 * Y - b)) != q[b] decides
     // Y >= tb[b] from the integers alone (all steps exact), ties read tb[b].
     alignas(16) uint32_t bw[4097];
+    // fprod[c][v] = (float)prod[c][v] (round to nearest): K1's FP32 screen
+    float fprod[3][256];
 };
 constexpr int kLstarBuckets = 4096;
 
