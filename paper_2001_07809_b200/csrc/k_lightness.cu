@@ -171,13 +171,14 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_lstar2(Frame f, const LstarTa
     // the bucket's threshold are exact; pixels inside the margin (threshold or
     // bucket edge: ~1 % of random RGB) are redone in FP64 below.
     constexpr uint32_t kMargin = 1u << 16;
-    const char* frb = reinterpret_cast<const char*>(tabs) + (threadIdx.x & (kL2Copies - 1)) * 4;
-    const char* fgb = frb + 256 * kL2Copies * 4;
-    const char* fbb = fgb + 256 * kL2Copies * 4;
+    // entry e of copy c at e * 16 + c: a lookup is one byte extract (PRMT) and
+    // one LEA (e << 6 onto the lane's copy base)
+    const float* fr = tabs + (threadIdx.x & (kL2Copies - 1));
+    const float* fg = fr + 256 * kL2Copies;
+    const float* fb = fg + 256 * kL2Copies;
     auto gray32 = [&](uint32_t v, bool& unsure) {  // v = R | G << 8 | B << 16
-        const float y = __fadd_rn(__fadd_rn(*reinterpret_cast<const float*>(frb + ((v << 6) & 0x3fc0u)),
-                                            *reinterpret_cast<const float*>(fgb + ((v >> 2) & 0x3fc0u))),
-                                  *reinterpret_cast<const float*>(fbb + ((v >> 10) & 0x3fc0u)));
+        const uint32_t r = __byte_perm(v, 0u, 0x4440), g = __byte_perm(v, 0u, 0x4441), b = __byte_perm(v, 0u, 0x4442);
+        const float y = __fadd_rn(__fadd_rn(fr[r * kL2Copies], fg[g * kL2Copies]), fb[b * kL2Copies]);
         const uint32_t m = __float_as_uint(__fadd_rz(y, 1.0f));
         const uint32_t bk = (m >> 11) & 0xfffu, pos = (m & 0x7ffu) << 13;
         const uint32_t w = bw[bk], q = w & 0xffffffu;
