@@ -313,7 +313,10 @@ __global__ void __launch_bounds__(PC * PS) k_peek_cols2(Frame f, const int16_t* 
 // K7 helpers for the two-columns-per-thread kernel (int16 pairs in 32-bit
 // loads/stores: a warp's 8 column pairs x 4 segments move 32 contiguous bytes
 // per row each).
-constexpr int P4B = 8;   // rows per load batch
+#ifndef STK_P4B
+#define STK_P4B 12
+#endif
+constexpr int P4B = STK_P4B;  // rows per load batch
 
 __device__ __forceinline__ uint32_t pack2(int a, int b) { return (uint32_t)(uint16_t)a | (uint32_t)b << 16; }
 __device__ __forceinline__ int lo16(uint32_t v) { return (int16_t)(v & 0xffffu); }
