@@ -9,7 +9,7 @@
 //                   remove, one warp per 30 word-columns x 32 rows, rows
 //                   streamed with a 3-row halo; refined bits + raw/refined
 //                   counts (raw bytes too in full mode).
-//   B2 ccl_region   CTA per 128x64 region, warp per 32x32 tile: run-level
+//   B2 ccl_region   CTA per 128x128 region, warp per 32x32 tile: run-level
 //                   union-find per tile, then the region's inner tile borders
 //                   merged in shared memory; every region component goes to
 //                   the root list with its size and its minimum raster index g
@@ -451,7 +451,15 @@ __device__ __forceinline__ unsigned long long budget_of(const Frame& f) {
 //  3. region components -> root list (g, size), par[g] = g; every run records
 //     its component's g; the region's outer borders record the g of their
 //     pixels for the global merge (B3).
-constexpr int RGX = 4, RGY = 2, NRW = RGX * RGY;  // 128 x 64-pixel regions
+// region = RGX x RGY tiles (STK_RGX / STK_RGY: experiment knobs; 4 x 2: boundary
+// stage 0.165 ms, 4 x 4: 0.150 ms -- half the borders left for B3)
+#ifndef STK_RGX
+#define STK_RGX 4
+#endif
+#ifndef STK_RGY
+#define STK_RGY 4
+#endif
+constexpr int RGX = STK_RGX, RGY = STK_RGY, NRW = RGX * RGY;  // 128 x 128-pixel regions
 constexpr int RW = RGX * CT, RH = RGY * CT;
 constexpr int RBORD = 2 * RW + 2 * RH;             // [top RW][bottom RW][left RH][right RH]
 
