@@ -100,6 +100,10 @@ __global__ void __launch_bounds__(kThreads) k_lstar(Frame f, const LstarTables* 
     }
 }
 
+__device__ __forceinline__ unsigned long long f2pack_l(float lo, float hi) {
+    return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+
 // floor(2^36 y) for 0 <= y <= 1 without a (slow, XU-pipe) F64->int
 // conversion: y + 2^16 rounded toward zero is 2^16 + floor(2^36 y) 2^-36, so
 // the low 52 bits of its pattern are floor(2^36 y) = bucket << 24 | position.
@@ -176,10 +180,21 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_lstar2(Frame f, const LstarTa
     const float* fr = tabs + (threadIdx.x & (kL2Copies - 1));
     const float* fg = fr + 256 * kL2Copies;
     const float* fb = fg + 256 * kL2Copies;
-    auto gray32 = [&](uint32_t v, bool& unsure) {  // v = R | G << 8 | B << 16
-        const uint32_t r = __byte_perm(v, 0u, 0x4440), g = __byte_perm(v, 0u, 0x4441), b = __byte_perm(v, 0u, 0x4442);
-        const float y = __fadd_rn(__fadd_rn(fr[r * kL2Copies], fg[g * kL2Copies]), fb[b * kL2Copies]);
-        const uint32_t m = __float_as_uint(__fadd_rz(y, 1.0f));
+    // bits of RZ(Y32 + 1) for the two pixels of a pair (x = 48 bits: R0 G0 B0 R1 G1 B1),
+    // the sums as f32x2 adds (both pixels per instruction, same roundings)
+    auto ybits2 = [&](unsigned long long x, uint32_t& m0, uint32_t& m1) {
+        const uint32_t v0 = (uint32_t)x, v1 = (uint32_t)(x >> 24);
+        const float r0 = fr[__byte_perm(v0, 0u, 0x4440) * kL2Copies], r1 = fr[__byte_perm(v1, 0u, 0x4440) * kL2Copies];
+        const float g0 = fg[__byte_perm(v0, 0u, 0x4441) * kL2Copies], g1 = fg[__byte_perm(v1, 0u, 0x4441) * kL2Copies];
+        const float b0 = fb[__byte_perm(v0, 0u, 0x4442) * kL2Copies], b1 = fb[__byte_perm(v1, 0u, 0x4442) * kL2Copies];
+        unsigned long long sum, t;
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(sum) : "l"(f2pack_l(r0, r1)), "l"(f2pack_l(g0, g1)));
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(sum) : "l"(sum), "l"(f2pack_l(b0, b1)));
+        asm("add.rz.f32x2 %0, %1, %2;" : "=l"(t) : "l"(sum), "l"(0x3f8000003f800000ull));
+        m0 = (uint32_t)t;
+        m1 = (uint32_t)(t >> 32);
+    };
+    auto gray32 = [&](uint32_t m, bool& unsure) {  // m = bits of RZ(Y32 + 1)
         const uint32_t bk = (m >> 11) & 0xfffu, pos = (m & 0x7ffu) << 13;
         const uint32_t w = bw[bk], q = w & 0xffffffu;
         unsure = m >= 0x40000000u || pos - kMargin > (1u << 24) - 2 * kMargin || pos - q + kMargin < 2 * kMargin;
@@ -229,11 +244,13 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_lstar2(Frame f, const LstarTa
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
             const unsigned long long x = pair_of(p);
+            uint32_t mm[2];
+            ybits2(x, mm[0], mm[1]);
             uint32_t g2 = 0;
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 bool u;
-                g2 |= gray32((uint32_t)(x >> (24 * e)), u) << (8 * e);
+                g2 |= gray32(mm[e], u) << (8 * e);
                 redo |= (u ? 1u : 0u) << (2 * p + e);
             }
             xo2[lane + 32 * p] = (uint16_t)g2;
