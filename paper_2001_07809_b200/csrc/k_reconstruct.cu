@@ -727,13 +727,110 @@ __global__ void __launch_bounds__(P5C * P5S, 2) k_peek_cols6(Frame f, const int1
     }
 }
 
+// K6 v2: two rows per CTA in int16x2 lanes (row y in the low, row y+1 in
+// the high half of every word): k_fill_rows16v's chunk / warp / block scans
+// and its per-pixel rule, with lane masks by sign replication and LOP3
+// selects -- one instruction per pixel pair where v1 spends one per pixel.
+__global__ void __launch_bounds__(1024) k_fill_rows16p(Frame f, const int16_t* __restrict__ in,
+                                                       int16_t* __restrict__ out) {
+    __shared__ uint32_t wl[32], wf[32];
+    const unsigned full = 0xffffffffu;
+    const int W = f.W, y0 = 2 * blockIdx.x, tid = threadIdx.x;
+    const bool two = y0 + 1 < f.H;
+    const bool act = tid < W / 16;
+    const int x0 = tid * 16;
+    uint32_t P[16];
+    {
+        uint4 a0 = make_uint4(full, full, full, full), a1 = a0, b0 = a0, b1 = a0;
+        if (act) {
+            const uint4* s0 = reinterpret_cast<const uint4*>(in + (size_t)y0 * W + x0);
+            a0 = __ldcs(s0);
+            a1 = __ldcs(s0 + 1);
+            if (two) {
+                const uint4* s1 = reinterpret_cast<const uint4*>(in + (size_t)(y0 + 1) * W + x0);
+                b0 = __ldcs(s1);
+                b1 = __ldcs(s1 + 1);
+            }
+        }
+        const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const uint32_t b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            P[2 * i] = __byte_perm(a[i], b[i], 0x5410);      // (row y px 2i, row y+1 px 2i)
+            P[2 * i + 1] = __byte_perm(a[i], b[i], 0x7632);  // (.. px 2i+1 ..)
+        }
+    }
+    auto pick = [](uint32_t cur, uint32_t cand) {  // per lane: cur if known, else cand
+        const uint32_t m = sgn2(cur);
+        return (cand & m) | (cur & ~m);
+    };
+    uint32_t lastv = full, firstv = full;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) lastv = pick(P[i], lastv);
+#pragma unroll
+    for (int i = 15; i >= 0; --i) firstv = pick(P[i], firstv);
+    const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    uint32_t inc = lastv;  // latest known over lanes <= lane
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(full, inc, o);
+        if (lane >= o) inc = pick(inc, t);
+    }
+    uint32_t sinc = firstv;  // earliest known over lanes >= lane
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_down_sync(full, sinc, o);
+        if (lane + o < 32) sinc = pick(sinc, t);
+    }
+    if (lane == 31) wl[wid] = inc;
+    if (lane == 0) wf[wid] = sinc;
+    __syncthreads();
+    uint32_t pd = __shfl_up_sync(full, inc, 1);
+    if (lane == 0) pd = full;
+    for (int i = wid - 1; i >= 0 && sgn2(pd); --i) pd = pick(pd, wl[i]);
+    uint32_t nd = __shfl_down_sync(full, sinc, 1);
+    if (lane == 31) nd = full;
+    for (int i = wid + 1; i < nw && sgn2(nd); ++i) nd = pick(nd, wf[i]);
+    if (!act) return;
+    // right context of each pixel: the nearest known at or right of it
+    uint32_t r[16];
+#pragma unroll
+    for (int i = 15; i >= 0; --i) {
+        r[i] = nd;
+        nd = pick(P[i], nd);
+    }
+    uint32_t o[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        // unknown: filled iff nearest left == nearest right (both -1 -> stays -1)
+        const uint32_t x = pd ^ r[i];
+        const uint32_t eq = sgn2(__vadd2(x, full) & ~x);  // lanes with pd == r
+        const uint32_t fillv = (pd & eq) | ~eq;           // pd where equal, else -1
+        const uint32_t md = sgn2(P[i]);
+        o[i] = (fillv & md) | (P[i] & ~md);
+        pd = pick(P[i], pd);
+    }
+    uint4* d0 = reinterpret_cast<uint4*>(out + (size_t)y0 * W + x0);
+    d0[0] = make_uint4(__byte_perm(o[0], o[1], 0x5410), __byte_perm(o[2], o[3], 0x5410),
+                       __byte_perm(o[4], o[5], 0x5410), __byte_perm(o[6], o[7], 0x5410));
+    d0[1] = make_uint4(__byte_perm(o[8], o[9], 0x5410), __byte_perm(o[10], o[11], 0x5410),
+                       __byte_perm(o[12], o[13], 0x5410), __byte_perm(o[14], o[15], 0x5410));
+    if (two) {
+        uint4* d1 = reinterpret_cast<uint4*>(out + (size_t)(y0 + 1) * W + x0);
+        d1[0] = make_uint4(__byte_perm(o[0], o[1], 0x7632), __byte_perm(o[2], o[3], 0x7632),
+                           __byte_perm(o[4], o[5], 0x7632), __byte_perm(o[6], o[7], 0x7632));
+        d1[1] = make_uint4(__byte_perm(o[8], o[9], 0x7632), __byte_perm(o[10], o[11], 0x7632),
+                           __byte_perm(o[12], o[13], 0x7632), __byte_perm(o[14], o[15], 0x7632));
+    }
+}
+
 }  // namespace
 
 void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStream_t st) {
     if (f.N == 0) return;
     if (f.W % 16 == 0 && f.W <= 16384) {
         const int nt = ((f.W / 16) + 31) / 32 * 32;
-        k_fill_rows16v<<<f.H, nt, 0, st>>>(f, in, out);
+        k_fill_rows16p<<<(f.H + 1) / 2, nt, 0, st>>>(f, in, out);
         return;
     }
     const size_t sm = (size_t)f.W * sizeof(int16_t);

@@ -443,6 +443,18 @@ def test_peek_wide_values_vs_oracle(dev, stk, port, w, h, p, vmax):
         eq(stk.peek_columns(m, thr, device=dev), port.peek_columns(m, thr))
 
 
+@pytest.mark.parametrize("w,h,p,vmax", [(256, 33, 0.2, 257), (4096, 7, 0.05, 32767), (64, 2, 0.5, 1024),
+                                        (16, 1, 0.3, 300), (1024, 300, 0.02, 32767)])
+def test_fill_wide_values_vs_oracle(dev, stk, port, w, h, p, vmax):
+    """K6 v2 keeps two rows in int16x2 lanes (widths a multiple of 16): values
+    with a high byte, odd heights (a lone last row), single rows."""
+    rng = np.random.default_rng(w * 31 + h)
+    m = np.where(rng.random((h, w)) < p, rng.integers(0, vmax + 1, (h, w)), -1).astype(np.int16)
+    # runs of equal knowns so that gaps get filled
+    m[:, ::7] = np.where(m[:, ::7] >= 0, 5, m[:, ::7])
+    eq(stk.fill_scanlines(m, device=dev), port.fill_scanlines(m))
+
+
 # ----------------------------------------------------------------- K8 -------
 def test_blur_map(dev, stk, golden, port, synth):
     eq(stk.build_blur_map(np.array([[2, 4, 11, 7]], np.int16), [(3, 5), (10, 12)], 16, device=dev),
