@@ -862,13 +862,28 @@ __global__ void __launch_bounds__(128) k_apply_runs(Frame f, const uint32_t* __r
         }
         const int32_t* rr = runroot + (size_t)tile * kRunCap + (rinc - nr);
         uint32_t pruned = 0;
-        int k = 0;
-        for (uint32_t t = s; t; t &= t - 1, ++k) {
-            const int a = __ffs(t) - 1, len = run_len(m, a);
-            const int id = __ldg(rr + k);
-            const int r = __ldcg(f.par + id);
-            if (!(__ldcg(f.cnt + r) & kRemoved))
-                pruned |= (len >= 32 ? 0xffffffffu : ((1u << len) - 1u)) << a;
+        // run -> region root id -> global root -> removed?  Three dependent L2
+        // reads per run: issued for up to 8 runs of the row at a time (one
+        // latency exposure per level instead of one per run)
+        constexpr int RB = 8;
+        uint32_t t = s;
+        for (int k0 = 0; k0 < nr; k0 += RB) {
+            int id[RB], rt[RB];
+            uint32_t cn[RB];
+#pragma unroll
+            for (int k = 0; k < RB; ++k) id[k] = k0 + k < nr ? __ldg(rr + k0 + k) : 0;
+#pragma unroll
+            for (int k = 0; k < RB; ++k) rt[k] = k0 + k < nr ? __ldcg(f.par + id[k]) : 0;
+#pragma unroll
+            for (int k = 0; k < RB; ++k) cn[k] = k0 + k < nr ? __ldcg(f.cnt + rt[k]) : kRemoved;
+#pragma unroll
+            for (int k = 0; k < RB; ++k) {
+                if (k0 + k < nr) {
+                    const int a = __ffs(t) - 1, len = run_len(m, a);
+                    t &= t - 1;
+                    if (!(cn[k] & kRemoved)) pruned |= (len >= 32 ? 0xffffffffu : ((1u << len) - 1u)) << a;
+                }
+            }
         }
         const int mg = f.hw, W = f.W, H = f.H;
         uint32_t anc = pruned;
