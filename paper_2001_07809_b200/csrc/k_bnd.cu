@@ -46,7 +46,10 @@ namespace {
 constexpr int CT = 32;         // CCL tile side
 constexpr int kRunCap = 512;   // max runs in a 32x32 tile (16 per row): runroot stride
 constexpr int kRunCapFast = 256;  // B2's shared-memory run table (overflow tiles: second pass)
-constexpr int MB_ROWS = 8;     // B1 output rows per warp (8: twice the warps of 16 -- the kernel is latency-bound)
+#ifndef STK_MB_ROWS
+#define STK_MB_ROWS 8
+#endif
+constexpr int MB_ROWS = STK_MB_ROWS;  // B1 output rows per warp (8: twice the warps of 16 -- the kernel is latency-bound)
 constexpr int MB_WPW = 30;     // B1 output words per warp (+1 halo word each side)
 
 __device__ __forceinline__ uint32_t upto_mask(int j) {  // bits 0..j
