@@ -504,6 +504,7 @@ def main():
                                     fps_e2e / world, frame_ms_dev)},
         "gpu_launches": int(kernels_per_frame * args.steps * 2),
         "kernels_per_frame": int(kernels_per_frame),
+        "gpu_launches_note": "kernels_per_frame x steps in each of the two timed regions (device-resident, e2e)",
         "roofline": roofline,
         "roofline_frame": roofline_frame,
         "roofline_stages": stages,
