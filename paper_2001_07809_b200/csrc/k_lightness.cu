@@ -126,7 +126,7 @@ __device__ __forceinline__ void split36(double y, uint32_t& bk, uint32_t& yq) {
 constexpr int kL2Threads = 1024, kL2Copies = 16;
 constexpr size_t kL2TabBytes = 3 * 256 * kL2Copies * sizeof(float);           // 48 KB
 constexpr size_t kL2Smem = 3 * 256 * sizeof(double) +                               // FP64 products (6 KB)
-                           kL2TabBytes + (kLstarBuckets + 4) * sizeof(uint32_t) +  // + 16 KB
+                           kL2TabBytes + 65536 +                                   // + screen table 64 KB
                            (size_t)(kL2Threads / 32) * (97 + 32) * sizeof(uint4) +   // + 64.5 KB
                            (size_t)(kL2Threads / 32) * 256 * sizeof(uint32_t);       // + 32 KB histograms
 
@@ -135,8 +135,9 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_lstar2(Frame f, const LstarTa
     extern __shared__ __align__(16) unsigned char l2s[];
     double* prod = reinterpret_cast<double*>(l2s);                        // [3][256] FP64 (redo path)
     float* tabs = reinterpret_cast<float*>(l2s + 3 * 256 * sizeof(double));  // [3][256][16]
-    uint32_t* bw = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(tabs) + kL2TabBytes);
-    uint4* xin_all = reinterpret_cast<uint4*>(bw + kLstarBuckets + 4);  // [32 warps][97]
+    uint8_t* sub = reinterpret_cast<unsigned char*>(tabs) + kL2TabBytes;     // [65536] screen table
+    const uint32_t* __restrict__ bw = tab->bw;                                // redo path: from L2
+    uint4* xin_all = reinterpret_cast<uint4*>(sub + 65536);             // [32 warps][97]
     uint4* xout_all = xin_all + (kL2Threads / 32) * 97;                 // [32 warps][32]
     // left view: warp-private 256-bin histograms of the converted bytes
     // (segmentation.cpp:11-44 fused into the conversion; K1b is then skipped)
@@ -152,29 +153,27 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_lstar2(Frame f, const LstarTa
             const int i = threadIdx.x + k * kL2Threads;  // = (table * 256 + e) * 16 + c
             t[k] = __ldg(&tab->fprod[0][0] + (i >> 4));
         }
-        constexpr int NV = kLstarBuckets / 4 / kL2Threads;
+        constexpr int NV = 65536 / 16 / kL2Threads;
         uint4 v[NV];
 #pragma unroll
-        for (int k = 0; k < NV; ++k) v[k] = __ldg(reinterpret_cast<const uint4*>(tab->bw) + threadIdx.x + k * kL2Threads);
+        for (int k = 0; k < NV; ++k) v[k] = __ldg(reinterpret_cast<const uint4*>(tab->sub) + threadIdx.x + k * kL2Threads);
 #pragma unroll
         for (int k = 0; k < NT; ++k) tabs[threadIdx.x + k * kL2Threads] = t[k];
 #pragma unroll
-        for (int k = 0; k < NV; ++k) reinterpret_cast<uint4*>(bw)[threadIdx.x + k * kL2Threads] = v[k];
-        if (threadIdx.x == 0) bw[kLstarBuckets] = tab->bw[kLstarBuckets];
+        for (int k = 0; k < NV; ++k) reinterpret_cast<uint4*>(sub)[threadIdx.x + k * kL2Threads] = v[k];
         for (int i = threadIdx.x; i < 3 * 256; i += kL2Threads) prod[i] = __ldg(&tab->prod[0][0] + i);
     }
     __syncthreads();
     // FP32 screen: Y32 = (f[R] + f[G]) + f[B] from the products rounded to
-    // float (f[c][v] = RN32(prod[c][v]), byte v of channel c at copy-base +
-    // 64 v) is within 3 * 2^-24 of the reference's FP64 Y (three product
-    // roundings <= 2^-24 * coefficient, two sums <= 2^-24 each; Y <= 1), and
-    // RZ(Y32 + 1) in [1, 2) adds <= 2^-23: |Y' - Y| <= 5 * 2^-24 < 2^-21.6,
-    // i.e. < 2^14.4 steps of 2^-36.  Y' = 1 + mantissa 2^-23: bucket = its top
-    // 12 bits, position in the bucket (2^-36 steps, as split36) = the low 11
-    // bits << 13.  With a margin of 2^16 steps the FP32 bucket and the side of
-    // the bucket's threshold are exact; pixels inside the margin (threshold or
-    // bucket edge: ~1 % of random RGB) are redone in FP64 below.
-    constexpr uint32_t kMargin = 1u << 16;
+    // float (f[c][v] = RN32(prod[c][v])) is within 3 * 2^-24 of the
+    // reference's FP64 Y (three product roundings <= 2^-24 * coefficient, two
+    // sums <= 2^-24 each; Y <= 1), and RZ(Y32 + 1) in [1, 2) adds <= 2^-23:
+    // |Y' - Y| <= 5 * 2^-24 < 2^-21.6.  Y''s mantissa / 2^7 is its 2^-16
+    // sub-bucket s; sub[s] is the gray of every Y within 2^-20 of s (the host
+    // checked that no L* threshold lies there), or 0xff where one does: those
+    // pixels (~0.4 % of random RGB) are redone in FP64 below.  Y' >= the
+    // bright bound (including Y32 >= 1) is gray 255.
+    const uint32_t bright = __ldg(&tab->bright);
     // entry e of copy c at e * 16 + c: a lookup is one byte extract (PRMT) and
     // one LEA (e << 6 onto the lane's copy base)
     const float* fr = tabs + (threadIdx.x & (kL2Copies - 1));
@@ -195,10 +194,10 @@ __global__ void __launch_bounds__(kL2Threads, 1) k_lstar2(Frame f, const LstarTa
         m1 = (uint32_t)(t >> 32);
     };
     auto gray32 = [&](uint32_t m, bool& unsure) {  // m = bits of RZ(Y32 + 1)
-        const uint32_t bk = (m >> 11) & 0xfffu, pos = (m & 0x7ffu) << 13;
-        const uint32_t w = bw[bk], q = w & 0xffffffu;
-        unsure = m >= 0x40000000u || pos - kMargin > (1u << 24) - 2 * kMargin || pos - q + kMargin < 2 * kMargin;
-        return (w >> 24) + (pos > q ? 1u : 0u);
+        const uint32_t g = sub[(m >> 7) & 0xffffu];
+        const bool br = m >= bright;
+        unsure = g == 0xffu && !br;
+        return br ? 255u : g;
     };
     // the reference's FP64 Y (host-tabulated products, __dadd_rn in its order)
     auto y64_of = [&](uint32_t v) {

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -202,6 +203,20 @@ void make_lstar_tables(LstarTables* t) {
         if (std::isfinite(t->tb[b])) q = (uint32_t)((t->tb[b] * NB - b) * 16777216.0);  // exact, < 2^24
         t->bw[b] = (uint32_t)t->base[b] << 24 | q;
     }
+    // K1's FP32 screen (k_lightness.cu): a screened Y' is within 5 * 2^-24 of
+    // the reference's Y, so with a 2^-20 margin a sub-bucket without a
+    // threshold in its widened span has one gray value for every pixel
+    // screened into it
+    const double E = std::ldexp(1.0, -20);
+    int c = 0;  // thresholds <= lo
+    for (int s = 0; s < 65536; ++s) {
+        const double lo = s * std::ldexp(1.0, -16) - E, hi = (s + 1) * std::ldexp(1.0, -16) + E;
+        while (c < 255 && t->thr[c + 1] <= lo) ++c;
+        const bool inside = c < 255 && t->thr[c + 1] <= hi;
+        t->sub[s] = inside || c >= 255 ? 0xffu : (uint8_t)c;
+    }
+    const double b255 = (t->thr[255] + E) * 8388608.0;  // 2^23: Y' mantissa units
+    t->bright = 0x3f800000u | (uint32_t)std::ceil(b255);
 }
 
 bool lstar_buckets_ok(const LstarTables* t) {
@@ -790,7 +805,8 @@ stk_status stk_create(int device, int max_width, int max_height, int slots, stk_
             break;
         }
         ctx->encode = (EncodeTiledFn)fn;
-        LstarTables tab;
+        std::unique_ptr<LstarTables> tabp(new LstarTables());
+        LstarTables& tab = *tabp;
         make_lstar_tables(&tab);
         if (!lstar_buckets_ok(&tab)) {
             rc = fail(ctx, STK_EINTERNAL, "stk_create: L* bucket table has a bucket with 2 thresholds");
@@ -916,10 +932,10 @@ void stk_host_free(void* p) {
 stk_status stk_validate_config(const stk_config* cfg) { return check_config(nullptr, cfg); }
 
 void stk_lstar_tables(double linear[256], double thr[256]) {
-    LstarTables t;
-    make_lstar_tables(&t);
-    std::memcpy(linear, t.linear, sizeof(t.linear));
-    std::memcpy(thr, t.thr, sizeof(t.thr));
+    std::unique_ptr<LstarTables> t(new LstarTables());
+    make_lstar_tables(t.get());
+    std::memcpy(linear, t->linear, sizeof(t->linear));
+    std::memcpy(thr, t->thr, sizeof(t->thr));
 }
 
 int stk_default_kernel_size(double sigma) { return 2 * (int)std::ceil(3.0 * sigma) + 1; }

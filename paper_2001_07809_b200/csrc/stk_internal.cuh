@@ -116,6 +116,12 @@ struct LstarTables {
     alignas(16) uint32_t bw[4097];
     // fprod[c][v] = (float)prod[c][v] (round to nearest): K1's FP32 screen
     float fprod[3][256];
+    // K1's screen table: sub[s] = the gray of every Y within 2^-20 of the
+    // sub-bucket [s 2^-16, (s+1) 2^-16) when no threshold lies in that span,
+    // else 0xff; bright = bits of 1 + (thr[255] + 2^-20) rounded up: a
+    // screened Y' at or above it is gray 255 (0xff in sub[] too)
+    alignas(16) uint8_t sub[65536];
+    uint32_t bright;
 };
 constexpr int kLstarBuckets = 4096;
 
