@@ -541,8 +541,12 @@ __device__ __forceinline__ uint32_t vmax2(uint32_t a, uint32_t b) { return __vma
 
 // K7 v6: K7 v5 with both columns of a thread in int16x2 lanes (PRMT sign
 // masks, LOP3 selects, VIADD/VIMNMX.16x2): half the instructions per row.
+// SMEM: the nearest-below scratch lives in shared memory ([H][P5C] u32, the
+// CTA's 16 columns) instead of in `out` (3 global passes instead of 5)
+template <bool SMEM>
 __global__ void __launch_bounds__(P5C * P5S, 2) k_peek_cols6(Frame f, const int16_t* __restrict__ in,
                                                           int16_t* __restrict__ out) {
+    extern __shared__ __align__(16) uint32_t scr[];
     __shared__ int s_cnt[P5S][2 * P5C];
     __shared__ uint32_t s_first[P5S][2 * P5C];  // f1 | f2 << 16 (int16 each, -1 = none)
     __shared__ uint32_t s_last[P5S][2 * P5C];   // l1 | l2 << 16 (last, second last)
@@ -567,7 +571,8 @@ __global__ void __launch_bounds__(P5C * P5S, 2) k_peek_cols6(Frame f, const int1
     uint32_t f1 = 0xffffffffu, f2 = 0xffffffffu, l1 = 0xffffffffu, l2 = 0xffffffffu, n2 = 0;
     if (col) {
         const uint32_t* ip = in2 + x / 2 + (size_t)(yb - 1) * W2;
-        uint32_t* op = out2 + x / 2 + (size_t)(yb - 1) * W2;
+        const size_t OS = SMEM ? (size_t)P5C : W2;  // scratch row stride
+        uint32_t* op = SMEM ? scr + cp + (size_t)(yb - 1) * P5C : out2 + x / 2 + (size_t)(yb - 1) * W2;
         auto row = [&](uint32_t v, uint32_t* dst) {
             *dst = f1;
             const uint32_t md = sgn2(v);  // unknown lanes
@@ -580,14 +585,14 @@ __global__ void __launch_bounds__(P5C * P5S, 2) k_peek_cols6(Frame f, const int1
             n2 += ~md & 0x00010001u;
         };
         int y = yb - 1;
-        for (; y - P4B + 1 >= ya; y -= P4B, ip -= P4B * W2, op -= P4B * W2) {
+        for (; y - P4B + 1 >= ya; y -= P4B, ip -= P4B * W2, op -= P4B * OS) {
             uint32_t v[P4B];
 #pragma unroll
             for (int k = 0; k < P4B; ++k) v[k] = __ldg(ip - k * W2);
 #pragma unroll
-            for (int k = 0; k < P4B; ++k) row(v[k], op - k * W2);
+            for (int k = 0; k < P4B; ++k) row(v[k], op - k * OS);
         }
-        for (; y >= ya; --y, ip -= W2, op -= W2) row(__ldg(ip), op);
+        for (; y >= ya; --y, ip -= W2, op -= OS) row(__ldg(ip), op);
     }
     s_cnt[s][2 * cp] = (int)(n2 & 0xffffu);
     s_cnt[s][2 * cp + 1] = (int)(n2 >> 16);
@@ -682,6 +687,8 @@ __global__ void __launch_bounds__(P5C * P5S, 2) k_peek_cols6(Frame f, const int1
         uint32_t kacc = 0;  // known counts per lane
         const uint32_t* ip = in2 + x / 2 + (size_t)ya * W2;
         uint32_t* op = out2 + x / 2 + (size_t)ya * W2;
+        const size_t OS = SMEM ? (size_t)P5C : W2;  // scratch row stride
+        const uint32_t* sp = SMEM ? scr + cp + (size_t)ya * P5C : op;
         auto row = [&](uint32_t v, uint32_t bw, uint32_t* dst) {
             const uint32_t mbw = sgn2(bw);
             const uint32_t b = (bl & mbw) | (bw & ~mbw);
@@ -704,17 +711,17 @@ __global__ void __launch_bounds__(P5C * P5S, 2) k_peek_cols6(Frame f, const int1
         // batches: all loads of P4B rows (input and scratch) issue before the
         // stores (the scratch loads would otherwise wait behind them)
         int y = ya;
-        for (; y + P4B <= yb; y += P4B, ip += P4B * W2, op += P4B * W2) {
+        for (; y + P4B <= yb; y += P4B, ip += P4B * W2, op += P4B * W2, sp += P4B * OS) {
             uint32_t v[P4B], bw[P4B];
 #pragma unroll
             for (int k = 0; k < P4B; ++k) {
                 v[k] = __ldg(ip + k * W2);
-                bw[k] = op[k * W2];
+                bw[k] = sp[k * OS];
             }
 #pragma unroll
             for (int k = 0; k < P4B; ++k) row(v[k], bw[k], op + k * W2);
         }
-        for (; y < yb; ++y, ip += W2, op += W2) row(__ldg(ip), *op, op);
+        for (; y < yb; ++y, ip += W2, op += W2, sp += OS) row(__ldg(ip), *sp, op);
         known = (kacc & 0xffffu) + (kacc >> 16);
     }
     for (int o = 16; o > 0; o >>= 1) known += __shfl_xor_sync(0xffffffffu, known, o);
@@ -842,7 +849,14 @@ void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStrea
 void launch_peek_cols(const Frame& f, const int16_t* in, int16_t* out, int16_t*, cudaStream_t st) {
     if (f.N == 0) return;
     if (f.W % 2 == 0 && (reinterpret_cast<uintptr_t>(in) & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 3) == 0) {
-        k_peek_cols6<<<(f.W + 2 * P5C - 1) / (2 * P5C), P5C * P5S, 0, st>>>(f, in, out);
+        // the scratch in shared memory when the strip fits (4K: 74 KB, 2 CTAs/SM)
+        const size_t sm = (size_t)f.H * P5C * sizeof(uint32_t);
+        if (sm <= 96 * 1024) {
+            cudaFuncSetAttribute(k_peek_cols6<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_peek_cols6<true><<<(f.W + 2 * P5C - 1) / (2 * P5C), P5C * P5S, sm, st>>>(f, in, out);
+        } else {
+            k_peek_cols6<false><<<(f.W + 2 * P5C - 1) / (2 * P5C), P5C * P5S, 0, st>>>(f, in, out);
+        }
         return;
     }
     k_peek_cols2<<<(f.W + PC - 1) / PC, PC * PS, 0, st>>>(f, in, out);
