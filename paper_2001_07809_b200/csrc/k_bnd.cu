@@ -602,22 +602,49 @@ __device__ __forceinline__ void ccl_region_body(const Frame& f, const uint32_t* 
         S.sz[i] = 0;
     }
     __syncwarp();
-    // 1. unions with the overlapping runs of the row above (8-connectivity)
-    for (int i = lane; i < nruns; i += 32) {
-        const int r = S.rrow[i];
-        if (r == 0) continue;
+    // 1. unions with the overlapping runs of the row above (8-connectivity).
+    //   a. each run links to its FIRST overlapping run above (a smaller index:
+    //      a forest whose roots are their trees' minima, no atomics);
+    //   b. pointer jumping flattens it (in place: a concurrently updated
+    //      par[par[i]] is still an ancestor; depth <= 32 rows -> 5 rounds);
+    //   c. the remaining overlaps (merges: a run touching two or more runs
+    //      above) are united with min-linking on the flattened forest, so
+    //      the finds are short and a component's root stays its first run.
+    auto overlaps = [&](int i, uint32_t& T, uint32_t& mu, uint32_t& su, int& r) {
+        r = S.rrow[i];
+        if (r == 0) return false;
         const int a = S.rstart[i], b = a + S.rlen[i] - 1;
         const int lo = a > 0 ? a - 1 : 0, hi = b < 31 ? b + 1 : 31;
-        const uint32_t mu = S.rowm[r - 1], su = S.rows[r - 1];
-        uint32_t T = mu & upto_mask(hi) & ~((1u << lo) - 1u);
-        while (T) {
-            const int j = __ffs(T) - 1;
-            const uint32_t below = su & upto_mask(j);
-            const int sa = 31 - __clz(below);
-            runite(S.par, i, S.rs[r - 1] + __popc(below) - 1);
-            const int e = sa + run_len(mu, sa) - 1;
-            T &= e >= 31 ? 0u : ~upto_mask(e);
-        }
+        mu = S.rowm[r - 1];
+        su = S.rows[r - 1];
+        T = mu & upto_mask(hi) & ~((1u << lo) - 1u);
+        return T != 0;
+    };
+    auto next_overlap = [&](uint32_t& T, uint32_t mu, uint32_t su, int r) {  // run index; T advanced
+        const int j = __ffs(T) - 1;
+        const uint32_t below = su & upto_mask(j);
+        const int sa = 31 - __clz(below);
+        const int e = sa + run_len(mu, sa) - 1;
+        T &= e >= 31 ? 0u : ~upto_mask(e);
+        return S.rs[r - 1] + __popc(below) - 1;
+    };
+    for (int i = lane; i < nruns; i += 32) {
+        uint32_t T, mu, su;
+        int r;
+        S.par[i] = overlaps(i, T, mu, su, r) ? next_overlap(T, mu, su, r) : i;
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int round = 0; round < 5; ++round) {
+        for (int i = lane; i < nruns; i += 32) S.par[i] = S.par[S.par[i]];
+        __syncwarp();
+    }
+    for (int i = lane; i < nruns; i += 32) {
+        uint32_t T, mu, su;
+        int r;
+        if (!overlaps(i, T, mu, su, r)) continue;
+        next_overlap(T, mu, su, r);  // the first one: linked in (a)
+        while (T) runite(S.par, i, next_overlap(T, mu, su, r));
     }
     __syncwarp();
     // flatten, sizes at the tile-local roots; switch to region node ids
