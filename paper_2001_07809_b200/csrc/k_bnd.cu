@@ -49,7 +49,8 @@ constexpr int kRunCapFast = 256;  // B2's shared-memory run table (overflow tile
 #ifndef STK_MB_ROWS
 #define STK_MB_ROWS 8
 #endif
-constexpr int MB_ROWS = STK_MB_ROWS;  // B1 output rows per warp (8: twice the warps of 16 -- the kernel is latency-bound)
+// B1 output rows per warp (STK_MB_ROWS: experiment knob; 4K: 4 rows 18.1 us, 6: 17.9, 8: 17.1, 12: 18.8)
+constexpr int MB_ROWS = STK_MB_ROWS;
 constexpr int MB_WPW = 30;     // B1 output words per warp (+1 halo word each side)
 
 __device__ __forceinline__ uint32_t upto_mask(int j) {  // bits 0..j

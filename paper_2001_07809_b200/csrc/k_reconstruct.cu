@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(PC * PS) k_peek_cols2(Frame f, const int16_t* 
 #ifndef STK_P4B
 #define STK_P4B 12
 #endif
-constexpr int P4B = STK_P4B;  // rows per load batch
+constexpr int P4B = STK_P4B;  // rows per load batch (4K peek: 8 rows 29 us, 12: 27.5, 16: 30.6)
 
 __device__ __forceinline__ uint32_t pack2(int a, int b) { return (uint32_t)(uint16_t)a | (uint32_t)b << 16; }
 __device__ __forceinline__ int lo16(uint32_t v) { return (int16_t)(v & 0xffffu); }
