@@ -8,8 +8,12 @@
 // inside a focus range (refocus.cpp:45-73, as a per-disparity LUT), so the
 // blur map never exists in HBM.  Tiles with no blurred pixel just copy.
 //
-//   k_blur_v3 (default; kernel sizes 3-13, 17, 19, 23, 25, 31, 37, 43, 49 --
-//             every integer sigma up to 8): separable FP32, 128 x 16 tiles,
+//   k_blur_tc (default in the frame path; kernel sizes 3-17 and 19, 23, 25,
+//             31, 37, 43, 49 -- every integer sigma up to 8): the separable
+//             blur as banded tensor-core products (mma.sync, f16 hi/lo
+//             splits, f32 accumulation), see K8t below;
+//   k_blur_v3 (the frame path's blur before K8t; STK_BLUR_TC=0, and frames
+//             of >= 2^31 / 3 pixels): separable FP32, 128 x 16 tiles,
 //             vertical pass first in registers (FFMA2 over column pairs),
 //             horizontal pass over 8-output items (FFMA2 over output pairs)
 //             -- within 1 LSB of the reference's 2-D FP64 sum (tests bound
