@@ -14,6 +14,10 @@
 //     one threshold per bucket), so gray = base[b] + (Y >= tb[b]) with
 //     b = floor(4096 Y): two cached loads and one compare instead of cbrt and
 //     lround.  Verified over all 2^24 RGB triples (tests).
+//   * The frame path's k_lstar2 screens in FP32 first (products rounded to
+//     float, a 64 KB table of 2^-16 sub-buckets whose gray is certain) and
+//     redoes only the pixels whose Y is within 2^-20 of a threshold with the
+//     exact FP64 rule above (details at k_lstar2).
 //   * Histogram without atomics: every thread owns one byte counter per bin
 //     in shared memory (bin-major, 64 KB), bumps it with a plain
 //     load/add/store, and a rotated (bank-conflict-free) pass sums the 256

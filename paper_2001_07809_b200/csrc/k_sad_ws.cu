@@ -17,7 +17,9 @@
 //             L byte (L, 0, L, 0) against a spread R pair (R(x), 0, R(x-1), 0)
 //             gives two disparities directly in u16x2 lanes; each row step
 //             adds the entering row and subtracts the leaving one in a single
-//             IADD3 per word.  All byte alignments are
+//             IADD3 per word.  With PAIRS, the R pairs come ready-made from a
+//             pair ring (each staged R row reversed into u16 lanes once per
+//             CTA, see pair_at).  All byte alignments are
 //             compile-time (K % 4 == 0, strip origin % 16 == 0, WIN fixed), so
 //             every shift/permute has an immediate selector.  The row's
 //             colsums go to shared memory buffer (row & 1).
