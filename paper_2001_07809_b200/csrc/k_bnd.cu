@@ -1223,6 +1223,11 @@ __global__ void __launch_bounds__(256) k_mask_to_bits(Frame f, const uint8_t* __
 
 }  // namespace
 
+size_t bord_bytes(int W, int H) {  // the border labels of every region (B2 -> B3)
+    const size_t nreg = (size_t)((W + RW - 1) / RW) * ((H + RH - 1) / RH);
+    return nreg * RBORD * sizeof(int32_t);
+}
+
 void launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
                            uint32_t* sbits, int sbits_words, bool anchors, cudaStream_t st) {
     // B2 - B8

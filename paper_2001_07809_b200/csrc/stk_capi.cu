@@ -261,7 +261,7 @@ Layout layout_for(int W, int H, int* P_out, int* lb_stride_out) {
     const size_t ctiles = (size_t)((W + 31) / 32) * ((H + 31) / 32);
     sz[L_RBITS] = sz[L_SBITS] = (size_t)H * TX * 4 * 4 + 64;
     sz[L_RUNR] = ctiles * 512 * 4 + 64;
-    sz[L_BORD] = ctiles * 128 * 4 + 64;  // >= regions * (2*128 + 2*64) entries
+    sz[L_BORD] = bord_bytes(W, H) + 64;  // region border labels (was sized per tile: short for tiny frames)
     Layout L;
     size_t o = 0;
     for (int i = 0; i < L_COUNT; ++i) {

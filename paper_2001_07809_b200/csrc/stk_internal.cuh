@@ -157,6 +157,8 @@ void launch_label_components_bits(const Frame& f, const uint8_t* mask, uint32_t*
                                   void* tmp, size_t tmp_bytes, int32_t* labels, uint32_t* sizes,
                                   int32_t* ids, cudaStream_t st);  // run CCL labels (k_bnd.cu)
 size_t label_components_tmp_bytes(int gbits_words);
+// bytes of the region border-label buffer (B2 / B3, k_bnd.cu) for a W x H frame
+size_t bord_bytes(int W, int H);
 // stage entry prune_components on a pitched byte mask (writes f.mprn / f.manc)
 void launch_prune_mask_bits(const Frame& f, const uint8_t* mask, uint32_t* rbits, int32_t* runroot,
                             int32_t* bord, uint32_t* sbits, int sbits_words, cudaStream_t st);
