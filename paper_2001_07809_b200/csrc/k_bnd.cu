@@ -45,7 +45,7 @@ namespace {
 
 constexpr int CT = 32;         // CCL tile side
 constexpr int kRunCap = 512;   // max runs in a 32x32 tile (16 per row): runroot stride
-constexpr int kRunCapFast = 256;  // B2's shared-memory run table (overflow tiles: second pass)
+constexpr int kRunCapFast = 224;  // B2's shared-memory run table (overflow tiles: second pass)
 #ifndef STK_MB_ROWS
 #define STK_MB_ROWS 8
 #endif
@@ -473,9 +473,16 @@ struct RunSmemT {
     int rs[CT + 1];                // first ridx of each row
     uint8_t rstart[CAP], rlen[CAP], rrow[CAP];
     int par[CAP];                  // region node ids after step 1
-    int sz[CAP];
     int key[CAP];                  // g of tile-local roots, INT_MAX otherwise
+    uint16_t sz[CAP];              // sizes (a region's components hold <= 128 x 128 pixels)
 };
+
+// sz[i] += v: a 32-bit shared atomic on the u16's word (v and the sums stay
+// below 2^16, so the low half never carries into the high one)
+template <int CAP>
+__device__ __forceinline__ void sz_add(uint16_t (&sz)[CAP], int i, unsigned v) {
+    atomicAdd(reinterpret_cast<unsigned*>(&sz[i & ~1]), v << (16 * (i & 1)));
+}
 
 __device__ __forceinline__ int rfind(int* p, int x) {  // with path halving
     int q = p[x];
@@ -545,7 +552,7 @@ __device__ __forceinline__ int node_at(const RunSmemT<CAP>* R, int w, int row, i
     return w * CAP + S.rs[row] + __popc(S.rows[row] & upto_mask(col)) - 1;
 }
 
-// Region body: CAP = the run table's per-tile capacity.  FIRST (CAP = 256):
+// Region body: CAP = the run table's per-tile capacity.  FIRST (CAP = 224):
 // a region with a tile of more runs appends itself to the overflow list
 // (f.list, count in sc->n_ovf) and writes nothing; the overflow pass (CAP =
 // 512, the most a 32x32 tile can hold) then runs those regions.
@@ -653,7 +660,7 @@ __device__ __forceinline__ void ccl_region_body(const Frame& f, const uint32_t* 
     for (int i = lane; i < nruns; i += 32) {
         const int rt = rfind(S.par, i);
         S.par[i] = rt;
-        atomicAdd(&S.sz[rt], (int)S.rlen[i]);
+        sz_add(S.sz, rt, S.rlen[i]);
     }
     __syncwarp();
     for (int i = lane; i < nruns; i += 32) {
@@ -697,7 +704,7 @@ __device__ __forceinline__ void ccl_region_body(const Frame& f, const uint32_t* 
         const int rt = cfind(R, self);
         if (S.key[i] != 0x7fffffff && rt != self) {  // a tile root merged into another
             RunSmem& Q = R[rt / CAP];
-            atomicAdd(&Q.sz[rt % CAP], S.sz[i]);
+            sz_add(Q.sz, rt % CAP, S.sz[i]);
             atomicMin(&Q.key[rt % CAP], S.key[i]);
         }
     }
@@ -759,8 +766,9 @@ __device__ __forceinline__ void ccl_region_body(const Frame& f, const uint32_t* 
     }
 }
 
-// B2 first pass: one CTA per region, 256-run tables (32 KB of shared memory
-// per CTA: twice the resident CTAs of the 512-run layout)
+// B2 first pass: one CTA per region, 224-run tables with u16 sizes (52.8 KB
+// of shared memory per 128x128 region: four CTAs per SM, so the 576 regions of
+// a 4K frame run in one wave; dead-leaves masks peak at 224 runs per tile)
 __global__ void __launch_bounds__(32 * NRW) k_ccl_region(Frame f, const uint32_t* __restrict__ rbits,
                                                          int32_t* __restrict__ runroot,
                                                          int32_t* __restrict__ bord) {
