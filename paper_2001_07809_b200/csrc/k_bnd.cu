@@ -813,14 +813,30 @@ void launch_ccl_region(const Frame& f, const uint32_t* rbits, int32_t* runroot, 
 // above-right), thread RW + r the left-border pixel r (the left region's right
 // column; the diagonals across region corners are covered by the top borders).
 // A lane whose predecessor has the same root only adds its one new neighbour.
-__global__ void __launch_bounds__(RW + RH) k_ccl_borders(Frame f, const int32_t* __restrict__ bord) {
-    const int t = threadIdx.x, lane = t & 31;
+// With at most capn region roots (every frame-path mask seen: 6.5 K at 4K,
+// 23 K at 8K) the unions are only listed (edges after the border labels in
+// bord) and B3b unites them in shared memory; above it they run here on the
+// global forest (lock-free, as B3b's fallback).
+constexpr int kUniteThreads = 1024;
+
+// the edge list: after the region border labels
+__device__ __forceinline__ int2* edge_list(const Frame& f, int32_t* bord) {
+    const int nreg = ((f.W + RW - 1) / RW) * ((f.H + RH - 1) / RH);
+    return reinterpret_cast<int2*>(bord + (size_t)nreg * RBORD);
+}
+
+__global__ void __launch_bounds__(RW + RH) k_ccl_borders(Frame f, int32_t* __restrict__ bord, int capn) {
+    __shared__ int s_wsum[(RW + RH) / 32];
+    __shared__ unsigned s_base;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const bool direct = (int)__ldcg(&f.sc->n_lroots) > capn;  // grid-uniform
     const int RXc = (f.W + RW - 1) / RW;
     const int reg = blockIdx.x;
     const int rx = reg % RXc, ry = reg / RXc;
     const int32_t* bd = bord + (size_t)reg * RBORD;
+    int a, nb = 0, b[3] = {-1, -1, -1};
     if (t < RW) {
-        const int a = ry > 0 ? bd[t] : -1;
+        a = ry > 0 ? bd[t] : -1;
         const int ap = __shfl_up_sync(0xffffffffu, a, 1);
         if (a >= 0) {
             const int32_t* up = bord + (size_t)(reg - RXc) * RBORD + RW;  // bottom row above
@@ -828,15 +844,13 @@ __global__ void __launch_bounds__(RW + RH) k_ccl_borders(Frame f, const int32_t*
             const int u1 = up[t];
             const int u2 = t < RW - 1 ? up[t + 1] : (rx + 1 < RXc ? bord[(size_t)(reg - RXc + 1) * RBORD + RW] : -1);
             const bool cont = lane > 0 && ap == a;  // u0, u1 were the predecessor's u1, u2
-            int nb = 0, b[3] = {-1, -1, -1};
             if (!cont && u0 >= 0) b[nb++] = u0;
             if (!cont && u1 >= 0 && u1 != u0) b[nb++] = u1;
             if (u2 >= 0 && u2 != u1) b[nb++] = u2;
-            if (nb) gunite_n(f.par, a, b, nb);
         }
     } else {
         const int r = t - RW;
-        const int a = rx > 0 ? bd[2 * RW + r] : -1;
+        a = rx > 0 ? bd[2 * RW + r] : -1;
         const int ap = __shfl_up_sync(0xffffffffu, a, 1);
         if (a >= 0) {
             const int32_t* lf = bord + (size_t)(reg - 1) * RBORD + 2 * RW + RH;  // right column, left
@@ -844,12 +858,87 @@ __global__ void __launch_bounds__(RW + RH) k_ccl_borders(Frame f, const int32_t*
             const int l1 = lf[r];
             const int l2 = r < RH - 1 ? lf[r + 1] : -1;
             const bool cont = lane > 0 && ap == a;
-            int nb = 0, b[3] = {-1, -1, -1};
             if (!cont && l0 >= 0) b[nb++] = l0;
             if (!cont && l1 >= 0 && l1 != l0) b[nb++] = l1;
             if (l2 >= 0 && l2 != l1) b[nb++] = l2;
-            if (nb) gunite_n(f.par, a, b, nb);
         }
+    }
+    if (direct) {
+        if (nb) gunite_n(f.par, a, b, nb);
+        return;
+    }
+    {   // a pair (a, b[i]) the previous lane also lists is dropped (along a
+        // border run the same pair repeats lane after lane)
+        const int ap = __shfl_up_sync(0xffffffffu, a, 1);
+        const int p0 = __shfl_up_sync(0xffffffffu, b[0], 1);
+        const int p1 = __shfl_up_sync(0xffffffffu, b[1], 1);
+        const int p2 = __shfl_up_sync(0xffffffffu, b[2], 1);
+        if (lane > 0 && ap == a) {
+            int m = 0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+                if (i < nb && b[i] != p0 && b[i] != p1 && b[i] != p2) b[m++] = b[i];
+            nb = m;
+        }
+    }
+    // the block's edges appended with one atomic
+    int incl = nb;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) s_wsum[wid] = incl;
+    __syncthreads();
+    if (t == 0) {
+        int tot = 0;
+        for (int w = 0; w < (RW + RH) / 32; ++w) {
+            const int v = s_wsum[w];
+            s_wsum[w] = tot;
+            tot += v;
+        }
+        s_base = tot ? atomicAdd(&f.sc->n_edges, (unsigned)tot) : 0u;
+    }
+    __syncthreads();
+    int2* const el = edge_list(f, bord) + s_base + s_wsum[wid] + (incl - nb);
+    for (int i = 0; i < nb; ++i) el[i] = make_int2(a, b[i]);
+}
+
+// B3b: one CTA unites the listed edges on a shared-memory forest of the n
+// region roots (min-linking, path halving: shared-memory latency instead of
+// the L2 round trips of global unions) and writes every non-root's final root
+// to f.par (a flat forest: the later finds are one step).  Edges are read
+// four per thread at a time so their L2 latencies overlap.  4K frame (6478
+// roots, 13431 edges before B3's dedupe): 19.6 us vs 28 us for B3's old
+// global unions.  Measured and dropped: hash-priority CAS linking (2.2x the
+// union cycles), waves of one edge per thread with a flatten after each
+// (1.5x), a converged lockstep walk with per-pair leader election (3x).
+__global__ void __launch_bounds__(kUniteThreads) k_ccl_unite(Frame f, const int32_t* __restrict__ bord, int capn) {
+    extern __shared__ int sp[];
+    const int n = (int)__ldcg(&f.sc->n_lroots);
+    if (n > capn) return;  // B3 united them directly
+    const int ne = (int)__ldcg(&f.sc->n_edges);
+    const int2* el = edge_list(f, const_cast<int32_t*>(bord));
+    const int tid = threadIdx.x;
+    for (int i = tid; i < n; i += kUniteThreads) sp[i] = i;
+    __syncthreads();
+    constexpr int EB = 4;
+    // a contiguous chunk of the list per thread: the lanes of a warp work on
+    // 32 distant parts of the frame instead of one border's edges, which all
+    // link the same region root (same-address atomics serialise)
+    const int per = (ne + kUniteThreads - 1) / kUniteThreads;
+    const int c0 = tid * per, c1 = min(c0 + per, ne);
+    for (int e0 = c0; e0 < c1; e0 += EB) {
+        int2 ed[EB];
+#pragma unroll
+        for (int j = 0; j < EB; ++j) ed[j] = e0 + j < c1 ? __ldcg(el + e0 + j) : make_int2(0, 0);
+#pragma unroll
+        for (int j = 0; j < EB; ++j) runite(sp, ed[j].x, ed[j].y);
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += kUniteThreads) {
+        const int r = rfind(sp, i);
+        if (r != i) f.par[i] = r;
     }
 }
 
@@ -1231,9 +1320,25 @@ __global__ void __launch_bounds__(256) k_mask_to_bits(Frame f, const uint8_t* __
 
 }  // namespace
 
-size_t bord_bytes(int W, int H) {  // the border labels of every region (B2 -> B3)
+size_t bord_bytes(int W, int H) {  // the border labels of every region (B2 -> B3) + B3's edges
     const size_t nreg = (size_t)((W + RW - 1) / RW) * ((H + RH - 1) / RH);
-    return nreg * RBORD * sizeof(int32_t);
+    return nreg * RBORD * sizeof(int32_t) + nreg * (RW + RH) * 3 * sizeof(int2);
+}
+
+// B3 + B3b.  capn: the most region roots B3b's shared-memory forest takes
+// (STK_UNITE_CAP: test / experiment knob; 0 forces the global unions)
+void launch_ccl_borders(const Frame& f, int32_t* bord, cudaStream_t st) {
+    static const int capn = [] {
+        const char* e = getenv("STK_UNITE_CAP");
+        return e ? atoi(e) : 32768;
+    }();
+    const int nreg = ((f.W + RW - 1) / RW) * ((f.H + RH - 1) / RH);
+    k_ccl_borders<<<nreg, RW + RH, 0, st>>>(f, bord, capn);
+    if (capn > 0) {
+        const int smem = capn * (int)sizeof(int);
+        cudaFuncSetAttribute(k_ccl_unite, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        k_ccl_unite<<<1, kUniteThreads, smem, st>>>(f, bord, capn);
+    }
 }
 
 void launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
@@ -1241,9 +1346,8 @@ void launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, in
     // B2 - B8
     const int ntiles = ((f.W + CT - 1) / CT) * ((f.H + CT - 1) / CT);
     const int tb = (ntiles + 3) / 4;
-    const int nreg = ((f.W + RW - 1) / RW) * ((f.H + RH - 1) / RH);
     launch_ccl_region(f, rbits, runroot, bord, st);
-    k_ccl_borders<<<nreg, RW + RH, 0, st>>>(f, bord);
+    launch_ccl_borders(f, bord, st);
     cudaMemsetAsync(sbits, 0, (size_t)sbits_words * 4, st);
     {   // B4-B7 in one cooperative launch (co-resident blocks, grid barriers)
         // co-resident blocks per SM depend only on the kernel (thread-safe
@@ -1434,9 +1538,8 @@ void launch_label_components_bits(const Frame& f, const uint8_t* mask, uint32_t*
     const long long nw = (long long)((f.W + 31) / 32) * f.H;
     const int gb = (int)std::min<long long>((nw + 255) / 256, f.sms * 8);
     k_mask_to_bits<<<gb, 256, 0, st>>>(f, mask, rbits);
-    const int nreg = ((f.W + RW - 1) / RW) * ((f.H + RH - 1) / RH);
     launch_ccl_region(f, rbits, runroot, bord, st);  // B2
-    k_ccl_borders<<<nreg, RW + RH, 0, st>>>(f, bord);                    // B3
+    launch_ccl_borders(f, bord, st);                  // B3, B3b
     const int ib = f.sms * 4;
     k_cc_compress<<<ib, 256, 0, st>>>(f);
     cudaMemsetAsync(gbits, 0, (size_t)gbits_words * 4, st);

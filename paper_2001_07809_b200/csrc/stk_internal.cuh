@@ -50,7 +50,7 @@ struct DevScalars {
     unsigned int psel_done;            // prune select: finished blocks
     unsigned int gbar_count;           // grid barrier (cooperative prune kernel)
     unsigned int gbar_gen;
-    unsigned int pad2;
+    unsigned int n_edges;              // B3 -> B3b border edge list length
     unsigned long long psel[128];      // prune select: per-block pixel sums
     unsigned long long gsum[512];      // cooperative prune: per-block pixel sums
     unsigned int gcnt[512];            // cooperative prune: per-block size-s* root counts

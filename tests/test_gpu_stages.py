@@ -3,6 +3,7 @@ mirror of the stereotk API) against the golden fixtures of the compiled
 reference and against the oracle on seeded random inputs, including the
 reference suite's edge cases.  Bit-exact everywhere except the separable
 blur (<= 1 LSB, tolerance written below)."""
+import os
 import numpy as np
 import pytest
 
@@ -216,6 +217,59 @@ def test_components_overflow_tiles(dev, stk, port, synth):
         eq(t.by_size, bys)
         for frac in (0.0, 0.04, 0.3):
             eq(stk.prune_components(m, frac, device=dev), port.prune(m, frac))
+
+
+def test_components_many_region_roots(dev, stk, port):
+    """B3 lists the border unions for B3b's shared-memory forest only up to
+    32768 region roots; above that it unites them on the global forest.  A
+    mask of isolated pixels (196 K region roots) crossed by lines that chain
+    them across every region border: labels, sizes, by_size, pruned masks."""
+    W, H = 1024, 768
+    m = np.zeros((H, W), np.uint8)
+    m[::2, ::2] = 1
+    m[1::96, :] = 1                      # joins rows 0/2 (and 96/98 ...) across regions
+    m[:, 127::128] = 1                   # vertical lines on region edges
+    m[300:700, 400:800:3] = 1            # vertical runs crossing region rows
+    t = stk.label_components(m, device=dev)
+    lab, sz, bys = port.label_components(m)
+    eq(t.labels, lab)
+    eq(t.sizes, sz)
+    eq(t.by_size, bys)
+    for frac in (0.0, 0.04, 0.3):
+        eq(stk.prune_components(m, frac, device=dev), port.prune(m, frac))
+
+
+_UNITE_CAP_SNIPPET = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2001_07809_b200 import stereotk as stk, synth
+import oracle
+port = oracle.port()
+d = stk.Device(0, slots=1)
+for seed, (w, h, pct) in enumerate([(1920, 1080, 40), (700, 300, 20), (517, 331, 30), (4096, 160, 12)]):
+    m = synth.random_mask(w, h, 70 + seed, pct)
+    t = stk.label_components(m, device=d)
+    lab, sz, bys = port.label_components(m)
+    assert np.array_equal(t.labels, lab) and np.array_equal(t.sizes, sz) and np.array_equal(t.by_size, bys), seed
+    for frac in (0.0, 0.04, 0.3):
+        assert np.array_equal(stk.prune_components(m, frac, device=d), port.prune(m, frac)), (seed, frac)
+d.close()
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("cap", ["0", "100"])
+def test_components_unite_cap(cap, tmp_path):
+    """B3's two union paths against the oracle in a fresh process: cap 0 (every
+    union on the global forest, no B3b) and cap 100 (small masks through B3b's
+    shared-memory forest, large ones directly)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, STK_UNITE_CAP=cap)
+    r = subprocess.run([sys.executable, "-c", _UNITE_CAP_SNIPPET, root], capture_output=True, text=True,
+                       timeout=600, env=env)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
 
 
 def test_prune_golden_and_spec(dev, stk, golden, synth):
