@@ -913,7 +913,8 @@ __global__ void __launch_bounds__(RW + RH) k_ccl_borders(Frame f, int32_t* __res
 // global unions.  Measured and dropped: hash-priority CAS linking (2.2x the
 // union cycles), waves of one edge per thread with a flatten after each
 // (1.5x), a converged lockstep walk with per-pair leader election (3x).
-__global__ void __launch_bounds__(kUniteThreads) k_ccl_unite(Frame f, const int32_t* __restrict__ bord, int capn) {
+__global__ void __launch_bounds__(kUniteThreads, 1) k_ccl_unite(Frame f, const int32_t* __restrict__ bord, int capn,
+                                                              int stats) {
     extern __shared__ int sp[];
     const int n = (int)__ldcg(&f.sc->n_lroots);
     if (n > capn) return;  // B3 united them directly
@@ -921,6 +922,20 @@ __global__ void __launch_bounds__(kUniteThreads) k_ccl_unite(Frame f, const int3
     const int2* el = edge_list(f, const_cast<int32_t*>(bord));
     const int tid = threadIdx.x;
     for (int i = tid; i < n; i += kUniteThreads) sp[i] = i;
+    // stats with n <= PF threads' worth: the region roots' sizes and keys
+    // fetched now, so their L2 latency hides behind the unions
+    constexpr int PF = 8;
+    const bool pf = stats && n <= PF * kUniteThreads;
+    uint32_t pc[PF];
+    int pk[PF];
+    if (pf) {
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            const int i = tid + k * kUniteThreads;
+            pc[k] = i < n ? __ldcg(f.cnt + i) : 0u;
+            pk[k] = i < n ? __ldcg(f.roots + i) : 0;
+        }
+    }
     __syncthreads();
     constexpr int EB = 4;
     // a contiguous chunk of the list per thread: the lanes of a warp work on
@@ -936,10 +951,53 @@ __global__ void __launch_bounds__(kUniteThreads) k_ccl_unite(Frame f, const int3
         for (int j = 0; j < EB; ++j) runite(sp, ed[j].x, ed[j].y);
     }
     __syncthreads();
-    for (int i = tid; i < n; i += kUniteThreads) {
-        const int r = rfind(sp, i);
-        if (r != i) f.par[i] = r;
+    // stats (the prune path): the prune's B4 (sizes and minimum raster index
+    // summed / min'ed at the roots) and B5 (root count, size histogram) here,
+    // where the final roots are known, instead of two grid-barrier phases
+    if (pf) {
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            const int i = tid + k * kUniteThreads;
+            const int r = i < n ? rfind(sp, i) : i;
+            if (r != i) {
+                f.par[i] = r;
+                atomicAdd(f.cnt + r, pc[k]);
+                atomicMin(f.roots + r, pk[k]);
+            }
+        }
+    } else {
+        for (int i = tid; i < n; i += kUniteThreads) {
+            const int r = rfind(sp, i);
+            if (r != i) {
+                f.par[i] = r;
+                if (stats) {
+                    atomicAdd(f.cnt + r, __ldcg(f.cnt + i));
+                    atomicMin(f.roots + r, __ldcg(f.roots + i));
+                }
+            }
+        }
     }
+    if (!stats) return;
+    __syncthreads();
+    const unsigned long long B = __ldcg(&f.sc->budget);
+    unsigned nr = 0;
+    for (int i0 = tid; i0 < n; i0 += PF * kUniteThreads) {  // PF roots' sizes in flight at once
+        uint32_t sz[PF];
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            const int i = i0 + k * kUniteThreads;
+            sz[k] = i < n && sp[i] == i ? __ldcg(f.cnt + i) : 0u;  // roots: unchanged since the unions
+        }
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            if (sz[k] == 0) continue;  // non-roots (a root holds >= 1 pixel)
+            ++nr;
+            if (sz[k] <= B + 1) atomicAdd(f.szhist + sz[k], 1u);
+        }
+    }
+    nr = __reduce_add_sync(0xffffffffu, nr);
+    if ((tid & 31) == 0 && nr) atomicAdd(&f.sc->n_roots, nr);
+    if (tid == 0) f.sc->united = 1u;
 }
 
 // 256-thread exclusive block scan (u64) used by the prune select.
@@ -1160,31 +1218,34 @@ __global__ void __launch_bounds__(256) k_prune_fused(Frame f, uint32_t* __restri
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int gt = blockIdx.x * 256 + tid, gs = G * 256;
     const int n = (int)sc->n_lroots;
-    // B4 compress
-    for (int id = gt; id < n; id += gs) {
-        const int r = gfind_ro(f.par, id);
-        if (r != id) {
-            f.par[id] = r;
-            atomicAdd(f.cnt + r, __ldcg(f.cnt + id));
-            atomicMin(f.roots + r, __ldcg(f.roots + id));
-        }
-    }
-    grid_barrier(sc, G);
-    // B5 root stats
     const unsigned long long B = sc->budget;
-    {
-        unsigned nr = 0;
+    // B4, B5: done by B3b unless B3 united on the global forest (grid-uniform)
+    if (!__ldcg(&sc->united)) {
+        // B4 compress
         for (int id = gt; id < n; id += gs) {
-            if (__ldcg(f.par + id) == id) {
-                ++nr;
-                const uint32_t sz = __ldcg(f.cnt + id);
-                if (sz <= B + 1) atomicAdd(f.szhist + sz, 1u);
+            const int r = gfind_ro(f.par, id);
+            if (r != id) {
+                f.par[id] = r;
+                atomicAdd(f.cnt + r, __ldcg(f.cnt + id));
+                atomicMin(f.roots + r, __ldcg(f.roots + id));
             }
         }
-        nr = __reduce_add_sync(0xffffffffu, nr);
-        if (lane == 0 && nr) atomicAdd(&sc->n_roots, nr);
+        grid_barrier(sc, G);
+        // B5 root stats
+        {
+            unsigned nr = 0;
+            for (int id = gt; id < n; id += gs) {
+                if (__ldcg(f.par + id) == id) {
+                    ++nr;
+                    const uint32_t sz = __ldcg(f.cnt + id);
+                    if (sz <= B + 1) atomicAdd(f.szhist + sz, 1u);
+                }
+            }
+            nr = __reduce_add_sync(0xffffffffu, nr);
+            if (lane == 0 && nr) atomicAdd(&sc->n_roots, nr);
+        }
+        grid_barrier(sc, G);
     }
-    grid_barrier(sc, G);
     // B6 select: block sums over sizes 1..B+1, then block 0 finds s*, q
     const long long L = (long long)B + 1;
     const long long per = (L + G - 1) / G;
@@ -1327,7 +1388,7 @@ size_t bord_bytes(int W, int H) {  // the border labels of every region (B2 -> B
 
 // B3 + B3b.  capn: the most region roots B3b's shared-memory forest takes
 // (STK_UNITE_CAP: test / experiment knob; 0 forces the global unions)
-void launch_ccl_borders(const Frame& f, int32_t* bord, cudaStream_t st) {
+void launch_ccl_borders(const Frame& f, int32_t* bord, bool stats, cudaStream_t st) {
     static const int capn = [] {
         const char* e = getenv("STK_UNITE_CAP");
         return e ? atoi(e) : 32768;
@@ -1337,7 +1398,7 @@ void launch_ccl_borders(const Frame& f, int32_t* bord, cudaStream_t st) {
     if (capn > 0) {
         const int smem = capn * (int)sizeof(int);
         cudaFuncSetAttribute(k_ccl_unite, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        k_ccl_unite<<<1, kUniteThreads, smem, st>>>(f, bord, capn);
+        k_ccl_unite<<<1, kUniteThreads, smem, st>>>(f, bord, capn, stats ? 1 : 0);
     }
 }
 
@@ -1347,7 +1408,7 @@ void launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, in
     const int ntiles = ((f.W + CT - 1) / CT) * ((f.H + CT - 1) / CT);
     const int tb = (ntiles + 3) / 4;
     launch_ccl_region(f, rbits, runroot, bord, st);
-    launch_ccl_borders(f, bord, st);
+    launch_ccl_borders(f, bord, true, st);
     cudaMemsetAsync(sbits, 0, (size_t)sbits_words * 4, st);
     {   // B4-B7 in one cooperative launch (co-resident blocks, grid barriers)
         // co-resident blocks per SM depend only on the kernel (thread-safe
@@ -1539,7 +1600,7 @@ void launch_label_components_bits(const Frame& f, const uint8_t* mask, uint32_t*
     const int gb = (int)std::min<long long>((nw + 255) / 256, f.sms * 8);
     k_mask_to_bits<<<gb, 256, 0, st>>>(f, mask, rbits);
     launch_ccl_region(f, rbits, runroot, bord, st);  // B2
-    launch_ccl_borders(f, bord, st);                  // B3, B3b
+    launch_ccl_borders(f, bord, false, st);           // B3, B3b (k_cc_compress aggregates)
     const int ib = f.sms * 4;
     k_cc_compress<<<ib, 256, 0, st>>>(f);
     cudaMemsetAsync(gbits, 0, (size_t)gbits_words * 4, st);
