@@ -9,7 +9,7 @@
 //                   remove, one warp per 30 word-columns x 32 rows, rows
 //                   streamed with a 3-row halo; refined bits + raw/refined
 //                   counts (raw bytes too in full mode).
-//   B2 ccl_region   CTA per 128x128 region, warp per 32x32 tile: run-level
+//   B2 ccl_region   CTA per 256x128 region, warp per 32x32 tile: run-level
 //                   union-find per tile, then the region's inner tile borders
 //                   merged in shared memory; every region component goes to
 //                   the root list with its size and its minimum raster index g
@@ -456,14 +456,15 @@ __device__ __forceinline__ unsigned long long budget_of(const Frame& f) {
 //     its component's g; the region's outer borders record the g of their
 //     pixels for the global merge (B3).
 // region = RGX x RGY tiles (STK_RGX / STK_RGY: experiment knobs; 4 x 2: boundary
-// stage 0.165 ms, 4 x 4: 0.150 ms -- half the borders left for B3)
+// stage 0.165 ms, 4 x 4: 0.150 ms -- half the borders left for B3; with B3b's
+// edge list, 4 x 4: 0.134 ms, 4 x 8: 0.128, 8 x 4: 0.126 -- fewer edges to unite)
 #ifndef STK_RGX
-#define STK_RGX 4
+#define STK_RGX 8
 #endif
 #ifndef STK_RGY
 #define STK_RGY 4
 #endif
-constexpr int RGX = STK_RGX, RGY = STK_RGY, NRW = RGX * RGY;  // 128 x 128-pixel regions
+constexpr int RGX = STK_RGX, RGY = STK_RGY, NRW = RGX * RGY;  // 256 x 128-pixel regions
 constexpr int RW = RGX * CT, RH = RGY * CT;
 constexpr int RBORD = 2 * RW + 2 * RH;             // [top RW][bottom RW][left RH][right RH]
 
@@ -474,7 +475,7 @@ struct RunSmemT {
     uint8_t rstart[CAP], rlen[CAP], rrow[CAP];
     int par[CAP];                  // region node ids after step 1
     int key[CAP];                  // g of tile-local roots, INT_MAX otherwise
-    uint16_t sz[CAP];              // sizes (a region's components hold <= 128 x 128 pixels)
+    uint16_t sz[CAP];              // sizes (a region's components hold <= 256 x 128 pixels)
 };
 
 // sz[i] += v: a 32-bit shared atomic on the u16's word (v and the sums stay
@@ -766,9 +767,10 @@ __device__ __forceinline__ void ccl_region_body(const Frame& f, const uint32_t* 
     }
 }
 
-// B2 first pass: one CTA per region, 224-run tables with u16 sizes (52.8 KB
-// of shared memory per 128x128 region: four CTAs per SM, so the 576 regions of
-// a 4K frame run in one wave; dead-leaves masks peak at 224 runs per tile)
+// B2 first pass: one CTA per region, 224-run tables with u16 sizes (105.6 KB
+// of shared memory per 256x128 region: two CTAs per SM, so the 288 regions of
+// a 4K frame run in one wave; dead-leaves masks peak at 224 runs per tile.
+// 4 x 4 regions with 256-run tables: 45 us, 224-run: 38.7 us)
 __global__ void __launch_bounds__(32 * NRW) k_ccl_region(Frame f, const uint32_t* __restrict__ rbits,
                                                          int32_t* __restrict__ runroot,
                                                          int32_t* __restrict__ bord) {

@@ -161,7 +161,7 @@ def test_components_and_prune_random(dev, stk, port, synth, w, h, pct):
 @pytest.mark.parametrize("case", ["random_1080p", "comb", "frame_mask"])
 def test_components_run_ccl_large(dev, stk, port, synth, case):
     """label_components on the frame path's run CCL (B2 region merge, B3
-    global union, label kernels): large masks crossing many 128x64 regions,
+    global union, label kernels): large masks crossing many 256x128 regions,
     one giant component, and a real frame's refined boundary mask."""
     if case == "random_1080p":
         m = synth.random_mask(1920, 1080, 99, 45)
@@ -305,7 +305,7 @@ def test_prune_many_equal_sizes_partial_class(dev, stk, port):
                                          (129, 65, 4, 45), (700, 140, 5, 22)])
 def test_prune_bitpacked_vs_oracle(dev, stk, port, synth, w, h, seed, pct):
     """prune_components runs the frame path's bit-packed run CCL (region merge
-    across 128x64 regions, global union-find, s*/q select, first-q bitmap scan):
+    across 256x128 regions, global union-find, s*/q select, first-q bitmap scan):
     random masks with many small components, crossing tile and region borders,
     at fractions that cut inside a size class (q > 0) and beyond."""
     m = synth.random_mask(w, h, seed, pct)
