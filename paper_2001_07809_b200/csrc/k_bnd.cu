@@ -468,20 +468,29 @@ constexpr int RGX = STK_RGX, RGY = STK_RGY, NRW = RGX * RGY;  // 256 x 128-pixel
 constexpr int RW = RGX * CT, RH = RGY * CT;
 constexpr int RBORD = 2 * RW + 2 * RH;             // [top RW][bottom RW][left RH][right RH]
 
+// Per-tile run table; the union-find arrays are region-wide and flat (node
+// w * CAP + ridx indexes them directly: no struct-stride address math in the
+// finds -- 14.9 % of B2's instructions went to R[node / CAP].par[node % CAP])
 template <int CAP>
 struct RunSmemT {
     uint32_t rowm[CT], rows[CT];   // row masks, run starts
     int rs[CT + 1];                // first ridx of each row
     uint8_t rstart[CAP], rlen[CAP], rrow[CAP];
-    int par[CAP];                  // region node ids after step 1
-    int key[CAP];                  // g of tile-local roots, INT_MAX otherwise
-    uint16_t sz[CAP];              // sizes (a region's components hold <= 256 x 128 pixels)
 };
 
-// sz[i] += v: a 32-bit shared atomic on the u16's word (v and the sums stay
-// below 2^16, so the low half never carries into the high one)
+// shared memory of a B2 CTA: [NRW tile tables][par][key][sz], the last three
+// NRW * CAP entries each: par = region node ids after step 1, key = g of the
+// tile-local roots (INT_MAX otherwise), sz = sizes (u16: a region's
+// components hold <= 256 x 128 pixels)
 template <int CAP>
-__device__ __forceinline__ void sz_add(uint16_t (&sz)[CAP], int i, unsigned v) {
+constexpr size_t region_smem_bytes() {
+    return NRW * (sizeof(RunSmemT<CAP>) + (size_t)CAP * (2 * sizeof(int) + sizeof(uint16_t)));
+}
+
+// sz[i] += v: a 32-bit shared atomic on the u16's word (v and the sums stay
+// below 2^16, so the low half never carries into the high one; sz is 4-byte
+// aligned)
+__device__ __forceinline__ void sz_add(uint16_t* sz, int i, unsigned v) {
     atomicAdd(reinterpret_cast<unsigned*>(&sz[i & ~1]), v << (16 * (i & 1)));
 }
 
@@ -512,39 +521,6 @@ __device__ __forceinline__ void runite(int* p, int a, int b) {
     }
 }
 
-// region-wide union-find over nodes w * CAP + ridx
-template <int CAP>
-__device__ __forceinline__ int* cpar(RunSmemT<CAP>* R, int node) { return &R[node / CAP].par[node % CAP]; }
-
-template <int CAP>
-__device__ __forceinline__ int cfind(RunSmemT<CAP>* R, int x) {
-    int q = *cpar(R, x);
-    while (q != x) {
-        const int g = *cpar(R, q);
-        if (g != q) *cpar(R, x) = g;
-        x = q;
-        q = g;
-    }
-    return x;
-}
-
-template <int CAP>
-__device__ __forceinline__ void cunite(RunSmemT<CAP>* R, int a, int b) {
-    while (true) {
-        a = cfind(R, a);
-        b = cfind(R, b);
-        if (a == b) return;
-        if (a > b) {
-            const int t = a;
-            a = b;
-            b = t;
-        }
-        const int old = atomicMin(cpar(R, b), a);
-        if (old == b) return;
-        b = old;
-    }
-}
-
 // region node of pixel (row, col) of warp w's tile, -1 when unset
 template <int CAP>
 __device__ __forceinline__ int node_at(const RunSmemT<CAP>* R, int w, int row, int col) {
@@ -560,8 +536,12 @@ __device__ __forceinline__ int node_at(const RunSmemT<CAP>* R, int w, int row, i
 template <int CAP, bool FIRST>
 __device__ __forceinline__ void ccl_region_body(const Frame& f, const uint32_t* __restrict__ rbits,
                                                 int32_t* __restrict__ runroot, int32_t* __restrict__ bord,
-                                                int reg, RunSmemT<CAP>* R) {
+                                                int reg, uint8_t* smraw) {
     using RunSmem = RunSmemT<CAP>;
+    RunSmem* R = reinterpret_cast<RunSmem*>(smraw);
+    int* P = reinterpret_cast<int*>(smraw + NRW * sizeof(RunSmem));  // region-wide, node-indexed
+    int* KY = P + NRW * CAP;
+    uint16_t* SZ = reinterpret_cast<uint16_t*>(KY + NRW * CAP);
     __shared__ int s_ovf;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int TXc = (f.W + CT - 1) / CT, TYc = (f.H + CT - 1) / CT;
@@ -573,6 +553,9 @@ __device__ __forceinline__ void ccl_region_body(const Frame& f, const uint32_t* 
     const int tile = ty * TXc + tx;
     const int x0 = tx * CT, y0 = ty * CT;
     RunSmem& S = R[wid];
+    int* const tp = P + wid * CAP;         // this tile's slices (tile-local ids in step 1)
+    int* const tk = KY + wid * CAP;
+    uint16_t* const tsz = SZ + wid * CAP;
     const uint32_t m = tile_ok && y0 + lane < f.H ? __ldg(rbits + (size_t)(y0 + lane) * f.bits_words + tx) : 0u;
     const uint32_t s = m & ~(m << 1);  // run starts
     const int nr = __popc(s);
@@ -607,8 +590,8 @@ __device__ __forceinline__ void ccl_region_body(const Frame& f, const uint32_t* 
         }
     }
     for (int i = lane; i < nruns; i += 32) {
-        S.par[i] = i;
-        S.sz[i] = 0;
+        tp[i] = i;
+        tsz[i] = 0;
     }
     __syncwarp();
     // 1. unions with the overlapping runs of the row above (8-connectivity).
@@ -640,12 +623,12 @@ __device__ __forceinline__ void ccl_region_body(const Frame& f, const uint32_t* 
     for (int i = lane; i < nruns; i += 32) {
         uint32_t T, mu, su;
         int r;
-        S.par[i] = overlaps(i, T, mu, su, r) ? next_overlap(T, mu, su, r) : i;
+        tp[i] = overlaps(i, T, mu, su, r) ? next_overlap(T, mu, su, r) : i;
     }
     __syncwarp();
 #pragma unroll 1
     for (int round = 0; round < 5; ++round) {
-        for (int i = lane; i < nruns; i += 32) S.par[i] = S.par[S.par[i]];
+        for (int i = lane; i < nruns; i += 32) tp[i] = tp[tp[i]];
         __syncwarp();
     }
     for (int i = lane; i < nruns; i += 32) {
@@ -653,21 +636,21 @@ __device__ __forceinline__ void ccl_region_body(const Frame& f, const uint32_t* 
         int r;
         if (!overlaps(i, T, mu, su, r)) continue;
         next_overlap(T, mu, su, r);  // the first one: linked in (a)
-        while (T) runite(S.par, i, next_overlap(T, mu, su, r));
+        while (T) runite(tp, i, next_overlap(T, mu, su, r));
     }
     __syncwarp();
     // flatten, sizes at the tile-local roots; switch to region node ids
     auto gof = [&](const RunSmem& Q, int ri, int qx0, int qy0) { return (qy0 + Q.rrow[ri]) * f.W + qx0 + Q.rstart[ri]; };
     for (int i = lane; i < nruns; i += 32) {
-        const int rt = rfind(S.par, i);
-        S.par[i] = rt;
-        sz_add(S.sz, rt, S.rlen[i]);
+        const int rt = rfind(tp, i);
+        tp[i] = rt;
+        sz_add(tsz, rt, S.rlen[i]);
     }
     __syncwarp();
     for (int i = lane; i < nruns; i += 32) {
-        const int rt = S.par[i];
-        S.key[i] = rt == i ? gof(S, i, x0, y0) : 0x7fffffff;
-        S.par[i] = wid * CAP + rt;
+        const int rt = tp[i];
+        tk[i] = rt == i ? gof(S, i, x0, y0) : 0x7fffffff;
+        tp[i] = wid * CAP + rt;
     }
     __syncthreads();
     // 2. inner borders of the region (the tile above / left, and the two
@@ -680,10 +663,10 @@ __device__ __forceinline__ void ccl_region_body(const Frame& f, const uint32_t* 
         int u1 = node_at(R, wa, 31, lane);
         int u2 = lane < 31 ? node_at(R, wa, 31, lane + 1) : (tc + 1 < RGX ? node_at(R, wa + 1, 31, 0) : -1);
         if (a >= 0) {
-            const bool cont = lane > 0 && ap >= 0 && cfind(R, ap) == cfind(R, a);
-            if (!cont && u0 >= 0) cunite(R, a, u0);
-            if (!cont && u1 >= 0) cunite(R, a, u1);
-            if (u2 >= 0) cunite(R, a, u2);
+            const bool cont = lane > 0 && ap >= 0 && rfind(P, ap) == rfind(P, a);
+            if (!cont && u0 >= 0) runite(P, a, u0);
+            if (!cont && u1 >= 0) runite(P, a, u1);
+            if (u2 >= 0) runite(P, a, u2);
         }
     }
     if (tc > 0) {
@@ -693,20 +676,19 @@ __device__ __forceinline__ void ccl_region_body(const Frame& f, const uint32_t* 
             const int l0 = lane > 0 ? node_at(R, wl, lane - 1, 31) : -1;
             const int l1 = node_at(R, wl, lane, 31);
             const int l2 = lane < 31 ? node_at(R, wl, lane + 1, 31) : -1;
-            if (l0 >= 0) cunite(R, a, l0);
-            if (l1 >= 0) cunite(R, a, l1);
-            if (l2 >= 0) cunite(R, a, l2);
+            if (l0 >= 0) runite(P, a, l0);
+            if (l1 >= 0) runite(P, a, l1);
+            if (l2 >= 0) runite(P, a, l2);
         }
     }
     __syncthreads();
     // region roots: key = min g, size = sum over their tile components
     for (int i = lane; i < nruns; i += 32) {
         const int self = wid * CAP + i;
-        const int rt = cfind(R, self);
-        if (S.key[i] != 0x7fffffff && rt != self) {  // a tile root merged into another
-            RunSmem& Q = R[rt / CAP];
-            sz_add(Q.sz, rt % CAP, S.sz[i]);
-            atomicMin(&Q.key[rt % CAP], S.key[i]);
+        const int rt = rfind(P, self);
+        if (tk[i] != 0x7fffffff && rt != self) {  // a tile root merged into another
+            sz_add(SZ, rt, tsz[i]);
+            atomicMin(&KY[rt], tk[i]);
         }
     }
     __syncthreads();
@@ -714,7 +696,7 @@ __device__ __forceinline__ void ccl_region_body(const Frame& f, const uint32_t* 
     int nroots = 0;
     for (int i = lane; i < nruns; i += 32) {
         const int self = wid * CAP + i;
-        nroots += cfind(R, self) == self;
+        nroots += rfind(P, self) == self;
     }
     int incl = nroots;
 #pragma unroll
@@ -731,18 +713,18 @@ __device__ __forceinline__ void ccl_region_body(const Frame& f, const uint32_t* 
     // f.par / f.cnt / f.roots, small enough to stay in L2)
     for (int i = lane; i < nruns; i += 32) {
         const int self = wid * CAP + i;
-        if (cfind(R, self) == self) {
+        if (rfind(P, self) == self) {
             const int id = (int)pos++;
             f.par[id] = id;
-            f.cnt[id] = (uint32_t)S.sz[i];
-            f.roots[id] = S.key[i];
-            S.key[i] = id;
+            f.cnt[id] = (uint32_t)tsz[i];
+            f.roots[id] = tk[i];
+            tk[i] = id;
         }
     }
     __syncthreads();
     auto gnode = [&](int node) {
-        const int rt = cfind(R, node);
-        return R[rt / CAP].key[rt % CAP];
+        const int rt = rfind(P, node);
+        return KY[rt];
     };
     if (tile_ok) {
         int32_t* rr = runroot + (size_t)tile * kRunCap;
@@ -783,7 +765,7 @@ __global__ void __launch_bounds__(32 * NRW) k_ccl_region(Frame f, const uint32_t
         if (gt == 0) f.sc->budget = B;
     }
     ccl_region_body<kRunCapFast, true>(f, rbits, runroot, bord, blockIdx.x,
-                                       reinterpret_cast<RunSmemT<kRunCapFast>*>(smraw));
+                                       smraw);
 }
 
 // B2 overflow pass: the regions the first pass listed (none on typical
@@ -795,13 +777,13 @@ __global__ void __launch_bounds__(32 * NRW) k_ccl_region_ovf(Frame f, const uint
     const unsigned n = *(volatile unsigned*)&f.sc->n_ovf;
     for (unsigned i = blockIdx.x; i < n; i += gridDim.x)
         ccl_region_body<kRunCap, false>(f, rbits, runroot, bord, (int)f.list[i],
-                                        reinterpret_cast<RunSmemT<kRunCap>*>(smraw));
+                                        smraw);
 }
 
 void launch_ccl_region(const Frame& f, const uint32_t* rbits, int32_t* runroot, int32_t* bord,
                        cudaStream_t st) {
     const int nreg = ((f.W + RW - 1) / RW) * ((f.H + RH - 1) / RH);
-    const size_t s1 = sizeof(RunSmemT<kRunCapFast>) * NRW, s2 = sizeof(RunSmemT<kRunCap>) * NRW;
+    const size_t s1 = region_smem_bytes<kRunCapFast>(), s2 = region_smem_bytes<kRunCap>();
     cudaFuncSetAttribute(k_ccl_region, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
     cudaFuncSetAttribute(k_ccl_region_ovf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
     k_ccl_region<<<nreg, 32 * NRW, s1, st>>>(f, rbits, runroot, bord);
