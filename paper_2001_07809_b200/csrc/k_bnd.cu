@@ -787,8 +787,11 @@ void launch_ccl_region(const Frame& f, const uint32_t* rbits, int32_t* runroot, 
     cudaFuncSetAttribute(k_ccl_region, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
     cudaFuncSetAttribute(k_ccl_region_ovf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
     k_ccl_region<<<nreg, 32 * NRW, s1, st>>>(f, rbits, runroot, bord);
-    // a small grid: the pass is empty on typical masks (its launch is all it costs)
-    k_ccl_region_ovf<<<std::min(nreg, 32), 32 * NRW, s2, st>>>(f, rbits, runroot, bord);
+    // a small grid: the pass is empty on typical masks (its launch is all it
+    // costs), and each of its CTAs needs an SM's whole shared memory, so it
+    // waits for SMs to drain while other frames run: 2 CTAs instead of 32,
+    // +0.25 % frames/s (3 alternating runs)
+    k_ccl_region_ovf<<<std::min(nreg, 2), 32 * NRW, s2, st>>>(f, rbits, runroot, bord);
 }
 
 // ------------------------------------------------------------------ B3 ----
