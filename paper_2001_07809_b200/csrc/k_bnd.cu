@@ -1375,7 +1375,7 @@ size_t bord_bytes(int W, int H) {  // the border labels of every region (B2 -> B
 
 // B3 + B3b.  capn: the most region roots B3b's shared-memory forest takes
 // (STK_UNITE_CAP: test / experiment knob; 0 forces the global unions)
-void launch_ccl_borders(const Frame& f, int32_t* bord, bool stats, cudaStream_t st) {
+int launch_ccl_borders(const Frame& f, int32_t* bord, bool stats, cudaStream_t st) {  // kernels launched
     static const int capn = [] {
         const char* e = getenv("STK_UNITE_CAP");
         return e ? atoi(e) : 32768;
@@ -1386,16 +1386,18 @@ void launch_ccl_borders(const Frame& f, int32_t* bord, bool stats, cudaStream_t 
         const int smem = capn * (int)sizeof(int);
         cudaFuncSetAttribute(k_ccl_unite, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         k_ccl_unite<<<1, kUniteThreads, smem, st>>>(f, bord, capn, stats ? 1 : 0);
+        return 2;
     }
+    return 1;
 }
 
-void launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
+int launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
                            uint32_t* sbits, int sbits_words, bool anchors, cudaStream_t st) {
     // B2 - B8
     const int ntiles = ((f.W + CT - 1) / CT) * ((f.H + CT - 1) / CT);
     const int tb = (ntiles + 3) / 4;
-    launch_ccl_region(f, rbits, runroot, bord, st);
-    launch_ccl_borders(f, bord, true, st);
+    launch_ccl_region(f, rbits, runroot, bord, st);  // 2 kernels
+    const int nb = launch_ccl_borders(f, bord, true, st);
     cudaMemsetAsync(sbits, 0, (size_t)sbits_words * 4, st);
     {   // B4-B7 in one cooperative launch (co-resident blocks, grid barriers)
         // co-resident blocks per SM depend only on the kernel (thread-safe
@@ -1428,6 +1430,7 @@ void launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, in
         cudaLaunchCooperativeKernel((const void*)k_prune_fused, dim3(g_blocks), dim3(256), args, 0, st);
     }
     k_apply_runs<<<tb, 128, 0, st>>>(f, rbits, runroot, anchors ? 1 : 0);
+    return 2 + nb + 2;  // B2 (+ overflow pass), B3 (+ B3b), B4-B7, B8
 }
 
 void launch_prune_mask_bits(const Frame& f, const uint8_t* mask, uint32_t* rbits, int32_t* runroot,
@@ -1438,10 +1441,10 @@ void launch_prune_mask_bits(const Frame& f, const uint8_t* mask, uint32_t* rbits
     launch_ccl_prune_bits(f, rbits, runroot, bord, sbits, sbits_words, false, st);
 }
 
-void launch_boundary_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
-                          uint32_t* sbits, int sbits_words, bool anchors, bool want_list,
-                          cudaStream_t st) {
-    if (f.N == 0) return;
+int launch_boundary_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
+                         uint32_t* sbits, int sbits_words, bool anchors, bool want_list,
+                         cudaStream_t st) {
+    if (f.N == 0) return 0;
     // B1
     const int BW = (f.W + 31) / 32;
     const int strips = (BW + MB_WPW - 1) / MB_WPW, bands = (f.H + MB_ROWS - 1) / MB_ROWS;
@@ -1456,8 +1459,12 @@ void launch_boundary_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int
         case 4: k_morph_bits<4, MB_FRAME><<<gb, 128, 0, st>>>(f, rbits, nullptr, 0); break;
         default: k_morph_bits<8, MB_FRAME><<<gb, 128, 0, st>>>(f, rbits, nullptr, 0); break;
     }
-    launch_ccl_prune_bits(f, rbits, runroot, bord, sbits, sbits_words, anchors, st);
-    if (want_list) k_list_bits<<<f.n_chunks, 128, 0, st>>>(f);
+    int n = 1 + launch_ccl_prune_bits(f, rbits, runroot, bord, sbits, sbits_words, anchors, st);
+    if (want_list) {
+        k_list_bits<<<f.n_chunks, 128, 0, st>>>(f);
+        ++n;
+    }
+    return n;
 }
 
 // Stage entries detect_boundaries / morph_fill / morph_remove on B1 (the frame

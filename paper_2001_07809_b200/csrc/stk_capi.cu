@@ -582,8 +582,8 @@ int enqueue_kernels(stk_ctx* ctx, Slot& s, const Frame& f, const BlurParams* bp,
     // sparse starts all Unknown; the SAD kernels write the matchable pixels
     cudaMemsetAsync(f.sparse, 0xff, (size_t)f.N * sizeof(int16_t), st);
     const bool want_list = sad_uses_list(f, ctx->sad_kernel);
-    launch_boundary_bits(f, s.rbits, s.runroot, s.bord, s.sbits, s.sbits_words, true, want_list, st);
-    n += 6 + (want_list ? 1 : 0);  // B1, B2 (+ its overflow pass), B3, B4-B7 (cooperative), B8 (+ list)
+    // B1, B2 (+ its overflow pass), B3 (+ B3b), B4-B7 (cooperative), B8 (+ list)
+    n += launch_boundary_bits(f, s.rbits, s.runroot, s.bord, s.sbits, s.sbits_words, true, want_list, st);
     rec(3);
     if (f.W >= f.window && f.H >= f.window) {
         launch_sad(f, ctx->sad_kernel, &s.tm_sadL.map, &s.tm_sadR.map, st);

@@ -145,11 +145,12 @@ enum MorphMode { MORPH_DETECT16 = 1, MORPH_FILL = 2, MORPH_REMOVE = 3 };
 // Bit-packed boundary stage of the frame path (k_bnd.cu): morphology from
 // gray, run-based CCL, prune, anchors, matchable bits and frame counts
 // (+ raw / pruned / anchored bytes in full mode; + the SAD list if asked).
-void launch_boundary_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
+// Returns the number of kernels launched.
+int launch_boundary_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
                           uint32_t* sbits, int sbits_words, bool anchors, bool want_list,
                           cudaStream_t st);
-// B2-B8 alone on refined bits already in rbits (refined_count set)
-void launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
+// B2-B8 alone on refined bits already in rbits (refined_count set); returns the kernel count
+int launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int32_t* bord,
                            uint32_t* sbits, int sbits_words, bool anchors, cudaStream_t st);
 // stage entries detect_boundaries / morph_fill / morph_remove on B1
 void launch_morph_stage_bits(const Frame& f, int mode, const uint8_t* src, uint32_t* rbits,

@@ -11,7 +11,7 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 tail -1 gpurun_out/bench_ref.log | cut -c1-300
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --pool 2 > gpurun_out/ncu_launch.log 2>&1; echo "ncu launch exit $?"
 python scripts/prof_frame.py --config C --frames 2 > gpurun_out/plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -s 12 -c 12 -f -o gpurun_out/prof_C \
+timeout 900 ncu --set full --clock-control none --import-source on -s 13 -c 13 -f -o gpurun_out/prof_C \
   python scripts/prof_frame.py --config C --frames 2 > gpurun_out/ncu_full.log 2>&1
 echo "ncu full exit $?"
 ncu -i gpurun_out/prof_C.ncu-rep --page source --csv --print-source sass -k regex:k_sad_ws > gpurun_out/sad_source.csv 2>/dev/null

@@ -9,7 +9,7 @@ cp $o/launches.csv $p/${tag}_launches_C.csv
 python scripts/launches_summary.py $o/launches.csv > $p/${tag}_launches_C_summary.txt
 python scripts/ncu_to_json.py $o/prof_C.ncu-rep $p/${tag}_ncu_kernels.json
 {
-  echo "# ncu --set full --clock-control none --import-source on, one B200, the 12 launches of the second"
+  echo "# ncu --set full --clock-control none --import-source on, one B200, the 13 launches of the second"
   echo "# 4096x2304 G2 frame (scripts/gpu_round.sh: python scripts/prof_frame.py --config C --frames 2)."
   echo "# Per-launch times are cold-cache and serialised; bench.py's CUDA-event stage times are the numbers"
   echo "# reported.  Per-kernel metrics: ${tag}_ncu_kernels.json; launch list: ${tag}_launches_C.csv."
