@@ -775,9 +775,10 @@ __global__ void __launch_bounds__(32 * NRW) k_ccl_region_ovf(Frame f, const uint
                                                              int32_t* __restrict__ bord) {
     extern __shared__ __align__(16) uint8_t smraw[];
     const unsigned n = *(volatile unsigned*)&f.sc->n_ovf;
-    for (unsigned i = blockIdx.x; i < n; i += gridDim.x)
-        ccl_region_body<kRunCap, false>(f, rbits, runroot, bord, (int)f.list[i],
-                                        smraw);
+    for (unsigned i = blockIdx.x; i < n; i += gridDim.x) {
+        ccl_region_body<kRunCap, false>(f, rbits, runroot, bord, (int)f.list[i], smraw);
+        __syncthreads();  // the next region reuses the tables the last phase still reads
+    }
 }
 
 void launch_ccl_region(const Frame& f, const uint32_t* rbits, int32_t* runroot, int32_t* bord,

@@ -198,7 +198,7 @@ def test_components_and_prune_repeated_large(dev, stk, port, synth):
 
 
 def test_components_overflow_tiles(dev, stk, port, synth):
-    """B2 keeps 256 runs per 32x32 tile in shared memory; regions with a
+    """B2 keeps 224 runs per 32x32 tile in shared memory; regions with a
     denser tile go through the 512-run overflow pass.  Checkerboard rows (16
     runs per row: every tile overflows), a mask where only some regions
     overflow, and a dense random mask: labels, sizes, by_size and the pruned
@@ -217,6 +217,24 @@ def test_components_overflow_tiles(dev, stk, port, synth):
         eq(t.by_size, bys)
         for frac in (0.0, 0.04, 0.3):
             eq(stk.prune_components(m, frac, device=dev), port.prune(m, frac))
+
+
+def test_components_overflow_pass_loops(dev, stk, port):
+    """The overflow pass runs on two CTAs, so each loops over many listed
+    regions reusing its shared-memory tables: a 1536x768 checkerboard-row mask
+    (every one of its 36 regions overflows), three times."""
+    W, H = 1536, 768
+    yy, xx = np.mgrid[0:H, 0:W]
+    m = (((xx + (yy // 3)) % 2) == 0).astype(np.uint8)
+    m[::7, :] = 1                                       # long runs joining the columns
+    lab, sz, bys = port.label_components(m)
+    pr = port.prune(m, 0.04)
+    for _ in range(3):
+        t = stk.label_components(m, device=dev)
+        eq(t.labels, lab)
+        eq(t.sizes, sz)
+        eq(t.by_size, bys)
+        eq(stk.prune_components(m, 0.04, device=dev), pr)
 
 
 def test_components_many_region_roots(dev, stk, port):
