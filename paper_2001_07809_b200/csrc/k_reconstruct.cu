@@ -739,7 +739,8 @@ __global__ void __launch_bounds__(P5C * P5S, 2) k_peek_cols6(Frame f, const int1
 // and its per-pixel rule, with lane masks by sign replication and LOP3
 // selects -- one instruction per pixel pair where v1 spends one per pixel.
 __global__ void __launch_bounds__(1024) k_fill_rows16p(Frame f, const int16_t* __restrict__ in,
-                                                       int16_t* __restrict__ out) {
+                                                       int16_t* __restrict__ out,
+                                                       const uint32_t* __restrict__ mbits) {
     __shared__ uint32_t wl[32], wf[32];
     const unsigned full = 0xffffffffu;
     const int W = f.W, y0 = 2 * blockIdx.x, tid = threadIdx.x;
@@ -765,6 +766,18 @@ __global__ void __launch_bounds__(1024) k_fill_rows16p(Frame f, const int16_t* _
         for (int i = 0; i < 8; ++i) {
             P[2 * i] = __byte_perm(a[i], b[i], 0x5410);      // (row y px 2i, row y+1 px 2i)
             P[2 * i + 1] = __byte_perm(a[i], b[i], 0x7632);  // (.. px 2i+1 ..)
+        }
+        // frame path: the SAD writes only the matchable pixels (mbits) and
+        // sparse is not pre-set, so every other pixel reads as unknown (-1)
+        if (mbits) {
+            uint32_t ma = 0, mb = 0;
+            if (act) {
+                ma = (__ldg(mbits + (size_t)y0 * f.bits_words + (x0 >> 5)) >> (x0 & 31)) & 0xffffu;
+                if (two) mb = (__ldg(mbits + (size_t)(y0 + 1) * f.bits_words + (x0 >> 5)) >> (x0 & 31)) & 0xffffu;
+            }
+            const uint32_t keep = ma | (mb << 16);  // bit j: row y px j; bit 16 + j: row y+1 px j
+#pragma unroll
+            for (int j = 0; j < 16; ++j) P[j] |= ~((((keep >> j) & 0x10001u)) * 0xffffu);
         }
     }
     auto pick = [](uint32_t cur, uint32_t cand) {  // per lane: cur if known, else cand
@@ -833,11 +846,13 @@ __global__ void __launch_bounds__(1024) k_fill_rows16p(Frame f, const int16_t* _
 
 }  // namespace
 
-void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStream_t st) {
+bool fill_rows_masks(int W) { return W % 16 == 0 && W <= 16384; }
+
+void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStream_t st, const uint32_t* mbits) {
     if (f.N == 0) return;
-    if (f.W % 16 == 0 && f.W <= 16384) {
+    if (fill_rows_masks(f.W)) {
         const int nt = ((f.W / 16) + 31) / 32 * 32;
-        k_fill_rows16p<<<(f.H + 1) / 2, nt, 0, st>>>(f, in, out);
+        k_fill_rows16p<<<(f.H + 1) / 2, nt, 0, st>>>(f, in, out, mbits);
         return;
     }
     const size_t sm = (size_t)f.W * sizeof(int16_t);

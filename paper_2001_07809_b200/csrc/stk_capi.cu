@@ -579,8 +579,11 @@ int enqueue_kernels(stk_ctx* ctx, Slot& s, const Frame& f, const BlurParams* bp,
         ++n;
     }
     rec(2);
-    // sparse starts all Unknown; the SAD kernels write the matchable pixels
-    cudaMemsetAsync(f.sparse, 0xff, (size_t)f.N * sizeof(int16_t), st);
+    // sparse starts all Unknown; the SAD kernels write the matchable pixels.
+    // Lean frames skip the 2N-byte preset: the row fill reads the matchable
+    // bits and takes every other pixel as unknown (full mode copies sparse out)
+    const bool fill_masks = !f.full && fill_rows_masks(f.W);
+    if (!fill_masks) cudaMemsetAsync(f.sparse, 0xff, (size_t)f.N * sizeof(int16_t), st);
     const bool want_list = sad_uses_list(f, ctx->sad_kernel);
     // B1, B2 (+ its overflow pass), B3 (+ B3b), B4-B7 (cooperative), B8 (+ list)
     n += launch_boundary_bits(f, s.rbits, s.runroot, s.bord, s.sbits, s.sbits_words, true, want_list, st);
@@ -590,7 +593,7 @@ int enqueue_kernels(stk_ctx* ctx, Slot& s, const Frame& f, const BlurParams* bp,
         ++n;
     }
     rec(4);
-    launch_fill_rows(f, f.sparse, f.rowf, st);
+    launch_fill_rows(f, f.sparse, f.rowf, st, fill_masks ? f.mbits : nullptr);
     ++n;
     rec(5);
     launch_peek_cols(f, f.rowf, f.dense, nullptr, st);

@@ -188,7 +188,11 @@ bool launch_sad_strip(const Frame& f, cudaStream_t st, bool dry = false);
 bool launch_sad_ws(const Frame& f, cudaStream_t st, bool dry = false);
 void launch_sad(const Frame& f, int kernel, const CUtensorMap* tmL, const CUtensorMap* tmR,
                 cudaStream_t st);
-void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStream_t st);
+// mbits (frame path, k_fill_rows16p only): pixels outside it read as unknown,
+// so sparse needs no -1 preset; fill_rows_masks(W) says whether it applies
+void launch_fill_rows(const Frame& f, const int16_t* in, int16_t* out, cudaStream_t st,
+                      const uint32_t* mbits = nullptr);
+bool fill_rows_masks(int W);
 void launch_peek_cols(const Frame& f, const int16_t* in, int16_t* out, int16_t* seg_scratch,
                       cudaStream_t st);
 size_t peek_scratch_bytes(int W, int H);

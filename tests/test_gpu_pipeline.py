@@ -171,6 +171,18 @@ def test_pipeline_determinism_and_modes(dev, stk, synth):
     lean = stk.run_depth_pipeline(l, r, stk.PipelineConfig(k=6, window=11, max_disparity=32),
                                   full=False, device=dev)
     eq(lean.dense, outs[0][0], "lean mode")
+    # lean frames do not preset sparse (the row fill masks with the matchable
+    # bits): a lean frame after other frames left their disparities in the
+    # slot's sparse plane still equals the full-mode result
+    for other in (6, 7):
+        l2, r2 = synth.dead_leaves(640, 480, 32, frame=other)
+        cfg2 = stk.PipelineConfig(k=6, window=11, max_disparity=32)
+        full2 = stk.run_depth_pipeline(l2, r2, cfg2, device=dev)
+        stk.run_depth_pipeline(l2, r2, cfg2, full=False, device=dev)
+        lean = stk.run_depth_pipeline(l, r, stk.PipelineConfig(k=6, window=11, max_disparity=32),
+                                      full=False, device=dev)
+        eq(lean.dense, outs[0][0], "lean mode after other frames")
+        eq(stk.run_depth_pipeline(l2, r2, cfg2, full=False, device=dev).dense, full2.dense, "lean, other")
 
 
 def test_pipeline_stage_times(dev, stk, synth):
