@@ -813,10 +813,13 @@ __device__ __forceinline__ int2* edge_list(const Frame& f, int32_t* bord) {
     return reinterpret_cast<int2*>(bord + (size_t)nreg * RBORD);
 }
 
-__global__ void __launch_bounds__(RW + RH) k_ccl_borders(Frame f, int32_t* __restrict__ bord, int capn) {
+__global__ void __launch_bounds__(RW + RH) k_ccl_borders(Frame f, int32_t* __restrict__ bord, int capn,
+                                                        uint32_t* __restrict__ sbits, int sbits_words) {
     __shared__ int s_wsum[(RW + RH) / 32];
     __shared__ unsigned s_base;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    // the prune's size-s* bitmap is cleared here (no memset node in the chain)
+    for (int i = blockIdx.x * (RW + RH) + t; i < sbits_words; i += gridDim.x * (RW + RH)) sbits[i] = 0u;
     const bool direct = (int)__ldcg(&f.sc->n_lroots) > capn;  // grid-uniform
     const int RXc = (f.W + RW - 1) / RW;
     const int reg = blockIdx.x;
@@ -1376,13 +1379,15 @@ size_t bord_bytes(int W, int H) {  // the border labels of every region (B2 -> B
 
 // B3 + B3b.  capn: the most region roots B3b's shared-memory forest takes
 // (STK_UNITE_CAP: test / experiment knob; 0 forces the global unions)
-int launch_ccl_borders(const Frame& f, int32_t* bord, bool stats, cudaStream_t st) {  // kernels launched
+// sbits (prune path): cleared by B3 for B4-B7
+int launch_ccl_borders(const Frame& f, int32_t* bord, bool stats, uint32_t* sbits, int sbits_words,
+                       cudaStream_t st) {  // kernels launched
     static const int capn = [] {
         const char* e = getenv("STK_UNITE_CAP");
         return e ? atoi(e) : 32768;
     }();
     const int nreg = ((f.W + RW - 1) / RW) * ((f.H + RH - 1) / RH);
-    k_ccl_borders<<<nreg, RW + RH, 0, st>>>(f, bord, capn);
+    k_ccl_borders<<<nreg, RW + RH, 0, st>>>(f, bord, capn, sbits, sbits ? sbits_words : 0);
     if (capn > 0) {
         const int smem = capn * (int)sizeof(int);
         cudaFuncSetAttribute(k_ccl_unite, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1398,8 +1403,7 @@ int launch_ccl_prune_bits(const Frame& f, uint32_t* rbits, int32_t* runroot, int
     const int ntiles = ((f.W + CT - 1) / CT) * ((f.H + CT - 1) / CT);
     const int tb = (ntiles + 3) / 4;
     launch_ccl_region(f, rbits, runroot, bord, st);  // 2 kernels
-    const int nb = launch_ccl_borders(f, bord, true, st);
-    cudaMemsetAsync(sbits, 0, (size_t)sbits_words * 4, st);
+    const int nb = launch_ccl_borders(f, bord, true, sbits, sbits_words, st);
     {   // B4-B7 in one cooperative launch (co-resident blocks, grid barriers)
         // co-resident blocks per SM depend only on the kernel (thread-safe
         // static init); the grid follows the context's device SM count
@@ -1595,7 +1599,7 @@ void launch_label_components_bits(const Frame& f, const uint8_t* mask, uint32_t*
     const int gb = (int)std::min<long long>((nw + 255) / 256, f.sms * 8);
     k_mask_to_bits<<<gb, 256, 0, st>>>(f, mask, rbits);
     launch_ccl_region(f, rbits, runroot, bord, st);  // B2
-    launch_ccl_borders(f, bord, false, st);           // B3, B3b (k_cc_compress aggregates)
+    launch_ccl_borders(f, bord, false, nullptr, 0, st);  // B3, B3b (k_cc_compress aggregates)
     const int ib = f.sms * 4;
     k_cc_compress<<<ib, 256, 0, st>>>(f);
     cudaMemsetAsync(gbits, 0, (size_t)gbits_words * 4, st);
