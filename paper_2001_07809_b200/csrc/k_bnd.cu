@@ -1016,8 +1016,10 @@ __global__ void __launch_bounds__(kUniteThreads, 1) k_ccl_unite(Frame f, const i
     __syncthreads();
     const unsigned long long B = __ldcg(&f.sc->budget);
     unsigned nr = 0;
+    uint32_t sz[PF];  // with pf: the sizes of this thread's roots (0: not a root)
+#pragma unroll
+    for (int k = 0; k < PF; ++k) sz[k] = 0u;
     for (int i0 = tid; i0 < n; i0 += PF * kUniteThreads) {  // PF roots' sizes in flight at once
-        uint32_t sz[PF];
 #pragma unroll
         for (int k = 0; k < PF; ++k) {
             const int i = i0 + k * kUniteThreads;
@@ -1033,6 +1035,102 @@ __global__ void __launch_bounds__(kUniteThreads, 1) k_ccl_unite(Frame f, const i
     nr = __reduce_add_sync(0xffffffffu, nr);
     if ((tid & 31) == 0 && nr) atomicAdd(&f.sc->n_roots, nr);
     if (tid == 0) f.sc->united = 1u;
+    // B6 + B7 here too when s* <= SB and at most LCAP components have size s*
+    // (every frame-path mask seen): the cooperative prune then has nothing
+    // left and returns at once.  Same rule as its phases: s* = the smallest
+    // size whose class-cumulative pixel count CS(s*) exceeds B (B + 2 when
+    // CS(B + 1) <= B), q = (B - CS(s* - 1)) / s*; sizes < s* removed and the
+    // q size-s* components with the smallest raster keys.
+    constexpr int SB = 4096, LCAP = 2048;
+    if (!pf || n + SB + 2 * LCAP > capn) return;  // block-uniform
+    int* const hist = sp + n;  // hist[s - 1], s = 1..SB
+    int* const lkey = hist + SB;
+    int* const lid = lkey + LCAP;
+    __shared__ unsigned long long s_wtot[kUniteThreads / 32];
+    __shared__ unsigned long long s_q;
+    __shared__ int s_star, s_cnt;
+    const long long L = min((long long)B + 1, (long long)SB);
+    for (int i = tid; i < SB; i += kUniteThreads) hist[i] = 0;
+    if (tid == 0) {
+        s_star = -1;
+        s_cnt = 0;
+        s_q = 0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < PF; ++k)
+        if (sz[k] != 0 && (long long)sz[k] <= L) atomicAdd(&hist[sz[k] - 1], 1);
+    __syncthreads();
+    static_assert(SB == 4 * kUniteThreads, "four bins per thread");
+    unsigned long long v[4], tsum = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const long long sv = 4 * tid + j + 1;
+        v[j] = sv <= L ? (unsigned long long)sv * (unsigned)hist[sv - 1] : 0ull;
+        tsum += v[j];
+    }
+    {   // exclusive block scan of tsum
+        const int lane = tid & 31, wid = tid >> 5;
+        unsigned long long x = tsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_wtot[wid] = x;
+        __syncthreads();
+        unsigned long long off = 0;
+        for (int w = 0; w < wid; ++w) off += s_wtot[w];
+        unsigned long long cs = off + x - tsum;  // CS(4 tid)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (cs <= B && cs + v[j] > B) {  // the first crossing (CS is non-decreasing)
+                s_star = 4 * tid + j + 1;
+                s_q = (B - cs) / (unsigned long long)(4 * tid + j + 1);
+            }
+            cs += v[j];
+        }
+    }
+    __syncthreads();
+    long long sst = s_star;
+    const unsigned long long q = s_q;
+    if (sst < 0) {
+        if (L < (long long)B + 1) return;  // s* > SB: the cooperative prune decides
+        sst = (long long)B + 2;             // CS(B + 1) <= B: every size <= B + 1 goes
+    }
+    // the size-s* class (q > 0): listed first, so an over-long list falls back
+    // before anything is written
+    if (q > 0) {
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            if (sz[k] != sst) continue;
+            const int i = tid + k * kUniteThreads;
+            const int at = atomicAdd(&s_cnt, 1);
+            if (at < LCAP) {
+                lkey[at] = __ldcg(f.roots + i);
+                lid[at] = i;
+            }
+        }
+        __syncthreads();
+        if (s_cnt > LCAP) return;  // block-uniform
+    }
+#pragma unroll
+    for (int k = 0; k < PF; ++k)
+        if (sz[k] != 0 && (long long)sz[k] < sst) f.cnt[tid + k * kUniteThreads] = sz[k] | kRemoved;
+    if (q > 0) {
+        const int c = s_cnt;
+        for (int e = tid; e < c; e += kUniteThreads) {  // rank by key (keys are distinct raster indices)
+            const int ke = lkey[e];
+            int r = 0;
+            for (int j = 0; j < c; ++j) r += lkey[j] < ke;
+            if ((unsigned long long)r < q) f.cnt[lid[e]] = (uint32_t)sst | kRemoved;
+        }
+    }
+    if (tid == 0) {
+        f.sc->s_star = (unsigned long long)sst;
+        f.sc->q = q;
+        f.sc->pruned = 1u;
+    }
 }
 
 // 256-thread exclusive block scan (u64) used by the prune select.
@@ -1251,6 +1349,7 @@ __global__ void __launch_bounds__(256) k_prune_fused(Frame f, uint32_t* __restri
     __shared__ uint32_t s_wsum[8];
     pdl_wait();
     DevScalars* sc = f.sc;
+    if (__ldcg(&sc->pruned)) return;  // grid-uniform: B3b did B6 + B7
     const unsigned G = gridDim.x;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int gt = blockIdx.x * 256 + tid, gs = G * 256;

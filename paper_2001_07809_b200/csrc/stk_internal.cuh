@@ -52,7 +52,7 @@ struct DevScalars {
     unsigned int gbar_gen;
     unsigned int n_edges;              // B3 -> B3b border edge list length
     unsigned int united;               // 1: B3b did the prune's compress + root stats (B4, B5)
-    unsigned int pad3;
+    unsigned int pruned;               // 1: B3b also did the prune's select + classes (B6, B7)
     unsigned long long psel[128];      // prune select: per-block pixel sums
     unsigned long long gsum[512];      // cooperative prune: per-block pixel sums
     unsigned int gcnt[512];            // cooperative prune: per-block size-s* root counts

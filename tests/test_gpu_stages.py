@@ -319,6 +319,27 @@ def test_prune_many_equal_sizes_partial_class(dev, stk, port):
         eq(stk.prune_components(m, frac, device=dev), port.prune(m, frac))
 
 
+def test_prune_select_fallbacks(dev, stk, port):
+    """B3b does the prune's s*/q select and size classes itself when s* <= 4096
+    and at most 2048 components have size s*; otherwise the cooperative prune
+    does.  Large blobs only (s* beyond 4096 at high fractions), 3600 equal
+    singletons (a size-s* class too long for B3b's list when q > 0), and the
+    in-CTA cases next to them."""
+    blobs = np.zeros((768, 1024), np.uint8)
+    for j in range(12):
+        y, x = 40 + 240 * (j // 4), 30 + 250 * (j % 4)
+        blobs[y:y + 90 + 5 * j, x:x + 100 + 7 * j] = 1     # 9000 .. 25000 pixels each
+    single = np.zeros((480, 640), np.uint8)
+    single[::8, ::8] = 1                                   # 4800 isolated pixels
+    single[200:260, 300:420] = 1                           # and one blob
+    few = np.zeros((480, 640), np.uint8)
+    few[::16, ::16] = 1                                    # 1200 singletons: the in-CTA list
+    few[100:140, 100:300] = 1
+    for m in (blobs, single, few):
+        for frac in (0.0, 0.01, 0.2, 0.5, 0.9):
+            eq(stk.prune_components(m, frac, device=dev), port.prune(m, frac))
+
+
 @pytest.mark.parametrize("w,h,seed,pct", [(300, 200, 1, 15), (517, 331, 2, 30), (1024, 256, 3, 8),
                                          (129, 65, 4, 45), (700, 140, 5, 22)])
 def test_prune_bitpacked_vs_oracle(dev, stk, port, synth, w, h, seed, pct):
