@@ -1029,9 +1029,16 @@ __global__ void __launch_bounds__(kUniteThreads, 1) k_ccl_unite(Frame f, const i
         for (int k = 0; k < PF; ++k) {
             if (sz[k] == 0) continue;  // non-roots (a root holds >= 1 pixel)
             ++nr;
-            if (sz[k] <= B + 1) atomicAdd(f.szhist + sz[k], 1u);
+            // with pf the global size histogram is only needed if the select
+            // below falls back to the cooperative prune (hist_out)
+            if (!pf && sz[k] <= B + 1) atomicAdd(f.szhist + sz[k], 1u);
         }
     }
+    auto hist_out = [&]() {
+#pragma unroll
+        for (int k = 0; k < PF; ++k)
+            if (sz[k] != 0 && sz[k] <= B + 1) atomicAdd(f.szhist + sz[k], 1u);
+    };
     nr = __reduce_add_sync(0xffffffffu, nr);
     if ((tid & 31) == 0 && nr) atomicAdd(&f.sc->n_roots, nr);
     if (tid == 0) f.sc->united = 1u;
@@ -1042,7 +1049,11 @@ __global__ void __launch_bounds__(kUniteThreads, 1) k_ccl_unite(Frame f, const i
     // CS(B + 1) <= B), q = (B - CS(s* - 1)) / s*; sizes < s* removed and the
     // q size-s* components with the smallest raster keys.
     constexpr int SB = 4096, LCAP = 2048;
-    if (!pf || n + SB + 2 * LCAP > capn) return;  // block-uniform
+    if (!pf) return;
+    if (n + SB + 2 * LCAP > capn) {  // block-uniform
+        hist_out();
+        return;
+    }
     int* const hist = sp + n;  // hist[s - 1], s = 1..SB
     int* const lkey = hist + SB;
     int* const lid = lkey + LCAP;
@@ -1095,7 +1106,10 @@ __global__ void __launch_bounds__(kUniteThreads, 1) k_ccl_unite(Frame f, const i
     long long sst = s_star;
     const unsigned long long q = s_q;
     if (sst < 0) {
-        if (L < (long long)B + 1) return;  // s* > SB: the cooperative prune decides
+        if (L < (long long)B + 1) {  // s* > SB: the cooperative prune decides
+            hist_out();
+            return;
+        }
         sst = (long long)B + 2;             // CS(B + 1) <= B: every size <= B + 1 goes
     }
     // the size-s* class (q > 0): listed first, so an over-long list falls back
@@ -1112,7 +1126,10 @@ __global__ void __launch_bounds__(kUniteThreads, 1) k_ccl_unite(Frame f, const i
             }
         }
         __syncthreads();
-        if (s_cnt > LCAP) return;  // block-uniform
+        if (s_cnt > LCAP) {  // block-uniform
+            hist_out();
+            return;
+        }
     }
 #pragma unroll
     for (int k = 0; k < PF; ++k)
