@@ -942,11 +942,15 @@ __global__ void __launch_bounds__(RW + RH) k_ccl_borders(Frame f, int32_t* __res
 // region roots (min-linking, path halving: shared-memory latency instead of
 // the L2 round trips of global unions) and writes every non-root's final root
 // to f.par (a flat forest: the later finds are one step).  Edges are read
-// four per thread at a time so their L2 latencies overlap.  4K frame (6478
-// roots, 13431 edges before B3's dedupe): 19.6 us vs 28 us for B3's old
-// global unions.  Measured and dropped: hash-priority CAS linking (2.2x the
-// union cycles), waves of one edge per thread with a flatten after each
-// (1.5x), a converged lockstep walk with per-pair leader election (3x).
+// four per thread at a time so their L2 latencies overlap.  4K frame with
+// 256x128 regions: 5411 roots, 9387 edges, ~20 us (B3's old global unions on
+// 128x128 regions: 28 us).  Measured and dropped: hash-priority CAS linking
+// (2.2x the union cycles), waves of one edge per thread with a flatten after
+// each (1.5x), a converged lockstep walk with per-pair leader election (3x),
+// lockstep walks of a thread's 8 roots, lanes of a warp on edges 32 apart
+// (+17 %), an 8-CTA cluster with the forest in distributed shared memory
+// (-5 %, not worth the cluster launch), shared-memory aggregation of the
+// sizes (no change).
 __global__ void __launch_bounds__(kUniteThreads, 1) k_ccl_unite(Frame f, const int32_t* __restrict__ bord, int capn,
                                                               int stats) {
     extern __shared__ int sp[];
